@@ -1,0 +1,170 @@
+/*
+ * mdsx.h — C-ABI of the B200-native big-data MDS hot path (libmdsx.so).
+ *
+ * Every entry point takes caller-owned DEVICE pointers (row-major, explicit
+ * leading dimension), plain sizes and a cudaStream_t passed as void*; it
+ * enqueues work on that stream and returns an mdsx_status.  Arrays marked
+ * "host" are read on the host before the call returns.  Nothing here ever
+ * frees caller memory; each handle owns its own device workspace (one
+ * stream at a time per handle).
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/scalemds):
+ *   mdsx_classical_pieces   <- classical_mds_from_data via _piece_mds
+ *                              (classical.py:153-160, algorithms.py:115-119),
+ *                              batched over every piece of a plan
+ *   mdsx_classical_delta    <- classical_mds (classical.py:109-150)
+ *   mdsx_sqdist_self        <- euclidean_distance_matrix (linalg.py:61-82)
+ *   mdsx_sqdist_cross       <- cross_squared_distances (linalg.py:85-104)
+ *   mdsx_double_center      <- double_center (linalg.py:107-121)
+ *   mdsx_gower_context      <- gower_context (algorithms.py:193-217)
+ *   mdsx_gower_interpolate  <- gower_interpolate (algorithms.py:220-242)
+ *   mdsx_procrustes_fit     <- fit_procrustes (procrustes.py:53-78), batched
+ *   mdsx_procrustes_apply   <- apply_procrustes (procrustes.py:99-105), batched
+ *   mdsx_divide_conquer     <- divide_and_conquer_mds (algorithms.py:128-172)
+ *   mdsx_interpolation      <- interpolation_mds (algorithms.py:245-274)
+ *   mdsx_recenter           <- _recentered (algorithms.py:122-125)
+ *   mdsx_scatter_rows       <- points[root.indices] = block (algorithms.py:341-342)
+ * fast_mds (algorithms.py:323-348) is composed from mdsx_classical_pieces,
+ * mdsx_procrustes_fit/apply, mdsx_scatter_rows and mdsx_recenter by the host
+ * (see INTEGRATION.md).
+ */
+#ifndef MDSX_H
+#define MDSX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the host shim maps them onto scalemds.errors (errors.py:4-41). */
+enum mdsx_status {
+  MDSX_OK = 0,
+  MDSX_PARAM = 1,          /* ParamError */
+  MDSX_SHAPE = 2,          /* ShapeError */
+  MDSX_INVALID_INPUT = 3,  /* InvalidInputError */
+  MDSX_NUMERICAL = 4,      /* NumericalError */
+  MDSX_DEGENERATE = 5,     /* DegenerateRankError */
+  MDSX_CUDA = 6,           /* CUDA runtime failure */
+  MDSX_UNSUPPORTED = 7     /* shape outside what this build handles */
+};
+
+/* Element type of data matrices: the reference coerces to float64
+ * (linalg.py:30); float32 storage is read and widened to float64 in-kernel. */
+enum mdsx_dtype { MDSX_F64 = 0, MDSX_F32 = 1 };
+
+/* Per-piece status record written by the batched classical-MDS kernels. */
+typedef struct mdsx_piece_status {
+  int32_t code;        /* mdsx_status */
+  int32_t index;       /* DegenerateRank: 1-based failing eigenvalue index */
+  double value;        /* DegenerateRank: the failing eigenvalue (snapped) */
+} mdsx_piece_status;
+
+typedef struct mdsx_handle mdsx_handle;
+
+int mdsx_create(int device, mdsx_handle** out);
+void mdsx_destroy(mdsx_handle* h);
+const char* mdsx_last_error(const mdsx_handle* h);
+/* Number of kernels this handle has launched since creation. */
+int64_t mdsx_launch_count(const mdsx_handle* h);
+int mdsx_version(void);
+
+/* ---- dense primitives (function-level seams) ---------------------------- */
+/* out (m x m, ldo) = squared distances between rows of x (m x p, ld);
+ * symmetrised, clamped at 0, exact-zero diagonal. */
+int mdsx_sqdist_self(mdsx_handle* h, const void* x, int dtype, int64_t ld,
+                     int64_t m, int32_t p, double* out, int64_t ldo, void* stream);
+/* out (ma x mb, ldo) = squared distances rows(a) x rows(b), clamped at 0. */
+int mdsx_sqdist_cross(mdsx_handle* h, const void* a, int64_t lda, int64_t ma,
+                      const void* b, int64_t ldb, int64_t mb, int dtype, int32_t p,
+                      double* out, int64_t ldo, void* stream);
+/* q (m x m) = -1/2 (d - rowmean_i - rowmean_j + grandmean), symmetrised. */
+int mdsx_double_center(mdsx_handle* h, const double* delta, int64_t m, double* q,
+                       void* stream);
+
+/* ---- batched classical MDS of the pieces of a plan ---------------------- */
+/* Piece j is rows row_idx[piece_off[j] .. piece_off[j+1]) of data (n x p).
+ * points  (total x r): configuration of every piece, piece order, rows in
+ *                      row_idx order, canonical column signs (linalg.py:139-146)
+ * estimates (npieces x r): lambda_i / m_j   gof (npieces x 2): G1, G2
+ * status (npieces): per-piece mdsx_piece_status.
+ * piece_off is a HOST array of npieces+1 offsets. */
+int mdsx_classical_pieces(mdsx_handle* h, const void* data, int dtype, int64_t ld,
+                          int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                          int32_t npieces, int32_t r, double* points, double* estimates,
+                          double* gof, mdsx_piece_status* status, void* stream);
+
+/* Validity flags of a squared-distance matrix (linalg.py:41-58), OR-ed into
+ * *flags (device int32, caller-zeroed): 1 non-finite, 2 asymmetric,
+ * 4 nonzero diagonal, 8 negative entries (tolerance 1e-9 max(|d|max, 1)). */
+int mdsx_delta_check(mdsx_handle* h, const double* delta, int64_t m, int32_t* flags, void* stream);
+
+/* Classical MDS of a precomputed squared-distance matrix (m x m). */
+int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t r,
+                         double* points, double* estimates, double* gof,
+                         mdsx_piece_status* status, void* stream);
+
+/* ---- Gower interpolation ------------------------------------------------ */
+/* Context packed as doubles: [mean(p) | M(p x r) | v(r) | S(r x r) | q(l)],
+ * size mdsx_gower_context_size(l, p, r).  base rows are data[base_idx[j]]
+ * (base_idx may be NULL: rows 0..l-1), base_config is (l x r). cond (1 double,
+ * device) receives the covariance condition estimate; flag (1 int32, device)
+ * 0 ok, 1 condition > 1e12, 2 covariance not positive definite. */
+int64_t mdsx_gower_context_size(int64_t l, int32_t p, int32_t r);
+int mdsx_gower_context(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                       const int64_t* base_idx, int64_t l, const double* base_config,
+                       int32_t r, double* ctx, double* cond, int32_t* flag, void* stream);
+/* out (m x r, ldo) = Gower coordinates of rows data[0..m) in the base frame;
+ * *nonfinite (device int32, caller-zeroed) is set if an input is not finite. */
+int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
+                           const void* rows, int dtype, int64_t ld, int64_t m,
+                           double* out, int64_t ldo, int32_t* nonfinite, void* stream);
+
+/* ---- Procrustes ----------------------------------------------------------- */
+/* Job j aligns src rows src_rows[job_off[j]..job_off[j+1]) of src (ld = r)
+ * onto tgt rows tgt_rows[...] of tgt.  job_off is a HOST array.
+ * rot (njobs x r x r), trans (njobs x r), loss (njobs), degenerate (njobs). */
+int mdsx_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
+                        const double* src, const int64_t* src_rows, const int64_t* job_off,
+                        int32_t njobs, int32_t r, double* rot, double* trans, double* loss,
+                        int32_t* degenerate, void* stream);
+/* In place: buf[start_j + i] = buf[start_j + i] @ rot_j + trans_j for
+ * i < len_j.  start/len are DEVICE arrays of njobs int64. */
+int mdsx_procrustes_apply(mdsx_handle* h, double* buf, int32_t r, const int64_t* start,
+                          const int64_t* len, int32_t njobs, int64_t max_len,
+                          const double* rot, const double* trans, void* stream);
+
+/* ---- stitching / finishing ------------------------------------------------ */
+/* out[idx[i]] = src[i] (rows of r doubles), i < n. */
+int mdsx_scatter_rows(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n,
+                      int32_t r, double* out, void* stream);
+/* points (n x r) -= column means (fixed-order, deterministic reduction). */
+int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* stream);
+
+/* ---- whole algorithms ------------------------------------------------------ */
+/* divide_and_conquer_mds with an explicit plan (partition.py:184-214 layout:
+ * every subset = c connecting rows then own rows).  out (n x r) in original
+ * row order, re-centred (callers handle the n <= l passthrough with
+ * mdsx_classical_pieces, as algorithms.py:142-143 does).  Per-piece estimates/gof/status as in
+ * mdsx_classical_pieces; the host aggregates them in plan order. */
+int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                        int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                        int32_t npieces, int32_t c, int32_t r, double* out,
+                        double* estimates, double* gof, mdsx_piece_status* status,
+                        void* stream);
+/* interpolation_mds with an explicit landmark sample (sample_idx, device, l).
+ * out (n x r) in original row order, re-centred; estimates (r), gof (2),
+ * status (1) describe the landmark MDS; cond (1) the covariance condition;
+ * flags (2 int32, device, caller-zeroed): [0] context flag as in
+ * mdsx_gower_context, [1] non-finite input seen. */
+int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                       int32_t p, const int64_t* sample_idx, int64_t l, int32_t r,
+                       double* out, double* estimates, double* gof,
+                       mdsx_piece_status* status, double* cond, int32_t* flags,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDSX_H */

@@ -1,0 +1,90 @@
+"""Device plumbing: input coercion/staging, streams, small D2H reads.
+
+PyTorch is used only for device memory, streams and copies."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidInputError
+
+
+def require_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA device is required: this package has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError(f"device {dev} is not a CUDA device (no CPU fallback)")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def stream_ptr(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def handle(dev: torch.device) -> _lib.Handle:
+    return _lib.Handle.get(dev.index)
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    return _lib.F32 if t.dtype == torch.float32 else _lib.F64
+
+
+def host_matrix(data, name: str = "data") -> np.ndarray:
+    """Shape checks of linalg.py:28-38 on the host (finiteness is checked by
+    the kernels that read the data).  float32 stays float32 (read and widened
+    to float64 on the device); anything else becomes float64."""
+    if isinstance(data, np.ndarray) and data.dtype in (np.float32, np.float64):
+        arr = data
+    else:
+        arr = np.asarray(data, dtype=np.float64)
+    if arr.ndim != 2:
+        raise InvalidInputError(f"{name} must be 2-dimensional, got ndim={arr.ndim}")
+    if arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise InvalidInputError(f"{name} must be non-empty, got shape {arr.shape}")
+    return arr
+
+
+def to_device_matrix(data, dev: torch.device, name: str = "data") -> torch.Tensor:
+    """Device-resident row-major float32/float64 matrix for the C-ABI."""
+    if isinstance(data, torch.Tensor):
+        t = data
+        if t.dim() != 2:
+            raise InvalidInputError(f"{name} must be 2-dimensional, got ndim={t.dim()}")
+        if t.shape[0] < 1 or t.shape[1] < 1:
+            raise InvalidInputError(f"{name} must be non-empty, got shape {tuple(t.shape)}")
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        if t.device != dev:
+            t = t.to(dev, non_blocking=t.device.type == "cpu" and t.is_pinned())
+        return t.contiguous()
+    arr = np.ascontiguousarray(host_matrix(data, name))
+    return torch.from_numpy(arr).to(dev)
+
+
+def index_tensor(idx: np.ndarray, dev: torch.device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64)).to(dev)
+
+
+def empty(shape, dev: torch.device, dtype=torch.float64) -> torch.Tensor:
+    return torch.empty(shape, dtype=dtype, device=dev)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+STATUS_DTYPE = np.dtype([("code", np.int32), ("index", np.int32), ("value", np.float64)])
+
+
+def status_tensor(n: int, dev: torch.device) -> torch.Tensor:
+    return torch.zeros((n, 2), dtype=torch.float64, device=dev)  # 16 B per record
+
+
+def decode_status(t: torch.Tensor) -> np.ndarray:
+    raw = t.detach().cpu().numpy().view(np.uint8).reshape(-1, 16)
+    return raw.copy().view(STATUS_DTYPE).reshape(-1)

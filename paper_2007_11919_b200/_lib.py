@@ -1,0 +1,125 @@
+"""ctypes binding of libmdsx.so (the C-ABI in include/mdsx.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+compute entry point raises ``RuntimeError`` naming what is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+from .errors import (DegenerateRankError, InvalidInputError, MdsError, NumericalError,
+                     ParamError, ShapeError)
+
+LIB_PATH = Path(__file__).resolve().parent / "libmdsx.so"
+
+OK, PARAM, SHAPE, INVALID, NUMERICAL, DEGENERATE, CUDA, UNSUPPORTED = range(8)
+F64, F32 = 0, 1
+
+
+class PieceStatus(C.Structure):
+    _fields_ = [("code", C.c_int32), ("index", C.c_int32), ("value", C.c_double)]
+
+
+_vp = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+_int = C.c_int
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "mdsx_version": (_int, []),
+    "mdsx_create": (_int, [_int, C.POINTER(_vp)]),
+    "mdsx_destroy": (None, [_vp]),
+    "mdsx_last_error": (C.c_char_p, [_vp]),
+    "mdsx_launch_count": (_i64, [_vp]),
+    "mdsx_sqdist_self": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _vp]),
+    "mdsx_sqdist_cross": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _int, _i32, _vp, _i64, _vp]),
+    "mdsx_double_center": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "mdsx_delta_check": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "mdsx_classical_pieces": (_int, [_vp, _vp, _int, _i64, _i32, _vp, _vp, _i32, _i32,
+                                     _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_classical_delta": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_gower_context_size": (_i64, [_i64, _i32, _i32]),
+    "mdsx_gower_context": (_int, [_vp, _vp, _int, _i64, _i32, _vp, _i64, _vp, _i32, _vp, _vp,
+                                  _vp, _vp]),
+    "mdsx_gower_interpolate": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _int, _i64, _i64, _vp,
+                                      _i64, _vp, _vp]),
+    "mdsx_procrustes_fit": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
+                                   _vp, _vp]),
+    "mdsx_procrustes_apply": (_int, [_vp, _vp, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
+    "mdsx_scatter_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "mdsx_recenter": (_int, [_vp, _vp, _i64, _i32, _vp]),
+    "mdsx_divide_conquer": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
+                                   _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,
+                                  _vp, _vp, _vp, _vp, _vp]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load and type the shared library (no device work)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2007_11919_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class Handle:
+    """One mdsx_handle per CUDA device (owns that device's workspace)."""
+
+    _by_device: dict = {}
+    _lock = threading.Lock()
+
+    def __init__(self, device: int):
+        lib = load()
+        ptr = C.c_void_p()
+        rc = lib.mdsx_create(device, C.byref(ptr))
+        if rc != OK:
+            raise RuntimeError(f"mdsx_create(device={device}) failed with status {rc}")
+        self.ptr = ptr
+        self.device = device
+        self.lib = lib
+
+    @classmethod
+    def get(cls, device: int) -> "Handle":
+        with cls._lock:
+            h = cls._by_device.get(device)
+            if h is None:
+                h = cls._by_device[device] = Handle(device)
+            return h
+
+    def launches(self) -> int:
+        return int(self.lib.mdsx_launch_count(self.ptr))
+
+    def call(self, name: str, *args) -> None:
+        rc = getattr(self.lib, name)(self.ptr, *args)
+        if rc != OK:
+            msg = self.lib.mdsx_last_error(self.ptr).decode(errors="replace")
+            raise status_error(rc, msg or name)
+
+
+def status_error(code: int, msg: str) -> Exception:
+    return {
+        PARAM: ParamError, SHAPE: ShapeError, INVALID: InvalidInputError,
+        NUMERICAL: NumericalError, DEGENERATE: DegenerateRankError,
+    }.get(code, MdsError if code == UNSUPPORTED else RuntimeError)(msg)
+
+
+def total_launches() -> int:
+    return sum(h.launches() for h in Handle._by_device.values())

@@ -1,0 +1,245 @@
+"""The three partition-based MDS algorithms on the GPU — drop-in for
+``interpolation_mds``, ``divide_and_conquer_mds``, ``fast_mds`` and
+``run_algorithm`` (algorithms.py:128-363): same names, positional arguments,
+defaults, results and exceptions.  Extra keyword-only arguments:
+
+  device=        CUDA device (default: current)
+  plan=          explicit plan (DcPlan / InterpPlan / FastPlan) instead of
+                 drawing one from params.seed
+  return_device= keep ``points`` as a CUDA tensor (no D2H copy)
+  threads=       accepted and ignored (results never depend on it)
+
+Each algorithm is split into prepare (plan flattening, H2D of indices),
+launch (pure device work, no host sync — what bench.py times) and finish
+(one small D2H read of statuses/fit figures, error mapping, host-side
+aggregation of per-piece G1/G2/estimates in plan order).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as D
+from .errors import InvalidInputError, NumericalError, ParamError
+from .params import ALGORITHM_NAMES, AlgorithmParams
+from .plans import (DcPlan, FastPlan, InterpPlan, flatten_fast, flatten_subsets,
+                    interpolation_sample, plan_divide_conquer, plan_fast)
+from .primitives import classical_mds_from_data, raise_piece_status
+from .results import MdsConfiguration
+
+
+def _finish_points(points: torch.Tensor, return_device: bool):
+    return points if return_device else points.cpu().numpy()
+
+
+# ====================================================================== D&C
+class DivideRun:
+    """divide_and_conquer_mds (algorithms.py:128-172) with an explicit plan."""
+
+    def __init__(self, x: torch.Tensor, plan: DcPlan, r: int, c: int):
+        self.x, self.plan, self.r, self.c = x, plan, r, c
+        self.dev = x.device
+        rows, off = flatten_subsets(plan.subsets)
+        self.row_idx = D.index_tensor(rows, self.dev)
+        self.piece_off = off
+        n, npc = plan.n, plan.p
+        self.out = D.empty((n, r), self.dev)
+        self.est = D.empty((npc, r), self.dev)
+        self.gof = D.empty((npc, 2), self.dev)
+        self.status = D.status_tensor(npc, self.dev)
+
+    def launch(self) -> None:
+        x = self.x
+        D.handle(self.dev).call(
+            "mdsx_divide_conquer", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
+            x.shape[1], self.row_idx.data_ptr(), self.piece_off.ctypes.data, self.plan.p, self.c,
+            self.r, self.out.data_ptr(), self.est.data_ptr(), self.gof.data_ptr(),
+            self.status.data_ptr(), D.stream_ptr(self.dev))
+
+    def finish(self, return_device: bool = False) -> MdsConfiguration:
+        st = D.decode_status(self.status)
+        if np.any(st["code"] == 3):
+            raise InvalidInputError("data contains non-finite values")
+        for j, rec in enumerate(st):                      # first failing subset in plan order
+            raise_piece_status(rec, self.r, f"subset {j + 1}")
+        gof = self.gof.cpu().numpy()
+        est = self.est.cpu().numpy()
+        n, c = self.plan.n, self.c
+        sizes = np.array([len(q) for q in self.plan.subsets], dtype=np.float64)
+        weights = sizes.copy()
+        weights[1:] -= c                                  # algorithms.py:158-166
+        g1 = float(np.dot(weights, gof[:, 0]) / n)
+        g2 = float(np.dot(weights, gof[:, 1]) / n)
+        per = np.stack([est[j] * (sizes[j] / weights[j]) for j in range(len(sizes))])
+        return MdsConfiguration(_finish_points(self.out, return_device), per.mean(axis=0), g1, g2)
+
+
+def divide_and_conquer_mds(data, params: AlgorithmParams, *, threads=None, device=None,
+                           plan: DcPlan | None = None, return_device: bool = False):
+    dev = D.require_device(device)
+    x = D.to_device_matrix(data, dev)
+    prm = params.resolved("divide")
+    n = x.shape[0]
+    if n <= prm.l:
+        return classical_mds_from_data(x, prm.r, device=dev, return_device=return_device)
+    plan = plan if plan is not None else plan_divide_conquer(n, prm.l, prm.c, prm.seed)
+    run = DivideRun(x, plan, prm.r, prm.c)
+    run.launch()
+    return run.finish(return_device)
+
+
+# ============================================================ interpolation
+class InterpolationRun:
+    """interpolation_mds (algorithms.py:245-274) given the landmark sample."""
+
+    def __init__(self, x: torch.Tensor, sample: np.ndarray, r: int):
+        self.x, self.r = x, r
+        self.dev = x.device
+        self.sample = D.index_tensor(sample, self.dev)
+        self.l = len(sample)
+        self.out = D.empty((x.shape[0], r), self.dev)
+        self.est = D.empty((1, r), self.dev)
+        self.gof = D.empty((1, 2), self.dev)
+        self.status = D.status_tensor(1, self.dev)
+        self.cond = D.empty((1,), self.dev)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=self.dev)
+
+    def launch(self) -> None:
+        x = self.x
+        D.handle(self.dev).call(
+            "mdsx_interpolation", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
+            x.shape[1], self.sample.data_ptr(), self.l, self.r, self.out.data_ptr(),
+            self.est.data_ptr(), self.gof.data_ptr(), self.status.data_ptr(),
+            self.cond.data_ptr(), self.flags.data_ptr(), D.stream_ptr(self.dev))
+
+    def finish(self, return_device: bool = False) -> MdsConfiguration:
+        flags = self.flags.cpu().numpy()
+        st = D.decode_status(self.status)[0]
+        if int(st["code"]) == 3 or flags[1]:
+            raise InvalidInputError("data contains non-finite values")
+        raise_piece_status(st, self.r, "sample subset")
+        if flags[0] == 1:
+            raise NumericalError(f"base covariance is ill-conditioned (condition estimate "
+                                 f"{float(self.cond.item()):.3e}); the requested dimension "
+                                 "exceeds the usable rank")
+        if flags[0] == 2:
+            raise NumericalError("base covariance is not positive definite")
+        g = self.gof.cpu().numpy()[0]
+        return MdsConfiguration(_finish_points(self.out, return_device),
+                                self.est.cpu().numpy()[0], float(g[0]), float(g[1]))
+
+
+def interpolation_mds(data, params: AlgorithmParams, *, threads=None, device=None,
+                      plan: InterpPlan | None = None, return_device: bool = False):
+    dev = D.require_device(device)
+    x = D.to_device_matrix(data, dev)
+    prm = params.resolved("interpolate")
+    n = x.shape[0]
+    if n <= prm.l:
+        return classical_mds_from_data(x, prm.r, device=dev, return_device=return_device)
+    sample = plan.subsets[0] if plan is not None else interpolation_sample(n, prm.l, prm.seed)
+    run = InterpolationRun(x, sample, prm.r)
+    run.launch()
+    return run.finish(return_device)
+
+
+# ==================================================================== fast
+class FastRun:
+    """fast_mds (algorithms.py:285-348) as three device waves: one batched
+    classical-MDS launch over every leaf and alignment set, then per depth
+    (deepest first) one batched Procrustes fit + one batched in-place apply,
+    then scatter to input order and re-centre."""
+
+    def __init__(self, x: torch.Tensor, plan: FastPlan, r: int):
+        self.x, self.plan, self.r = x, plan, r
+        self.dev = dev = x.device
+        flat = self.flat = flatten_fast(plan)
+        self.piece_rows = D.index_tensor(flat.piece_rows, dev)
+        self.order = D.index_tensor(flat.order, dev)
+        self.levels = []
+        for lv in flat.levels:
+            nj = len(lv.start)
+            self.levels.append(dict(
+                tgt=D.index_tensor(lv.tgt_rows, dev), src=D.index_tensor(lv.src_rows, dev),
+                job_off=np.ascontiguousarray(lv.job_off), start=D.index_tensor(lv.start, dev),
+                length=D.index_tensor(lv.length, dev), max_len=int(lv.length.max()), nj=nj,
+                rot=D.empty((nj, r, r), dev), trans=D.empty((nj, r), dev),
+                loss=D.empty((nj,), dev), deg=torch.empty(nj, dtype=torch.int32, device=dev)))
+        npc = len(flat.piece_off) - 1
+        total = int(flat.piece_off[-1])
+        self.pts = D.empty((total, r), dev)
+        self.est = D.empty((npc, r), dev)
+        self.gof = D.empty((npc, 2), dev)
+        self.status = D.status_tensor(npc, dev)
+        self.out = D.empty((plan.n, r), dev)
+
+    def launch(self) -> None:
+        x, r, dev = self.x, self.r, self.dev
+        h, sp = D.handle(dev), D.stream_ptr(dev)
+        npc = len(self.flat.piece_off) - 1
+        h.call("mdsx_classical_pieces", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[1],
+               self.piece_rows.data_ptr(), self.flat.piece_off.ctypes.data, npc, r,
+               self.pts.data_ptr(), self.est.data_ptr(), self.gof.data_ptr(),
+               self.status.data_ptr(), sp)
+        P = self.pts.data_ptr()
+        for lv in self.levels:
+            h.call("mdsx_procrustes_fit", P, lv["tgt"].data_ptr(), P, lv["src"].data_ptr(),
+                   lv["job_off"].ctypes.data, lv["nj"], r, lv["rot"].data_ptr(),
+                   lv["trans"].data_ptr(), lv["loss"].data_ptr(), lv["deg"].data_ptr(), sp)
+            h.call("mdsx_procrustes_apply", P, r, lv["start"].data_ptr(), lv["length"].data_ptr(),
+                   lv["nj"], lv["max_len"], lv["rot"].data_ptr(), lv["trans"].data_ptr(), sp)
+        h.call("mdsx_scatter_rows", P, self.order.data_ptr(), self.plan.n, r,
+               self.out.data_ptr(), sp)
+        h.call("mdsx_recenter", self.out.data_ptr(), self.plan.n, r, sp)
+
+    def finish(self, return_device: bool = False) -> MdsConfiguration:
+        st = D.decode_status(self.status)
+        if np.any(st["code"] == 3):
+            raise InvalidInputError("data contains non-finite values")
+        for pid in self.flat.eval_order:
+            raise_piece_status(st[pid], self.r, self.flat.labels[pid])
+        gof = self.gof.cpu().numpy()
+        est = self.est.cpu().numpy()
+        leaf = iter(range(self.flat.n_leaves))
+
+        def agg(node):                                 # algorithms.py:289-320
+            if node.is_leaf:
+                j = next(leaf)
+                return gof[j, 0], gof[j, 1], est[j], node.size
+            fits = [agg(ch) for ch in node.children]
+            sizes = np.array([f[3] for f in fits], dtype=np.float64)
+            tot = sizes.sum()
+            return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
+                    float(np.dot(sizes, [f[1] for f in fits]) / tot),
+                    np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
+
+        g1, g2, e, _ = agg(self.plan.root)
+        return MdsConfiguration(_finish_points(self.out, return_device), e, float(g1), float(g2))
+
+
+def fast_mds(data, params: AlgorithmParams, *, threads=None, device=None,
+             plan: FastPlan | None = None, return_device: bool = False):
+    dev = D.require_device(device)
+    x = D.to_device_matrix(data, dev)
+    prm = params.resolved("fast")
+    n = x.shape[0]
+    if n <= prm.l:
+        return classical_mds_from_data(x, prm.r, device=dev, return_device=return_device)
+    plan = plan if plan is not None else plan_fast(n, prm.l, prm.s, prm.seed)
+    run = FastRun(x, plan, prm.r)
+    run.launch()
+    return run.finish(return_device)
+
+
+def run_algorithm(name: str, data, params: AlgorithmParams, *, threads=None, **kw):
+    """algorithms.py:351-363."""
+    if name == "classical":
+        return classical_mds_from_data(data, params.r, **kw)
+    if name == "divide":
+        return divide_and_conquer_mds(data, params, threads=threads, **kw)
+    if name == "interpolate":
+        return interpolation_mds(data, params, threads=threads, **kw)
+    if name == "fast":
+        return fast_mds(data, params, threads=threads, **kw)
+    raise ParamError(f"unknown algorithm {name!r}; expected one of {ALGORITHM_NAMES}")

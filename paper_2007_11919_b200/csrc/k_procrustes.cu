@@ -1,0 +1,334 @@
+// K5 Procrustes (procrustes.py:46-105, linalg.py:186-205) and K6/K7
+// stitching: recentering (algorithms.py:122-125) and row scatters
+// (algorithms.py:146-156, 341-342).
+//
+// fit: one warp per job.  Cross-product of the centred configurations
+// (r x r), then a one-sided (Hestenes) Jacobi SVD in shared memory: the
+// columns of B = cross are orthogonalised by plane rotations accumulated in
+// V, so cross = L diag(sigma) V^T with L = B / sigma.  The rotation is
+// T = V L^T = sum_i v_i l_i^T, which is independent of the order and paired
+// signs of the singular triplets — the same T thin_svd + right @ left.T gives.
+#include "mdsx_common.cuh"
+
+#include <algorithm>
+
+namespace {
+
+constexpr int FIT_WARPS = 4;
+
+__global__ void __launch_bounds__(FIT_WARPS * 32)
+procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
+                      const double* __restrict__ src, const int64_t* __restrict__ src_rows,
+                      const int64_t* __restrict__ job_off, int njobs, int r,
+                      double* __restrict__ rot, double* __restrict__ trans,
+                      double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * FIT_WARPS + warp;
+  if (job >= njobs) return;
+  double* B = sm + (size_t)warp * (2 * r * r + 3 * r);
+  double* V = B + r * r;
+  double* mt = V + r * r;
+  double* ms = mt + r;
+  double* sg = ms + r;
+  const int64_t o = job_off[job];
+  const int K = (int)(job_off[job + 1] - o);
+  const int64_t* tr = tgt_rows + o;
+  const int64_t* sr = src_rows + o;
+
+  if (lane < r) {
+    double a = 0.0, b = 0.0;
+    for (int t = 0; t < K; ++t) {
+      a += tgt[tr[t] * r + lane];
+      b += src[sr[t] * r + lane];
+    }
+    mt[lane] = a / K;
+    ms[lane] = b / K;
+  }
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {
+    const int a = e / r, b = e % r;
+    double s = 0.0;
+    for (int t = 0; t < K; ++t)
+      s = fma(tgt[tr[t] * r + a] - mt[a], src[sr[t] * r + b] - ms[b], s);
+    B[e] = s;
+    V[e] = (a == b) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+
+  // one-sided Jacobi on the columns of B (lane a owns row a)
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int nrot = 0;
+    for (int i = 0; i < r - 1; ++i)
+      for (int j = i + 1; j < r; ++j) {
+        const double x = lane < r ? B[lane * r + i] : 0.0;
+        const double y = lane < r ? B[lane * r + j] : 0.0;
+        const double al = mdsx::warp_sum(x * x);
+        const double be = mdsx::warp_sum(y * y);
+        const double ga = mdsx::warp_sum(x * y);
+        if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          if (lane < r) {
+            B[lane * r + i] = c * x - s * y;
+            B[lane * r + j] = s * x + c * y;
+            const double vx = V[lane * r + i], vy = V[lane * r + j];
+            V[lane * r + i] = c * vx - s * vy;
+            V[lane * r + j] = s * vx + c * vy;
+          }
+          ++nrot;
+        }
+        __syncwarp();
+      }
+    if (nrot == 0) break;
+  }
+  // singular values and left vectors (columns of B normalised)
+  double smax = 0.0, smin = 1e308;
+  for (int i = 0; i < r; ++i) {
+    const double x = lane < r ? B[lane * r + i] : 0.0;
+    const double s = sqrt(mdsx::warp_sum(x * x));
+    if (lane == 0) sg[i] = s;
+    smax = fmax(smax, s);
+    smin = fmin(smin, s);
+  }
+  __syncwarp();
+  for (int i = 0; i < r; ++i) {
+    const double s = sg[i];
+    if (s > 1e-15 * smax && s > 0.0 && lane < r) B[lane * r + i] /= s;
+  }
+  __syncwarp();
+  for (int i = 0; i < r; ++i) {
+    const double s = sg[i];
+    if (s > 1e-15 * smax && s > 0.0) continue;
+    // rank-deficient: complete the left basis by Gram-Schmidt on e_q
+    for (int q = 0; q < r; ++q) {
+      double v = (lane == q) ? 1.0 : 0.0;
+      for (int l = 0; l < r; ++l) {
+        if (l == i) continue;
+        const bool good = sg[l] > 1e-15 * smax && sg[l] > 0.0;
+        if (!good && l > i) continue;
+        const double ll = lane < r ? B[lane * r + l] : 0.0;
+        const double dot = __shfl_sync(0xffffffffu, ll, q);
+        v -= dot * ll;
+      }
+      const double nv = sqrt(mdsx::warp_sum(lane < r ? v * v : 0.0));
+      if (nv > 0.5) {
+        if (lane < r) B[lane * r + i] = v / nv;
+        break;
+      }
+    }
+    __syncwarp();
+  }
+  // T = V L^T  (row a of T on lane a)
+  double* T = rot + (size_t)job * r * r;
+  if (lane < r)
+    for (int b = 0; b < r; ++b) {
+      double s = 0.0;
+      for (int i = 0; i < r; ++i) s = fma(V[lane * r + i], B[b * r + i], s);
+      T[lane * r + b] = s;
+    }
+  __syncwarp();
+  // translation t = mean(tgt) - mean(src) T ; loss
+  double* tv = trans + (size_t)job * r;
+  if (lane < r) {
+    double s = 0.0;
+    for (int a = 0; a < r; ++a) s = fma(ms[a], T[a * r + lane], s);
+    tv[lane] = mt[lane] - s;
+  }
+  __syncwarp();
+  double ls = 0.0;
+  if (lane < r) {
+    const double tl = tv[lane];
+    for (int t = 0; t < K; ++t) {
+      double s = 0.0;
+      for (int a = 0; a < r; ++a) s = fma(src[sr[t] * r + a], T[a * r + lane], s);
+      const double e = tgt[tr[t] * r + lane] - s - tl;
+      ls = fma(e, e, ls);
+    }
+  }
+  ls = mdsx::warp_sum(ls);
+  if (lane == 0) {
+    loss[job] = ls;
+    degenerate[job] = (r == 0 || smin <= 1e-12 * smax) ? 1 : 0;
+  }
+}
+
+template <int RM>
+__global__ void __launch_bounds__(256)
+apply_kernel(double* __restrict__ buf, int r, const int64_t* __restrict__ start,
+             const int64_t* __restrict__ len, const double* __restrict__ rot,
+             const double* __restrict__ trans) {
+  const int job = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len[job]) return;
+  const double* T = rot + (size_t)job * r * r;
+  const double* tv = trans + (size_t)job * r;
+  double* row = buf + (start[job] + i) * r;
+  double x[RM];
+#pragma unroll
+  for (int a = 0; a < RM; ++a) x[a] = a < r ? row[a] : 0.0;
+#pragma unroll
+  for (int b = 0; b < RM; ++b) {
+    if (b >= r) break;
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+      if (a < r) s = fma(x[a], T[a * r + b], s);
+    row[b] = s + tv[b];
+  }
+}
+
+// D&C stitch (algorithms.py:151-156): piece 0 verbatim, piece j>0 rows c..
+// through fit j-1, scattered to original rows.
+template <int RM>
+__global__ void __launch_bounds__(256)
+dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_idx,
+                 const int64_t* __restrict__ off, int c, int r, const double* __restrict__ rot,
+                 const double* __restrict__ trans, double* __restrict__ out) {
+  const int j = blockIdx.y;
+  const int64_t o = off[j], m = off[j + 1] - o;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (j == 0 ? 0 : c);
+  if (i >= m) return;
+  const double* src = P + (o + i) * r;
+  double* dst = out + row_idx[o + i] * r;
+  if (j == 0) {
+    for (int b = 0; b < r; ++b) dst[b] = src[b];
+    return;
+  }
+  const double* T = rot + (size_t)(j - 1) * r * r;
+  const double* tv = trans + (size_t)(j - 1) * r;
+  double x[RM];
+#pragma unroll
+  for (int a = 0; a < RM; ++a) x[a] = a < r ? src[a] : 0.0;
+#pragma unroll
+  for (int b = 0; b < RM; ++b) {
+    if (b >= r) break;
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+      if (a < r) s = fma(x[a], T[a * r + b], s);
+    dst[b] = s + tv[b];
+  }
+}
+
+__global__ void scatter_kernel(const double* __restrict__ src, const int64_t* __restrict__ idx,
+                               int64_t n, int r, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * r) return;
+  const int64_t i = e / r;
+  const int b = (int)(e - i * r);
+  out[idx[i] * r + b] = src[e];
+}
+
+constexpr int RC_BLOCKS = 296;
+
+// deterministic column sums: block b owns a fixed contiguous row range
+template <int RM>
+__global__ void __launch_bounds__(256)
+colsum_partial_kernel(const double* __restrict__ X, int64_t n, int r, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+  double acc[RM];
+#pragma unroll
+  for (int c = 0; c < RM; ++c) acc[c] = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += 256)
+#pragma unroll
+    for (int c = 0; c < RM; ++c)
+      if (c < r) acc[c] += X[i * r + c];
+  for (int c = 0; c < r; ++c) {
+    red[threadIdx.x] = acc[c];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * r + c] = red[0];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256)
+subtract_mean_kernel(double* __restrict__ X, int64_t n, int r, const double* __restrict__ part,
+                     int nparts) {
+  __shared__ double mean[MDSX_MAX_R];
+  if (threadIdx.x < r) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * r + threadIdx.x];
+    mean[threadIdx.x] = s / (double)n;
+  }
+  __syncthreads();
+  const int64_t total = n * r;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    X[e] -= mean[e % r];
+}
+
+}  // namespace
+
+namespace mdsx {
+
+int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
+                          const double* src, const int64_t* src_rows, const int64_t* job_off_dev,
+                          int njobs, int r, double* rot, double* trans, double* loss,
+                          int32_t* degenerate, cudaStream_t st) {
+  if (njobs == 0) return MDSX_OK;
+  const size_t smem = (size_t)FIT_WARPS * (2 * r * r + 3 * r) * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(procrustes_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  const int blocks = (njobs + FIT_WARPS - 1) / FIT_WARPS;
+  procrustes_fit_kernel<<<blocks, FIT_WARPS * 32, smem, st>>>(tgt, tgt_rows, src, src_rows,
+                                                               job_off_dev, njobs, r, rot, trans,
+                                                               loss, degenerate);
+  return launched(h, "procrustes_fit_kernel");
+}
+
+int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const int64_t* len,
+                 int njobs, int64_t max_len, const double* rot, const double* trans,
+                 cudaStream_t st) {
+  if (njobs == 0 || max_len == 0) return MDSX_OK;
+  dim3 grid((unsigned)((max_len + 255) / 256), (unsigned)njobs);
+  if (r <= 4) apply_kernel<4><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
+  else if (r <= 8) apply_kernel<8><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
+  else if (r <= 16) apply_kernel<16><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
+  else apply_kernel<32><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
+  return launched(h, "apply_kernel");
+}
+
+int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
+                     int npieces, int64_t max_m, int c, int r, const double* rot,
+                     const double* trans, double* out, cudaStream_t st) {
+  dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)npieces);
+  if (r <= 4) dc_stitch_kernel<4><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
+  else if (r <= 8) dc_stitch_kernel<8><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
+  else if (r <= 16) dc_stitch_kernel<16><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
+  else dc_stitch_kernel<32><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
+  return launched(h, "dc_stitch_kernel");
+}
+
+int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
+                   double* out, cudaStream_t st) {
+  if (n == 0) return MDSX_OK;
+  const int64_t total = n * r;
+  scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(src, idx, n, r, out);
+  return launched(h, "scatter_kernel");
+}
+
+size_t recenter_ws_bytes(int r) { return (size_t)RC_BLOCKS * r * sizeof(double); }
+
+int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st) {
+  if (n == 0) return MDSX_OK;
+  if (r <= 4) colsum_partial_kernel<4><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
+  else if (r <= 8) colsum_partial_kernel<8><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
+  else if (r <= 16) colsum_partial_kernel<16><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
+  else colsum_partial_kernel<32><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
+  int rc = launched(h, "colsum_partial_kernel");
+  if (rc) return rc;
+  const int64_t total = n * r;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)h->num_sms * 8);
+  subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, RC_BLOCKS);
+  return launched(h, "subtract_mean_kernel");
+}
+
+}  // namespace mdsx

@@ -1,0 +1,499 @@
+// C-ABI entry points and the handle runtime (workspace, staging, errors).
+#include "mdsx_common.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace mdsx {
+int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
+                          const double* src, const int64_t* src_rows, const int64_t* job_off_dev,
+                          int njobs, int r, double* rot, double* trans, double* loss,
+                          int32_t* degenerate, cudaStream_t st);
+int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const int64_t* len,
+                 int njobs, int64_t max_len, const double* rot, const double* trans,
+                 cudaStream_t st);
+int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
+                     int npieces, int64_t max_m, int c, int r, const double* rot,
+                     const double* trans, double* out, cudaStream_t st);
+int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
+                   double* out, cudaStream_t st);
+size_t recenter_ws_bytes(int r);
+int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st);
+int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
+                         const int64_t* idx, int64_t l, const double* X1, int r, double* mean,
+                         double* M, double* v, double* S, double* q, double* cond, int32_t* flag,
+                         cudaStream_t st);
+int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, int64_t m, int p,
+                        int r, const double* mean, const double* M, const double* v, double* out,
+                        int64_t ldo, int32_t* nonfinite, cudaStream_t st);
+int launch_sqdist(mdsx_handle* h, const void* A, int64_t lda, int64_t ma, const void* B,
+                  int64_t ldb, int64_t mb, int dtype, int p, double* na, double* nb, double* out,
+                  int64_t ldo, int self, cudaStream_t st);
+int launch_double_center(mdsx_handle* h, const double* D, int64_t m, double* mu, double* g,
+                         double* Q, cudaStream_t st);
+int launch_delta_check(mdsx_handle* h, const double* D, int64_t m, unsigned long long* mx,
+                       int32_t* flags, cudaStream_t st);
+
+int fail(mdsx_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_check(mdsx_handle* h, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return MDSX_OK;
+  return fail(h, MDSX_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ws_reset(mdsx_handle* h) { h->ws_top = 0; }
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Grow the workspace to hold `bytes` for this call (device sync on growth).
+static int ws_reserve(mdsx_handle* h, size_t bytes) {
+  h->ws_top = 0;
+  if (bytes <= h->ws_size) return MDSX_OK;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_check(h, e, "workspace sync");
+  if (h->ws) cudaFree(h->ws);
+  h->ws = nullptr;
+  h->ws_size = 0;
+  size_t want = std::max(bytes, (size_t)64 << 20);
+  e = cudaMalloc(&h->ws, want);
+  if (e != cudaSuccess) return cuda_check(h, e, "workspace cudaMalloc");
+  h->ws_size = want;
+  return MDSX_OK;
+}
+
+void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t) {
+  const size_t b = align_up(bytes ? bytes : 1);
+  if (h->ws_top + b > h->ws_size) {
+    fail(h, MDSX_CUDA, "workspace overflow (internal sizing error)");
+    return nullptr;
+  }
+  void* p = h->ws + h->ws_top;
+  h->ws_top += b;
+  return p;
+}
+
+// Small host->device uploads go through a pinned buffer; before reusing it we
+// wait for the previous batch of copies (event) so the source stays valid.
+struct Stager {
+  mdsx_handle* h;
+  cudaStream_t st;
+  size_t top = 0;
+  Stager(mdsx_handle* hh, cudaStream_t s) : h(hh), st(s) {}
+  int begin(size_t total) {
+    if (h->pinned_free) cudaEventSynchronize(h->pinned_free);
+    total = align_up(total) + 4096;
+    if (total > h->pinned_size) {
+      if (h->pinned) cudaFreeHost(h->pinned);
+      h->pinned = nullptr;
+      h->pinned_size = 0;
+      cudaError_t e = cudaMallocHost(&h->pinned, std::max(total, (size_t)1 << 20));
+      if (e != cudaSuccess) return cuda_check(h, e, "cudaMallocHost");
+      h->pinned_size = std::max(total, (size_t)1 << 20);
+    }
+    top = 0;
+    return MDSX_OK;
+  }
+  int put(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return MDSX_OK;
+    std::memcpy(h->pinned + top, src, bytes);
+    cudaError_t e = cudaMemcpyAsync(dst, h->pinned + top, bytes, cudaMemcpyHostToDevice, st);
+    top += align_up(bytes);
+    return cuda_check(h, e, "cudaMemcpyAsync(H2D descriptors)");
+  }
+  int end() {
+    if (!h->pinned_free) cudaEventCreateWithFlags(&h->pinned_free, cudaEventDisableTiming);
+    return cuda_check(h, cudaEventRecord(h->pinned_free, st), "cudaEventRecord");
+  }
+};
+
+// ------------------------------------------------------ classical pipeline
+struct ClassicalPlan {
+  std::vector<PieceDesc> pd;
+  std::vector<int4> tiles;
+  std::vector<int64_t> off;
+  int kmax = 0;
+  int64_t total = 0;
+  size_t a_doubles = 0, u_doubles = 0;
+  int64_t max_m = 0;
+};
+
+static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int npieces, int r,
+                          ClassicalPlan& cp) {
+  if (npieces < 1) return fail(h, MDSX_PARAM, "no pieces");
+  if (r < 1 || r > MDSX_MAX_R)
+    return fail(h, MDSX_PARAM, "r must satisfy 1 <= r <= " + std::to_string(MDSX_MAX_R));
+  cp.pd.resize(npieces);
+  cp.off.assign(piece_off, piece_off + npieces + 1);
+  int64_t a_off = 0, u_off = 0;
+  for (int j = 0; j < npieces; ++j) {
+    const int64_t m = piece_off[j + 1] - piece_off[j];
+    if (m < 2 || r > m - 1)
+      return fail(h, MDSX_PARAM, "r must satisfy 1 <= r <= n-1, got r=" + std::to_string(r) +
+                                     ", n=" + std::to_string(m));
+    if (m > 20000) return fail(h, MDSX_PARAM, "piece exceeds the exact-size guard (20000)");
+    PieceDesc d{};
+    d.row_off = piece_off[j];
+    d.m = (int)m;
+    d.form = (p < m) ? 0 : 1;
+    d.k = d.form == 0 ? p : (int)m;
+    if (d.k > MDSX_JACOBI_KMAX)
+      return fail(h, MDSX_UNSUPPORTED,
+                  "piece eigenproblem of order " + std::to_string(d.k) +
+                      " exceeds the shared-memory solver (" + std::to_string(MDSX_JACOBI_KMAX) + ")");
+    d.a_off = a_off;
+    d.u_off = u_off;
+    d.pt_off = piece_off[j] - piece_off[0];
+    a_off += (int64_t)d.k * d.k;
+    u_off += (int64_t)d.k * r;
+    cp.kmax = std::max(cp.kmax, d.k);
+    cp.max_m = std::max<int64_t>(cp.max_m, m);
+    cp.pd[j] = d;
+    const int T = (d.k + 63) / 64;
+    for (int ti = 0; ti < T; ++ti)
+      for (int tj = 0; tj <= ti; ++tj) cp.tiles.push_back(make_int4(j, ti, tj, 0));
+  }
+  cp.total = piece_off[npieces] - piece_off[0];
+  cp.a_doubles = (size_t)a_off;
+  cp.u_doubles = (size_t)u_off;
+  return MDSX_OK;
+}
+
+static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
+  const size_t np = cp.pd.size();
+  return align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+         align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
+         align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double));
+}
+
+// Runs K2 -> K1 -> K3 -> points for all pieces.  Workspace must be reserved.
+static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* data, int dtype,
+                         int64_t ld, int p, const int64_t* row_idx, int r, double* points,
+                         double* estimates, double* gof, mdsx_piece_status* status,
+                         cudaStream_t st) {
+  const int np = (int)cp.pd.size();
+  PieceDesc* dpd = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
+  int4* dtiles = (int4*)ws_alloc(h, cp.tiles.size() * sizeof(int4), st);
+  double* mu = (double*)ws_alloc(h, (size_t)np * p * sizeof(double), st);
+  double* A = (double*)ws_alloc(h, cp.a_doubles * sizeof(double), st);
+  double* U = (double*)ws_alloc(h, cp.u_doubles * sizeof(double), st);
+  double* lam = (double*)ws_alloc(h, (size_t)np * r * sizeof(double), st);
+  if (!dpd || !dtiles || !mu || !A || !U || !lam) return MDSX_CUDA;
+  const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
+  const int64_t* ridx = row_idx;
+  Stager sg(h, st);
+  int rc = sg.begin(np * sizeof(PieceDesc) + cp.tiles.size() * sizeof(int4) + 512);
+  if (rc) return rc;
+  if ((rc = sg.put(dpd, pd.data(), np * sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(dtiles, cp.tiles.data(), cp.tiles.size() * sizeof(int4)))) return rc;
+  if ((rc = sg.end())) return rc;
+  if ((rc = launch_piece_means(h, data, dtype, ld, p, ridx, dpd, np, mu, status, st))) return rc;
+  if (dtype == MDSX_F64 || dtype == MDSX_F32) {
+    if ((rc = launch_gram(h, data, dtype, ld, p, ridx, dpd, mu, dtiles, (int)cp.tiles.size(), A, st)))
+      return rc;
+  }
+  if ((rc = launch_jacobi(h, dpd, np, cp.kmax, r, A, U, lam, estimates, gof, status, 1, st)))
+    return rc;
+  return launch_points(h, data, dtype, ld, p, ridx, dpd, np, r, mu, U, lam, points, st);
+}
+
+}  // namespace mdsx
+
+using namespace mdsx;
+
+extern "C" {
+
+int mdsx_version(void) { return 1; }
+
+int mdsx_create(int device, mdsx_handle** out) {
+  if (!out) return MDSX_PARAM;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return MDSX_CUDA;
+  auto* h = new mdsx_handle();
+  h->device = device;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&h->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  *out = h;
+  return MDSX_OK;
+}
+
+void mdsx_destroy(mdsx_handle* h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  if (h->ws) cudaFree(h->ws);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->pinned_free) cudaEventDestroy(h->pinned_free);
+  delete h;
+}
+
+const char* mdsx_last_error(const mdsx_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t mdsx_launch_count(const mdsx_handle* h) { return h ? h->launches : 0; }
+
+int mdsx_sqdist_self(mdsx_handle* h, const void* x, int dtype, int64_t ld, int64_t m, int32_t p,
+                     double* out, int64_t ldo, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (m < 1 || p < 1) return fail(h, MDSX_INVALID_INPUT, "data must be non-empty");
+  int rc = ws_reserve(h, align_up(m * sizeof(double)));
+  if (rc) return rc;
+  double* na = (double*)ws_alloc(h, m * sizeof(double), st);
+  return launch_sqdist(h, x, ld, m, x, ld, m, dtype, p, na, na, out, ldo, 1, st);
+}
+
+int mdsx_sqdist_cross(mdsx_handle* h, const void* a, int64_t lda, int64_t ma, const void* b,
+                      int64_t ldb, int64_t mb, int dtype, int32_t p, double* out, int64_t ldo,
+                      void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = ws_reserve(h, align_up(ma * sizeof(double)) + align_up(mb * sizeof(double)));
+  if (rc) return rc;
+  double* na = (double*)ws_alloc(h, ma * sizeof(double), st);
+  double* nb = (double*)ws_alloc(h, mb * sizeof(double), st);
+  return launch_sqdist(h, a, lda, ma, b, ldb, mb, dtype, p, na, nb, out, ldo, 0, st);
+}
+
+int mdsx_double_center(mdsx_handle* h, const double* delta, int64_t m, double* q, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = ws_reserve(h, align_up(m * sizeof(double)) + 256);
+  if (rc) return rc;
+  double* mu = (double*)ws_alloc(h, m * sizeof(double), st);
+  double* g = (double*)ws_alloc(h, sizeof(double), st);
+  return launch_double_center(h, delta, m, mu, g, q, st);
+}
+
+int mdsx_classical_pieces(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                          const int64_t* row_idx, const int64_t* piece_off, int32_t npieces,
+                          int32_t r, double* points, double* estimates, double* gof,
+                          mdsx_piece_status* status, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  ClassicalPlan cp;
+  int rc = plan_classical(h, p, piece_off, npieces, r, cp);
+  if (rc) return rc;
+  if ((rc = ws_reserve(h, classical_ws_bytes(cp, p, r)))) return rc;
+  return run_classical(h, cp, data, dtype, ld, p, row_idx, r, points, estimates, gof, status, st);
+}
+
+int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t r, double* points,
+                         double* estimates, double* gof, mdsx_piece_status* status, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (r < 1 || r > m - 1 || r > MDSX_MAX_R)
+    return fail(h, MDSX_PARAM, "r must satisfy 1 <= r <= n-1, got r=" + std::to_string(r) +
+                                   ", n=" + std::to_string(m));
+  if (m > MDSX_JACOBI_KMAX)
+    return fail(h, MDSX_UNSUPPORTED, "classical_mds(delta) on the GPU handles n <= " +
+                                         std::to_string(MDSX_JACOBI_KMAX));
+  PieceDesc d{};
+  d.m = (int)m; d.k = (int)m; d.form = 1;
+  const size_t need = align_up(sizeof(PieceDesc)) + align_up(m * m * sizeof(double)) * 2 +
+                      align_up(m * r * sizeof(double)) + align_up(r * sizeof(double)) +
+                      align_up(m * sizeof(double)) + 512 + 256;
+  int rc = ws_reserve(h, need);
+  if (rc) return rc;
+  PieceDesc* dpd = (PieceDesc*)ws_alloc(h, sizeof(PieceDesc), st);
+  double* Q = (double*)ws_alloc(h, m * m * sizeof(double), st);
+  double* U = (double*)ws_alloc(h, m * r * sizeof(double), st);
+  double* lam = (double*)ws_alloc(h, r * sizeof(double), st);
+  double* mu = (double*)ws_alloc(h, m * sizeof(double), st);
+  double* g = (double*)ws_alloc(h, sizeof(double), st);
+  Stager sg(h, st);
+  if ((rc = sg.begin(sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(dpd, &d, sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.end())) return rc;
+  if ((rc = launch_double_center(h, delta, m, mu, g, Q, st))) return rc;
+  if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, sizeof(mdsx_piece_status), st), "memset")))
+    return rc;
+  if ((rc = launch_jacobi(h, dpd, 1, (int)m, r, Q, U, lam, estimates, gof, status, 1, st))) return rc;
+  return launch_points(h, nullptr, MDSX_F64, 0, 0, nullptr, dpd, 1, r, nullptr, U, lam, points, st);
+}
+
+int mdsx_delta_check(mdsx_handle* h, const double* delta, int64_t m, int32_t* flags, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = ws_reserve(h, 256);
+  if (rc) return rc;
+  auto* mx = (unsigned long long*)ws_alloc(h, sizeof(unsigned long long), st);
+  if ((rc = cuda_check(h, cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st), "memset")))
+    return rc;
+  return launch_delta_check(h, delta, m, mx, flags, st);
+}
+
+int64_t mdsx_gower_context_size(int64_t l, int32_t p, int32_t r) {
+  return (int64_t)p + (int64_t)p * r + r + (int64_t)r * r + l;
+}
+
+int mdsx_gower_context(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                       const int64_t* base_idx, int64_t l, const double* base_config, int32_t r,
+                       double* ctx, double* cond, int32_t* flag, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  double* mean = ctx;
+  double* M = mean + p;
+  double* v = M + (int64_t)p * r;
+  double* S = v + r;
+  double* q = S + (int64_t)r * r;
+  return launch_gower_context(h, data, dtype, ld, p, base_idx, l, base_config, r, mean, M, v, S, q,
+                              cond, flag, st);
+}
+
+int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
+                           const void* rows, int dtype, int64_t ld, int64_t m, double* out,
+                           int64_t ldo, int32_t* nonfinite, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int32_t* nf = nonfinite;
+  int rc;
+  const double* mean = ctx;
+  const double* M = mean + p;
+  const double* v = M + (int64_t)p * r;
+  (void)l;
+  return launch_gower_affine(h, rows, dtype, ld, m, p, r, mean, M, v, out, ldo, nf, st);
+}
+
+int mdsx_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
+                        const double* src, const int64_t* src_rows, const int64_t* job_off,
+                        int32_t njobs, int32_t r, double* rot, double* trans, double* loss,
+                        int32_t* degenerate, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  for (int j = 0; j < njobs; ++j)
+    if (job_off[j + 1] - job_off[j] < 2)
+      return fail(h, MDSX_SHAPE, "need at least 2 rows and 1 column");
+  int rc = ws_reserve(h, align_up((size_t)(njobs + 1) * sizeof(int64_t)));
+  if (rc) return rc;
+  int64_t* doff = (int64_t*)ws_alloc(h, (size_t)(njobs + 1) * sizeof(int64_t), st);
+  Stager sg(h, st);
+  if ((rc = sg.begin((size_t)(njobs + 1) * sizeof(int64_t)))) return rc;
+  if ((rc = sg.put(doff, job_off, (size_t)(njobs + 1) * sizeof(int64_t)))) return rc;
+  if ((rc = sg.end())) return rc;
+  return launch_procrustes_fit(h, tgt, tgt_rows, src, src_rows, doff, njobs, r, rot, trans, loss,
+                               degenerate, st);
+}
+
+int mdsx_procrustes_apply(mdsx_handle* h, double* buf, int32_t r, const int64_t* start,
+                          const int64_t* len, int32_t njobs, int64_t max_len, const double* rot,
+                          const double* trans, void* stream) {
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  return launch_apply(h, buf, r, start, len, njobs, max_len, rot, trans, as_stream(stream));
+}
+
+int mdsx_scatter_rows(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int32_t r,
+                      double* out, void* stream) {
+  return launch_scatter(h, src, idx, n, r, out, as_stream(stream));
+}
+
+int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  int rc = ws_reserve(h, recenter_ws_bytes(r));
+  if (rc) return rc;
+  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
+  return launch_recenter(h, points, n, r, part, st);
+}
+
+int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                        int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                        int32_t npieces, int32_t c, int32_t r, double* out, double* estimates,
+                        double* gof, mdsx_piece_status* status, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  ClassicalPlan cp;
+  int rc = plan_classical(h, p, piece_off, npieces, r, cp);
+  if (rc) return rc;
+  if (piece_off[0] != 0) return fail(h, MDSX_PARAM, "piece_off[0] must be 0");
+  if (npieces > 1) {
+    if (c < 2 || c < r) return fail(h, MDSX_PARAM, "c must be >= max(r, 2)");
+    for (int j = 0; j < npieces; ++j)
+      if (piece_off[j + 1] - piece_off[j] <= c) return fail(h, MDSX_PARAM, "l must exceed c");
+  }
+  const int nj = std::max(npieces - 1, 0);
+  const size_t fit_rows = (size_t)nj * c;
+  const size_t need = classical_ws_bytes(cp, p, r) + align_up(cp.total * r * sizeof(double)) +
+                      align_up(fit_rows * sizeof(int64_t)) * 2 +
+                      align_up((size_t)(nj + 1) * sizeof(int64_t)) +
+                      align_up((size_t)(npieces + 1) * sizeof(int64_t)) +
+                      align_up((size_t)nj * r * r * sizeof(double)) +
+                      align_up((size_t)nj * r * sizeof(double)) + align_up(nj * sizeof(double)) +
+                      align_up(nj * sizeof(int32_t)) + recenter_ws_bytes(r) + 4096;
+  if ((rc = ws_reserve(h, need))) return rc;
+  double* P = (double*)ws_alloc(h, cp.total * r * sizeof(double), st);
+  if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, P, estimates, gof, status, st)))
+    return rc;
+  int64_t* toff = (int64_t*)ws_alloc(h, (size_t)(npieces + 1) * sizeof(int64_t), st);
+  double* rot = (double*)ws_alloc(h, (size_t)nj * r * r * sizeof(double), st);
+  double* trans = (double*)ws_alloc(h, (size_t)nj * r * sizeof(double), st);
+  if (nj > 0) {
+    int64_t* trows = (int64_t*)ws_alloc(h, fit_rows * sizeof(int64_t), st);
+    int64_t* srows = (int64_t*)ws_alloc(h, fit_rows * sizeof(int64_t), st);
+    int64_t* joff = (int64_t*)ws_alloc(h, (size_t)(nj + 1) * sizeof(int64_t), st);
+    double* loss = (double*)ws_alloc(h, nj * sizeof(double), st);
+    int32_t* degen = (int32_t*)ws_alloc(h, nj * sizeof(int32_t), st);
+    std::vector<int64_t> ht(fit_rows), hs(fit_rows), hj(nj + 1);
+    for (int j = 0; j < nj; ++j) {
+      hj[j] = (int64_t)j * c;
+      for (int t = 0; t < c; ++t) {
+        ht[(size_t)j * c + t] = t;                          // anchor: piece 1 rows 0..c-1
+        hs[(size_t)j * c + t] = piece_off[j + 1] + t;       // piece j+1 connecting rows
+      }
+    }
+    hj[nj] = (int64_t)nj * c;
+    Stager sg(h, st);
+    if ((rc = sg.begin(fit_rows * 16 + (nj + 1) * 8 + (npieces + 1) * 8 + 1024))) return rc;
+    if ((rc = sg.put(trows, ht.data(), fit_rows * sizeof(int64_t)))) return rc;
+    if ((rc = sg.put(srows, hs.data(), fit_rows * sizeof(int64_t)))) return rc;
+    if ((rc = sg.put(joff, hj.data(), (nj + 1) * sizeof(int64_t)))) return rc;
+    if ((rc = sg.put(toff, piece_off, (npieces + 1) * sizeof(int64_t)))) return rc;
+    if ((rc = sg.end())) return rc;
+    if ((rc = launch_procrustes_fit(h, P, trows, P, srows, joff, nj, r, rot, trans, loss, degen, st)))
+      return rc;
+  } else {
+    Stager sg(h, st);
+    if ((rc = sg.begin((npieces + 1) * 8))) return rc;
+    if ((rc = sg.put(toff, piece_off, (npieces + 1) * sizeof(int64_t)))) return rc;
+    if ((rc = sg.end())) return rc;
+  }
+  if ((rc = launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st)))
+    return rc;
+  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
+  return launch_recenter(h, out, n, r, part, st);
+}
+
+int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                       int32_t p, const int64_t* sample_idx, int64_t l, int32_t r, double* out,
+                       double* estimates, double* gof, mdsx_piece_status* status, double* cond,
+                       int32_t* flags, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t off[2] = {0, l};
+  ClassicalPlan cp;
+  int rc = plan_classical(h, p, off, 1, r, cp);
+  if (rc) return rc;
+  const int64_t csz = mdsx_gower_context_size(l, p, r);
+  const size_t need = classical_ws_bytes(cp, p, r) + align_up(l * r * sizeof(double)) +
+                      align_up(csz * sizeof(double)) + recenter_ws_bytes(r) + 1024;
+  if ((rc = ws_reserve(h, need))) return rc;
+  double* base = (double*)ws_alloc(h, l * r * sizeof(double), st);
+  if ((rc = run_classical(h, cp, data, dtype, ld, p, sample_idx, r, base, estimates, gof, status, st)))
+    return rc;
+  if (n <= l) {  // passthrough (algorithms.py:257-258): sample is 0..n-1
+    return launch_scatter(h, base, sample_idx, l, r, out, st);
+  }
+  double* ctx = (double*)ws_alloc(h, csz * sizeof(double), st);
+  int32_t* flag = flags;
+  double* mean = ctx;
+  double* M = mean + p;
+  double* v = M + (int64_t)p * r;
+  double* S = v + r;
+  double* q = S + (int64_t)r * r;
+  if ((rc = cuda_check(h, cudaMemsetAsync(flag, 0, 2 * sizeof(int32_t), st), "memset"))) return rc;
+  if ((rc = launch_gower_context(h, data, dtype, ld, p, sample_idx, l, base, r, mean, M, v, S, q,
+                                 cond, flag, st)))
+    return rc;
+  if ((rc = launch_gower_affine(h, data, dtype, ld, n, p, r, mean, M, v, out, r, flag + 1, st)))
+    return rc;
+  if ((rc = launch_scatter(h, base, sample_idx, l, r, out, st))) return rc;
+  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
+  if ((rc = launch_recenter(h, out, n, r, part, st))) return rc;
+  return MDSX_OK;
+}
+
+}  // extern "C"

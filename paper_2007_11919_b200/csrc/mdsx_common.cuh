@@ -1,0 +1,96 @@
+// Shared device helpers and the handle/workspace runtime of libmdsx.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mdsx.h"
+
+#define MDSX_MAX_R 32          // largest target dimension r handled in-kernel
+#define MDSX_JACOBI_KMAX 112   // largest k for the shared-memory Jacobi solver
+
+// ---------------------------------------------------------------- handle
+struct mdsx_handle {
+  int device = 0;
+  int num_sms = 148;
+  int max_smem_optin = 0;
+  char* ws = nullptr;          // grow-only device workspace
+  size_t ws_size = 0;
+  size_t ws_top = 0;           // bump pointer for the current call
+  char* pinned = nullptr;      // pinned host staging for small descriptor uploads
+  size_t pinned_size = 0;
+  cudaEvent_t pinned_free = nullptr;  // recorded after the last upload from `pinned`
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace mdsx {
+
+int fail(mdsx_handle* h, int code, const std::string& msg);
+int cuda_check(mdsx_handle* h, cudaError_t e, const char* what);
+// Begin a call: resets the bump allocator.  Workspace from a previous call on
+// the same stream is safe to reuse (stream order).
+void ws_reset(mdsx_handle* h);
+// Reserve `bytes` (256-aligned) of device workspace; grows (after a device
+// sync) when needed.  Returns nullptr and sets h->err on failure.
+void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t st);
+// Upload a small host array via the pinned staging buffer (async on st).
+int upload(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st);
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int launched(mdsx_handle* h, const char* what) {
+  h->launches++;
+  return cuda_check(h, cudaGetLastError(), what);
+}
+
+// ------------------------------------------------------------ device helpers
+template <typename T> __device__ __forceinline__ double ld_val(const T* p) {
+  return static_cast<double>(__ldg(p));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Rutishauser/Golub-Van Loan symmetric 2x2 rotation zeroing a_pq.
+__device__ __forceinline__ void sym_rotation(double app, double aqq, double apq,
+                                             double& c, double& s, double& t) {
+  double tau = (aqq - app) / (2.0 * apq);
+  double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+  c = 1.0 / sqrt(1.0 + tt * tt);
+  s = tt * c;
+  t = tt;
+}
+
+}  // namespace mdsx
+
+// ---------------------------------------------------------------- descriptors
+// One classical-MDS piece.  form 0: A = Xc^T Xc (k = p);  form 1: A = Xc Xc^T (k = m).
+struct PieceDesc {
+  int64_t row_off;   // offset into row_idx
+  int64_t a_off;     // offset (doubles) of the k x k matrix in the A workspace
+  int64_t u_off;     // offset (doubles) of the k x r eigenvector block
+  int64_t pt_off;    // offset (rows) of the m x r output block
+  int32_t m, k, form, pad;
+};
+
+// Host launchers implemented in the kernel translation units.
+namespace mdsx {
+int launch_piece_means(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                       const int64_t* row_idx, const PieceDesc* pd, int npieces,
+                       double* mu, mdsx_piece_status* status, cudaStream_t st);
+int launch_gram(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                const int64_t* row_idx, const PieceDesc* pd, const double* mu,
+                const int4* tiles, int ntiles, double* A, cudaStream_t st);
+int launch_jacobi(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r, double* A,
+                  double* U, double* lam, double* estimates, double* gof,
+                  mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int r,
+                  const double* mu, const double* U, const double* lam, double* points,
+                  cudaStream_t st);
+}  // namespace mdsx
