@@ -69,6 +69,12 @@ const char* mdsx_last_error(const mdsx_handle* h);
 /* Number of kernels this handle has launched since creation. */
 int64_t mdsx_launch_count(const mdsx_handle* h);
 int mdsx_version(void);
+/* Per-kernel CUDA-event timing of this handle's launches (off by default).
+ * mdsx_timing_report synchronises on the recorded events and returns the
+ * length of the report "<kernel> <total_ms> <count>\n"...; with a buffer
+ * (cap bytes, NUL-terminated) it also copies the report and resets it. */
+int mdsx_timing_enable(mdsx_handle* h, int on);
+int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap);
 
 /* ---- dense primitives (function-level seams) ---------------------------- */
 /* out (m x m, ldo) = squared distances between rows of x (m x p, ld);

@@ -35,6 +35,8 @@ SIGNATURES = {
     "mdsx_destroy": (None, [_vp]),
     "mdsx_last_error": (C.c_char_p, [_vp]),
     "mdsx_launch_count": (_i64, [_vp]),
+    "mdsx_timing_enable": (_int, [_vp, _int]),
+    "mdsx_timing_report": (_i64, [_vp, C.c_char_p, _i64]),
     "mdsx_sqdist_self": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _vp]),
     "mdsx_sqdist_cross": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _int, _i32, _vp, _i64, _vp]),
     "mdsx_double_center": (_int, [_vp, _vp, _i64, _vp, _vp]),
@@ -106,6 +108,20 @@ class Handle:
 
     def launches(self) -> int:
         return int(self.lib.mdsx_launch_count(self.ptr))
+
+    def timing(self, on: bool) -> None:
+        self.lib.mdsx_timing_enable(self.ptr, 1 if on else 0)
+
+    def timing_report(self) -> dict:
+        """{kernel: (total_ms, launches)} since the last report."""
+        n = int(self.lib.mdsx_timing_report(self.ptr, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        self.lib.mdsx_timing_report(self.ptr, buf, n + 1)
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, ms, cnt = line.split()
+            out[name] = (float(ms), int(cnt))
+        return out
 
     def call(self, name: str, *args) -> None:
         rc = getattr(self.lib, name)(self.ptr, *args)

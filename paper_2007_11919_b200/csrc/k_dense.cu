@@ -141,42 +141,50 @@ int launch_sqdist(mdsx_handle* h, const void* A, int64_t lda, int64_t ma, const 
   if (ma == 0 || mb == 0) return MDSX_OK;
   auto go = [&](auto tag) {
     using T = decltype(tag);
+    mdsx::pre(h, st);
     rownorm_kernel<T><<<(unsigned)((ma + 255) / 256), 256, 0, st>>>((const T*)A, lda, ma, p, na);
-    int rc = launched(h, "rownorm_kernel");
+    int rc = launched(h, "rownorm_kernel", st);
     if (rc) return rc;
     if (!self) {
+      mdsx::pre(h, st);
       rownorm_kernel<T><<<(unsigned)((mb + 255) / 256), 256, 0, st>>>((const T*)B, ldb, mb, p, nb);
-      rc = launched(h, "rownorm_kernel");
+      rc = launched(h, "rownorm_kernel", st);
       if (rc) return rc;
     }
     dim3 grid((unsigned)((mb + DT - 1) / DT), (unsigned)((ma + DT - 1) / DT));
+    mdsx::pre(h, st);
     sqdist_kernel<T><<<grid, DT * 8, 0, st>>>((const T*)A, lda, ma, (const T*)B, ldb, mb, p, na,
                                                 self ? na : nb, out, ldo, self);
-    return launched(h, "sqdist_kernel");
+    return launched(h, "sqdist_kernel", st);
   };
   return dtype == MDSX_F64 ? go(double{}) : go(float{});
 }
 
 int launch_double_center(mdsx_handle* h, const double* D, int64_t m, double* mu, double* g,
                          double* Q, cudaStream_t st) {
+  mdsx::pre(h, st);
   rowmean_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(D, m, mu);
-  int rc = launched(h, "rowmean_kernel");
+  int rc = launched(h, "rowmean_kernel", st);
   if (rc) return rc;
+  mdsx::pre(h, st);
   grandmean_kernel<<<1, 256, 0, st>>>(mu, m, g);
-  rc = launched(h, "grandmean_kernel");
+  rc = launched(h, "grandmean_kernel", st);
   if (rc) return rc;
+  mdsx::pre(h, st);
   dcenter_kernel<<<(unsigned)((m * m + 255) / 256), 256, 0, st>>>(D, m, mu, g, Q);
-  return launched(h, "dcenter_kernel");
+  return launched(h, "dcenter_kernel", st);
 }
 
 int launch_delta_check(mdsx_handle* h, const double* D, int64_t m, unsigned long long* mx,
                        int32_t* flags, cudaStream_t st) {
   const int blocks = (int)std::min<int64_t>((m * m + 255) / 256, (int64_t)h->num_sms * 4);
+  mdsx::pre(h, st);
   absmax_kernel<<<blocks, 256, 0, st>>>(D, m * m, mx, flags);
-  int rc = launched(h, "absmax_kernel");
+  int rc = launched(h, "absmax_kernel", st);
   if (rc) return rc;
+  mdsx::pre(h, st);
   delta_check_kernel<<<blocks, 256, 0, st>>>(D, m, mx, flags);
-  return launched(h, "delta_check_kernel");
+  return launched(h, "delta_check_kernel", st);
 }
 
 }  // namespace mdsx

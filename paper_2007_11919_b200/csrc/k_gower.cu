@@ -234,19 +234,21 @@ int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, i
   auto feat = [&](auto tag) {
     using T = decltype(tag);
     const T* x = (const T*)X;
-    if (r <= 4) ctx_feature_kernel<T, 4><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M);
-    else if (r <= 8) ctx_feature_kernel<T, 8><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M);
-    else if (r <= 16) ctx_feature_kernel<T, 16><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M);
-    else ctx_feature_kernel<T, 32><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M);
-    int rc = launched(h, "ctx_feature_kernel");
+    if (r <= 4) { mdsx::pre(h, st); ctx_feature_kernel<T, 4><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M); }
+    else if (r <= 8) { mdsx::pre(h, st); ctx_feature_kernel<T, 8><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M); }
+    else if (r <= 16) { mdsx::pre(h, st); ctx_feature_kernel<T, 16><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M); }
+    else { mdsx::pre(h, st); ctx_feature_kernel<T, 32><<<p, 256, 0, st>>>(x, ld, idx, l, p, X1, r, mean, M); }
+    int rc = launched(h, "ctx_feature_kernel", st);
     if (rc) return rc;
+    mdsx::pre(h, st);
     ctx_qdiag_kernel<T><<<(unsigned)((l + 255) / 256), 256, 0, st>>>(x, ld, idx, l, p, mean, q);
-    return launched(h, "ctx_qdiag_kernel");
+    return launched(h, "ctx_qdiag_kernel", st);
   };
   int rc = dtype == MDSX_F64 ? feat(double{}) : feat(float{});
   if (rc) return rc;
+  mdsx::pre(h, st);
   ctx_finalize_kernel<<<1, 256, 0, st>>>(X1, l, p, r, M, v, S, cond, flag);
-  return launched(h, "ctx_finalize_kernel");
+  return launched(h, "ctx_finalize_kernel", st);
 }
 
 int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, int64_t m, int p,
@@ -263,8 +265,9 @@ int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, in
     int per_sm = 4;
     const int64_t need = (m + 255) / 256;
     const int blocks = (int)std::min<int64_t>(need, (int64_t)h->num_sms * per_sm);
+    mdsx::pre(h, st);
     kern<<<blocks, 256, smem, st>>>((const T*)X, ld, m, p, r, mean, M, v, out, ldo, nonfinite);
-    return launched(h, "gower_affine_kernel");
+    return launched(h, "gower_affine_kernel", st);
   };
   using I4 = std::integral_constant<int, 4>;
   using I8 = std::integral_constant<int, 8>;

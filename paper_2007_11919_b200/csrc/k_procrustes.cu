@@ -278,10 +278,11 @@ int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_
     cudaFuncSetAttribute(procrustes_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   const int blocks = (njobs + FIT_WARPS - 1) / FIT_WARPS;
+  mdsx::pre(h, st);
   procrustes_fit_kernel<<<blocks, FIT_WARPS * 32, smem, st>>>(tgt, tgt_rows, src, src_rows,
                                                                job_off_dev, njobs, r, rot, trans,
                                                                loss, degenerate);
-  return launched(h, "procrustes_fit_kernel");
+  return launched(h, "procrustes_fit_kernel", st);
 }
 
 int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const int64_t* len,
@@ -289,46 +290,48 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
                  cudaStream_t st) {
   if (njobs == 0 || max_len == 0) return MDSX_OK;
   dim3 grid((unsigned)((max_len + 255) / 256), (unsigned)njobs);
-  if (r <= 4) apply_kernel<4><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
-  else if (r <= 8) apply_kernel<8><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
-  else if (r <= 16) apply_kernel<16><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
-  else apply_kernel<32><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
-  return launched(h, "apply_kernel");
+  if (r <= 4) { mdsx::pre(h, st); apply_kernel<4><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
+  else if (r <= 8) { mdsx::pre(h, st); apply_kernel<8><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
+  else if (r <= 16) { mdsx::pre(h, st); apply_kernel<16><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
+  else { mdsx::pre(h, st); apply_kernel<32><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
+  return launched(h, "apply_kernel", st);
 }
 
 int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
                      int npieces, int64_t max_m, int c, int r, const double* rot,
                      const double* trans, double* out, cudaStream_t st) {
   dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)npieces);
-  if (r <= 4) dc_stitch_kernel<4><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
-  else if (r <= 8) dc_stitch_kernel<8><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
-  else if (r <= 16) dc_stitch_kernel<16><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
-  else dc_stitch_kernel<32><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out);
-  return launched(h, "dc_stitch_kernel");
+  if (r <= 4) { mdsx::pre(h, st); dc_stitch_kernel<4><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
+  else if (r <= 8) { mdsx::pre(h, st); dc_stitch_kernel<8><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
+  else if (r <= 16) { mdsx::pre(h, st); dc_stitch_kernel<16><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
+  else { mdsx::pre(h, st); dc_stitch_kernel<32><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
+  return launched(h, "dc_stitch_kernel", st);
 }
 
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st) {
   if (n == 0) return MDSX_OK;
   const int64_t total = n * r;
+  mdsx::pre(h, st);
   scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(src, idx, n, r, out);
-  return launched(h, "scatter_kernel");
+  return launched(h, "scatter_kernel", st);
 }
 
 size_t recenter_ws_bytes(int r) { return (size_t)RC_BLOCKS * r * sizeof(double); }
 
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st) {
   if (n == 0) return MDSX_OK;
-  if (r <= 4) colsum_partial_kernel<4><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
-  else if (r <= 8) colsum_partial_kernel<8><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
-  else if (r <= 16) colsum_partial_kernel<16><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
-  else colsum_partial_kernel<32><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part);
-  int rc = launched(h, "colsum_partial_kernel");
+  if (r <= 4) { mdsx::pre(h, st); colsum_partial_kernel<4><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
+  else if (r <= 8) { mdsx::pre(h, st); colsum_partial_kernel<8><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
+  else if (r <= 16) { mdsx::pre(h, st); colsum_partial_kernel<16><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
+  else { mdsx::pre(h, st); colsum_partial_kernel<32><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
+  int rc = launched(h, "colsum_partial_kernel", st);
   if (rc) return rc;
   const int64_t total = n * r;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)h->num_sms * 8);
+  mdsx::pre(h, st);
   subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, RC_BLOCKS);
-  return launched(h, "subtract_mean_kernel");
+  return launched(h, "subtract_mean_kernel", st);
 }
 
 }  // namespace mdsx

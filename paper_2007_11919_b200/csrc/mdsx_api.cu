@@ -35,6 +35,18 @@ int launch_double_center(mdsx_handle* h, const double* D, int64_t m, double* mu,
                          double* Q, cudaStream_t st);
 int launch_delta_check(mdsx_handle* h, const double* D, int64_t m, unsigned long long* mx,
                        int32_t* flags, cudaStream_t st);
+size_t subspace_smem_bytes(int kmax);
+int subspace_prof(long long* out, int n);
+int lanczos_kmax();
+int lanczos_rmax();
+size_t lanczos_smem_bytes(int kmax);
+int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                        const double* A, double* U, double* lam, double* estimates, double* gof,
+                        mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+int subspace_block();
+int launch_subspace_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                         const double* A, double* U, double* lam, double* estimates, double* gof,
+                         mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
 
 int fail(mdsx_handle* h, int code, const std::string& msg) {
   if (h) h->err = msg;
@@ -47,6 +59,17 @@ int cuda_check(mdsx_handle* h, cudaError_t e, const char* what) {
 }
 
 void ws_reset(mdsx_handle* h) { h->ws_top = 0; }
+
+cudaEvent_t pooled_event(mdsx_handle* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -114,6 +137,8 @@ struct Stager {
 // ------------------------------------------------------ classical pipeline
 struct ClassicalPlan {
   std::vector<PieceDesc> pd;
+  std::vector<PieceDesc> pd_jac, pd_sub;   // K3 solver split: full Jacobi / subspace iteration
+  int kmax_jac = 0, kmax_sub = 0;
   std::vector<int4> tiles;
   std::vector<int64_t> off;
   int kmax = 0;
@@ -148,9 +173,18 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
     d.a_off = a_off;
     d.u_off = u_off;
     d.pt_off = piece_off[j] - piece_off[0];
+    d.id = j;
     a_off += (int64_t)d.k * d.k;
     u_off += (int64_t)d.k * r;
     cp.kmax = std::max(cp.kmax, d.k);
+    // full Jacobi for small k or large r; Lanczos (top-r) otherwise
+    if (d.k <= 32 || d.k > lanczos_kmax() || r > lanczos_rmax()) {
+      cp.pd_jac.push_back(d);
+      cp.kmax_jac = std::max(cp.kmax_jac, d.k);
+    } else {
+      cp.pd_sub.push_back(d);
+      cp.kmax_sub = std::max(cp.kmax_sub, d.k);
+    }
     cp.max_m = std::max<int64_t>(cp.max_m, m);
     cp.pd[j] = d;
     const int T = (d.k + 63) / 64;
@@ -165,7 +199,7 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
 
 static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
   const size_t np = cp.pd.size();
-  return align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+  return 3 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
          align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double));
 }
@@ -177,6 +211,8 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
                          cudaStream_t st) {
   const int np = (int)cp.pd.size();
   PieceDesc* dpd = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
+  PieceDesc* dpd_jac = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
+  PieceDesc* dpd_sub = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   int4* dtiles = (int4*)ws_alloc(h, cp.tiles.size() * sizeof(int4), st);
   double* mu = (double*)ws_alloc(h, (size_t)np * p * sizeof(double), st);
   double* A = (double*)ws_alloc(h, cp.a_doubles * sizeof(double), st);
@@ -186,9 +222,11 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
   const int64_t* ridx = row_idx;
   Stager sg(h, st);
-  int rc = sg.begin(np * sizeof(PieceDesc) + cp.tiles.size() * sizeof(int4) + 512);
+  int rc = sg.begin(3 * np * sizeof(PieceDesc) + cp.tiles.size() * sizeof(int4) + 2048);
   if (rc) return rc;
   if ((rc = sg.put(dpd, pd.data(), np * sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(dpd_jac, cp.pd_jac.data(), cp.pd_jac.size() * sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(dpd_sub, cp.pd_sub.data(), cp.pd_sub.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dtiles, cp.tiles.data(), cp.tiles.size() * sizeof(int4)))) return rc;
   if ((rc = sg.end())) return rc;
   if ((rc = launch_piece_means(h, data, dtype, ld, p, ridx, dpd, np, mu, status, st))) return rc;
@@ -196,7 +234,13 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     if ((rc = launch_gram(h, data, dtype, ld, p, ridx, dpd, mu, dtiles, (int)cp.tiles.size(), A, st)))
       return rc;
   }
-  if ((rc = launch_jacobi(h, dpd, np, cp.kmax, r, A, U, lam, estimates, gof, status, 1, st)))
+  if (!cp.pd_jac.empty() &&
+      (rc = launch_jacobi(h, dpd_jac, (int)cp.pd_jac.size(), cp.kmax_jac, r, A, U, lam, estimates,
+                          gof, status, 1, st)))
+    return rc;
+  if (!cp.pd_sub.empty() &&
+      (rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
+                                estimates, gof, status, 1, st)))
     return rc;
   return launch_points(h, data, dtype, ld, p, ridx, dpd, np, r, mu, U, lam, points, st);
 }
@@ -208,6 +252,9 @@ using namespace mdsx;
 extern "C" {
 
 int mdsx_version(void) { return 1; }
+
+// diagnostics only (not in the public header): block-0 phase cycle counters
+int mdsx_debug_subspace_prof(long long* out, int n) { return mdsx::subspace_prof(out, n); }
 
 int mdsx_create(int device, mdsx_handle** out) {
   if (!out) return MDSX_PARAM;
@@ -228,12 +275,47 @@ void mdsx_destroy(mdsx_handle* h) {
   if (h->ws) cudaFree(h->ws);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pinned_free) cudaEventDestroy(h->pinned_free);
+  for (auto& t : h->timed) { cudaEventDestroy(t.second.first); cudaEventDestroy(t.second.second); }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
   delete h;
 }
 
 const char* mdsx_last_error(const mdsx_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t mdsx_launch_count(const mdsx_handle* h) { return h ? h->launches : 0; }
+
+int mdsx_timing_enable(mdsx_handle* h, int on) {
+  if (!h) return MDSX_PARAM;
+  h->timing = on != 0;
+  return MDSX_OK;
+}
+
+int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap) {
+  if (!h) return -1;
+  // fold pending event pairs into the running per-kernel totals
+  for (auto& t : h->timed) {
+    cudaEventSynchronize(t.second.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.second.first, t.second.second);
+    auto it = std::find_if(h->report.begin(), h->report.end(),
+                           [&](auto& a) { return a.first == t.first; });
+    if (it == h->report.end()) h->report.push_back({t.first, {ms, 1}});
+    else { it->second.first += ms; it->second.second += 1; }
+    h->event_pool.push_back(t.second.first);
+    h->event_pool.push_back(t.second.second);
+  }
+  h->timed.clear();
+  std::string out;
+  for (auto& a : h->report)
+    out += a.first + " " + std::to_string(a.second.first) + " " + std::to_string(a.second.second) + "\n";
+  if (buf && cap > 0) {  // a call with a buffer consumes the totals
+    const size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+    h->report.clear();
+  }
+  return (int64_t)out.size();
+}
 
 int mdsx_sqdist_self(mdsx_handle* h, const void* x, int dtype, int64_t ld, int64_t m, int32_t p,
                      double* out, int64_t ldo, void* stream) {

@@ -25,6 +25,12 @@ struct mdsx_handle {
   cudaEvent_t pinned_free = nullptr;  // recorded after the last upload from `pinned`
   int64_t launches = 0;
   std::string err;
+  // optional per-kernel CUDA-event timing (mdsx_timing_enable)
+  bool timing = false;
+  cudaEvent_t cur_start = nullptr;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> timed;
+  std::vector<std::pair<std::string, std::pair<double, int64_t>>> report;
 };
 
 namespace mdsx {
@@ -40,8 +46,23 @@ void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t st);
 // Upload a small host array via the pinned staging buffer (async on st).
 int upload(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-inline int launched(mdsx_handle* h, const char* what) {
+cudaEvent_t pooled_event(mdsx_handle* h);
+// Call immediately before a kernel launch on stream st.
+inline void pre(mdsx_handle* h, cudaStream_t st) {
+  if (h->timing) {
+    h->cur_start = pooled_event(h);
+    cudaEventRecord(h->cur_start, st);
+  }
+}
+// Call immediately after a kernel launch on stream st.
+inline int launched(mdsx_handle* h, const char* what, cudaStream_t st) {
   h->launches++;
+  if (h->timing && h->cur_start) {
+    cudaEvent_t e = pooled_event(h);
+    cudaEventRecord(e, st);
+    h->timed.push_back({what, {h->cur_start, e}});
+    h->cur_start = nullptr;
+  }
   return cuda_check(h, cudaGetLastError(), what);
 }
 
@@ -75,7 +96,7 @@ struct PieceDesc {
   int64_t a_off;     // offset (doubles) of the k x k matrix in the A workspace
   int64_t u_off;     // offset (doubles) of the k x r eigenvector block
   int64_t pt_off;    // offset (rows) of the m x r output block
-  int32_t m, k, form, pad;
+  int32_t m, k, form, id;   // id: global piece index (output slot)
 };
 
 // Host launchers implemented in the kernel translation units.
