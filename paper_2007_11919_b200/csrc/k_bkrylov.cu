@@ -1,0 +1,400 @@
+// K3 for large pieces (k > 104, e.g. config 5: p = 784): block Krylov with
+// full re-orthogonalisation and Rayleigh-Ritz, restarted, batched over all
+// large pieces of a plan.
+//
+// cycle:  Q_0 (k x b, orthonormal);  for s < S:  Z_s = A Q_s,
+//         Q_{s+1} = orth(Z_s - Q_{0..s} Q_{0..s}^T Z_s)   (CGS2 + shifted Cholesky-QR2)
+//         H = Q^T Z (M x M, M = S b);  top-b eigenpairs of H (Lanczos kernel, smem)
+//         Y = Q S_b,  residual |Z S_i - theta_i Y_i| <= 1e-12 theta_1 for i < r;
+//         converged -> outputs; otherwise restart with Q_0 = Y.
+// All products are batched fp64 GEMMs (k_bgemm.cu): the k x k matrix is read
+// once per block of b = 16 vectors instead of once per vector, so the solver
+// is compute-bound rather than HBM-bound.  G1/G2 from trace(A) (PSD).
+#include "mdsx_common.cuh"
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+namespace {
+
+constexpr int B = 16;          // block width
+constexpr int S = 6;           // blocks per cycle
+constexpr int M = B * S;       // Krylov dimension per cycle (= Rayleigh-Ritz size, <= 104)
+constexpr int MAX_CYCLES = 8;
+constexpr int KT = 256;
+
+struct BigDesc {
+  const double* A;     // k x k
+  double* Q;           // k x M
+  double* Z;           // k x M
+  double* Y;           // k x B
+  double* ZS;          // k x B
+  double* H;           // M x M
+  double* Sv;          // M x B
+  int k, m, id, pad;   // id: global piece index (output slot); m: rows of the piece
+  int64_t u_off;       // Uout offset of the piece
+};
+
+__device__ __forceinline__ double hash_unit(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return (double)(x >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+}
+
+__global__ void bk_init_kernel(const BigDesc* __restrict__ bd) {
+  const BigDesc d = bd[blockIdx.x];
+  for (int e = threadIdx.x; e < d.k * B; e += blockDim.x) {
+    const int a = e / B, c = e % B;
+    d.Q[(int64_t)a * M + c] = hash_unit(((uint64_t)a << 8) ^ (uint64_t)c);
+  }
+}
+
+// Orthonormalise the k x B block at column `col` of Q: two passes of
+// Cholesky-QR with a small diagonal shift (keeps rank-deficient blocks finite;
+// an all-zero column stays zero and only contributes a zero Ritz value).
+__global__ void __launch_bounds__(KT)
+bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int col) {
+  __shared__ double G[B * B];
+  const BigDesc d = bd[blockIdx.x];
+  if (done[blockIdx.x]) return;
+  double* W = d.Q + col;
+  const int tid = threadIdx.x;
+  for (int pass = 0; pass < 2; ++pass) {
+    {  // G = W^T W (B x B): thread per entry, fixed order over rows
+      const int i = tid / B, j = tid % B;
+      double acc = 0.0;
+      for (int a = 0; a < d.k; ++a) acc = fma(W[(int64_t)a * M + i], W[(int64_t)a * M + j], acc);
+      G[tid] = acc;
+    }
+    __syncthreads();
+    if (tid < 32) {  // shifted upper Cholesky G + delta I = R^T R (warp 0)
+      double tr = 0.0;
+      for (int i = 0; i < B; ++i) tr += G[i * B + i];
+      const double delta = (pass == 0 ? 1e-13 : 1e-15) * tr + 1e-300;
+      const int l = tid;
+      for (int j = 0; j < B; ++j) {
+        const double piv = G[j * B + j] + delta;
+        const double rjj = sqrt(piv > 0.0 ? piv : delta);
+        __syncwarp();
+        if (l > j && l < B) G[j * B + l] /= rjj;
+        if (l == j) G[j * B + j] = rjj;
+        __syncwarp();
+        if (l > j && l < B) {
+          const double rjl = G[j * B + l];
+          for (int i = j + 1; i <= l; ++i) G[i * B + l] = fma(-G[j * B + i], rjl, G[i * B + l]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int a = tid; a < d.k; a += KT) {   // W <- W R^-1, row per thread
+      double* w = W + (int64_t)a * M;
+      double x[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        double s = w[j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) s = fma(-x[i], G[i * B + j], s);
+        x[j] = s / G[j * B + j];
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j) w[j] = x[j];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void bk_sym_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done) {
+  const BigDesc d = bd[blockIdx.x];
+  if (done[blockIdx.x]) return;
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int i = e / M, j = e % M;
+    if (i < j) {
+      const double h = 0.5 * (d.H[i * M + j] + d.H[j * M + i]);
+      d.H[i * M + j] = h;
+      d.H[j * M + i] = h;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(KT)
+bk_resid_kernel(const BigDesc* __restrict__ bd, int* __restrict__ done, int r,
+                const double* __restrict__ theta, int last, double* __restrict__ Uout,
+                double* __restrict__ lam_out, double* __restrict__ estimates,
+                double* __restrict__ gof, mdsx_piece_status* __restrict__ status) {
+  __shared__ double part[KT / 32][B];
+  __shared__ double tr_part[KT / 32];
+  __shared__ int conv;
+  const int q = blockIdx.x;
+  const BigDesc d = bd[q];
+  if (done[q]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* th = theta + (int64_t)q * B;
+  double tr = 0.0;
+  for (int a = tid; a < d.k; a += KT) tr += d.A[(int64_t)a * d.k + a];
+  tr = mdsx::warp_sum(tr);
+  if (lane == 0) tr_part[warp] = tr;
+  for (int i = 0; i < r; ++i) {
+    double acc = 0.0;
+    for (int a = tid; a < d.k; a += KT) {
+      const double e = d.ZS[(int64_t)a * B + i] - th[i] * d.Y[(int64_t)a * B + i];
+      acc = fma(e, e, acc);
+    }
+    acc = mdsx::warp_sum(acc);
+    if (lane == 0) part[warp][i] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int ok = 1;
+    for (int i = 0; i < r; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < KT / 32; ++w) s += part[w][i];
+      if (!(sqrt(s) <= 1e-12 * fabs(th[0]))) ok = 0;
+    }
+    conv = ok;
+  }
+  __syncthreads();
+  if (conv || last) {
+    for (int e = tid; e < d.k * r; e += KT) {
+      const int a = e / r, i = e % r;
+      Uout[d.u_off + e] = d.Y[(int64_t)a * B + i];
+    }
+    if (tid == 0) {
+      double trace = 0.0;
+      for (int w = 0; w < KT / 32; ++w) trace += tr_part[w];
+      const double tol = 1e-8 * fabs(th[0]);
+      mdsx_piece_status st{MDSX_OK, 0, 0.0};
+      if (status[d.id].code != MDSX_OK) st.code = status[d.id].code;
+      else if (!conv) st.code = MDSX_NUMERICAL;
+      double kept = 0.0;
+      for (int i = 0; i < r; ++i) {
+        double v = th[i];
+        if (fabs(v) <= tol) v = 0.0;
+        if (st.code == MDSX_OK && v <= 0.0) { st.code = MDSX_DEGENERATE; st.index = i + 1; st.value = v; }
+        kept += v;
+        lam_out[(int64_t)d.id * r + i] = v;
+        estimates[(int64_t)d.id * r + i] = v / d.m;
+      }
+      status[d.id] = st;
+      const double g = st.code == MDSX_OK ? kept / trace : 0.0;
+      gof[2 * (int64_t)d.id] = g;
+      gof[2 * (int64_t)d.id + 1] = g;
+      done[q] = 1;
+    }
+  } else {
+    for (int e = tid; e < d.k * B; e += KT) {   // restart block: Q_0 = Y
+      const int a = e / B, c = e % B;
+      d.Q[(int64_t)a * M + c] = d.Y[(int64_t)a * B + c];
+    }
+  }
+}
+
+}  // namespace
+
+namespace mdsx {
+
+int lanczos_rmax();
+int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                        const double* A, double* U, double* lam, double* estimates, double* gof,
+                        mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t);
+
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t bk_ws_bytes(const std::vector<PieceDesc>& big) {
+  size_t n = big.size(), tot = 0;
+  for (const auto& d : big) tot += al((size_t)d.k * (2 * M + 2 * B) * sizeof(double));
+  tot += n * al((size_t)(M * M + M * B) * sizeof(double));
+  tot += al(n * sizeof(BigDesc)) + al(n * sizeof(int)) + al(n * B * sizeof(double)) * 2 +
+         al(n * 2 * sizeof(double)) + al(n * sizeof(mdsx_piece_status)) +
+         al(n * sizeof(PieceDesc));
+  // GEMM tasks / work items of one cycle (see run_big_pieces)
+  size_t ntask = n * (S + 4 * (S - 1) + 3), nitem = 0;
+  for (const auto& d : big) {
+    const size_t kt = (d.k + 127) / 128;
+    nitem += (S + 2 * (S - 1) + 2) * kt + 2 * (S - 1) * ((M + 127) / 128) +
+             ((M + 63) / 64) * ((M + 63) / 64);
+  }
+  tot += al(ntask * sizeof(GemmTask)) + al((nitem + n * 64) * sizeof(int4));
+  return tot + 4096;
+}
+
+// Large-piece K3 driver.  Workspace must have been reserved for bk_ws_bytes.
+int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const double* A, int r,
+                   double* Uout, double* lam_out, double* estimates, double* gof,
+                   mdsx_piece_status* status, cudaStream_t st,
+                   int (*put)(mdsx_handle*, void*, const void*, size_t, cudaStream_t)) {
+  const int n = (int)big.size();
+  if (n == 0) return MDSX_OK;
+  if (r > B - 4)
+    return fail(h, MDSX_UNSUPPORTED, "r > 12 with pieces larger than 104 (block Krylov needs b >= r+4)");
+  std::vector<BigDesc> bd(n);
+  for (int q = 0; q < n; ++q) {
+    const PieceDesc& d = big[q];
+    BigDesc& b = bd[q];
+    b.A = A + d.a_off;
+    b.k = d.k;
+    b.m = d.m;
+    b.id = d.id;
+    b.u_off = d.u_off;
+    b.Q = (double*)ws_alloc(h, (size_t)d.k * M * sizeof(double), st);
+    b.Z = (double*)ws_alloc(h, (size_t)d.k * M * sizeof(double), st);
+    b.Y = (double*)ws_alloc(h, (size_t)d.k * B * sizeof(double), st);
+    b.ZS = (double*)ws_alloc(h, (size_t)d.k * B * sizeof(double), st);
+    b.H = (double*)ws_alloc(h, (size_t)M * M * sizeof(double), st);
+    b.Sv = (double*)ws_alloc(h, (size_t)M * B * sizeof(double), st);
+    if (!b.Q || !b.Z || !b.Y || !b.ZS || !b.H || !b.Sv) return MDSX_CUDA;
+  }
+  BigDesc* dbd = (BigDesc*)ws_alloc(h, n * sizeof(BigDesc), st);
+  int* done = (int*)ws_alloc(h, n * sizeof(int), st);
+  double* theta = (double*)ws_alloc(h, (size_t)n * B * sizeof(double), st);
+  double* sc_est = (double*)ws_alloc(h, (size_t)n * B * sizeof(double), st);
+  double* sc_gof = (double*)ws_alloc(h, (size_t)n * 2 * sizeof(double), st);
+  mdsx_piece_status* sc_st = (mdsx_piece_status*)ws_alloc(h, n * sizeof(mdsx_piece_status), st);
+  PieceDesc* hpd = (PieceDesc*)ws_alloc(h, n * sizeof(PieceDesc), st);
+  if (!dbd || !done || !theta || !sc_est || !sc_gof || !sc_st || !hpd) return MDSX_CUDA;
+
+  // H_q as Lanczos "pieces": A = H (M x M) relative to a zero base, U = Sv
+  std::vector<PieceDesc> hdesc(n);
+  for (int q = 0; q < n; ++q) {
+    PieceDesc p{};
+    p.a_off = bd[q].H - (double*)h->ws;      // offsets from the workspace base
+    p.u_off = bd[q].Sv - (double*)h->ws;
+    p.m = 1;
+    p.k = M;
+    p.form = 0;
+    p.id = q;
+    hdesc[q] = p;
+  }
+
+  // all GEMM tasks of one cycle
+  std::vector<GemmTask> tasks;
+  std::vector<int4> items;
+  std::vector<GemmBatch> g1(S), g2(S), g3(S), g4(S), g5(S);
+  GemmBatch g6, g7, g8;
+  auto base = [&](int q) {
+    GemmTask t{};
+    t.skip = done + q;
+    t.alpha = 1.0;
+    t.beta = 0.0;
+    return t;
+  };
+  for (int s = 0; s < S; ++s) {
+    std::vector<GemmTask> v;
+    for (int q = 0; q < n; ++q) {
+      GemmTask t = base(q);
+      t.A = bd[q].A; t.lda = bd[q].k; t.transA = 0;
+      t.B = bd[q].Q + s * B; t.ldb = M;
+      t.C = bd[q].Z + s * B; t.ldc = M;
+      t.M = bd[q].k; t.N = B; t.K = bd[q].k;
+      v.push_back(t);
+    }
+    g1[s] = append_bgemm(tasks, items, v);
+    if (s == S - 1) break;
+    const int w = (s + 1) * B;   // columns of Q_{0..s}
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<GemmTask> proj, upd;
+      for (int q = 0; q < n; ++q) {
+        double* P = bd[q].H;     // H doubles as (w x B) scratch during the cycle
+        GemmTask a = base(q);
+        a.A = bd[q].Q; a.lda = M; a.transA = 1;
+        a.B = pass == 0 ? bd[q].Z + s * B : bd[q].Q + w; a.ldb = M;
+        a.C = P; a.ldc = B;
+        a.M = w; a.N = B; a.K = bd[q].k;
+        proj.push_back(a);
+        GemmTask u = base(q);
+        u.A = bd[q].Q; u.lda = M; u.transA = 0;
+        u.B = P; u.ldb = B;
+        u.C = bd[q].Q + w; u.ldc = M;
+        u.D = pass == 0 ? bd[q].Z + s * B : bd[q].Q + w; u.ldd = M;
+        u.alpha = -1.0; u.beta = 1.0;
+        u.M = bd[q].k; u.N = B; u.K = w;
+        upd.push_back(u);
+      }
+      (pass == 0 ? g2 : g4)[s] = append_bgemm(tasks, items, proj);
+      (pass == 0 ? g3 : g5)[s] = append_bgemm(tasks, items, upd);
+    }
+  }
+  {
+    std::vector<GemmTask> v6, v7, v8;
+    for (int q = 0; q < n; ++q) {
+      GemmTask t = base(q);
+      t.A = bd[q].Q; t.lda = M; t.transA = 1;
+      t.B = bd[q].Z; t.ldb = M;
+      t.C = bd[q].H; t.ldc = M;
+      t.M = M; t.N = M; t.K = bd[q].k;
+      v6.push_back(t);
+      GemmTask y = base(q);
+      y.A = bd[q].Q; y.lda = M; y.transA = 0;
+      y.B = bd[q].Sv; y.ldb = B;
+      y.C = bd[q].Y; y.ldc = B;
+      y.M = bd[q].k; y.N = B; y.K = M;
+      v7.push_back(y);
+      GemmTask z = y;
+      z.A = bd[q].Z;
+      z.C = bd[q].ZS;
+      v8.push_back(z);
+    }
+    g6 = append_bgemm(tasks, items, v6);
+    g7 = append_bgemm(tasks, items, v7);
+    g8 = append_bgemm(tasks, items, v8);
+  }
+  GemmTask* dtasks = (GemmTask*)ws_alloc(h, tasks.size() * sizeof(GemmTask), st);
+  int4* ditems = (int4*)ws_alloc(h, items.size() * sizeof(int4), st);
+  if (!dtasks || !ditems) return MDSX_CUDA;
+  int rc;
+  if ((rc = put(h, dbd, bd.data(), n * sizeof(BigDesc), st))) return rc;
+  if ((rc = put(h, dtasks, tasks.data(), tasks.size() * sizeof(GemmTask), st))) return rc;
+  if ((rc = put(h, ditems, items.data(), items.size() * sizeof(int4), st))) return rc;
+  if ((rc = put(h, hpd, hdesc.data(), n * sizeof(PieceDesc), st))) return rc;
+  if ((rc = cuda_check(h, cudaMemsetAsync(done, 0, n * sizeof(int), st), "memset"))) return rc;
+
+  mdsx::pre(h, st);
+  bk_init_kernel<<<n, KT, 0, st>>>(dbd);
+  if ((rc = launched(h, "bk_init_kernel", st))) return rc;
+  std::vector<int> hdone(n, 0);
+  for (int cyc = 0; cyc < MAX_CYCLES; ++cyc) {
+    mdsx::pre(h, st);
+    bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, 0);
+    if ((rc = launched(h, "bk_orth_kernel", st))) return rc;
+    for (int s = 0; s < S; ++s) {
+      if ((rc = launch_bgemm(h, dtasks, ditems, g1[s], st))) return rc;
+      if (s == S - 1) break;
+      if ((rc = launch_bgemm(h, dtasks, ditems, g2[s], st))) return rc;
+      if ((rc = launch_bgemm(h, dtasks, ditems, g3[s], st))) return rc;
+      if ((rc = launch_bgemm(h, dtasks, ditems, g4[s], st))) return rc;
+      if ((rc = launch_bgemm(h, dtasks, ditems, g5[s], st))) return rc;
+      mdsx::pre(h, st);
+      bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, (s + 1) * B);
+      if ((rc = launched(h, "bk_orth_kernel", st))) return rc;
+    }
+    if ((rc = launch_bgemm(h, dtasks, ditems, g6, st))) return rc;
+    mdsx::pre(h, st);
+    bk_sym_kernel<<<n, KT, 0, st>>>(dbd, done);
+    if ((rc = launched(h, "bk_sym_kernel", st))) return rc;
+    if ((rc = cuda_check(h, cudaMemsetAsync(sc_st, 0, n * sizeof(mdsx_piece_status), st), "memset")))
+      return rc;
+    if ((rc = launch_lanczos_smem(h, hpd, n, M, B, (const double*)h->ws, (double*)h->ws, theta,
+                                  sc_est, sc_gof, sc_st, 0, st)))
+      return rc;
+    if ((rc = launch_bgemm(h, dtasks, ditems, g7, st))) return rc;
+    if ((rc = launch_bgemm(h, dtasks, ditems, g8, st))) return rc;
+    const int last = cyc == MAX_CYCLES - 1;
+    mdsx::pre(h, st);
+    bk_resid_kernel<<<n, KT, 0, st>>>(dbd, done, r, theta, last, Uout, lam_out, estimates, gof,
+                                      status);
+    if ((rc = launched(h, "bk_resid_kernel", st))) return rc;
+    if (last) break;
+    if ((rc = cuda_check(h, cudaMemcpyAsync(hdone.data(), done, n * sizeof(int),
+                                            cudaMemcpyDeviceToHost, st), "D2H done")))
+      return rc;
+    if ((rc = cuda_check(h, cudaStreamSynchronize(st), "sync"))) return rc;
+    if (std::all_of(hdone.begin(), hdone.end(), [](int v) { return v != 0; })) break;
+  }
+  return MDSX_OK;
+}
+
+}  // namespace mdsx

@@ -164,109 +164,6 @@ jacobi_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict_
                           qform_trivial, sm, ps);
 }
 
-// ------------------------------------------------------------ points + signs
-template <typename T, int RM>
-__global__ void __launch_bounds__(256)
-points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
-              const PieceDesc* __restrict__ pd, int r, const double* __restrict__ mu_all,
-              const double* __restrict__ Uall, const double* __restrict__ lam_all,
-              double* __restrict__ points) {
-  extern __shared__ double sm[];
-  __shared__ double bval[256];
-  __shared__ int bidx[256];
-  __shared__ double sgn[RM];
-  const PieceDesc d = pd[blockIdx.x];
-  const int tid = threadIdx.x;
-  const int64_t* ridx = row_idx + d.row_off;
-  double* out = points + d.pt_off * r;
-  const double* Ug = Uall + d.u_off;
-  double* sU = sm;                 // p x r (form 0)
-  double* smu = sm + (int64_t)p * r;
-  if (d.form == 0) {
-    for (int e = tid; e < p * r; e += 256) sU[e] = Ug[e];
-    for (int e = tid; e < p; e += 256) smu[e] = mu_all[(int64_t)d.id * p + e];
-  }
-  __syncthreads();
-  double sl[RM];
-#pragma unroll
-  for (int c = 0; c < RM; ++c) sl[c] = (c < r) ? sqrt(lam_all[(int64_t)d.id * r + c]) : 0.0;
-
-  double best[RM];
-  int bi[RM];
-#pragma unroll
-  for (int c = 0; c < RM; ++c) { best[c] = -1.0; bi[c] = 0x7fffffff; }
-  for (int i = tid; i < d.m; i += 256) {
-    double acc[RM];
-#pragma unroll
-    for (int c = 0; c < RM; ++c) acc[c] = 0.0;
-    if (d.form == 0) {
-      const T* row = X + ridx[i] * ld;
-      for (int a = 0; a < p; ++a) {
-        const double y = mdsx::ld_val(row + a) - smu[a];
-#pragma unroll
-        for (int c = 0; c < RM; ++c)
-          if (c < r) acc[c] = fma(y, sU[a * r + c], acc[c]);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < RM; ++c)
-        if (c < r) acc[c] = Ug[(int64_t)i * r + c] * sl[c];
-    }
-#pragma unroll
-    for (int c = 0; c < RM; ++c)
-      if (c < r) {
-        out[(int64_t)i * r + c] = acc[c];
-        const double a = fabs(acc[c]);
-        if (a > best[c]) { best[c] = a; bi[c] = i; }   // rows visited ascending
-      }
-  }
-  // block argmax per column: largest |.|, lowest index on ties
-  for (int c = 0; c < r; ++c) {
-    bval[tid] = best[c];
-    bidx[tid] = bi[c];
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-      if (tid < s) {
-        const double v2 = bval[tid + s];
-        const int i2 = bidx[tid + s];
-        if (v2 > bval[tid] || (v2 == bval[tid] && i2 < bidx[tid])) { bval[tid] = v2; bidx[tid] = i2; }
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      const int lead = bidx[0];
-      double s = 1.0;
-      if (lead < d.m) {
-        const double v = out[(int64_t)lead * r + c];
-        s = v < 0.0 ? -1.0 : 1.0;
-      }
-      sgn[c] = s;
-    }
-    __syncthreads();
-  }
-  for (int i = tid; i < d.m; i += 256)
-    for (int c = 0; c < r; ++c)
-      if (sgn[c] < 0.0) out[(int64_t)i * r + c] = -out[(int64_t)i * r + c];
-}
-
-template <typename T>
-int points_dispatch(mdsx_handle* h, const T* X, int64_t ld, int p, const int64_t* row_idx,
-                    const PieceDesc* pd, int npieces, int r, const double* mu, const double* U,
-                    const double* lam, double* points, cudaStream_t st) {
-  const size_t smem = ((size_t)p * r + p) * sizeof(double);
-  auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    mdsx::pre(h, st);
-    kern<<<npieces, 256, smem, st>>>(X, ld, p, row_idx, pd, r, mu, U, lam, points);
-    return mdsx::launched(h, "points_kernel", st);
-  };
-  if (r <= 4) return go(points_kernel<T, 4>);
-  if (r <= 8) return go(points_kernel<T, 8>);
-  if (r <= 16) return go(points_kernel<T, 16>);
-  return go(points_kernel<T, 32>);
-}
-
 }  // namespace
 
 namespace mdsx {
@@ -306,17 +203,6 @@ int launch_jacobi(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, in
   jacobi_kernel<<<npieces, mdsx::JAC_THREADS, smem, st>>>(pd, r, A, U, lam, estimates, gof, status,
                                                      qform_trivial);
   return launched(h, "jacobi_kernel", st);
-}
-
-int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
-                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int r,
-                  const double* mu, const double* U, const double* lam, double* points,
-                  cudaStream_t st) {
-  if (dtype == MDSX_F64)
-    return points_dispatch(h, (const double*)data, ld, p, row_idx, pd, npieces, r, mu, U, lam,
-                           points, st);
-  return points_dispatch(h, (const float*)data, ld, p, row_idx, pd, npieces, r, mu, U, lam,
-                         points, st);
 }
 
 }  // namespace mdsx

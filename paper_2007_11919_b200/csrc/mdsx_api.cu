@@ -43,6 +43,11 @@ size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+size_t bk_ws_bytes(const std::vector<PieceDesc>& big);
+int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const double* A, int r,
+                   double* Uout, double* lam_out, double* estimates, double* gof,
+                   mdsx_piece_status* status, cudaStream_t st,
+                   int (*put)(mdsx_handle*, void*, const void*, size_t, cudaStream_t));
 int subspace_block();
 int launch_subspace_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                          const double* A, double* U, double* lam, double* estimates, double* gof,
@@ -134,10 +139,19 @@ struct Stager {
   }
 };
 
+// One-shot staged upload (waits for the previous staged copy to finish first).
+static int stage_put(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  Stager sg(h, st);
+  int rc = sg.begin(bytes);
+  if (rc) return rc;
+  if ((rc = sg.put(dst, src, bytes))) return rc;
+  return sg.end();
+}
+
 // ------------------------------------------------------ classical pipeline
 struct ClassicalPlan {
   std::vector<PieceDesc> pd;
-  std::vector<PieceDesc> pd_jac, pd_sub;   // K3 solver split: full Jacobi / subspace iteration
+  std::vector<PieceDesc> pd_jac, pd_sub, pd_big;   // K3 split: Jacobi / Lanczos / block Krylov
   int kmax_jac = 0, kmax_sub = 0;
   std::vector<int4> tiles;
   std::vector<int64_t> off;
@@ -166,10 +180,6 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
     d.m = (int)m;
     d.form = (p < m) ? 0 : 1;
     d.k = d.form == 0 ? p : (int)m;
-    if (d.k > MDSX_JACOBI_KMAX)
-      return fail(h, MDSX_UNSUPPORTED,
-                  "piece eigenproblem of order " + std::to_string(d.k) +
-                      " exceeds the shared-memory solver (" + std::to_string(MDSX_JACOBI_KMAX) + ")");
     d.a_off = a_off;
     d.u_off = u_off;
     d.pt_off = piece_off[j] - piece_off[0];
@@ -177,8 +187,10 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
     a_off += (int64_t)d.k * d.k;
     u_off += (int64_t)d.k * r;
     cp.kmax = std::max(cp.kmax, d.k);
-    // full Jacobi for small k or large r; Lanczos (top-r) otherwise
-    if (d.k <= 32 || d.k > lanczos_kmax() || r > lanczos_rmax()) {
+    // full Jacobi for small k or large r; Lanczos (top-r) up to 104; block Krylov above
+    if (d.k > lanczos_kmax() && !(r > 12 && d.k <= MDSX_JACOBI_KMAX)) {
+      cp.pd_big.push_back(d);
+    } else if (d.k <= 32 || d.k > lanczos_kmax() || r > lanczos_rmax()) {
       cp.pd_jac.push_back(d);
       cp.kmax_jac = std::max(cp.kmax_jac, d.k);
     } else {
@@ -201,7 +213,9 @@ static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
   const size_t np = cp.pd.size();
   return 3 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
-         align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double));
+         align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double)) +
+         align_up(points_ws_bytes((int)np, cp.max_m, r)) +
+         (cp.pd_big.empty() ? 0 : bk_ws_bytes(cp.pd_big));
 }
 
 // Runs K2 -> K1 -> K3 -> points for all pieces.  Workspace must be reserved.
@@ -218,7 +232,8 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   double* A = (double*)ws_alloc(h, cp.a_doubles * sizeof(double), st);
   double* U = (double*)ws_alloc(h, cp.u_doubles * sizeof(double), st);
   double* lam = (double*)ws_alloc(h, (size_t)np * r * sizeof(double), st);
-  if (!dpd || !dtiles || !mu || !A || !U || !lam) return MDSX_CUDA;
+  double2* cand = (double2*)ws_alloc(h, points_ws_bytes(np, cp.max_m, r), st);
+  if (!dpd || !dtiles || !mu || !A || !U || !lam || !cand) return MDSX_CUDA;
   const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
   const int64_t* ridx = row_idx;
   Stager sg(h, st);
@@ -242,7 +257,11 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
       (rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
                                 estimates, gof, status, 1, st)))
     return rc;
-  return launch_points(h, data, dtype, ld, p, ridx, dpd, np, r, mu, U, lam, points, st);
+  if (!cp.pd_big.empty() &&
+      (rc = run_big_pieces(h, cp.pd_big, A, r, U, lam, estimates, gof, status, st, stage_put)))
+    return rc;
+  return launch_points(h, data, dtype, ld, p, ridx, dpd, np, cp.max_m, r, mu, U, lam, points,
+                       cand, st);
 }
 
 }  // namespace mdsx
@@ -372,7 +391,7 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
   d.m = (int)m; d.k = (int)m; d.form = 1;
   const size_t need = align_up(sizeof(PieceDesc)) + align_up(m * m * sizeof(double)) * 2 +
                       align_up(m * r * sizeof(double)) + align_up(r * sizeof(double)) +
-                      align_up(m * sizeof(double)) + 512 + 256;
+                      align_up(m * sizeof(double)) + align_up(points_ws_bytes(1, m, r)) + 512 + 256;
   int rc = ws_reserve(h, need);
   if (rc) return rc;
   PieceDesc* dpd = (PieceDesc*)ws_alloc(h, sizeof(PieceDesc), st);
@@ -381,6 +400,7 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
   double* lam = (double*)ws_alloc(h, r * sizeof(double), st);
   double* mu = (double*)ws_alloc(h, m * sizeof(double), st);
   double* g = (double*)ws_alloc(h, sizeof(double), st);
+  double2* cand = (double2*)ws_alloc(h, points_ws_bytes(1, m, r), st);
   Stager sg(h, st);
   if ((rc = sg.begin(sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd, &d, sizeof(PieceDesc)))) return rc;
@@ -389,7 +409,8 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
   if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, sizeof(mdsx_piece_status), st), "memset")))
     return rc;
   if ((rc = launch_jacobi(h, dpd, 1, (int)m, r, Q, U, lam, estimates, gof, status, 1, st))) return rc;
-  return launch_points(h, nullptr, MDSX_F64, 0, 0, nullptr, dpd, 1, r, nullptr, U, lam, points, st);
+  return launch_points(h, nullptr, MDSX_F64, 0, 0, nullptr, dpd, 1, m, r, nullptr, U, lam, points,
+                       cand, st);
 }
 
 int mdsx_delta_check(mdsx_handle* h, const double* delta, int64_t m, int32_t* flags, void* stream) {

@@ -99,6 +99,25 @@ struct PieceDesc {
   int32_t m, k, form, id;   // id: global piece index (output slot)
 };
 
+// One batched-GEMM task: C = alpha * op(A) B + beta * D  (row-major, op(A) = A
+// (M x K, lda) or A^T with A stored K x M); skipped when *skip != 0.
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* C;
+  const double* D;
+  const int* skip;
+  int M, N, K;
+  int lda, ldb, ldc, ldd;
+  int transA;
+  double alpha, beta;
+};
+
+struct GemmBatch {
+  int64_t item_off, nitems;
+  int narrow;
+};
+
 // Host launchers implemented in the kernel translation units.
 namespace mdsx {
 int launch_piece_means(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
@@ -110,8 +129,13 @@ int launch_gram(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
 int launch_jacobi(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r, double* A,
                   double* U, double* lam, double* estimates, double* gof,
                   mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+size_t points_ws_bytes(int npieces, int64_t max_m, int r);
 int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
-                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int r,
+                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int64_t max_m, int r,
                   const double* mu, const double* U, const double* lam, double* points,
-                  cudaStream_t st);
+                  double2* cand, cudaStream_t st);
+GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
+                       const std::vector<GemmTask>& batch);
+int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_items,
+                 const GemmBatch& b, cudaStream_t st);
 }  // namespace mdsx
