@@ -1,0 +1,135 @@
+// K1+K2 fused for form-0 pieces (p < m): the p x p Gram of the centred rows
+// on the fp64 tensor pipe (DMMA, mma.sync.m8n8k4.f64; tcgen05 has no f64 kind).
+//
+// Centring without a second pass over the rows: with a shift row x0 (the
+// piece's first row) and y = x - x0,
+//     C = sum_i (x_i - mu)(x_i - mu)^T = sum_i y_i y_i^T - s s^T / m,  s = sum_i y_i
+// which is exact in real arithmetic and, because y is centred to within one
+// row's spread, free of the cancellation an unshifted Gram trick suffers.
+// The diagonal tiles also publish mu = x0 + s/m (needed by the points
+// kernel) and flag non-finite input.  Output: lower triangle computed,
+// mirrored to the upper -> exactly symmetric; fixed reduction order.
+#include "mdsx_common.cuh"
+
+namespace {
+
+constexpr int TT = 64;          // output tile (features x features)
+constexpr int KC = 32;          // rows staged per chunk
+constexpr int LD = TT + 4;      // smem row pitch (conflict-free fragment loads)
+constexpr int NT = 256;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT)
+gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
+                 const PieceDesc* __restrict__ pd, const int4* __restrict__ tiles,
+                 double* __restrict__ A, double* __restrict__ mu_all,
+                 mdsx_piece_status* __restrict__ status) {
+  __shared__ __align__(16) double ya[KC][LD];
+  __shared__ __align__(16) double yb[KC][LD];
+  __shared__ double x0a[TT], x0b[TT], sa[TT], sb[TT];
+  __shared__ int bad;
+  const int4 tl = tiles[blockIdx.x];
+  const PieceDesc d = pd[tl.x];
+  const int ti = tl.y, tj = tl.z, k = d.k, m = d.m;
+  const bool diag = ti == tj;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;     // warp sub-tile: rows 16*wr.., cols 32*wc..
+  const int64_t* ridx = row_idx + d.row_off;
+  const int ca = ti * TT, cb = tj * TT;
+
+  if (tid == 0) bad = 0;
+  if (tid < TT) {
+    const T* r0 = X + ridx[0] * ld;
+    x0a[tid] = ca + tid < k ? mdsx::ld_val(r0 + ca + tid) : 0.0;
+    x0b[tid] = cb + tid < k ? mdsx::ld_val(r0 + cb + tid) : 0.0;
+    sa[tid] = 0.0;
+    sb[tid] = 0.0;
+  }
+  __syncthreads();
+
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  bool nonfinite = false;
+  for (int r0 = 0; r0 < m; r0 += KC) {
+    const int nr = min(KC, m - r0);
+    // stage y = x - x0 for the tile's column blocks (warp per row: coalesced)
+    for (int rr = warp; rr < KC; rr += NT / 32) {
+      const bool live = rr < nr;
+      const T* src = live ? X + ridx[r0 + rr] * ld : nullptr;
+      for (int c = lane; c < TT; c += 32) {
+        double va = 0.0, vb = 0.0;
+        if (live && ca + c < k) {
+          const double v = mdsx::ld_val(src + ca + c);
+          nonfinite |= !isfinite(v);
+          va = v - x0a[c];
+        }
+        if (live && cb + c < k) vb = mdsx::ld_val(src + cb + c) - x0b[c];
+        ya[rr][c] = va;
+        yb[rr][c] = vb;
+      }
+    }
+    __syncthreads();
+    if (tid < TT) {                       // column sums of the chunk, fixed order
+      double s = 0.0;
+      for (int rr = 0; rr < nr; ++rr) s += ya[rr][tid];
+      sa[tid] += s;
+    } else if (tid < 2 * TT) {
+      double s = 0.0;
+      for (int rr = 0; rr < nr; ++rr) s += yb[rr][tid - TT];
+      sb[tid - TT] += s;
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < KC; k4 += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = ya[k4 + tig][wr * 16 + i * 8 + gid];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = yb[k4 + tig][wc * 32 + j * 8 + gid];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  if (nonfinite) bad = 1;
+  __syncthreads();
+
+  const double inv_m = 1.0 / (double)m;
+  double* out = A + d.a_off;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int li = wr * 16 + i * 8 + gid, lj = wc * 32 + j * 8 + 2 * tig + v;
+        const int gi = ca + li, gj = cb + lj;
+        if (gi < k && gj < k && (!diag || gi >= gj)) {
+          const double c = fma(-sa[li] * inv_m, sb[lj], acc[i][j][v]);
+          out[(int64_t)gi * k + gj] = c;
+          out[(int64_t)gj * k + gi] = c;
+        }
+      }
+  if (diag) {
+    if (tid < TT && ca + tid < k) mu_all[(int64_t)d.id * p + ca + tid] = x0a[tid] + sa[tid] * inv_m;
+    if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
+  }
+}
+
+}  // namespace
+
+namespace mdsx {
+
+}  // namespace mdsx

@@ -117,6 +117,32 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
+// w -= Q[:, 0..nc) (Q[:, 0..nc)^T w): dot products one warp each (lanes split
+// the k entries, shuffle tree), then the update one row per thread.  Ends
+// with hv[0..nc) = the coefficients; caller syncs before reading wv.
+__device__ void cgs_project(const double* Q, int kq, int k, int nc, double* wv, double* hv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < nc; c += LT / 32) {
+    const double* qc = Q + (size_t)c * kq;
+    double h = 0.0;
+    for (int a = lane; a < k; a += 32) h = fma(qc[a], wv[a], h);
+    h = mdsx::warp_sum(h);
+    if (lane == 0) hv[c] = h;
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid < k) {
+    double s0 = wv[tid], s1 = 0.0;
+    int c = 0;
+    for (; c + 1 < nc; c += 2) {
+      s0 = fma(-Q[(size_t)c * kq + tid], hv[c], s0);
+      s1 = fma(-Q[(size_t)(c + 1) * kq + tid], hv[c + 1], s1);
+    }
+    if (c < nc) s0 = fma(-Q[(size_t)c * kq + tid], hv[c], s0);
+    wv[tid] = s0 + s1;
+  }
+}
+
 __global__ void __launch_bounds__(LT)
 lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
                     double* __restrict__ Uout, double* __restrict__ lam_out,
@@ -165,31 +191,29 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   bool done = false;
   bool broke = false;        // last step hit an invariant subspace (restarted)
   int nconv_checks = 0;
+  // Krylov dimension of the first convergence test (earlier tests never pass)
+  const int first_check = max(2 * r + 4, 24);
   while (!done) {
     const double* q = Q + (size_t)m * kq;
-    // w = A q  (A symmetric: read A[a][row] across threads)
+    // w = A q  (A symmetric: read A[a][row] across threads; 4 independent chains)
     if (row < k) {
-      double acc = 0.0;
-      for (int a = a_lo; a < a_hi; ++a) acc = fma(A[a * k + row], q[a], acc);
-      part[half][row] = acc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int a = a_lo;
+      for (; a + 3 < a_hi; a += 4) {
+        a0 = fma(A[a * k + row], q[a], a0);
+        a1 = fma(A[(a + 1) * k + row], q[a + 1], a1);
+        a2 = fma(A[(a + 2) * k + row], q[a + 2], a2);
+        a3 = fma(A[(a + 3) * k + row], q[a + 3], a3);
+      }
+      for (; a < a_hi; ++a) a0 = fma(A[a * k + row], q[a], a0);
+      part[half][row] = (a0 + a1) + (a2 + a3);
     }
     __syncthreads();
     if (tid < k) wv[tid] = part[0][tid] + part[1][tid];
     __syncthreads();
     double al = 0.0;
     for (int pass = 0; pass < 2; ++pass) {     // CGS2 against Q[:, 0..m]
-      if (tid <= m) {
-        const double* qc = Q + (size_t)tid * kq;
-        double h = 0.0;
-        for (int a = 0; a < k; ++a) h = fma(qc[a], wv[a], h);
-        hv[tid] = h;
-      }
-      __syncthreads();
-      if (tid < k) {
-        double s = wv[tid];
-        for (int c = 0; c <= m; ++c) s = fma(-Q[(size_t)c * kq + tid], hv[c], s);
-        wv[tid] = s;
-      }
+      cgs_project(Q, kq, k, m + 1, wv, hv);
       al += hv[m];
       __syncthreads();
     }
@@ -213,18 +237,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
         if (tid < k) wv[tid] = hash_unit(((uint64_t)m << 20) ^ (uint64_t)tid);
         __syncthreads();
         for (int pass = 0; pass < 2; ++pass) {
-          if (tid < m) {
-            const double* qc = Q + (size_t)tid * kq;
-            double h = 0.0;
-            for (int a = 0; a < k; ++a) h = fma(qc[a], wv[a], h);
-            hv[tid] = h;
-          }
-          __syncthreads();
-          if (tid < k) {
-            double s = wv[tid];
-            for (int c = 0; c < m; ++c) s = fma(-Q[(size_t)c * kq + tid], hv[c], s);
-            wv[tid] = s;
-          }
+          cgs_project(Q, kq, k, m, wv, hv);
           __syncthreads();
         }
         const double nb = sqrt(block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red));
@@ -232,7 +245,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       }
     }
     __syncthreads();
-    if (!(full || (!broke && m >= r + 4 && m % CHECK_EVERY == 0))) continue;
+    if (!(full || (!broke && m >= first_check && m % CHECK_EVERY == 0))) continue;
 
     // ---- top-r eigenpairs of T_m: multisection (16 threads per eigenvalue)
     ++nconv_checks;
@@ -277,20 +290,27 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       for (int i = 0; i < m; ++i) S[(size_t)tid * k + i] = x[i];
     }
     __syncthreads();
-    if (tid == 0) {            // MGS across the r vectors (clusters), fixed order
+    if (tid < 32) {            // MGS across the r vectors (clusters), fixed order, warp 0
+      const int lane = tid;
       for (int i = 1; i < rr; ++i) {
         double* si = S + (size_t)i * k;
         for (int j = 0; j < i; ++j) {
           const double* sj = S + (size_t)j * k;
           double dt = 0.0;
-          for (int t = 0; t < m; ++t) dt = fma(si[t], sj[t], dt);
-          for (int t = 0; t < m; ++t) si[t] = fma(-dt, sj[t], si[t]);
+          for (int t = lane; t < m; t += 32) dt = fma(si[t], sj[t], dt);
+          dt = mdsx::warp_sum(dt);
+          for (int t = lane; t < m; t += 32) si[t] = fma(-dt, sj[t], si[t]);
+          __syncwarp();
         }
         double nr = 0.0;
-        for (int t = 0; t < m; ++t) nr = fma(si[t], si[t], nr);
-        nr = sqrt(nr);
-        for (int t = 0; t < m; ++t) si[t] /= nr;
+        for (int t = lane; t < m; t += 32) nr = fma(si[t], si[t], nr);
+        nr = sqrt(mdsx::warp_sum(nr));
+        for (int t = lane; t < m; t += 32) si[t] /= nr;
+        __syncwarp();
       }
+    }
+    __syncthreads();
+    if (tid == 0) {
       int ok = rr == r;
       const double bm = full ? 0.0 : beta[m - 1];
       for (int i = 0; i < rr && ok; ++i)

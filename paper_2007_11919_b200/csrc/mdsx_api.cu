@@ -43,6 +43,9 @@ size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                     const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
+                     double* A, double* mu, mdsx_piece_status* status, cudaStream_t st);
 size_t bk_ws_bytes(const std::vector<PieceDesc>& big);
 int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const double* A, int r,
                    double* Uout, double* lam_out, double* estimates, double* gof,
@@ -152,6 +155,8 @@ static int stage_put(mdsx_handle* h, void* dst, const void* src, size_t bytes, c
 struct ClassicalPlan {
   std::vector<PieceDesc> pd;
   std::vector<PieceDesc> pd_jac, pd_sub, pd_big;   // K3 split: Jacobi / Lanczos / block Krylov
+  std::vector<PieceDesc> pd_f1;                    // form-1 pieces (separate means pass)
+  std::vector<int4> tiles1;                        // form-1 Gram tiles (tiles: form 0, DMMA)
   int kmax_jac = 0, kmax_sub = 0;
   std::vector<int4> tiles;
   std::vector<int64_t> off;
@@ -201,7 +206,9 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
     cp.pd[j] = d;
     const int T = (d.k + 63) / 64;
     for (int ti = 0; ti < T; ++ti)
-      for (int tj = 0; tj <= ti; ++tj) cp.tiles.push_back(make_int4(j, ti, tj, 0));
+      for (int tj = 0; tj <= ti; ++tj)
+        (d.form == 0 ? cp.tiles : cp.tiles1).push_back(make_int4(j, ti, tj, 0));
+    if (d.form == 1) cp.pd_f1.push_back(d);
   }
   cp.total = piece_off[npieces] - piece_off[0];
   cp.a_doubles = (size_t)a_off;
@@ -211,7 +218,8 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
 
 static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
   const size_t np = cp.pd.size();
-  return 3 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+  return 5 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+         align_up(cp.tiles1.size() * sizeof(int4)) +
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
          align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double)) +
          align_up(points_ws_bytes((int)np, cp.max_m, r)) +
@@ -227,7 +235,9 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   PieceDesc* dpd = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   PieceDesc* dpd_jac = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   PieceDesc* dpd_sub = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
+  PieceDesc* dpd_f1 = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   int4* dtiles = (int4*)ws_alloc(h, cp.tiles.size() * sizeof(int4), st);
+  int4* dtiles1 = (int4*)ws_alloc(h, cp.tiles1.size() * sizeof(int4), st);
   double* mu = (double*)ws_alloc(h, (size_t)np * p * sizeof(double), st);
   double* A = (double*)ws_alloc(h, cp.a_doubles * sizeof(double), st);
   double* U = (double*)ws_alloc(h, cp.u_doubles * sizeof(double), st);
@@ -237,16 +247,28 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
   const int64_t* ridx = row_idx;
   Stager sg(h, st);
-  int rc = sg.begin(3 * np * sizeof(PieceDesc) + cp.tiles.size() * sizeof(int4) + 2048);
+  int rc = sg.begin(5 * np * sizeof(PieceDesc) + (cp.tiles.size() + cp.tiles1.size()) * sizeof(int4) +
+                    4096);
   if (rc) return rc;
   if ((rc = sg.put(dpd, pd.data(), np * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd_jac, cp.pd_jac.data(), cp.pd_jac.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd_sub, cp.pd_sub.data(), cp.pd_sub.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dtiles, cp.tiles.data(), cp.tiles.size() * sizeof(int4)))) return rc;
+  if ((rc = sg.put(dpd_f1, cp.pd_f1.data(), cp.pd_f1.size() * sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(dtiles1, cp.tiles1.data(), cp.tiles1.size() * sizeof(int4)))) return rc;
   if ((rc = sg.end())) return rc;
-  if ((rc = launch_piece_means(h, data, dtype, ld, p, ridx, dpd, np, mu, status, st))) return rc;
-  if (dtype == MDSX_F64 || dtype == MDSX_F32) {
-    if ((rc = launch_gram(h, data, dtype, ld, p, ridx, dpd, mu, dtiles, (int)cp.tiles.size(), A, st)))
+  if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, np * sizeof(mdsx_piece_status), st), "memset")))
+    return rc;
+  // form 0: DMMA Gram with fused shifted means;  form 1: means pass + row Gram
+  if ((rc = launch_gram_dmma(h, data, dtype, ld, p, ridx, dpd, dtiles, (int)cp.tiles.size(), A, mu,
+                             status, st)))
+    return rc;
+  if (!cp.pd_f1.empty()) {
+    if ((rc = launch_piece_means(h, data, dtype, ld, p, ridx, dpd_f1, (int)cp.pd_f1.size(), mu,
+                                 status, st)))
+      return rc;
+    if ((rc = launch_gram(h, data, dtype, ld, p, ridx, dpd, mu, dtiles1, (int)cp.tiles1.size(), A,
+                          st)))
       return rc;
   }
   if (!cp.pd_jac.empty() &&
