@@ -132,4 +132,18 @@ gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __re
 
 namespace mdsx {
 
+int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                     const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
+                     double* A, double* mu, mdsx_piece_status* status, cudaStream_t st) {
+  if (ntiles == 0) return MDSX_OK;
+  mdsx::pre(h, st);
+  if (dtype == MDSX_F64)
+    gram_dmma_kernel<double><<<ntiles, NT, 0, st>>>((const double*)data, ld, p, row_idx, pd, tiles,
+                                                   A, mu, status);
+  else
+    gram_dmma_kernel<float><<<ntiles, NT, 0, st>>>((const float*)data, ld, p, row_idx, pd, tiles, A,
+                                                  mu, status);
+  return launched(h, "gram_dmma_kernel", st);
+}
+
 }  // namespace mdsx
