@@ -66,6 +66,18 @@ WORKLOADS = {
 }
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
+# captures committed under profiles/ (same workload, same kernel build).
+TRAFFIC = {
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (88.29 + 7.73) * 1e6,
+                                     "src": "profiles/r01_ncu_dc2_full.txt"},
+    ("dc2", "gram_dmma_kernel"): {"bytes": (887.46 + 70.59) * 1e6,
+                                  "src": "profiles/r01_ncu_dc2_full.txt"},
+    ("dc2", "points_kernel"): {"bytes": (896.65 + 89.09) * 1e6,
+                               "src": "profiles/r01_ncu_dc2_full.txt"},
+}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -198,38 +210,45 @@ def make_run(w: dict, x, plan):
 
 
 # ------------------------------------------------------------------ work models
-def kernel_work(w: dict, plan, kernel: str) -> dict | None:
-    """Algorithmic work of ONE launch of `kernel` in one step (see DESIGN.md
-    'Work model'): flops for compute-bound kernels, bytes for streaming ones."""
+def piece_sizes(w: dict, plan) -> list:
+    if w["algo"] == "divide":
+        return [len(q) for q in plan.subsets]
+    if w["algo"] == "fast":
+        from paper_2007_11919_b200.plans import flatten_fast
+        return list(np.diff(flatten_fast(plan).piece_off))
+    return [w["l"]]
+
+
+def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
+    """Work of ONE launch of `kernel` in one step (DESIGN.md §3 work models):
+    flops for compute-bound kernels (fp64), bytes for streaming ones."""
     p, r = w["p"], w["r"]
     esize = 4 if w["dtype"] == "f32" else 8
-    if w["algo"] == "divide":
-        sizes = [len(q) for q in plan.subsets]
-    elif w["algo"] == "fast":
-        from paper_2007_11919_b200.plans import flatten_fast
-        off = flatten_fast(plan).piece_off
-        sizes = list(np.diff(off))
-    else:
-        sizes = [w["l"]]
-    if kernel == "gram_kernel":
+    sizes = piece_sizes(w, plan)
+    if kernel in ("gram_dmma_kernel", "gram_kernel"):
         fl = 0.0
         for m in sizes:
-            k = p if p < m else m
-            K = m if p < m else p
-            fl += K * k * (k + 1)          # symmetric rank-K update, k x k
-        return {"bound": "tensor", "flops": fl}
-    if kernel == "jacobi_kernel":
+            if (p < m) == (kernel == "gram_dmma_kernel"):
+                k, K = (p, m) if p < m else (m, p)
+                fl += K * k * (k + 1)          # symmetric rank-K update of a k x k Gram
+        return {"bound": "tensor", "flops": fl, "model": "SYRK m*p*(p+1) per piece"}
+    if kernel == "lanczos_smem_kernel" and krylov_dims is not None:
         fl = 0.0
-        for m in sizes:
-            k = p if p < m else m
-            fl += 9.0 * k ** 3             # dense symmetric eigensolve with vectors (LAPACK count)
-        return {"bound": "tensor", "flops": fl}
+        for m, steps in zip(sizes, krylov_dims):
+            k = min(m, p)
+            if steps > 0:
+                j = np.arange(int(steps))
+                fl += float(np.sum(2.0 * k * k + 8.0 * k * (j + 1)))
+        return {"bound": "tensor", "flops": fl,
+                "model": "sum over Krylov steps of 2k^2 (matvec) + 8k(j+1) (CGS2)"}
     if kernel == "gower_affine_kernel":
         n = w["n"]
-        return {"bound": "hbm", "bytes": n * p * esize + n * r * 8}
+        return {"bound": "hbm", "bytes": n * p * esize + n * r * 8,
+                "model": "n*p*sizeof(in) + n*r*8"}
     if kernel == "points_kernel":
         tot = sum(sizes)
-        return {"bound": "hbm", "bytes": tot * p * esize + tot * r * 8}
+        return {"bound": "hbm", "bytes": tot * p * esize + tot * r * 8,
+                "model": "rows*p*sizeof(in) + rows*r*8"}
     return None
 
 
@@ -392,6 +411,11 @@ def run_ours(args, w):
         ms = float(tm.item())
     cfg_out = run.finish(return_device=True)
     value = w["n"] * ws / (ms / 1e3)
+    try:       # Krylov dimension per piece (solver diagnostics in the status records)
+        st = D.decode_status(run.status)
+        krylov = [float(v) for v in st["value"]]
+    except Exception:
+        krylov = None
 
     # roofline of the dominant kernel (average launch duration over the timed region)
     total_k = sum(v[0] for v in kernels.values())
@@ -400,22 +424,41 @@ def run_ours(args, w):
     if dom:
         ms_k, cnt = kernels[dom]
         per_launch_ms = ms_k / cnt
-        work = kernel_work(w, plan, dom)
+        work = kernel_work(w, plan, dom, krylov)
         launches_per_step = cnt / args.steps
         if work and work["bound"] == "hbm":
             ach = work["bytes"] / launches_per_step / (per_launch_ms / 1e3) / 1e9
             peak = peaks["hbm_gbs"]
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": None, "peak_src": peaks["hbm_src"]}
+                    "frac": ach / peak, "traffic": None, "peak_src": peaks["hbm_src"],
+                    "work_model": work["model"]}
         elif work:
             ach = work["flops"] / launches_per_step / (per_launch_ms / 1e3) / 1e12
             peak = peaks["fp64_tflops"]
             roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak,
                     "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-                    "precision": "fp64", "peak_src": peaks["fp64_src"]}
+                    "precision": "fp64", "peak_src": peaks["fp64_src"],
+                    "work_model": work["model"]}
         if roof is not None:
             roof["share_of_kernel_time"] = ms_k / total_k
             roof["avg_launch_ms"] = per_launch_ms
+            traffic = TRAFFIC.get((args.workload, dom))
+            if traffic:
+                roof["traffic"] = traffic["bytes"]
+                roof["traffic_src"] = traffic["src"]
+    per_kernel = {}
+    for kname, (ms_k, cnt) in kernels.items():
+        wk = kernel_work(w, plan, kname, krylov)
+        if not wk:
+            continue
+        t = ms_k / cnt / 1e3
+        lps = cnt / args.steps
+        if wk["bound"] == "hbm":
+            per_kernel[kname] = {"GB/s": wk["bytes"] / lps / t / 1e9,
+                                 "frac_hbm": wk["bytes"] / lps / t / 1e9 / peaks["hbm_gbs"]}
+        else:
+            per_kernel[kname] = {"TFLOP/s": wk["flops"] / lps / t / 1e12,
+                                 "frac_fp64": wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]}
 
     # e2e through the public API from pinned host memory
     e2e = None
@@ -468,6 +511,7 @@ def run_ours(args, w):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(kernels.items())},
+            "kernel_rooflines": per_kernel,
             "peaks": peaks,
             "fit": {"g1": cfg_out.gof_g1, "estimates": [float(v) for v in cfg_out.eigenvalue_estimates]},
         }

@@ -1,0 +1,323 @@
+"""The reference's own test suite (tests/test_linalg.py, test_classical.py,
+test_procrustes.py, test_algorithms.py) re-expressed against the GPU-backed
+drop-in API.  Same inputs, same assertions, same exception types/messages.
+Deliberate difference (documented in DESIGN.md §3): classical_mds_from_data
+uses the Gram-of-centred-rows path, so it equals classical_mds(Delta) to
+round-off (1e-12) rather than bitwise."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mds(cuda):
+    import paper_2007_11919_b200 as m
+    return m
+
+
+def naive_sq(data):
+    n, k = data.shape
+    out = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            out[i, j] = sum((data[i, s] - data[j, s]) ** 2 for s in range(k))
+    return out
+
+
+def aligned_corr(mds, cfg, dominant):
+    """simulation.py:83-108 on the GPU Procrustes."""
+    fit = mds.fit_procrustes(dominant, cfg.points)
+    al = mds.apply_procrustes(cfg.points, fit)
+    a = al - al.mean(axis=0)
+    d = dominant - dominant.mean(axis=0)
+    return np.einsum("ij,ij->j", a, d) / np.sqrt(np.einsum("ij,ij->j", a, a) * np.einsum("ij,ij->j", d, d))
+
+
+class TestDistances:
+    def test_345(self, mds):
+        assert np.array_equal(mds.euclidean_distance_matrix(np.array([[0.0, 0.0], [3.0, 4.0]])),
+                              [[0.0, 25.0], [25.0, 0.0]])
+
+    def test_single_row(self, mds):
+        assert np.array_equal(mds.euclidean_distance_matrix([[7.0]]), [[0.0]])
+
+    def test_naive_loop(self, mds):
+        data = np.random.default_rng(0).standard_normal((5, 3))
+        assert np.abs(mds.euclidean_distance_matrix(data) - naive_sq(data)).max() <= 1e-12
+
+    def test_symmetric_zero_diag_nonneg(self, mds):
+        d = mds.euclidean_distance_matrix(np.random.default_rng(1).standard_normal((40, 6)))
+        assert np.array_equal(d, d.T) and np.all(np.diagonal(d) == 0.0) and d.min() >= 0.0
+
+    def test_non_finite_and_guard(self, mds):
+        with pytest.raises(mds.InvalidInputError):
+            mds.euclidean_distance_matrix([[1.0, np.nan]])
+        with pytest.raises(mds.ParamError, match="exact-size guard"):
+            mds.euclidean_distance_matrix(np.zeros((11, 2)), exact_guard=10)
+
+    def test_cross(self, mds):
+        assert np.array_equal(mds.cross_squared_distances([[0.0]], [[3.0], [4.0]]), [[9.0, 16.0]])
+        a = np.random.default_rng(2).standard_normal((6, 4))
+        assert np.abs(np.diagonal(mds.cross_squared_distances(a, a))).max() <= 1e-12
+        rng = np.random.default_rng(3)
+        a, b = rng.standard_normal((4, 3)), rng.standard_normal((6, 3))
+        st = mds.euclidean_distance_matrix(np.vstack([a, b]))
+        assert np.abs(mds.cross_squared_distances(a, b) - st[:4, 4:]).max() <= 1e-12
+        with pytest.raises(mds.ShapeError):
+            mds.cross_squared_distances(np.zeros((2, 3)), np.zeros((2, 4)))
+
+
+class TestDoubleCenter:
+    def test_hand_values(self, mds):
+        assert np.allclose(mds.double_center([[0.0, 1.0], [1.0, 0.0]]),
+                           [[0.25, -0.25], [-0.25, 0.25]], atol=1e-15)
+        assert np.array_equal(mds.double_center(np.zeros((3, 3))), np.zeros((3, 3)))
+
+    def test_collinear_and_gram(self, mds):
+        coords = np.array([-4.0, -1.0, 5.0]) / 3.0
+        delta = mds.euclidean_distance_matrix(np.array([[0.0], [1.0], [3.0]]))
+        assert np.abs(mds.double_center(delta) - np.outer(coords, coords)).max() <= 1e-12
+        data = np.random.default_rng(4).standard_normal((30, 5)) * 3.0
+        c = data - data.mean(axis=0)
+        q = mds.double_center(mds.euclidean_distance_matrix(data))
+        assert np.abs(q - c @ c.T).max() <= 1e-9 * np.abs(c @ c.T).max()
+        assert np.array_equal(q, q.T)
+
+    def test_annihilates_ones(self, mds):
+        q = mds.double_center(mds.euclidean_distance_matrix(np.random.default_rng(5).standard_normal((25, 4))))
+        assert np.abs(q @ np.ones(25)).max() <= 1e-9 * 25 * np.abs(q).max()
+
+    def test_invalid_delta(self, mds):
+        with pytest.raises(mds.InvalidInputError, match="symmetric"):
+            mds.double_center([[0.0, 1.0], [2.0, 0.0]])
+        with pytest.raises(mds.InvalidInputError, match="diagonal"):
+            mds.double_center([[1.0, 1.0], [1.0, 0.0]])
+        with pytest.raises(mds.InvalidInputError, match="negative"):
+            mds.double_center([[0.0, -1.0], [-1.0, 0.0]])
+
+
+class TestClassical:
+    def test_collinear(self, mds):
+        cfg = mds.classical_mds(mds.euclidean_distance_matrix(np.array([[0.0], [1.0], [3.0]])), 1)
+        coords = np.array([-4.0, -1.0, 5.0]) / 3.0
+        col = cfg.points[:, 0]
+        assert min(np.abs(col - coords).max(), np.abs(col + coords).max()) <= 1e-12
+        assert cfg.eigenvalue_estimates[0] == pytest.approx(14.0 / 9.0, rel=1e-12)
+        assert cfg.gof_g1 == 1.0 and cfg.gof_g2 == 1.0
+
+    def test_degenerate_and_range(self, mds):
+        with pytest.raises(mds.DegenerateRankError):
+            mds.classical_mds(np.zeros((4, 4)), 1)
+        delta = mds.euclidean_distance_matrix(np.random.default_rng(1).standard_normal((20, 2)))
+        with pytest.raises(mds.DegenerateRankError, match="3"):
+            mds.classical_mds(delta, 3)
+        with pytest.raises(mds.ParamError):
+            mds.classical_mds(np.zeros((3, 3)), 3)
+        with pytest.raises(mds.ParamError, match="exact-size guard"):
+            mds.classical_mds(np.zeros((12, 12)), 1, exact_guard=10)
+        with pytest.raises(mds.ParamError):
+            mds.classical_mds_from_data(np.array([[1.0, 2.0]]), 1)
+
+    def test_round_trip(self, mds):
+        data = np.random.default_rng(0).standard_normal((50, 5))
+        delta = mds.euclidean_distance_matrix(data)
+        back = mds.euclidean_distance_matrix(mds.classical_mds(delta, 5).points)
+        assert np.abs(back - delta).max() <= 1e-8
+
+    def test_variance_centering_nesting(self, mds):
+        data = np.random.default_rng(2).standard_normal((60, 4))
+        cfg = mds.classical_mds_from_data(data, 4)
+        var = (cfg.points ** 2).sum(axis=0) / 60
+        assert np.abs(var - cfg.eigenvalue_estimates).max() <= 1e-9 * cfg.eigenvalue_estimates[0]
+        assert np.abs(cfg.points.mean(axis=0)).max() <= 1e-9 * cfg.points.std(axis=0).min()
+        delta = mds.euclidean_distance_matrix(np.random.default_rng(4).standard_normal((30, 6)))
+        wide, narrow = mds.classical_mds(delta, 5), mds.classical_mds(delta, 2)
+        assert np.array_equal(wide.points[:, :2], narrow.points)
+
+    def test_rotation_invariance_and_recovery(self, mds):
+        rng = np.random.default_rng(5)
+        data = rng.standard_normal((40, 5))
+        basis, _ = np.linalg.qr(rng.standard_normal((5, 5)))
+        a = mds.classical_mds_from_data(data, 3)
+        b = mds.classical_mds_from_data(data @ basis, 3)
+        assert np.abs(a.eigenvalue_estimates - b.eigenvalue_estimates).max() <= 1e-9
+        rng = np.random.default_rng(6)
+        raw = rng.standard_normal((40, 4))
+        raw -= raw.mean(axis=0)
+        u, _, _ = np.linalg.svd(raw, full_matrices=False)
+        d = u * np.array([8.0, 4.0, 2.0, 1.0])
+        cfg = mds.classical_mds_from_data(d, 4)
+        for i in range(4):
+            assert min(np.abs(cfg.points[:, i] - d[:, i]).max(), np.abs(cfg.points[:, i] + d[:, i]).max()) <= 1e-9
+
+    def test_composition_to_roundoff(self, mds):
+        data = np.random.default_rng(7).standard_normal((100, 10))
+        a = mds.classical_mds_from_data(data, 3)
+        b = mds.classical_mds(mds.euclidean_distance_matrix(data), 3)
+        assert np.abs(a.points - b.points).max() <= 1e-11
+        assert abs(a.gof_g1 - b.gof_g1) <= 1e-12
+
+    def test_g1_equals_g2_euclidean(self, mds):
+        rng = np.random.default_rng(1004)
+        for _ in range(20):
+            n, k = int(rng.integers(20, 80)), int(rng.integers(2, 8))
+            cfg = mds.classical_mds_from_data(rng.standard_normal((n, k)) * rng.uniform(0.1, 10.0), min(k, n - 1))
+            assert cfg.gof_g1 == cfg.gof_g2
+
+
+class TestProcrustes:
+    ROT90 = np.array([[0.0, -1.0], [1.0, 0.0]])
+
+    def test_identity_rotation_translation(self, mds):
+        x = np.random.default_rng(0).standard_normal((10, 3))
+        fit = mds.fit_procrustes(x, x)
+        assert np.abs(fit.rotation - np.eye(3)).max() <= 1e-10 and fit.loss <= 1e-10
+        x = np.random.default_rng(1).standard_normal((12, 2))
+        fit = mds.fit_procrustes(x, x @ self.ROT90)
+        assert np.abs(fit.rotation - self.ROT90.T).max() <= 1e-12 and fit.loss <= 1e-18
+        assert np.abs(mds.apply_procrustes(x @ self.ROT90, fit) - x).max() <= 1e-10
+        x = np.random.default_rng(2).standard_normal((8, 2))
+        fit = mds.fit_procrustes(x, x + np.array([5.0, -3.0]))
+        assert np.allclose(fit.translation, [-5.0, 3.0], atol=1e-12)
+
+    def test_shape_and_degenerate(self, mds):
+        with pytest.raises(mds.ShapeError):
+            mds.fit_procrustes(np.zeros((4, 2)), np.zeros((4, 3)))
+        with pytest.raises(mds.ShapeError):
+            mds.fit_procrustes(np.zeros((1, 2)), np.zeros((1, 2)))
+        fit = mds.fit_procrustes(np.ones((5, 2)), np.ones((5, 2)))
+        assert fit.degenerate
+        assert np.abs(fit.rotation @ fit.rotation.T - np.eye(2)).max() <= 1e-10
+
+    def test_random_recovery_and_kristof(self, mds):
+        rng = np.random.default_rng(3)
+        for r in (2, 5, 10):
+            for _ in range(3):
+                x = rng.standard_normal((30, r))
+                q, _ = np.linalg.qr(rng.standard_normal((r, r)))
+                moved = x @ q + rng.standard_normal(r) * 3.0
+                fit = mds.fit_procrustes(x, moved)
+                assert fit.loss <= 1e-18 * max(1.0, (x ** 2).sum())
+                assert np.abs(mds.apply_procrustes(moved, fit) - x).max() <= 1e-10
+        rng = np.random.default_rng(5)
+        t, s = rng.standard_normal((20, 3)), rng.standard_normal((20, 3))
+        best = mds.fit_procrustes(t, s)
+        assert abs(abs(np.linalg.det(best.rotation)) - 1.0) <= 1e-10
+        for _ in range(200):
+            q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+            res = t - s @ q - (t - s @ q).mean(axis=0)
+            assert best.loss <= np.sum(res * res) + 1e-12
+
+    def test_apply_identity_bitwise(self, mds):
+        pts = np.random.default_rng(9).standard_normal((11, 3))
+        ident = mds.ProcrustesTransform(rotation=np.eye(3), translation=np.zeros(3), loss=0.0)
+        assert np.array_equal(mds.apply_procrustes(pts, ident), pts)
+        with pytest.raises(mds.ShapeError):
+            mds.apply_procrustes(np.zeros((4, 2)), ident)
+
+
+class TestGower:
+    @pytest.fixture(scope="class")
+    def ctx(self, mds):
+        base = np.random.default_rng(21).standard_normal((200, 10)) * 2.0
+        cfg = mds.classical_mds_from_data(base, 5)
+        return base, cfg, mds.gower_context(base, cfg.points)
+
+    def test_self_single_centroid(self, mds, ctx):
+        base, cfg, c = ctx
+        assert np.abs(mds.gower_interpolate(c, base) - cfg.points).max() <= 1e-8
+        assert np.abs(mds.gower_interpolate(c, base[42:43]) - cfg.points[42]).max() <= 1e-8
+        got = mds.gower_interpolate(c, base.mean(axis=0, keepdims=True))
+        assert np.linalg.norm(got) <= 1e-6 * np.abs(cfg.points).max()
+
+    def test_errors(self, mds, ctx):
+        _, _, c = ctx
+        with pytest.raises(mds.ShapeError):
+            mds.gower_interpolate(c, np.zeros((3, 4)))
+        base = np.random.default_rng(22).standard_normal((50, 5))
+        cfg = mds.classical_mds_from_data(base, 3)
+        crushed = cfg.points.copy()
+        crushed[:, 2] *= 1e-9
+        with pytest.raises(mds.NumericalError, match="condition"):
+            mds.gower_context(base, crushed)
+
+
+@pytest.fixture(scope="module")
+def scenario_data(cuda):
+    from paper_2007_11919_b200.synthetic import scenario
+    return scenario(3000, 10, 5, seed=17)
+
+
+ALGS = [("divide", dict(r=5, l=400, c=10, seed=7)), ("interpolate", dict(r=5, l=1000, seed=7)),
+        ("fast", dict(r=5, l=1000, s=10, seed=7))]
+
+
+class TestAlgorithms:
+    def test_dc_recovery_shape_centering(self, mds, scenario_data):
+        cfg = mds.divide_and_conquer_mds(scenario_data, mds.AlgorithmParams(r=5, l=400, c=10, seed=3))
+        assert aligned_corr(mds, cfg, scenario_data[:, :5]).min() >= 0.99
+        assert cfg.points.shape == (3000, 5)
+        assert np.abs(cfg.points.mean(axis=0)).max() <= 1e-6 * cfg.points.std(axis=0).min()
+        assert np.all(np.diff(cfg.eigenvalue_estimates) <= 0) and cfg.gof_g1 <= cfg.gof_g2
+
+    def test_connecting_rows_from_first_subset(self, mds, scenario_data):
+        cfg = mds.divide_and_conquer_mds(scenario_data, mds.AlgorithmParams(r=5, l=400, c=10, seed=3))
+        plan = mds.plan_divide_conquer(3000, 400, 10, seed=3)
+        first = mds.classical_mds_from_data(scenario_data[plan.subsets[0]], 5)
+        delta = cfg.points[plan.subsets[0]] - first.points
+        assert np.abs(delta - delta.mean(axis=0)).max() <= 1e-12
+
+    def test_degenerate_subset_reported(self, mds):
+        rank2 = np.random.default_rng(0).standard_normal((2000, 2)) @ \
+            np.random.default_rng(1).standard_normal((2, 6))
+        with pytest.raises(mds.DegenerateRankError, match="subset"):
+            mds.divide_and_conquer_mds(rank2, mds.AlgorithmParams(r=4, l=400, c=8, seed=0))
+
+    def test_non_finite_rejected(self, mds, scenario_data):
+        bad = scenario_data.copy()
+        bad[1234, 3] = np.inf
+        for name, prm in ALGS:
+            with pytest.raises(mds.InvalidInputError):
+                mds.run_algorithm(name, bad, mds.AlgorithmParams(**prm))
+
+    def test_interp_gof_from_sample(self, mds, scenario_data):
+        cfg = mds.interpolation_mds(scenario_data, mds.AlgorithmParams(r=5, l=1000, seed=3))
+        plan = mds.plan_interpolation(3000, 1000, seed=3)
+        first = mds.classical_mds_from_data(scenario_data[plan.subsets[0]], 5)
+        assert cfg.gof_g1 == first.gof_g1 and cfg.gof_g2 == first.gof_g2
+        assert np.array_equal(cfg.eigenvalue_estimates, first.eigenvalue_estimates)
+        assert aligned_corr(mds, cfg, scenario_data[:, :5]).min() >= 0.995
+
+    def test_fast(self, mds, scenario_data):
+        cfg = mds.fast_mds(scenario_data, mds.AlgorithmParams(r=5, l=1000, s=10, seed=3))
+        assert aligned_corr(mds, cfg, scenario_data[:, :5]).min() >= 0.95
+        assert cfg.gof_g1 <= cfg.gof_g2 and np.all(np.diff(cfg.eigenvalue_estimates) <= 0)
+        from paper_2007_11919_b200.synthetic import scenario
+        data = scenario(600, 6, 3, seed=5)
+        cfg = mds.fast_mds(data, mds.AlgorithmParams(r=3, l=60, s=20, seed=5))
+        assert cfg.points.shape == (600, 3) and aligned_corr(mds, cfg, data[:, :3]).min() >= 0.8
+
+    @pytest.mark.parametrize("name,prm", ALGS)
+    def test_local_isometry_and_seed(self, mds, scenario_data, name, prm):
+        cfg = mds.run_algorithm(name, scenario_data, mds.AlgorithmParams(**prm))
+        assert np.isfinite(cfg.points).all()
+        pairs = np.random.default_rng(0).integers(0, 3000, size=(100, 2))
+        o = np.sqrt(((scenario_data[pairs[:, 0], :5] - scenario_data[pairs[:, 1], :5]) ** 2).sum(1))
+        e = np.sqrt(((cfg.points[pairs[:, 0]] - cfg.points[pairs[:, 1]]) ** 2).sum(1))
+        assert np.corrcoef(o, e)[0, 1] >= 0.95
+        import dataclasses
+        b = mds.run_algorithm(name, scenario_data, dataclasses.replace(mds.AlgorithmParams(**prm), seed=99))
+        if name == "interpolate":
+            assert not np.array_equal(cfg.points, b.points)
+        assert aligned_corr(mds, b, scenario_data[:, :5]).min() >= 0.95
+
+    def test_device_resident_api(self, mds, scenario_data):
+        import torch
+        x = torch.from_numpy(scenario_data).cuda()
+        cfg = mds.divide_and_conquer_mds(x, mds.AlgorithmParams(r=5, l=400, c=10, seed=3),
+                                         return_device=True)
+        assert isinstance(cfg.points, torch.Tensor) and cfg.points.is_cuda
+        host = mds.divide_and_conquer_mds(scenario_data, mds.AlgorithmParams(r=5, l=400, c=10, seed=3))
+        assert np.array_equal(cfg.points.cpu().numpy(), host.points)
