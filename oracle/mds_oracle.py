@@ -288,7 +288,8 @@ def plan_divide(n: int, l: int, c: int, seed: int):
     step = l - c
     parts = [order[i:i + step] for i in range(0, order.size, step)]
     if len(parts) > 1 and parts[-1].size < c + 1:
-        parts[-2] = np.concatenate([parts[-2], parts.pop()])
+        tail = parts.pop()
+        parts[-1] = np.concatenate([parts[-1], tail])
     return conn, [np.concatenate([conn, np.sort(q)]) for q in parts]
 
 

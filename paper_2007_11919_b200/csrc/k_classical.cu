@@ -153,6 +153,24 @@ gram_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restric
 }
 
 // ------------------------------------------------------------- K3 Jacobi
+// Re-solve, with the full Jacobi method, the pieces the Lanczos kernel flagged
+// (status NUMERICAL with value -2: Krylov basis capacity exhausted).
+__global__ void __launch_bounds__(mdsx::JAC_THREADS)
+jacobi_fallback_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
+                       double* __restrict__ Uout, double* __restrict__ lam_out,
+                       double* __restrict__ estimates, double* __restrict__ gof,
+                       mdsx_piece_status* __restrict__ status) {
+  extern __shared__ double sm[];
+  __shared__ mdsx::PieceScratch ps;
+  const PieceDesc d = pd[blockIdx.x];
+  const mdsx_piece_status s0 = status[d.id];
+  if (!(s0.code == MDSX_NUMERICAL && s0.value == -2.0)) return;
+  __syncthreads();
+  if (threadIdx.x == 0) status[d.id] = mdsx_piece_status{MDSX_OK, 0, 0.0};
+  __syncthreads();
+  mdsx::full_jacobi_piece(d, r, Aall, Uout, lam_out, estimates, gof, status, 1, sm, ps);
+}
+
 __global__ void __launch_bounds__(mdsx::JAC_THREADS)
 jacobi_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
               double* __restrict__ Uout, double* __restrict__ lam_out,
@@ -167,6 +185,20 @@ jacobi_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict_
 }  // namespace
 
 namespace mdsx {
+
+int launch_jacobi_fallback(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                           double* A, double* U, double* lam, double* estimates, double* gof,
+                           mdsx_piece_status* status, cudaStream_t st) {
+  if (npieces == 0) return MDSX_OK;
+  const int kk = kmax + (kmax & 1);
+  const size_t smem = (size_t)2 * kk * kk * sizeof(double);
+  cudaFuncSetAttribute(jacobi_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  mdsx::pre(h, st);
+  jacobi_fallback_kernel<<<npieces, mdsx::JAC_THREADS, smem, st>>>(pd, r, A, U, lam, estimates,
+                                                                   gof, status);
+  return launched(h, "jacobi_fallback_kernel", st);
+}
 
 int launch_piece_means(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                        const int64_t* row_idx, const PieceDesc* pd, int npieces, double* mu,

@@ -1,6 +1,11 @@
 // K3 top-r eigensolver for the per-piece k x k PSD Gram matrices (k <= 104):
 // Krylov subspace iteration (Lanczos) with full re-orthogonalisation, one CTA
-// per piece, the matrix A and the Krylov basis Q resident in shared memory.
+// per piece, the matrix A (packed upper triangle) and a Krylov basis Q of at
+// most QMAX columns resident in shared memory — ~105 KB, so two pieces run
+// per SM and hide each other's barrier/latency stalls.  A piece that needs
+// more than QMAX Krylov vectors is flagged (status NUMERICAL, value -2) and
+// re-solved by the full Jacobi kernel launched right after (in stream order,
+// no host sync).
 //
 //   step j:  w = A q_j ;  w -= Q (Q^T w) twice (CGS2) ;  alpha_j = q_j^T A q_j ;
 //            beta_j = |w| ;  q_{j+1} = w / beta_j
@@ -10,8 +15,9 @@
 // tridiagonalisation restricted to the Krylov space, so it reaches the exact
 // answer at j = k at the latest.  Every 8 steps the top-r eigenpairs of T_j
 // are computed in parallel — eigenvalues by 16-way multisection on Sturm
-// counts (one half-warp per eigenvalue), vectors by inverse iteration with a
-// pivoted tridiagonal LU — and the Lanczos residual |beta_j s_i(j)|, which
+// counts (one half-warp per eigenvalue), vectors by a twisted factorisation
+// of T - theta I (one O(j) pass, as LAPACK's dlar1v) with MGS only inside
+// eigenvalue clusters — and the Lanczos residual |beta_j s_i(j)|, which
 // equals |A y_i - theta_i y_i|, is tested against 1e-12 theta_1.  Ritz
 // vectors y_i = Q s_i are the eigenvectors returned.
 //
@@ -28,6 +34,7 @@ constexpr int LT = 256;          // threads per CTA
 constexpr int MS = 16;           // multisection width (threads per eigenvalue)
 constexpr int LMAX = 104;        // largest k for this kernel (smem budget)
 constexpr int RMAX = 16;         // largest r (16 half-warps of 16 threads)
+constexpr int QCAP_PIECES = 56;  // Krylov basis capacity for plan pieces (2 CTAs / SM)
 constexpr int CHECK_EVERY = 8;
 
 __device__ __forceinline__ double hash_unit(uint64_t x) {
@@ -51,59 +58,39 @@ __device__ int sturm_below(const double* al, const double* be2, int m, double x,
   return cnt;
 }
 
-// inverse iteration for the eigenvector of tridiagonal T (al, be) at theta:
-// LU of (T - theta I) with partial pivoting (dgttrf layout), two solves.
-__device__ void tri_inverse_iteration(const double* al, const double* be, int m, double theta,
-                                      double tiny, double* x /* m, out */) {
-  double d[LMAX], du[LMAX], du2[LMAX], dl[LMAX];
-  int piv[LMAX];
+// Eigenvector of the m x m tridiagonal T (al, be) at its eigenvalue theta by a
+// twisted factorisation of T - theta I: top-down LDL^T pivots d, bottom-up
+// UDU^T pivots u, twist index with the smallest |d_k + u_k - (al_k - theta)|,
+// then the vector outward from the twist (z_k = 1).  O(m), no pivoting needed.
+template <int QMAX>
+__device__ void tri_twisted_vector(const double* al, const double* be, int m, double theta,
+                                   double pivmin, double* z /* m, out, unit norm */) {
+  double d[QMAX], u[QMAX];
+  double t = al[0] - theta;
+  d[0] = fabs(t) < pivmin ? -pivmin : t;
+  for (int i = 1; i < m; ++i) {
+    t = (al[i] - theta) - be[i - 1] * be[i - 1] / d[i - 1];
+    d[i] = fabs(t) < pivmin ? -pivmin : t;
+  }
+  t = al[m - 1] - theta;
+  u[m - 1] = fabs(t) < pivmin ? -pivmin : t;
+  for (int i = m - 2; i >= 0; --i) {
+    t = (al[i] - theta) - be[i] * be[i] / u[i + 1];
+    u[i] = fabs(t) < pivmin ? -pivmin : t;
+  }
+  int kt = 0;
+  double best = 1e308;
   for (int i = 0; i < m; ++i) {
-    d[i] = al[i] - theta;
-    du[i] = i + 1 < m ? be[i] : 0.0;
-    dl[i] = i + 1 < m ? be[i] : 0.0;
-    du2[i] = 0.0;
+    const double g = fabs(d[i] + u[i] - (al[i] - theta));
+    if (g < best) { best = g; kt = i; }
   }
-  for (int i = 0; i + 1 < m; ++i) {
-    if (fabs(d[i]) >= fabs(dl[i])) {           // no interchange
-      piv[i] = 0;
-      if (d[i] == 0.0) d[i] = tiny;
-      const double f = dl[i] / d[i];
-      dl[i] = f;
-      d[i + 1] -= f * du[i];
-    } else {                                   // interchange rows i, i+1
-      piv[i] = 1;
-      const double f = d[i] / dl[i];
-      d[i] = dl[i];
-      dl[i] = f;
-      const double t = du[i];
-      du[i] = d[i + 1];
-      d[i + 1] = t - f * d[i + 1];
-      if (i + 2 < m) {
-        du2[i] = du[i + 1];
-        du[i + 1] = -f * du[i + 1];
-      }
-    }
-  }
-  if (d[m - 1] == 0.0) d[m - 1] = tiny;
-  for (int i = 0; i < m; ++i) x[i] = 1.0;
-  for (int it = 0; it < 3; ++it) {
-    for (int i = 0; i + 1 < m; ++i) {          // apply L^-1 (with interchanges)
-      if (piv[i]) {
-        const double t = x[i];
-        x[i] = x[i + 1];
-        x[i + 1] = t - dl[i] * x[i + 1];
-      } else {
-        x[i + 1] -= dl[i] * x[i];
-      }
-    }
-    x[m - 1] /= d[m - 1];                      // U^-1
-    if (m > 1) x[m - 2] = (x[m - 2] - du[m - 2] * x[m - 1]) / d[m - 2];
-    for (int i = m - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / d[i];
-    double nrm = 0.0;
-    for (int i = 0; i < m; ++i) nrm = fma(x[i], x[i], nrm);
-    nrm = sqrt(nrm);
-    for (int i = 0; i < m; ++i) x[i] /= nrm;
-  }
+  z[kt] = 1.0;
+  for (int i = kt - 1; i >= 0; --i) z[i] = -(be[i] / d[i]) * z[i + 1];
+  for (int i = kt + 1; i < m; ++i) z[i] = -(be[i - 1] / u[i]) * z[i - 1];
+  double nrm = 0.0;
+  for (int i = 0; i < m; ++i) nrm = fma(z[i], z[i], nrm);
+  nrm = 1.0 / sqrt(nrm);
+  for (int i = 0; i < m; ++i) z[i] *= nrm;
 }
 
 __device__ double block_sum(double v, double* red) {
@@ -143,15 +130,15 @@ __device__ void cgs_project(const double* Q, int kq, int k, int nc, double* wv, 
   }
 }
 
-__global__ void __launch_bounds__(LT)
+template <int QMAX>
+__global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
 lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
                     double* __restrict__ Uout, double* __restrict__ lam_out,
                     double* __restrict__ estimates, double* __restrict__ gof,
                     mdsx_piece_status* __restrict__ status, int qform_trivial) {
   extern __shared__ double sm[];
-  __shared__ mdsx::PieceScratch ps;
-  __shared__ double alpha[LMAX], beta[LMAX], beta2[LMAX];
-  __shared__ double wv[LMAX], hv[LMAX + 1], part[2][LMAX];
+  __shared__ double alpha[QMAX], beta[QMAX], beta2[QMAX];
+  __shared__ double wv[LMAX], hv[QMAX + 1];
   __shared__ double theta[RMAX], lo_s[RMAX], hi_s[RMAX];
   __shared__ double red[LT / 32];
   __shared__ double trace_s, anorm_s;
@@ -162,16 +149,20 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   const int kq = k | 1;                        // odd leading dim of Q (conflict-free columns)
   const int tid = threadIdx.x;
   const double* Ag = Aall + d.a_off;
-  double* A = sm;                              // k x k
-  double* Q = A + (size_t)k * k;               // column j at Q + j*kq
-  double* S = Q + (size_t)k * kq;              // m x r Ritz coefficients (column i at S + i*k)
+  double* A = sm;                              // packed upper: row i = A[i][i..k)
+  double* Q = A + (size_t)k * (k + 1) / 2;     // column j at Q + j*kq, j < QMAX
+  double* S = Q + (size_t)QMAX * kq;           // Ritz coefficients, S[c*RMAX + i]
+  const int qcap = min(QMAX, k);
 
   double fro = 0.0, tr = 0.0;
-  for (int e = tid; e < k * k; e += LT) {
-    const double v = Ag[e];
-    A[e] = v;
-    fro = fma(v, v, fro);
-    if (e / k == e % k) tr += v;
+  for (int i = 0; i < k; ++i) {                // packed copy, coalesced per row
+    const int off = i * k - i * (i - 1) / 2;
+    for (int a = i + tid; a < k; a += LT) {
+      const double v = Ag[(int64_t)i * k + a];
+      A[off + a - i] = v;
+      fro = fma((a == i ? 1.0 : 2.0) * v, v, fro);   // off-diagonal entries count twice
+      if (a == i) tr += v;
+    }
   }
   fro = block_sum(fro, red);
   tr = block_sum(tr, red);
@@ -182,34 +173,30 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   if (tid < k) Q[tid] = q0 / n0;
   __syncthreads();
   const double anorm = anorm_s;
-
-  // matvec mapping: two halves of the reduction index, thread -> (row, half)
-  const int half = tid >> 7, row = tid & 127;
-  const int a_lo = half ? k / 2 : 0, a_hi = half ? k : k / 2;
+  const int row_off = tid < k ? tid * k - tid * (tid - 1) / 2 - tid : 0;   // packed row base
 
   int m = 0;                 // current Krylov dimension (columns 0..m-1 of Q valid)
-  bool done = false;
-  bool broke = false;        // last step hit an invariant subspace (restarted)
-  int nconv_checks = 0;
-  // Krylov dimension of the first convergence test (earlier tests never pass)
+  bool done = false, broke = false, capped = false;
   const int first_check = max(2 * r + 4, 24);
   while (!done) {
     const double* q = Q + (size_t)m * kq;
-    // w = A q  (A symmetric: read A[a][row] across threads; 4 independent chains)
-    if (row < k) {
+    // w = A q with the packed symmetric A: row i = sum_{a<i} A[a][i] q_a + sum_{a>=i} A[i][a] q_a
+    if (tid < k) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int a = a_lo;
-      for (; a + 3 < a_hi; a += 4) {
-        a0 = fma(A[a * k + row], q[a], a0);
-        a1 = fma(A[(a + 1) * k + row], q[a + 1], a1);
-        a2 = fma(A[(a + 2) * k + row], q[a + 2], a2);
-        a3 = fma(A[(a + 3) * k + row], q[a + 3], a3);
+      int off = 0;
+      int a = 0;
+      for (; a < tid; ++a) {                   // column part (coalesced across threads)
+        a1 = fma(A[off + tid - a], q[a], a1);
+        off += k - a;
       }
-      for (; a < a_hi; ++a) a0 = fma(A[a * k + row], q[a], a0);
-      part[half][row] = (a0 + a1) + (a2 + a3);
+      const double* rowp = A + row_off;
+      for (; a + 1 < k; a += 2) {              // own row part
+        a0 = fma(rowp[a], q[a], a0);
+        a2 = fma(rowp[a + 1], q[a + 1], a2);
+      }
+      if (a < k) a3 = fma(rowp[a], q[a], a3);
+      wv[tid] = (a0 + a1) + (a2 + a3);
     }
-    __syncthreads();
-    if (tid < k) wv[tid] = part[0][tid] + part[1][tid];
     __syncthreads();
     double al = 0.0;
     for (int pass = 0; pass < 2; ++pass) {     // CGS2 against Q[:, 0..m]
@@ -226,7 +213,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     m += 1;
     const bool full = (m >= k);
     broke = false;
-    if (!full) {
+    if (!full && m < qcap) {
       if (b > 1e-13 * anorm) {
         if (tid < k) Q[(size_t)m * kq + tid] = wv[tid] / b;
       } else {
@@ -245,10 +232,10 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       }
     }
     __syncthreads();
-    if (!(full || (!broke && m >= first_check && m % CHECK_EVERY == 0))) continue;
+    capped = !full && m >= qcap;
+    if (!(full || capped || (!broke && m >= first_check && m % CHECK_EVERY == 0))) continue;
 
     // ---- top-r eigenpairs of T_m: multisection (16 threads per eigenvalue)
-    ++nconv_checks;
     const int rr = r < m ? r : m;
     double gl = 1e308, gu = -1e308, bmax = 0.0;
     for (int i = 0; i < m; ++i) {
@@ -283,30 +270,34 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     }
     if (tid < rr) theta[tid] = 0.5 * (lo_s[tid] + hi_s[tid]);
     __syncthreads();
-    // eigenvectors of T_m by inverse iteration (one thread per eigenvalue)
+    // eigenvectors of T_m (one thread per eigenvalue), S[c*RMAX + i]
     if (tid < rr) {
-      double x[LMAX];
-      tri_inverse_iteration(alpha, beta, m, theta[tid], 1e-300 + 1e-16 * anorm, x);
-      for (int i = 0; i < m; ++i) S[(size_t)tid * k + i] = x[i];
+      double z[QMAX];
+      tri_twisted_vector<QMAX>(alpha, beta, m, theta[tid], pivmin + 1e-300, z);
+      for (int c = 0; c < m; ++c) S[c * RMAX + tid] = z[c];
     }
     __syncthreads();
-    if (tid < 32) {            // MGS across the r vectors (clusters), fixed order, warp 0
+    if (tid < 32) {            // MGS inside eigenvalue clusters only (fixed order, warp 0)
       const int lane = tid;
+      const double ctol = 1e-3 * fabs(theta[0]);
       for (int i = 1; i < rr; ++i) {
-        double* si = S + (size_t)i * k;
+        bool touched = false;
         for (int j = 0; j < i; ++j) {
-          const double* sj = S + (size_t)j * k;
+          if (fabs(theta[i] - theta[j]) > ctol) continue;
+          touched = true;
           double dt = 0.0;
-          for (int t = lane; t < m; t += 32) dt = fma(si[t], sj[t], dt);
+          for (int t = lane; t < m; t += 32) dt = fma(S[t * RMAX + i], S[t * RMAX + j], dt);
           dt = mdsx::warp_sum(dt);
-          for (int t = lane; t < m; t += 32) si[t] = fma(-dt, sj[t], si[t]);
+          for (int t = lane; t < m; t += 32) S[t * RMAX + i] = fma(-dt, S[t * RMAX + j], S[t * RMAX + i]);
           __syncwarp();
         }
-        double nr = 0.0;
-        for (int t = lane; t < m; t += 32) nr = fma(si[t], si[t], nr);
-        nr = sqrt(mdsx::warp_sum(nr));
-        for (int t = lane; t < m; t += 32) si[t] /= nr;
-        __syncwarp();
+        if (touched) {
+          double nr = 0.0;
+          for (int t = lane; t < m; t += 32) nr = fma(S[t * RMAX + i], S[t * RMAX + i], nr);
+          nr = sqrt(mdsx::warp_sum(nr));
+          for (int t = lane; t < m; t += 32) S[t * RMAX + i] /= nr;
+          __syncwarp();
+        }
       }
     }
     __syncthreads();
@@ -314,21 +305,23 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       int ok = rr == r;
       const double bm = full ? 0.0 : beta[m - 1];
       for (int i = 0; i < rr && ok; ++i)
-        if (!(fabs(bm * S[(size_t)i * k + m - 1]) <= 1e-12 * fabs(theta[0]))) ok = 0;
-      conv_s = ok || full;
+        if (!(fabs(bm * S[(m - 1) * RMAX + i]) <= 1e-12 * fabs(theta[0]))) ok = 0;
+      conv_s = ok || full ? 1 : (capped ? 2 : 0);
     }
     __syncthreads();
     done = conv_s != 0;
+  }
+  if (conv_s == 2) {          // basis capacity exhausted: the full Jacobi kernel takes over
+    if (tid == 0 && status[pid].code == MDSX_OK) status[pid] = mdsx_piece_status{MDSX_NUMERICAL, 0, -2.0};
+    return;
   }
 
   // Ritz vectors y_i = Q s_i  (k x r) and outputs
   for (int e = tid; e < k * r; e += LT) {
     const int a = e / r, i = e % r;
     double u = 0.0;
-    if (i < m) {
-      const double* si = S + (size_t)i * k;
-      for (int c = 0; c < m; ++c) u = fma(Q[(size_t)c * kq + a], si[c], u);
-    }
+    if (i < m)
+      for (int c = 0; c < m; ++c) u = fma(Q[(size_t)c * kq + a], S[c * RMAX + i], u);
     Uout[d.u_off + e] = u;
   }
   if (tid == 0) {
@@ -360,20 +353,29 @@ namespace mdsx {
 int lanczos_kmax() { return LMAX; }
 int lanczos_rmax() { return RMAX; }
 
-size_t lanczos_smem_bytes(int kmax) {
-  return ((size_t)kmax * kmax + (size_t)kmax * (kmax | 1) + (size_t)kmax * RMAX) * sizeof(double);
+static size_t lanczos_bytes(int kmax, int qmax) {
+  return ((size_t)kmax * (kmax + 1) / 2 + (size_t)qmax * (kmax | 1) + (size_t)qmax * RMAX) *
+         sizeof(double);
 }
 
+size_t lanczos_smem_bytes(int kmax) { return lanczos_bytes(kmax, LMAX); }
+
+// full_basis: Krylov capacity = LMAX (one CTA / SM, never flags -2; used for
+// the Rayleigh-Ritz matrices of the block-Krylov solver); otherwise
+// QCAP_PIECES (two CTAs / SM, capacity overflow -> Jacobi fallback).
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                        mdsx_piece_status* status, int qform_trivial, cudaStream_t st) {
+                        mdsx_piece_status* status, int full_basis, cudaStream_t st) {
   if (npieces == 0) return MDSX_OK;
-  const size_t smem = lanczos_smem_bytes(kmax);
-  cudaFuncSetAttribute(lanczos_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mdsx::pre(h, st);
-  lanczos_smem_kernel<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status,
-                                                 qform_trivial);
-  return launched(h, "lanczos_smem_kernel", st);
+  auto go = [&](auto kern, int qmax) {
+    const size_t smem = lanczos_bytes(kmax, qmax);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mdsx::pre(h, st);
+    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, 1);
+    return launched(h, "lanczos_smem_kernel", st);
+  };
+  return full_basis ? go(lanczos_smem_kernel<LMAX>, LMAX)
+                    : go(lanczos_smem_kernel<QCAP_PIECES>, QCAP_PIECES);
 }
 
 }  // namespace mdsx

@@ -42,10 +42,13 @@ int lanczos_rmax();
 size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                        mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+                        mdsx_piece_status* status, int full_basis, cudaStream_t st);
 int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                      const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
                      double* A, double* mu, mdsx_piece_status* status, cudaStream_t st);
+int launch_jacobi_fallback(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                           double* A, double* U, double* lam, double* estimates, double* gof,
+                           mdsx_piece_status* status, cudaStream_t st);
 size_t bk_ws_bytes(const std::vector<PieceDesc>& big);
 int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const double* A, int r,
                    double* Uout, double* lam_out, double* estimates, double* gof,
@@ -275,10 +278,14 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
       (rc = launch_jacobi(h, dpd_jac, (int)cp.pd_jac.size(), cp.kmax_jac, r, A, U, lam, estimates,
                           gof, status, 1, st)))
     return rc;
-  if (!cp.pd_sub.empty() &&
-      (rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
-                                estimates, gof, status, 1, st)))
-    return rc;
+  if (!cp.pd_sub.empty()) {
+    if ((rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
+                                  estimates, gof, status, 0, st)))
+      return rc;
+    if ((rc = launch_jacobi_fallback(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
+                                     estimates, gof, status, st)))
+      return rc;
+  }
   if (!cp.pd_big.empty() &&
       (rc = run_big_pieces(h, cp.pd_big, A, r, U, lam, estimates, gof, status, st, stage_put)))
     return rc;

@@ -219,7 +219,7 @@ class TestProcrustes:
 
 
 class TestGower:
-    @pytest.fixture(scope="class")
+    @pytest.fixture
     def ctx(self, mds):
         base = np.random.default_rng(21).standard_normal((200, 10)) * 2.0
         cfg = mds.classical_mds_from_data(base, 5)

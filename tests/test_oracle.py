@@ -85,3 +85,38 @@ class TestAlgorithms:
     def test_generator_matches_package_generator(self):
         assert np.array_equal(orc.scenario(700, 9, 3, seed=5, rep=2),
                               synthetic.scenario(700, 9, 3, seed=5, rep=2))
+
+
+class TestOraclePlans:
+    """The oracle's planners against the reference's partition contracts and
+    the (digest-pinned) product planner, including the short-remainder merge."""
+
+    def test_divide_merge_case(self):
+        conn, subs = orc.plan_divide(285, 100, 10, 1)
+        assert [len(s) for s in subs] == [100, 100, 105]
+        merged = np.concatenate([conn] + [s[10:] for s in subs])
+        assert np.array_equal(np.sort(merged), np.arange(285))
+
+    @pytest.mark.parametrize("n,l,c,seed", [(1300, 650, 20, 1), (285, 100, 10, 1), (5000, 1000, 20, 0),
+                                            (1000, 400, 20, 5), (999, 300, 7, 3)])
+    def test_divide_matches_product_planner(self, n, l, c, seed):
+        from paper_2007_11919_b200.plans import plan_divide_conquer
+        _, subs = orc.plan_divide(n, l, c, seed)
+        ref = plan_divide_conquer(n, l, c, seed).subsets
+        assert len(subs) == len(ref) and all(np.array_equal(a, b) for a, b in zip(subs, ref))
+
+    def test_interp_and_fast_match_product_planner(self):
+        from paper_2007_11919_b200.plans import plan_fast, plan_interpolation
+        for n, l, seed in [(10, 4, 0), (1001, 100, 2), (3000, 1000, 3)]:
+            a = orc.plan_interp(n, l, seed)
+            b = plan_interpolation(n, l, seed).subsets
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
+        ta, tb = orc.plan_fast_tree(5000, 100, 10, 4), plan_fast(5000, 100, 10, 4).root
+        def walk(x, y):
+            assert np.array_equal(x.indices, y.indices)
+            if x.positions is not None:
+                assert np.array_equal(x.positions, y.sampling_positions)
+            assert len(x.children) == len(y.children)
+            for cx, cy in zip(x.children, y.children):
+                walk(cx, cy)
+        walk(ta, tb)
