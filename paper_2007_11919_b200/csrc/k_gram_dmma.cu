@@ -60,33 +60,57 @@ gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __re
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // register prefetch of chunk c+1 while the DMMAs run on chunk c:
+  // warp w owns rows 4w..4w+3 of a chunk, lane owns columns lane, lane+32
+  constexpr int RPW = KC / (NT / 32);          // 4 rows per warp
+  double pre[2][RPW][2];
   bool nonfinite = false;
-  for (int r0 = 0; r0 < m; r0 += KC) {
-    const int nr = min(KC, m - r0);
-    // stage y = x - x0 for the tile's column blocks (warp per row: coalesced)
-    for (int rr = warp; rr < KC; rr += NT / 32) {
+  const int nchunks = (m + KC - 1) / KC;
+  auto fetch = [&](int c) {
+    const int r0 = c * KC, nr = min(KC, m - r0);
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int rr = warp * RPW + j;
       const bool live = rr < nr;
-      const T* src = live ? X + ridx[r0 + rr] * ld : nullptr;
-      for (int c = lane; c < TT; c += 32) {
-        double va = 0.0, vb = 0.0;
-        if (live && ca + c < k) {
-          const double v = mdsx::ld_val(src + ca + c);
-          nonfinite |= !isfinite(v);
-          va = v - x0a[c];
-        }
-        if (live && cb + c < k) vb = mdsx::ld_val(src + cb + c) - x0b[c];
-        ya[rr][c] = va;
-        yb[rr][c] = vb;
+      const T* src = X + (live ? ridx[r0 + rr] : ridx[0]) * ld;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = lane + 32 * h;
+        pre[0][j][h] = (live && ca + col < k) ? mdsx::ld_val(src + ca + col) : 0.0;
+        pre[1][j][h] = (!diag && live && cb + col < k) ? mdsx::ld_val(src + cb + col) : 0.0;
       }
     }
+  };
+  auto store = [&](int c) {
+    const int nr = min(KC, m - c * KC);
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int rr = warp * RPW + j;
+      const bool live = rr < nr;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = lane + 32 * h;
+        const double va = pre[0][j][h];
+        nonfinite |= !isfinite(va);
+        ya[rr][col] = (live && ca + col < k) ? va - x0a[col] : 0.0;
+        if (!diag) yb[rr][col] = (live && cb + col < k) ? pre[1][j][h] - x0b[col] : 0.0;
+      }
+    }
+  };
+  const double (*YB)[LD] = diag ? ya : yb;     // diagonal tiles: one operand block
+  fetch(0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int nr = min(KC, m - c * KC);
+    store(c);
     __syncthreads();
-    if (tid < TT) {                       // column sums of the chunk, fixed order
+    if (c + 1 < nchunks) fetch(c + 1);          // in flight during the DMMAs below
+    if (tid < TT) {                              // column sums of the chunk, fixed order
       double s = 0.0;
       for (int rr = 0; rr < nr; ++rr) s += ya[rr][tid];
       sa[tid] += s;
     } else if (tid < 2 * TT) {
       double s = 0.0;
-      for (int rr = 0; rr < nr; ++rr) s += yb[rr][tid - TT];
+      for (int rr = 0; rr < nr; ++rr) s += YB[rr][tid - TT];
       sb[tid - TT] += s;
     }
 #pragma unroll
@@ -95,7 +119,7 @@ gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __re
 #pragma unroll
       for (int i = 0; i < 2; ++i) af[i] = ya[k4 + tig][wr * 16 + i * 8 + gid];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = yb[k4 + tig][wc * 32 + j * 8 + gid];
+      for (int j = 0; j < 4; ++j) bf[j] = YB[k4 + tig][wc * 32 + j * 8 + gid];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll

@@ -26,8 +26,6 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
               const double* __restrict__ Uall, const double* __restrict__ lam_all,
               double* __restrict__ points, double2* __restrict__ cand, int maxch, int tr) {
   extern __shared__ double sm[];
-  __shared__ double bval[PT];
-  __shared__ int bidx[PT];
   const PieceDesc d = pd[blockIdx.y];
   const int chunk = blockIdx.x;
   const int r0 = chunk * CH;
@@ -54,27 +52,58 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
         out[(int64_t)i * r + c] = v;
       }
   } else {
+    // form 0: double-buffered 32-row tiles; every thread owns EPT tile elements
+    // (loads issued for tile t+1 before the FMAs on tile t)
     const int pp = p + 1;                        // padded tile row (conflict-free)
     double* sU = sm;                             // p x rp
     double* smu = sU + (size_t)p * rp;           // p
-    double* tile = smu + p;                      // tr x pp
+    double* tiles = smu + p;                     // 2 x tr x pp
     for (int e = tid; e < p * rp; e += PT) {
       const int a = e / rp, c = e % rp;
       sU[e] = c < r ? Ug[(int64_t)a * r + c] : 0.0;
     }
     for (int e = tid; e < p; e += PT) smu[e] = mu_all[(int64_t)d.id * p + e];
-    for (int t0 = 0; t0 < rows; t0 += tr) {
-      const int nr = min(tr, rows - t0);
-      __syncthreads();
-      for (int i = tid / 32; i < nr; i += PT / 32) {   // warp per row: coalesced
-        const T* src = X + ridx[t0 + i] * ld;
-        for (int a = tid % 32; a < p; a += 32) tile[i * pp + a] = mdsx::ld_val(src + a) - smu[a];
+    __syncthreads();
+    // row offsets of this CTA's rows, staged once (no dependent index loads per element)
+    __shared__ int64_t rbase[CH];
+    for (int i = tid; i < rows; i += PT) rbase[i] = ridx[i] * ld;
+    const int ntiles = (rows + tr - 1) / tr;
+    const int rpw = tr / (PT / 32);              // rows per warp per tile (tr is a multiple of 8)
+    const int lane = tid & 31, wq = tid >> 5;
+    constexpr int EPT = 16;                      // 4 rows x 4 columns (128-column block) per lane
+    double pre[EPT];
+    auto fetch = [&](int t, int pass) {
+      const int t0 = t * tr, nr = min(tr, rows - t0);
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int j = q >> 2, a = pass * 128 + lane + 32 * (q & 3);
+        const int rr = wq * rpw + j;
+        // raw values only: consuming them here would stall on the loads
+        pre[q] = (j < rpw && rr < nr && a < p) ? mdsx::ld_val(X + rbase[t0 + rr] + a) : 0.0;
       }
-      __syncthreads();
+    };
+    auto store = [&](int b, int pass) {
+      double* tb = tiles + (size_t)b * tr * pp;
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        const int j = q >> 2, a = pass * 128 + lane + 32 * (q & 3);
+        if (j < rpw && a < p) tb[(wq * rpw + j) * pp + a] = pre[q] - smu[a];
+      }
+    };
+    __syncthreads();
+    const int passes = (p + 127) / 128;
+    for (int pass = 0; pass < passes; ++pass) { fetch(0, pass); store(0, pass); }
+    __syncthreads();
+    for (int t = 0; t < ntiles; ++t) {
+      const int b = t & 1;
+      const bool more = t + 1 < ntiles;
+      if (more) fetch(t + 1, 0);                 // first pass in flight during the FMAs
+      const int t0 = t * tr, nr = min(tr, rows - t0);
       if (worker && i_loc < nr) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* xr = tile + i_loc * pp;
+        const double* xr = tiles + (size_t)b * tr * pp + i_loc * pp;
         const double* ug = sU + 4 * g;
+#pragma unroll 4
         for (int a = 0; a < p; ++a) {
           const double x = xr[a];
           const double2 u01 = *reinterpret_cast<const double2*>(ug + a * rp);
@@ -94,11 +123,19 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
           }
         }
       }
+      if (more) {
+        store(b ^ 1, 0);
+        for (int pass = 1; pass < passes; ++pass) { fetch(t + 1, pass); store(b ^ 1, pass); }
+      }
+      __syncthreads();
     }
   }
-  // per-CTA candidates per column (ties -> lowest row), fixed-order tree
+  // per-CTA candidates per column (ties -> lowest row): warp shuffles, then
+  // one fixed-order pass over the 8 warp results
+  __shared__ double wv_s[PT / 32][MDSX_MAX_R];
+  __shared__ int wi_s[PT / 32][MDSX_MAX_R];
+  const int lane = tid & 31, warp = tid >> 5;
   for (int c = 0; c < r; ++c) {
-    __syncthreads();
     double v = -1.0;
     int ix = 0x7fffffff;
     if (d.form == 1) {
@@ -110,18 +147,24 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
       v = best[c % 4];
       ix = bi[c % 4];
     }
-    bval[tid] = v;
-    bidx[tid] = ix;
-    __syncthreads();
-    for (int s = PT / 2; s > 0; s >>= 1) {
-      if (tid < s) {
-        const double v2 = bval[tid + s];
-        const int i2 = bidx[tid + s];
-        if (v2 > bval[tid] || (v2 == bval[tid] && i2 < bidx[tid])) { bval[tid] = v2; bidx[tid] = i2; }
-      }
-      __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+      if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
     }
-    if (tid == 0) cand[((size_t)d.id * maxch + chunk) * r + c] = make_double2(bval[0], (double)bidx[0]);
+    if (lane == 0) { wv_s[warp][c] = v; wi_s[warp][c] = ix; }
+  }
+  __syncthreads();
+  if (tid < r) {
+    double v = -1.0;
+    int ix = 0x7fffffff;
+    for (int w = 0; w < PT / 32; ++w) {
+      const double v2 = wv_s[w][tid];
+      const int i2 = wi_s[w][tid];
+      if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+    }
+    cand[((size_t)d.id * maxch + chunk) * r + tid] = make_double2(v, (double)ix);
   }
 }
 
@@ -167,11 +210,12 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
                   double2* cand, cudaStream_t st) {
   const int maxch = (int)((max_m + CH - 1) / CH);
   const int G = (r + 3) / 4, rp = 4 * G;
-  // rows per tile: one per thread group, limited by the ~200 KB smem budget
-  int tr = PT / G;
+  // tile rows: 32 (one per lane) unless the double buffer would not fit
+  int tr = 32;
   const size_t fixed = ((size_t)p * rp + p) * sizeof(double);
-  while (tr > 8 && fixed + (size_t)tr * (p + 1) * sizeof(double) > 200 * 1024) tr >>= 1;
-  const size_t smem = fixed + (size_t)tr * (p + 1) * sizeof(double);
+  while (tr > 8 && fixed + 2 * (size_t)tr * (p + 1) * sizeof(double) > 200 * 1024) tr >>= 1;
+  if (tr * G > PT) tr = PT / G;
+  const size_t smem = fixed + 2 * (size_t)tr * (p + 1) * sizeof(double);
   dim3 grid((unsigned)maxch, (unsigned)npieces);
   int rc;
   if (dtype == MDSX_F32) {
