@@ -90,21 +90,27 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
   __shared__ double Ssh[MDSX_MAX_R * MDSX_MAX_R], E[MDSX_MAX_R * MDSX_MAX_R];
   __shared__ double L[MDSX_MAX_R * MDSX_MAX_R];
   __shared__ int ok;
-  const int tid = threadIdx.x;
-  if (tid < r) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // column sums / means of X1: warp per column, lanes split the l rows (fixed order)
+  for (int c = warp; c < r; c += nw) {
     double s = 0.0;
-    for (int64_t j = 0; j < l; ++j) s += X1[j * r + tid];
-    s1[tid] = s;
-    m1[tid] = s / (double)l;
+    for (int64_t j = lane; j < l; j += 32) s += X1[j * r + c];
+    s = mdsx::warp_sum(s);
+    if (lane == 0) { s1[c] = s; m1[c] = s / (double)l; }
   }
   __syncthreads();
-  for (int e = tid; e < r * r; e += blockDim.x) {
+  // S = X1c^T X1c / l: warp per entry (a <= b), mirrored
+  for (int e = warp; e < r * r; e += nw) {
     const int a = e / r, b = e % r;
+    if (a > b) continue;
     double s = 0.0;
-    for (int64_t j = 0; j < l; ++j) s = fma(X1[j * r + a] - m1[a], X1[j * r + b] - m1[b], s);
-    Ssh[e] = s / (double)l;
-    S[e] = s / (double)l;
-    E[e] = s / (double)l;
+    for (int64_t j = lane; j < l; j += 32) s = fma(X1[j * r + a] - m1[a], X1[j * r + b] - m1[b], s);
+    s = mdsx::warp_sum(s) / (double)l;
+    if (lane == 0) {
+      Ssh[a * r + b] = Ssh[b * r + a] = s;
+      S[a * r + b] = S[b * r + a] = s;
+      E[a * r + b] = E[b * r + a] = s;
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -223,6 +229,116 @@ gower_affine_kernel(const T* __restrict__ X, int64_t ld, int64_t m, int p, int r
   if (bad) atomicOr(nonfinite, 1);
 }
 
+
+// ---- streaming Gower over contiguous rows, cp.async double buffering.
+// Stage = TR rows x p inputs, copied global -> shared in 16-byte cp.async
+// chunks (the rows of a tile are one contiguous block), so the copy of tile
+// t+1 proceeds while the CTA computes tile t.  Thread i owns row i of the
+// stage: x read as float4/double2 vectors along the features (conflict-free),
+// centred with the broadcast mean; a thread pair shares a row, each thread
+// owning half of the r outputs (+ |x|^2) in registers; M rows are
+// warp-broadcast loads.  128-row stages -> two CTAs per SM.
+template <typename T, int RM>
+__global__ void __launch_bounds__(256, 2)
+gower_stream_kernel(const T* __restrict__ X, int64_t m, int p, int r,
+                    const double* __restrict__ ctx_mean, const double* __restrict__ ctx_M,
+                    const double* __restrict__ ctx_v, double* __restrict__ out,
+                    int32_t* __restrict__ nonfinite, int TR) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* sM = reinterpret_cast<double*>(smraw);          // p x RM
+  double* smu = sM + (size_t)p * RM;                      // p
+  T* stage0 = reinterpret_cast<T*>(smu + p);              // 2 x TR x p
+  const int tid = threadIdx.x;
+  for (int e = tid; e < p * RM; e += blockDim.x) {
+    const int a = e / RM, c = e % RM;
+    sM[e] = c < r ? ctx_M[(int64_t)a * r + c] : 0.0;
+  }
+  for (int e = tid; e < p; e += blockDim.x) smu[e] = ctx_mean[e];
+  double vv[RM];
+#pragma unroll
+  for (int c = 0; c < RM; ++c) vv[c] = c < r ? ctx_v[c] : 0.0;
+
+  const int64_t ntiles = (m + TR - 1) / TR;
+  const size_t stage_elems = (size_t)TR * p;
+  auto issue = [&](int64_t t, int b) {        // async copy of tile t into stage b
+    const int64_t r0 = t * TR;
+    const int64_t nr = min((int64_t)TR, m - r0);
+    const char* src = reinterpret_cast<const char*>(X + r0 * p);
+    char* dst = reinterpret_cast<char*>(stage0 + (size_t)b * stage_elems);
+    const int64_t bytes = nr * p * (int64_t)sizeof(T);
+    for (int64_t o = (int64_t)tid * 16; o < bytes; o += (int64_t)blockDim.x * 16) {
+      const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + o);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(saddr), "l"(src + o));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  bool bad = false;
+  int64_t t = blockIdx.x;
+  if (t < ntiles) issue(t, 0);
+  __syncthreads();
+  for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
+    const int64_t tn = t + gridDim.x;
+    if (tn < ntiles) {
+      issue(tn, b ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const int64_t r0 = t * TR;
+    const int nr = (int)min((int64_t)TR, m - r0);
+    constexpr int RH = RM / 2;                    // outputs per thread
+    const int half = tid & 1;
+    for (int i = tid >> 1; i < nr; i += blockDim.x >> 1) {
+      const T* xr = stage0 + (size_t)b * stage_elems + (size_t)i * p;
+      double acc[RH];
+#pragma unroll
+      for (int c = 0; c < RH; ++c) acc[c] = 0.0;
+      double nrm = 0.0;
+      const double* mh = sM + half * RH;
+      constexpr int VW = 16 / sizeof(T);           // features per vector load
+      int a = 0;
+      for (; a + VW <= p; a += VW) {
+        double xv[VW];
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = *reinterpret_cast<const float4*>(xr + a);
+          xv[0] = f.x; xv[1] = f.y; xv[2] = f.z; xv[3] = f.w;
+        } else {
+          const double2 f = *reinterpret_cast<const double2*>(xr + a);
+          xv[0] = f.x; xv[1] = f.y;
+        }
+#pragma unroll
+        for (int u = 0; u < VW; ++u) {
+          bad |= !isfinite(xv[u]);
+          const double y = xv[u] - smu[a + u];
+          nrm = fma(y, y, nrm);
+          const double2* mr = reinterpret_cast<const double2*>(mh + (size_t)(a + u) * RM);
+#pragma unroll
+          for (int c = 0; c < RH / 2; ++c) {
+            const double2 mm = mr[c];
+            acc[2 * c] = fma(y, mm.x, acc[2 * c]);
+            acc[2 * c + 1] = fma(y, mm.y, acc[2 * c + 1]);
+          }
+        }
+      }
+      for (; a < p; ++a) {
+        const double raw = (double)xr[a];
+        bad |= !isfinite(raw);
+        const double y = raw - smu[a];
+        nrm = fma(y, y, nrm);
+#pragma unroll
+        for (int c = 0; c < RH; ++c) acc[c] = fma(y, mh[(size_t)a * RM + c], acc[c]);
+      }
+      double* o = out + (r0 + i) * r + half * RH;
+#pragma unroll
+      for (int c = 0; c < RH; ++c)
+        if (half * RH + c < r) o[c] = fma(-nrm, vv[half * RH + c], acc[c]);
+    }
+    __syncthreads();                              // stage b is refilled next-but-one
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+
 }  // namespace
 
 namespace mdsx {
@@ -251,10 +367,47 @@ int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, i
   return launched(h, "ctx_finalize_kernel", st);
 }
 
+int launch_gower_stream(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
+                        const double* mean, const double* M, const double* v, double* out,
+                        int32_t* nonfinite, cudaStream_t st) {
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  auto go = [&](auto tag, auto rm) {
+    using T = decltype(tag);
+    constexpr int RM = decltype(rm)::value;
+    auto kern = gower_stream_kernel<T, RM>;
+    const size_t fixed = ((size_t)p * RM + p) * sizeof(double);
+    int TR = 128;                                 // rows per stage: one per thread pair
+    while (TR > 8 && fixed + 2 * (size_t)TR * p * es > 110 * 1024) TR >>= 1;
+    const size_t smem = fixed + 2 * (size_t)TR * p * es;
+    if (smem > 222 * 1024) return -1;             // caller falls back to the per-row kernel
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t ntiles = (m + TR - 1) / TR;
+    const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)h->num_sms * 2);
+    mdsx::pre(h, st);
+    kern<<<blocks, 256, smem, st>>>((const T*)X, m, p, r, mean, M, v, out, nonfinite, TR);
+    return launched(h, "gower_stream_kernel", st);
+  };
+  using I4 = std::integral_constant<int, 4>;
+  using I8 = std::integral_constant<int, 8>;
+  using I12 = std::integral_constant<int, 12>;
+  using I16 = std::integral_constant<int, 16>;
+  if (dtype == MDSX_F32)
+    return r <= 4 ? go(float{}, I4{}) : r <= 8 ? go(float{}, I8{}) : r <= 12 ? go(float{}, I12{}) : go(float{}, I16{});
+  return r <= 4 ? go(double{}, I4{}) : r <= 8 ? go(double{}, I8{}) : r <= 12 ? go(double{}, I12{}) : go(double{}, I16{});
+}
+
+
 int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, int64_t m, int p,
                         int r, const double* mean, const double* M, const double* v, double* out,
                         int64_t ldo, int32_t* nonfinite, cudaStream_t st) {
   if (m == 0) return MDSX_OK;
+  // dense rows (ld == p), dense output, 16-byte aligned rows: cp.async streaming kernel
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  if (ld == p && ldo == r && r <= 16 && ((size_t)p * es) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    const int rc = launch_gower_stream(h, X, dtype, m, p, r, mean, M, v, out, nonfinite, st);
+    if (rc >= 0) return rc;                       // -1: shape does not fit the staged kernel
+  }
   auto go = [&](auto tag, auto rm) {
     using T = decltype(tag);
     constexpr int RM = decltype(rm)::value;
