@@ -18,10 +18,14 @@ separate flush is needed.  `e2e` repeats the measurement through the public
 API from pinned HOST memory: H2D of the input, the plan's index upload, the
 kernels, and the D2H of the n x r result and the fit figures, every step.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling — rank k embeds its
-own config-sized shard (rows are i.i.d. draws, each rank's shard is an
-independent partition set of the same size); no data-path collective; the
-timed region is bracketed by barriers and the max over ranks is reported.
+Multi-GPU (torchrun, one process per GPU): weak scaling.  D&C and
+interpolation run ONE global problem of N x the config's rows through
+paper_2007_11919_b200.distributed (input replicated on every GPU outside the
+timed region; each rank solves its contiguous share of subsets / rows; only
+per-subset sums and fit figures are exchanged — all-gathers over NCCL).  Fast
+MDS runs an independent config-sized problem per rank.  The timed region is
+bracketed by barriers and the max over ranks is reported; the n x r result
+stays sharded on the devices (gathering it is not part of the metric).
 
 --impl reference: the CPU oracle port of the reference algorithm (this repo's
 oracle/, a restatement of /root/reference's numpy path) on the host cores,
@@ -200,6 +204,33 @@ def make_plan(w: dict, seed: int):
     return plans.interpolation_sample(w["n"], w["l"], seed)
 
 
+class ShardedRun:
+    """bench adapter for distributed.sharded_* (N>1, weak scaling)."""
+
+    def __init__(self, w, x, plan, dev):
+        from paper_2007_11919_b200 import AlgorithmParams
+        from paper_2007_11919_b200 import distributed as dd
+        self.dd, self.w = dd, w
+        self.be = dd.GpuBackend(x)
+        self.comm = dd.Comm(device=dev)
+        self.plan = plan
+        self.prm = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=0)
+        self.res = None
+
+    def launch(self):
+        if self.w["algo"] == "divide":
+            self.res = self.dd.sharded_divide_and_conquer(self.be, self.w["n"], self.prm, self.comm,
+                                                          plan=self.plan)
+        else:
+            self.res = self.dd.sharded_interpolation(self.be, self.w["n"], self.prm, self.comm,
+                                                     sample=self.plan)
+
+    def finish(self, return_device=True):
+        from paper_2007_11919_b200 import MdsConfiguration
+        r = self.res
+        return MdsConfiguration(r.out, r.estimates, r.gof_g1, r.gof_g2)
+
+
 def make_run(w: dict, x, plan):
     from paper_2007_11919_b200 import DivideRun, FastRun, InterpolationRun
     if w["algo"] == "divide":
@@ -371,10 +402,19 @@ def run_ours(args, w):
     from paper_2007_11919_b200 import _device as D
 
     peaks = measured_peaks(dev)
-    seed = rank                       # each rank: an independent shard of the same size
+    sharded = ws > 1 and w["algo"] in ("divide", "interpolate")
+    if sharded:
+        # one global problem of ws x n rows, replicated input, same seed everywhere
+        w = dict(w, n=w["n"] * ws)
+        seed = 0
+    else:
+        seed = rank                   # fast MDS at N>1: an independent problem per rank
     x = make_data(w, dev, seed)
     plan = make_plan(w, seed)
-    run = make_run(w, x, plan)
+    if sharded:
+        run = ShardedRun(w, x, plan, dev)
+    else:
+        run = make_run(w, x, plan)
     h = D.handle(dev)
     log(f"[rank {rank}] data {tuple(x.shape)} {x.dtype}; warmup {args.warmup}")
     for _ in range(args.warmup):
@@ -410,11 +450,11 @@ def run_ours(args, w):
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         ms = float(tm.item())
     cfg_out = run.finish(return_device=True)
-    value = w["n"] * ws / (ms / 1e3)
+    value = (w["n"] if sharded else w["n"] * ws) / (ms / 1e3)
     try:       # Krylov dimension per piece (solver diagnostics in the status records)
         st = D.decode_status(run.status)
         krylov = [float(v) for v in st["value"]]
-    except Exception:
+    except AttributeError:
         krylov = None
 
     # roofline of the dominant kernel (average launch duration over the timed region)
@@ -461,8 +501,34 @@ def run_ours(args, w):
                                  "frac_fp64": wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]}
 
     # e2e through the public API from pinned host memory
+    if sharded:                 # per-rank kernel times cover 1/ws of the plan: no roofline
+        roof, per_kernel = None, {}
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and sharded:
+        # public distributed API from pinned host memory: H2D of the (replicated)
+        # input on every rank, the sharded run, and the gather of n x r to rank 0
+        host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        host.copy_(x)
+        k_e2e = max(1, min(args.steps, 3))
+        from paper_2007_11919_b200 import distributed as dd
+        dist.barrier()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(k_e2e):
+            x.copy_(host, non_blocking=True)
+            run.launch()
+            dd.gather_points(run.res, w["n"], w["r"], run.comm)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t) / k_e2e
+        tm = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        e2e_s = float(tm.item())
+        e2e = {"value": w["n"] / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": int(x.numel() * x.element_size() * ws),
+               "d2h_bytes_per_step": int(w["n"] * w["r"] * 8), "steps": k_e2e,
+               "path": "paper_2007_11919_b200.distributed (pinned host input on every rank, "
+                       "gather to rank 0)"}
+    if not args.no_e2e and not sharded:
         host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         host.copy_(x)
         del run

@@ -159,6 +159,26 @@ int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld,
                         int32_t npieces, int32_t c, int32_t r, double* out,
                         double* estimates, double* gof, mdsx_piece_status* status,
                         void* stream);
+/* mdsx_divide_conquer with flags: MDSX_NO_RECENTER leaves the column means in
+ * place (a sharded run re-centres with globally reduced sums).  The anchor is
+ * piece 0 of the given (sub-)plan. */
+#define MDSX_NO_RECENTER 1
+int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                           int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                           int32_t npieces, int32_t c, int32_t r, double* out,
+                           double* estimates, double* gof, mdsx_piece_status* status,
+                           int32_t flags, void* stream);
+/* Column sums of points[idx[seg_off[j] .. seg_off[j+1])] per segment j
+ * (sums: nseg x r, device; seg_off: device).  Fixed-order reductions, so a
+ * sharded run that sums the same segments in the same order is independent
+ * of the number of ranks. */
+int mdsx_segment_colsums(mdsx_handle* h, const double* points, const int64_t* idx,
+                         const int64_t* seg_off, int32_t nseg, int32_t r, double* sums,
+                         void* stream);
+/* points[idx[i]] -= shift (r doubles, device), i < n. */
+int mdsx_shift_rows(mdsx_handle* h, double* points, const int64_t* idx, int64_t n, int32_t r,
+                    const double* shift, void* stream);
+
 /* interpolation_mds with an explicit landmark sample (sample_idx, device, l).
  * out (n x r) in original row order, re-centred; estimates (r), gof (2),
  * status (1) describe the landmark MDS; cond (1) the covariance condition;

@@ -56,6 +56,10 @@ SIGNATURES = {
     "mdsx_recenter": (_int, [_vp, _vp, _i64, _i32, _vp]),
     "mdsx_divide_conquer": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
                                    _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_divide_conquer_ex": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
+                                      _vp, _vp, _vp, _vp, _i32, _vp]),
+    "mdsx_segment_colsums": (_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "mdsx_shift_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp]),
 }

@@ -115,11 +115,13 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
   __syncthreads();
   if (tid == 0) {
     // cyclic Jacobi for the r x r eigenvalues (condition estimate, algorithms.py:209-216)
+    double fro = 0.0;
+    for (int e = 0; e < r * r; ++e) fro += E[e] * E[e];
     for (int sweep = 0; sweep < 60; ++sweep) {
       double off = 0.0;
       for (int i = 0; i < r; ++i)
         for (int j = i + 1; j < r; ++j) off += E[i * r + j] * E[i * r + j];
-      if (off == 0.0) break;
+      if (off <= 1e-32 * fro) break;             // off-diagonal at round-off level
       for (int pp = 0; pp < r - 1; ++pp)
         for (int qq = pp + 1; qq < r; ++qq) {
           const double apq = E[pp * r + qq];

@@ -264,9 +264,50 @@ subtract_mean_kernel(double* __restrict__ X, int64_t n, int r, const double* __r
     X[e] -= mean[e % r];
 }
 
+// per-segment column sums over listed rows (segment j = rows idx[off_j .. off_j+1)),
+// one warp per (segment, column), fixed order -> deterministic, world-size independent
+__global__ void seg_colsum_kernel(const double* __restrict__ X, const int64_t* __restrict__ idx,
+                                  const int64_t* __restrict__ off, int nseg, int r,
+                                  double* __restrict__ sums) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nseg * r) return;
+  const int seg = warp / r, c = warp % r;
+  double s = 0.0;
+  for (int64_t i = off[seg] + lane; i < off[seg + 1]; i += 32) s += X[idx[i] * r + c];
+  s = mdsx::warp_sum(s);
+  if (lane == 0) sums[(int64_t)seg * r + c] = s;
+}
+
+__global__ void shift_rows_kernel(double* __restrict__ X, const int64_t* __restrict__ idx, int64_t n,
+                                  int r, const double* __restrict__ shift) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * r) return;
+  const int64_t i = e / r;
+  const int c = (int)(e - i * r);
+  X[idx[i] * r + c] -= shift[c];
+}
+
 }  // namespace
 
 namespace mdsx {
+
+int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const int64_t* off,
+                      int nseg, int r, double* sums, cudaStream_t st) {
+  if (nseg == 0) return MDSX_OK;
+  const int64_t threads = (int64_t)nseg * r * 32;
+  mdsx::pre(h, st);
+  seg_colsum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(X, idx, off, nseg, r, sums);
+  return launched(h, "seg_colsum_kernel", st);
+}
+
+int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, int r,
+                      const double* shift, cudaStream_t st) {
+  if (n == 0) return MDSX_OK;
+  mdsx::pre(h, st);
+  shift_rows_kernel<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(X, idx, n, r, shift);
+  return launched(h, "shift_rows_kernel", st);
+}
+
 
 int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
                           const double* src, const int64_t* src_rows, const int64_t* job_off_dev,

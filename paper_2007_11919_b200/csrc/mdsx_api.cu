@@ -19,6 +19,10 @@ int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, co
                      const double* trans, double* out, cudaStream_t st);
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st);
+int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const int64_t* off,
+                      int nseg, int r, double* sums, cudaStream_t st);
+int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, int r,
+                      const double* shift, cudaStream_t st);
 size_t recenter_ws_bytes(int r);
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st);
 int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
@@ -524,10 +528,31 @@ int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* st
   return launch_recenter(h, points, n, r, part, st);
 }
 
+int mdsx_segment_colsums(mdsx_handle* h, const double* points, const int64_t* idx,
+                         const int64_t* seg_off, int32_t nseg, int32_t r, double* sums,
+                         void* stream) {
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  return launch_seg_colsum(h, points, idx, seg_off, nseg, r, sums, as_stream(stream));
+}
+
+int mdsx_shift_rows(mdsx_handle* h, double* points, const int64_t* idx, int64_t n, int32_t r,
+                    const double* shift, void* stream) {
+  if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
+  return launch_shift_rows(h, points, idx, n, r, shift, as_stream(stream));
+}
+
 int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
                         int32_t p, const int64_t* row_idx, const int64_t* piece_off,
                         int32_t npieces, int32_t c, int32_t r, double* out, double* estimates,
                         double* gof, mdsx_piece_status* status, void* stream) {
+  return mdsx_divide_conquer_ex(h, data, dtype, ld, n, p, row_idx, piece_off, npieces, c, r, out,
+                                estimates, gof, status, 0, stream);
+}
+
+int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                           int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                           int32_t npieces, int32_t c, int32_t r, double* out, double* estimates,
+                           double* gof, mdsx_piece_status* status, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
   ClassicalPlan cp;
   int rc = plan_classical(h, p, piece_off, npieces, r, cp);
@@ -586,6 +611,7 @@ int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld,
   }
   if ((rc = launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st)))
     return rc;
+  if (flags & MDSX_NO_RECENTER) return MDSX_OK;
   double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
   return launch_recenter(h, out, n, r, part, st);
 }
