@@ -185,8 +185,8 @@ def make_data(w: dict, dev, seed: int):
     import torch
     n, p = w["n"], w["p"]
     if w["data"] == "image":
-        from paper_2007_11919_b200.synthetic import image_like
-        return torch.from_numpy(image_like(n, seed=seed)).to(dev)
+        from paper_2007_11919_b200.synthetic import image_like_device
+        return image_like_device(n, seed=seed, device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     dt = torch.float32 if w["dtype"] == "f32" else torch.float64

@@ -88,3 +88,14 @@ def status_tensor(n: int, dev: torch.device) -> torch.Tensor:
 def decode_status(t: torch.Tensor) -> np.ndarray:
     raw = t.detach().cpu().numpy().view(np.uint8).reshape(-1, 16)
     return raw.copy().view(STATUS_DTYPE).reshape(-1)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """D2H through page-locked memory (torch's caching host allocator): pageable
+    copies of large results run at a few GB/s on the B200 hosts, pinned at
+    PCIe speed.  The returned array owns its pinned block until collected."""
+    if not t.is_cuda:
+        return t.numpy()
+    pin = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    pin.copy_(t)
+    return pin.numpy()

@@ -30,7 +30,7 @@ from .results import MdsConfiguration
 
 
 def _finish_points(points: torch.Tensor, return_device: bool):
-    return points if return_device else points.cpu().numpy()
+    return points if return_device else D.to_host(points)
 
 
 # ====================================================================== D&C

@@ -177,7 +177,7 @@ def classical_mds_from_data(data, r: int, *, exact_guard: int = EXACT_SIZE_GUARD
     pts, est, gof, st = classical_pieces(x, idx, np.array([0, n], dtype=np.int64), r)
     raise_piece_status(D.decode_status(st)[0], r)
     g = gof.cpu().numpy()[0]
-    return MdsConfiguration(pts if return_device else pts.cpu().numpy(),
+    return MdsConfiguration(pts if return_device else D.to_host(pts),
                             est.cpu().numpy()[0], float(g[0]), float(g[1]))
 
 

@@ -80,3 +80,31 @@ def image_like(n: int, seed: int = 0, chunk: int = 65536) -> np.ndarray:
         vals = np.clip(vals, 0.0, 1.0) * sup
         out[start:start + m] = vals.reshape(m, -1).astype(np.float32)
     return out
+
+
+def image_like_device(n: int, seed: int = 0, device="cuda", chunk: int = 131072):
+    """Same distribution as `image_like` (same 47 prototypes), drawn on the GPU
+    with torch's generator — for benchmark-scale inputs only (parity tests use
+    the numpy stream above)."""
+    import torch
+
+    masks_np, templates_np = _prototypes(seed)
+    masks = torch.from_numpy(masks_np).to(device)
+    templates = torch.from_numpy(templates_np).to(device=device, dtype=torch.float32)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    beta = torch.distributions.Beta(torch.tensor(2.0, device=device), torch.tensor(2.0, device=device))
+    out = torch.empty((n, SIDE * SIDE), dtype=torch.float32, device=device)
+    for start in range(0, n, chunk):
+        m = min(chunk, n - start)
+        cls = torch.randint(0, N_CLASSES, (m,), generator=g, device=device)
+        sh = torch.randint(-1, 2, (m, 2), generator=g, device=device)
+        sup = masks[cls]
+        yy = (torch.arange(SIDE, device=device)[None, :, None] - sh[:, 0, None, None]) % SIDE
+        xx = (torch.arange(SIDE, device=device)[None, None, :] - sh[:, 1, None, None]) % SIDE
+        sup = sup[torch.arange(m, device=device)[:, None, None], yy, xx]
+        torch.manual_seed(seed * 1000003 + start)      # Beta sampler uses the global stream
+        vals = 0.5 * beta.sample((m, SIDE, SIDE)) + 0.5 * templates[cls] \
+            + 0.05 * torch.randn((m, SIDE, SIDE), generator=g, device=device)
+        out[start:start + m] = (vals.clamp_(0.0, 1.0) * sup).reshape(m, -1)
+    return out
