@@ -67,7 +67,15 @@ def to_device_matrix(data, dev: torch.device, name: str = "data") -> torch.Tenso
 
 
 def index_tensor(idx: np.ndarray, dev: torch.device) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64)).to(dev)
+    """Upload an int64 index array.  Large arrays go through page-locked
+    staging and an async copy (stream-ordered; torch's caching host allocator
+    keeps the staging block alive until the copy has completed)."""
+    a = np.ascontiguousarray(idx, dtype=np.int64)
+    if a.nbytes < (1 << 20):
+        return torch.from_numpy(a).to(dev)
+    pin = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
+    pin.numpy()[...] = a
+    return pin.to(dev, non_blocking=True)
 
 
 def empty(shape, dev: torch.device, dtype=torch.float64) -> torch.Tensor:

@@ -24,6 +24,7 @@ from . import _device as D
 from .errors import InvalidInputError, NumericalError, ParamError
 from .params import ALGORITHM_NAMES, AlgorithmParams
 from .plans import (DcPlan, FastPlan, InterpPlan, flatten_fast, flatten_subsets,
+                    flatten_subsets_cached,
                     interpolation_sample, plan_divide_conquer, plan_fast)
 from .primitives import classical_mds_from_data, raise_piece_status
 from .results import MdsConfiguration
@@ -40,7 +41,7 @@ class DivideRun:
     def __init__(self, x: torch.Tensor, plan: DcPlan, r: int, c: int):
         self.x, self.plan, self.r, self.c = x, plan, r, c
         self.dev = x.device
-        rows, off = flatten_subsets(plan.subsets)
+        rows, off = flatten_subsets_cached(plan)
         self.row_idx = D.index_tensor(rows, self.dev)
         self.piece_off = off
         n, npc = plan.n, plan.p
@@ -61,17 +62,18 @@ class DivideRun:
         st = D.decode_status(self.status)
         if np.any(st["code"] == 3):
             raise InvalidInputError("data contains non-finite values")
-        for j, rec in enumerate(st):                      # first failing subset in plan order
-            raise_piece_status(rec, self.r, f"subset {j + 1}")
+        bad = np.flatnonzero(st["code"] != 0)
+        if bad.size:                                      # first failing subset in plan order
+            raise_piece_status(st[bad[0]], self.r, f"subset {bad[0] + 1}")
         gof = self.gof.cpu().numpy()
         est = self.est.cpu().numpy()
         n, c = self.plan.n, self.c
-        sizes = np.array([len(q) for q in self.plan.subsets], dtype=np.float64)
+        sizes = np.diff(self.piece_off).astype(np.float64)
         weights = sizes.copy()
         weights[1:] -= c                                  # algorithms.py:158-166
         g1 = float(np.dot(weights, gof[:, 0]) / n)
         g2 = float(np.dot(weights, gof[:, 1]) / n)
-        per = np.stack([est[j] * (sizes[j] / weights[j]) for j in range(len(sizes))])
+        per = est * (sizes / weights)[:, None]
         return MdsConfiguration(_finish_points(self.out, return_device), per.mean(axis=0), g1, g2)
 
 

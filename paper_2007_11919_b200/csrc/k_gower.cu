@@ -16,6 +16,8 @@
 #include "mdsx_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 namespace {
 
@@ -117,11 +119,14 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
     // cyclic Jacobi for the r x r eigenvalues (condition estimate, algorithms.py:209-216)
     double fro = 0.0;
     for (int e = 0; e < r * r; ++e) fro += E[e] * E[e];
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    for (int sweep = 0; sweep < 40; ++sweep) {
       double off = 0.0;
       for (int i = 0; i < r; ++i)
         for (int j = i + 1; j < r; ++j) off += E[i * r + j] * E[i * r + j];
-      if (off <= 1e-32 * fro) break;             // off-diagonal at round-off level
+      // |offdiag|_F <= 1e-14 |S|_F: eigenvalues to 1e-14 |S|, far inside what
+      // the 1e12 condition test resolves (rotations leave ~eps|S| residues,
+      // so a tighter stop would only spin)
+      if (off <= 1e-28 * fro) break;
       for (int pp = 0; pp < r - 1; ++pp)
         for (int qq = pp + 1; qq < r; ++qq) {
           const double apq = E[pp * r + qq];
@@ -341,9 +346,375 @@ gower_stream_kernel(const T* __restrict__ X, int64_t m, int p, int r,
   if (bad) atomicOr(nonfinite, 1);
 }
 
+// ---- bulk-copy streaming Gower (dense rows, 16-byte aligned rows).
+//
+// Warp-specialised pipeline.  A tile of TR contiguous rows is one contiguous
+// byte range: a producer warp moves it global -> shared with one
+// cp.async.bulk (the TMA engine) completing on the stage's `full` mbarrier;
+// NSTAGE tiles are in flight.  Eight compute warps consume the ring; each warp
+// releases a stage on its `empty` mbarrier, so no CTA-wide barrier sits in the
+// steady state.  Compute: a group of TPR lanes owns R = 2 rows of the tile; lane
+// j of the group takes the 16-byte feature chunks j, j+TPR, ... of both rows, so
+// every per-feature record (M row, mean, mask) read from shared memory feeds 2
+// rows.  The records are stored chunk-interleaved so the TPR lanes of a group
+// read consecutive 16-byte words (conflict-free) and the groups of a warp
+// broadcast.  Epilogue: a butterfly reduce-scatter leaves lane j of a group the
+// full sums of output columns [j*KF, (j+1)*KF); it writes them and adds them to
+// its per-column running sums (fixed order -> per-CTA column partials for the
+// final re-centring).
+namespace bulk {
+__device__ __forceinline__ unsigned saddr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void load(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)),
+               "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* b, unsigned phase) {
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}\n" ::"r"(saddr(b)), "r"(phase) : "memory");
+}
+}  // namespace bulk
+
+constexpr int GB_THREADS = 256;                  // compute threads (8 warps)
+constexpr int GB_CTA = GB_THREADS + 32;          // + one producer warp
+constexpr int GB_MAX_STAGES = 4;
+// header: full[4], empty[4] mbarriers [0, 64), c0 [64, 192), v [192, 320)
+constexpr int GB_HEADER = 512;
+
+template <typename T, int RM, int TPR, int CPS>
+__global__ void __launch_bounds__(GB_CTA, CPS)
+gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
+                  const double* __restrict__ ctx_mean, const double* __restrict__ ctx_M,
+                  const double* __restrict__ ctx_v, double* __restrict__ out,
+                  double* __restrict__ colpart, int32_t* __restrict__ nonfinite, int nstage) {
+  constexpr int VW = 16 / sizeof(T);        // features per 16-byte chunk
+  constexpr int W = RM / 2 + 1;             // double2 per feature record: M pairs, (mean, mask)
+  constexpr int G = GB_THREADS / TPR;       // row groups
+  constexpr int R = 2;                      // rows per group
+  constexpr int TR = R * G;                 // rows per tile
+  constexpr int RMP = (RM + TPR - 1) / TPR * TPR;   // columns padded to the group width
+  constexpr int KF = RMP / TPR;             // columns owned per lane after the reduce-scatter
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+  uint64_t* empty = full + GB_MAX_STAGES;
+  double* c0s = reinterpret_cast<double*>(smraw + 64);    // xbar^T M
+  double* vvs = c0s + 16;                                   // v
+  const int nchunks = p / VW;
+  const int nit = (nchunks + TPR - 1) / TPR;
+  double2* rec = reinterpret_cast<double2*>(smraw + GB_HEADER);
+  T* stage0 = reinterpret_cast<T*>(smraw + GB_HEADER + (size_t)nit * VW * W * TPR * sizeof(double2));
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (m + TR - 1) / TR;
+  const size_t stage_elems = (size_t)TR * p;
+
+  if (tid == 0) {
+    for (int s = 0; s < nstage; ++s) {
+      bulk::bar_init(&full[s], 1);
+      bulk::bar_init(&empty[s], GB_THREADS / 32);
+    }
+    bulk::bar_fence();
+  }
+  __syncthreads();
+
+  if (tid >= GB_THREADS) {                  // ---- producer warp
+    if (tid == GB_THREADS) {
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int s = k % nstage;
+        if (k >= nstage) bulk::wait(&empty[s], (unsigned)((k / nstage - 1) & 1));
+        const int64_t nr = min((int64_t)TR, m - t * TR);
+        bulk::load(stage0 + (size_t)s * stage_elems, X + t * TR * p,
+                   (unsigned)(nr * p * sizeof(T)), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps: feature records, chunk-interleaved ((it*VW + u)*W + w)*TPR + jj
+  const int nrec = nit * VW * W * TPR;
+  for (int e = tid; e < nrec; e += GB_THREADS) {
+    const int jj = e % TPR, w = (e / TPR) % W, fu = e / (TPR * W);
+    const int it = fu / VW, u = fu % VW;
+    const int a = (jj + TPR * it) * VW + u;
+    double2 v2 = make_double2(0.0, 0.0);
+    if (a < p) {
+      if (w < RM / 2) {
+        const int c = 2 * w;
+        v2.x = c < r ? ctx_M[(int64_t)a * r + c] : 0.0;
+        v2.y = c + 1 < r ? ctx_M[(int64_t)a * r + c + 1] : 0.0;
+      } else {
+        v2.x = ctx_mean[a];
+        v2.y = 1.0;                          // feature mask
+      }
+    }
+    rec[e] = v2;
+  }
+  if (tid < 16) {                            // c0 = xbar^T M (fixed order), v
+    double sacc = 0.0;
+    if (tid < r)
+      for (int a = 0; a < p; ++a) sacc = fma(ctx_mean[a], ctx_M[(int64_t)a * r + tid], sacc);
+    c0s[tid] = sacc;
+    vvs[tid] = tid < r ? ctx_v[tid] : 0.0;
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"n"(GB_THREADS) : "memory");
+  const int j = tid % TPR, g = tid / TPR, lane = tid & 31;
+  double c0r[KF], vr[KF], csum[KF];
+#pragma unroll
+  for (int i = 0; i < KF; ++i) {
+    const int c = j * KF + i;
+    c0r[i] = c < 16 ? c0s[c] : 0.0;
+    vr[i] = c < 16 ? vvs[c] : 0.0;
+    csum[i] = 0.0;
+  }
+  bool bad = false;
+
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % nstage;
+    bulk::wait(&full[s], (unsigned)((k / nstage) & 1));
+    const T* xs = stage0 + (size_t)s * stage_elems;
+    const int64_t r0 = t * TR;
+    const int nr = (int)min((int64_t)TR, m - r0);
+    double acc[R][RMP], nrm[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      nrm[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < RMP; ++c) acc[q][c] = 0.0;
+    }
+    const T* x0 = xs + (size_t)g * p;
+    const T* x1 = xs + (size_t)(g + G) * p;
+    // branch-free, software-pipelined chunk loads: chunk indices past the row
+    // are clamped to a valid chunk whose record is all-zero with mask 0
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    V n0 = *reinterpret_cast<const V*>(x0 + min(j, nchunks - 1) * VW);
+    V n1 = *reinterpret_cast<const V*>(x1 + min(j, nchunks - 1) * VW);
+#pragma unroll 1
+    for (int it = 0; it < nit; ++it) {
+      const V c0v = n0, c1v = n1;
+      {
+        const int chn = min(j + TPR * (it + 1), nchunks - 1);
+        n0 = *reinterpret_cast<const V*>(x0 + chn * VW);
+        n1 = *reinterpret_cast<const V*>(x1 + chn * VW);
+      }
+      double xv[R][VW];
+      if constexpr (sizeof(T) == 4) {
+        xv[0][0] = c0v.x; xv[0][1] = c0v.y; xv[0][2] = c0v.z; xv[0][3] = c0v.w;
+        xv[1][0] = c1v.x; xv[1][1] = c1v.y; xv[1][2] = c1v.z; xv[1][3] = c1v.w;
+      } else {
+        xv[0][0] = c0v.x; xv[0][1] = c0v.y;
+        xv[1][0] = c1v.x; xv[1][1] = c1v.y;
+      }
+      const double2* rp = rec + (size_t)it * VW * W * TPR + j;
+#pragma unroll
+      for (int u = 0; u < VW; ++u) {
+        double2 mw[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) mw[w] = rp[(u * W + w) * TPR];
+        const double mu = mw[W - 1].x, msk = mw[W - 1].y;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          // linear term on the raw value (its centring is the constant c0);
+          // the squared norm on the centred value (fma(x, 1, -mu) == x - mu)
+          const double xq = xv[q][u];
+          const double y = fma(xq, msk, -mu);
+          nrm[q] = fma(y, y, nrm[q]);
+#pragma unroll
+          for (int w = 0; w < RM / 2; ++w) {
+            acc[q][2 * w] = fma(xq, mw[w].x, acc[q][2 * w]);
+            acc[q][2 * w + 1] = fma(xq, mw[w].y, acc[q][2 * w + 1]);
+          }
+        }
+      }
+    }
+    // the stage is no longer read (the non-finite rescan below re-reads only
+    // rows whose norm overflowed, before the release)
+    bool rescan = false;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+#pragma unroll
+      for (int o = TPR / 2; o > 0; o >>= 1) nrm[q] += __shfl_xor_sync(0xffffffffu, nrm[q], o);
+      rescan |= (g + q * G < nr) && !isfinite(nrm[q]);
+    }
+    if (rescan && j == 0)
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (g + q * G < nr && !isfinite(nrm[q])) {
+          // a squared norm can overflow on finite fp64 data: decide on the values
+          const T* xr = xs + (size_t)(g + q * G) * p;
+          for (int a = 0; a < p; ++a) bad |= !isfinite((double)xr[a]);
+        }
+    __syncwarp();
+    if (lane == 0) bulk::arrive(&empty[s]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      // butterfly reduce-scatter: lane j keeps columns [j*KF, (j+1)*KF)
+#pragma unroll
+      for (int o = TPR / 2, K = RMP / 2; o > 0; o >>= 1, K >>= 1) {
+        const bool up = (j & o) != 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const double send = up ? acc[q][i] : acc[q][i + K];
+          const double keep = up ? acc[q][i + K] : acc[q][i];
+          acc[q][i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      const int row = g + q * G;
+      if (row < nr) {
+        double* o = out + (r0 + row) * r + j * KF;
+#pragma unroll
+        for (int i = 0; i < KF; ++i)
+          if (j * KF + i < r) {
+            const double val = fma(-nrm[q], vr[i], acc[q][i] - c0r[i]);
+            o[i] = val;
+            csum[i] += val;
+          }
+      }
+    }
+  }
+  if (bad) atomicOr(nonfinite, 1);
+  if (colpart != nullptr) {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(GB_THREADS) : "memory");   // all tiles consumed
+    double* red = reinterpret_cast<double*>(stage0);
+#pragma unroll
+    for (int c = 0; c < RMP; ++c) red[c * GB_THREADS + tid] = (c / KF == j) ? csum[c % KF] : 0.0;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(GB_THREADS) : "memory");
+    if (tid < r) {
+      double sacc = 0.0;
+      for (int i = 0; i < GB_THREADS; ++i) sacc += red[tid * GB_THREADS + i];
+      colpart[(int64_t)blockIdx.x * r + tid] = sacc;
+    }
+  }
+}
+
+// Interpolation's landmark overwrite (algorithms.py:264-268) fused with the
+// correction of the column sums: out[idx[i]] = base[i]; corr = sum(base - old).
+__global__ void __launch_bounds__(256)
+landmark_overwrite_kernel(const double* __restrict__ base, const int64_t* __restrict__ idx,
+                          int64_t l, int r, double* __restrict__ out, double* __restrict__ corr) {
+  __shared__ double red[256];
+  double acc[MDSX_MAX_R];
+  for (int c = 0; c < r; ++c) acc[c] = 0.0;
+  for (int64_t i = threadIdx.x; i < l; i += 256) {
+    double* o = out + idx[i] * r;
+    for (int c = 0; c < r; ++c) {
+      const double b = base[i * r + c];
+      acc[c] += b - o[c];
+      o[c] = b;
+    }
+  }
+  for (int c = 0; c < r; ++c) {
+    red[threadIdx.x] = acc[c];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int i = 0; i < 256; ++i) s += red[i];
+      corr[c] = s;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 namespace mdsx {
+
+int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
+                              int r, double* out, double* corr, cudaStream_t st) {
+  mdsx::pre(h, st);
+  landmark_overwrite_kernel<<<1, 256, 0, st>>>(base, idx, l, r, out, corr);
+  return launched(h, "landmark_overwrite_kernel", st);
+}
+
+// Bulk-copy Gower over m dense rows.  *nparts = number of column-sum partials
+// written to colpart (one per CTA; 0 when colpart is null or the shape does
+// not fit, in which case nothing is launched).
+int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
+                      const double* mean, const double* M, const double* v, double* out,
+                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st) {
+  *nparts = 0;
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  const int VW = (int)(16 / es);
+  const int RM = r <= 4 ? 4 : r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : 16;
+  const size_t cap = (size_t)(h->max_smem_optin > 0 ? h->max_smem_optin : 227 * 1024);
+  const size_t sm_total = 228 * 1024;               // shared memory per SM
+  const char* e_tpr = getenv("MDSX_GB_TPR");
+  const char* e_cps = getenv("MDSX_GB_CPS");
+  const int force_tpr = e_tpr ? atoi(e_tpr) : 0;
+  const int force_cps = e_cps ? atoi(e_cps) : 0;
+  int TPR = 0, nstage = 0, CPS = 0;
+  size_t smem = 0;
+  // one CTA (8 compute warps + producer) per SM; TPR as small as the stage allows
+  for (int cps = 1; cps >= 1 && !TPR; --cps) {
+    if (force_cps && cps != force_cps) continue;
+    for (int tpr = 2; tpr <= 32 && !TPR; tpr *= 2) {
+      if (force_tpr && tpr != force_tpr) continue;
+      const int TR = 2 * GB_THREADS / tpr;
+      const int nit = (p / VW + tpr - 1) / tpr;
+      const size_t recb = (size_t)nit * VW * (RM / 2 + 1) * tpr * 16;
+      const size_t stage = (size_t)TR * p * es;
+      const size_t red = (size_t)((RM + tpr - 1) / tpr * tpr) * GB_THREADS * 8;
+      for (int ns = GB_MAX_STAGES; ns >= 2; --ns) {
+        const size_t need = GB_HEADER + recb + std::max(ns * stage, red);
+        if (stage <= 112 * 1024 && need <= cap && cps * (need + 1024) <= sm_total) {
+          TPR = tpr; nstage = ns; smem = need; CPS = cps;
+          break;
+        }
+      }
+    }
+  }
+  if (!TPR || m == 0) return MDSX_OK;
+  auto go = [&](auto tag, auto rm, auto tpr) -> int {
+    using T = decltype(tag);
+    constexpr int RMc = decltype(rm)::value;
+    constexpr int TPRc = decltype(tpr)::value;
+    auto kern = gower_bulk_kernel<T, RMc, TPRc, 1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t TR = 2 * GB_THREADS / TPRc;
+    const int64_t ntiles = (m + TR - 1) / TR;
+    const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)h->num_sms * CPS);
+    mdsx::pre(h, st);
+    kern<<<blocks, GB_CTA, smem, st>>>((const T*)X, m, p, r, mean, M, v, out, colpart,
+                                           nonfinite, nstage);
+    const int rc = launched(h, "gower_bulk_kernel", st);
+    if (!rc) *nparts = colpart ? blocks : -1;
+    return rc;
+  };
+  auto by_tpr = [&](auto tag, auto rm) -> int {
+    switch (TPR) {
+      case 2: return go(tag, rm, std::integral_constant<int, 2>{});
+      case 4: return go(tag, rm, std::integral_constant<int, 4>{});
+      case 8: return go(tag, rm, std::integral_constant<int, 8>{});
+      case 16: return go(tag, rm, std::integral_constant<int, 16>{});
+      default: return go(tag, rm, std::integral_constant<int, 32>{});
+    }
+  };
+  auto by_rm = [&](auto tag) -> int {
+    switch (RM) {
+      case 4: return by_tpr(tag, std::integral_constant<int, 4>{});
+      case 8: return by_tpr(tag, std::integral_constant<int, 8>{});
+      case 10: return by_tpr(tag, std::integral_constant<int, 10>{});
+      case 12: return by_tpr(tag, std::integral_constant<int, 12>{});
+      default: return by_tpr(tag, std::integral_constant<int, 16>{});
+    }
+  };
+  return dtype == MDSX_F32 ? by_rm(float{}) : by_rm(double{});
+}
 
 int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
                          const int64_t* idx, int64_t l, const double* X1, int r, double* mean,
@@ -407,7 +778,11 @@ int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, in
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
   if (ld == p && ldo == r && r <= 16 && ((size_t)p * es) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
-    const int rc = launch_gower_stream(h, X, dtype, m, p, r, mean, M, v, out, nonfinite, st);
+    int launched_parts = 0;
+    int rc = launch_gower_bulk(h, X, dtype, m, p, r, mean, M, v, out, nullptr, nonfinite,
+                               &launched_parts, st);
+    if (rc || launched_parts) return rc;
+    rc = launch_gower_stream(h, X, dtype, m, p, r, mean, M, v, out, nonfinite, st);
     if (rc >= 0) return rc;                       // -1: shape does not fit the staged kernel
   }
   auto go = [&](auto tag, auto rm) {

@@ -11,6 +11,8 @@
 // mirrored to the upper -> exactly symmetric; fixed reduction order.
 #include "mdsx_common.cuh"
 
+#include <type_traits>
+
 namespace {
 
 constexpr int TT = 64;          // output tile (features x features)
@@ -152,9 +154,216 @@ gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __re
   }
 }
 
+
+// ---- one CTA per piece for k <= 104 (the config 2/3 shape).  The lower
+// triangle of the k x k Gram in 8x8 blocks (NB*(NB+1)/2 block pairs) is split
+// over the 4 warps; each warp runs all rows, so no cross-warp reduction.  Rows
+// are gathered 64 at a time with cp.async into a double-buffered stage whose
+// pitch P makes the m8n8k4 fragment loads bank-conflict free; one fragment
+// per 8-feature block and k4-step serves both the A (rows) and B (columns)
+// operand of every block pair that touches it.  Shift x0 = first row; column
+// sums (for C = sum y y^T - s s^T / m) by warp 0; mu = x0 + s/m published.
+constexpr int GP_THREADS = 128;
+constexpr int GP_KC = 64;
+
+__host__ __device__ constexpr int pair_i(int t) {
+  int i = 0;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  return i;
+}
+__host__ __device__ constexpr int pair_j(int t) { return t - pair_i(t) * (pair_i(t) + 1) / 2; }
+
+template <int NB, int Q>
+struct GpQuarter {
+  static constexpr int NP = NB * (NB + 1) / 2;
+  static constexpr int QS = (NP + 3) / 4;               // pairs per warp (max)
+  static constexpr int LO = Q * QS;
+  static constexpr int CNT = (NP - LO) < QS ? (NP - LO) : QS;
+};
+
+template <typename T, int NB, int Q>
+__device__ __forceinline__ void gp_chunk(const T* __restrict__ stg, int P, int nk4, int rows_left,
+                                         const double* x0r, unsigned fmask, int gid, int tig,
+                                         double (*acc)[2], double* colsum) {
+  using QQ = GpQuarter<NB, Q>;
+#pragma unroll 2
+  for (int k4 = 0; k4 < nk4; ++k4) {
+    const int row = 4 * k4 + tig;
+    const bool rok = row < rows_left;
+    const T* src = stg + (size_t)row * P + gid;
+    double f[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const bool fok = (fmask >> b) & 1u;           // feature < k (inside the staged row)
+      const double v = fok ? (double)src[8 * b] : 0.0;
+      f[b] = (rok && fok) ? v - x0r[b] : 0.0;
+    }
+    if constexpr (Q == 0) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) colsum[b] += f[b];
+    }
+#pragma unroll
+    for (int u = 0; u < QQ::CNT; ++u) {
+      const int t = QQ::LO + u;
+      dmma(acc[u][0], acc[u][1], f[pair_i(t)], f[pair_j(t)]);
+    }
+  }
+}
+
+template <typename T, int NB, int Q>
+__device__ __forceinline__ void gp_store(double (*acc)[2], const double* s, double inv_m, int k,
+                                         int gid, int tig, double* out) {
+  using QQ = GpQuarter<NB, Q>;
+#pragma unroll
+  for (int u = 0; u < QQ::CNT; ++u) {
+    const int t = QQ::LO + u;
+    const int bi = pair_i(t), bj = pair_j(t);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int gi = 8 * bi + gid, gj = 8 * bj + 2 * tig + v;
+      if (gi < k && gj < k && gi >= gj) {
+        const double c = fma(-s[gi] * inv_m, s[gj], acc[u][v]);
+        out[(int64_t)gi * k + gj] = c;
+        out[(int64_t)gj * k + gi] = c;
+      }
+    }
+  }
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(GP_THREADS, 2)
+gram_piece_kernel(const T* __restrict__ X, int64_t ld, int p, int P,
+                  const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
+                  double* __restrict__ A, double* __restrict__ mu_all,
+                  mdsx_piece_status* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char gp_smem[];
+  T* stage = reinterpret_cast<T*>(gp_smem);               // 2 x GP_KC x P
+  __shared__ double x0s[8 * NB], ssum[8 * NB];
+  __shared__ int bad;
+  const PieceDesc d = pd[blockIdx.x];
+  const int k = d.k, m = d.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int64_t* ridx = row_idx + d.row_off;
+  const int pieces16 = (int)((size_t)p * sizeof(T) / 16);
+  const size_t stage_elems = (size_t)GP_KC * P;
+  auto issue = [&](int c, int buf) {
+    const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
+    T* dst0 = stage + (size_t)buf * stage_elems;
+    for (int rr = warp; rr < nr; rr += GP_THREADS / 32) {
+      const char* src = reinterpret_cast<const char*>(X + ridx[r0 + rr] * ld);
+      char* dst = reinterpret_cast<char*>(dst0 + (size_t)rr * P);
+      for (int q = lane; q < pieces16; q += 32) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 16 * q);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * q));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int nchunks = (m + GP_KC - 1) / GP_KC;
+  issue(0, 0);
+  if (tid < 8 * NB) x0s[tid] = tid < k ? (double)X[ridx[0] * ld + tid] : 0.0;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  double x0r[NB];
+  unsigned fmask = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    x0r[b] = x0s[8 * b + gid];
+    fmask |= (8 * b + gid < k ? 1u : 0u) << b;
+  }
+  constexpr int QS = GpQuarter<NB, 0>::QS;
+  double acc[QS][2];
+#pragma unroll
+  for (int u = 0; u < QS; ++u) acc[u][0] = acc[u][1] = 0.0;
+  double colsum[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) colsum[b] = 0.0;
+
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      issue(c + 1, (c + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const T* stg = stage + (size_t)(c & 1) * stage_elems;
+    const int rows_left = m - c * GP_KC;
+    const int nk4 = (min(GP_KC, rows_left) + 3) / 4;
+    switch (warp) {
+      case 0: gp_chunk<T, NB, 0>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
+      case 1: gp_chunk<T, NB, 1>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
+      case 2: gp_chunk<T, NB, 2>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
+      default: gp_chunk<T, NB, 3>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
+    }
+    __syncthreads();                               // the buffer is refilled next iteration
+  }
+  if (warp == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double sv = colsum[b];
+      sv += __shfl_xor_sync(0xffffffffu, sv, 1);
+      sv += __shfl_xor_sync(0xffffffffu, sv, 2);
+      if (tig == 0) ssum[8 * b + gid] = sv;
+      if (tig == 0 && 8 * b + gid < k && !isfinite(sv)) bad = 1;
+    }
+  }
+  __syncthreads();
+  const double inv_m = 1.0 / (double)m;
+  double* out = A + d.a_off;
+  switch (warp) {
+    case 0: gp_store<T, NB, 0>(acc, ssum, inv_m, k, gid, tig, out); break;
+    case 1: gp_store<T, NB, 1>(acc, ssum, inv_m, k, gid, tig, out); break;
+    case 2: gp_store<T, NB, 2>(acc, ssum, inv_m, k, gid, tig, out); break;
+    default: gp_store<T, NB, 3>(acc, ssum, inv_m, k, gid, tig, out); break;
+  }
+  if (tid < k) mu_all[(int64_t)d.id * p + tid] = x0s[tid] + ssum[tid] * inv_m;
+  if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
+}
+
 }  // namespace
 
 namespace mdsx {
+
+// Pitch (elements) of a staged row: >= p, 16-byte multiple, and congruent so
+// that the 32 lanes of an m8n8k4 fragment load hit distinct banks.
+static int gp_pitch(int p, size_t es) {
+  int P = p;
+  if (es == 8) { while (P % 16 != 4) ++P; }
+  else { while (P % 32 != 8) ++P; }
+  return P;
+}
+
+bool gram_piece_ok(const void* data, int dtype, int64_t ld, int p) {
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  return p <= 104 && ((size_t)p * es) % 16 == 0 && ((size_t)ld * es) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(data) & 15) == 0;
+}
+
+int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                      const int64_t* row_idx, const PieceDesc* pd, int npieces, double* A,
+                      double* mu, mdsx_piece_status* status, cudaStream_t st) {
+  if (npieces == 0) return MDSX_OK;
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  const int P = gp_pitch(p, es);
+  const size_t smem = 2 * (size_t)GP_KC * P * es;
+  auto go = [&](auto tag, auto nb) {
+    using T = decltype(tag);
+    constexpr int NB = decltype(nb)::value;
+    auto kern = gram_piece_kernel<T, NB>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mdsx::pre(h, st);
+    kern<<<npieces, GP_THREADS, smem, st>>>((const T*)data, ld, p, P, row_idx, pd, A, mu, status);
+    return launched(h, "gram_piece_kernel", st);
+  };
+  using N4 = std::integral_constant<int, 4>;
+  using N8 = std::integral_constant<int, 8>;
+  using N13 = std::integral_constant<int, 13>;
+  if (dtype == MDSX_F64)
+    return p <= 32 ? go(double{}, N4{}) : p <= 64 ? go(double{}, N8{}) : go(double{}, N13{});
+  return p <= 32 ? go(float{}, N4{}) : p <= 64 ? go(float{}, N8{}) : go(float{}, N13{});
+}
 
 int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                      const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,

@@ -149,6 +149,15 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   const int kq = k | 1;                        // odd leading dim of Q (conflict-free columns)
   const int tid = threadIdx.x;
   const double* Ag = Aall + d.a_off;
+  if (status[pid].code == MDSX_INVALID_INPUT) {   // non-finite rows: nothing to solve
+    for (int e = tid; e < k * r; e += LT) Uout[d.u_off + e] = 0.0;
+    if (tid < r) {
+      estimates[(int64_t)pid * r + tid] = 0.0;
+      lam_out[(int64_t)pid * r + tid] = 0.0;
+    }
+    if (tid < 2) gof[2 * (int64_t)pid + tid] = 0.0;
+    return;
+  }
   double* A = sm;                              // packed upper: row i = A[i][i..k)
   double* Q = A + (size_t)k * (k + 1) / 2;     // column j at Q + j*kq, j < QMAX
   double* S = Q + (size_t)QMAX * kq;           // Ritz coefficients, S[c*RMAX + i]

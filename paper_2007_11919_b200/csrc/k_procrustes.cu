@@ -248,20 +248,39 @@ colsum_partial_kernel(const double* __restrict__ X, int64_t n, int r, double* __
   }
 }
 
+// X -= (sum_b part[b] + corr) / n, elementwise over the n x r block; four
+// independent loads in flight per thread, the column tracked incrementally
+// (no 64-bit modulo per element).
 __global__ void __launch_bounds__(256)
 subtract_mean_kernel(double* __restrict__ X, int64_t n, int r, const double* __restrict__ part,
-                     int nparts) {
+                     int nparts, const double* __restrict__ corr) {
   __shared__ double mean[MDSX_MAX_R];
   if (threadIdx.x < r) {
     double s = 0.0;
     for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * r + threadIdx.x];
+    if (corr) s += corr[threadIdx.x];
     mean[threadIdx.x] = s / (double)n;
   }
   __syncthreads();
   const int64_t total = n * r;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x)
-    X[e] -= mean[e % r];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int cs = (int)(stride % r);
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int c = (int)(e % r);
+  auto adv = [&](int c0) { c0 += cs; return c0 >= r ? c0 - r : c0; };
+  for (; e + 3 * stride < total; e += 4 * stride) {
+    const int c1 = adv(c), c2 = adv(c1), c3 = adv(c2);
+    const double x0 = X[e], x1 = X[e + stride], x2 = X[e + 2 * stride], x3 = X[e + 3 * stride];
+    X[e] = x0 - mean[c];
+    X[e + stride] = x1 - mean[c1];
+    X[e + 2 * stride] = x2 - mean[c2];
+    X[e + 3 * stride] = x3 - mean[c3];
+    c = adv(c3);
+  }
+  for (; e < total; e += stride) {
+    X[e] -= mean[c];
+    c = adv(c);
+  }
 }
 
 // per-segment column sums over listed rows (segment j = rows idx[off_j .. off_j+1)),
@@ -360,6 +379,9 @@ int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_
 
 size_t recenter_ws_bytes(int r) { return (size_t)RC_BLOCKS * r * sizeof(double); }
 
+int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
+                         int nparts, const double* corr, cudaStream_t st);
+
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st) {
   if (n == 0) return MDSX_OK;
   if (r <= 4) { mdsx::pre(h, st); colsum_partial_kernel<4><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
@@ -368,10 +390,16 @@ int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, c
   else { mdsx::pre(h, st); colsum_partial_kernel<32><<<RC_BLOCKS, 256, 0, st>>>(X, n, r, part); }
   int rc = launched(h, "colsum_partial_kernel", st);
   if (rc) return rc;
+  return launch_subtract_mean(h, X, n, r, part, RC_BLOCKS, nullptr, st);
+}
+
+int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
+                         int nparts, const double* corr, cudaStream_t st) {
+  if (n == 0) return MDSX_OK;
   const int64_t total = n * r;
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)h->num_sms * 8);
+  int blocks = (int)std::min<int64_t>((total + 1023) / 1024, (int64_t)h->num_sms * 8);
   mdsx::pre(h, st);
-  subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, RC_BLOCKS);
+  subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, nparts, corr);
   return launched(h, "subtract_mean_kernel", st);
 }
 

@@ -25,6 +25,13 @@ int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, 
                       const double* shift, cudaStream_t st);
 size_t recenter_ws_bytes(int r);
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st);
+int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
+                         int nparts, const double* corr, cudaStream_t st);
+int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
+                              int r, double* out, double* corr, cudaStream_t st);
+int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
+                      const double* mean, const double* M, const double* v, double* out,
+                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st);
 int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
                          const int64_t* idx, int64_t l, const double* X1, int r, double* mean,
                          double* M, double* v, double* S, double* q, double* cond, int32_t* flag,
@@ -47,6 +54,10 @@ size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int full_basis, cudaStream_t st);
+bool gram_piece_ok(const void* data, int dtype, int64_t ld, int p);
+int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                      const int64_t* row_idx, const PieceDesc* pd, int npieces, double* A,
+                      double* mu, mdsx_piece_status* status, cudaStream_t st);
 int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                      const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
                      double* A, double* mu, mdsx_piece_status* status, cudaStream_t st);
@@ -165,7 +176,9 @@ struct ClassicalPlan {
   std::vector<PieceDesc> pd_f1;                    // form-1 pieces (separate means pass)
   std::vector<int4> tiles1;                        // form-1 Gram tiles (tiles: form 0, DMMA)
   int kmax_jac = 0, kmax_sub = 0;
-  std::vector<int4> tiles;
+  std::vector<int4> tiles;                         // form-0 tiles of pieces not in pd_g
+  std::vector<PieceDesc> pd_g;                     // form 0, k <= 104: one CTA per piece
+  std::vector<int4> tiles_g;                       // ... and their tiles (unaligned-data fallback)
   std::vector<int64_t> off;
   int kmax = 0;
   int64_t total = 0;
@@ -212,9 +225,11 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
     cp.max_m = std::max<int64_t>(cp.max_m, m);
     cp.pd[j] = d;
     const int T = (d.k + 63) / 64;
+    const bool small0 = d.form == 0 && d.k <= 104;
+    if (small0) cp.pd_g.push_back(d);
     for (int ti = 0; ti < T; ++ti)
       for (int tj = 0; tj <= ti; ++tj)
-        (d.form == 0 ? cp.tiles : cp.tiles1).push_back(make_int4(j, ti, tj, 0));
+        (d.form == 1 ? cp.tiles1 : small0 ? cp.tiles_g : cp.tiles).push_back(make_int4(j, ti, tj, 0));
     if (d.form == 1) cp.pd_f1.push_back(d);
   }
   cp.total = piece_off[npieces] - piece_off[0];
@@ -225,7 +240,8 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
 
 static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
   const size_t np = cp.pd.size();
-  return 5 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+  return 6 * align_up(np * sizeof(PieceDesc)) + align_up(cp.tiles.size() * sizeof(int4)) +
+         align_up(cp.tiles_g.size() * sizeof(int4)) +
          align_up(cp.tiles1.size() * sizeof(int4)) +
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
          align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double)) +
@@ -243,7 +259,11 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   PieceDesc* dpd_jac = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   PieceDesc* dpd_sub = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   PieceDesc* dpd_f1 = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
-  int4* dtiles = (int4*)ws_alloc(h, cp.tiles.size() * sizeof(int4), st);
+  PieceDesc* dpd_g = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
+  const bool piece_gram = gram_piece_ok(data, dtype, ld, p);
+  std::vector<int4> tiles0 = cp.tiles;
+  if (!piece_gram) tiles0.insert(tiles0.end(), cp.tiles_g.begin(), cp.tiles_g.end());
+  int4* dtiles = (int4*)ws_alloc(h, tiles0.size() * sizeof(int4), st);
   int4* dtiles1 = (int4*)ws_alloc(h, cp.tiles1.size() * sizeof(int4), st);
   double* mu = (double*)ws_alloc(h, (size_t)np * p * sizeof(double), st);
   double* A = (double*)ws_alloc(h, cp.a_doubles * sizeof(double), st);
@@ -254,20 +274,25 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
   const int64_t* ridx = row_idx;
   Stager sg(h, st);
-  int rc = sg.begin(5 * np * sizeof(PieceDesc) + (cp.tiles.size() + cp.tiles1.size()) * sizeof(int4) +
+  int rc = sg.begin(6 * np * sizeof(PieceDesc) + (tiles0.size() + cp.tiles1.size()) * sizeof(int4) +
                     4096);
   if (rc) return rc;
   if ((rc = sg.put(dpd, pd.data(), np * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd_jac, cp.pd_jac.data(), cp.pd_jac.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd_sub, cp.pd_sub.data(), cp.pd_sub.size() * sizeof(PieceDesc)))) return rc;
-  if ((rc = sg.put(dtiles, cp.tiles.data(), cp.tiles.size() * sizeof(int4)))) return rc;
+  if ((rc = sg.put(dtiles, tiles0.data(), tiles0.size() * sizeof(int4)))) return rc;
+  if (piece_gram && (rc = sg.put(dpd_g, cp.pd_g.data(), cp.pd_g.size() * sizeof(PieceDesc))))
+    return rc;
   if ((rc = sg.put(dpd_f1, cp.pd_f1.data(), cp.pd_f1.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dtiles1, cp.tiles1.data(), cp.tiles1.size() * sizeof(int4)))) return rc;
   if ((rc = sg.end())) return rc;
   if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, np * sizeof(mdsx_piece_status), st), "memset")))
     return rc;
   // form 0: DMMA Gram with fused shifted means;  form 1: means pass + row Gram
-  if ((rc = launch_gram_dmma(h, data, dtype, ld, p, ridx, dpd, dtiles, (int)cp.tiles.size(), A, mu,
+  if (piece_gram && (rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd_g, (int)cp.pd_g.size(),
+                                            A, mu, status, st)))
+    return rc;
+  if ((rc = launch_gram_dmma(h, data, dtype, ld, p, ridx, dpd, dtiles, (int)tiles0.size(), A, mu,
                              status, st)))
     return rc;
   if (!cp.pd_f1.empty()) {
@@ -479,7 +504,6 @@ int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t
                            int64_t ldo, int32_t* nonfinite, void* stream) {
   cudaStream_t st = as_stream(stream);
   int32_t* nf = nonfinite;
-  int rc;
   const double* mean = ctx;
   const double* M = mean + p;
   const double* v = M + (int64_t)p * r;
@@ -627,7 +651,8 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
   if (rc) return rc;
   const int64_t csz = mdsx_gower_context_size(l, p, r);
   const size_t need = classical_ws_bytes(cp, p, r) + align_up(l * r * sizeof(double)) +
-                      align_up(csz * sizeof(double)) + recenter_ws_bytes(r) + 1024;
+                      align_up(csz * sizeof(double)) + recenter_ws_bytes(r) +
+                      align_up(r * sizeof(double)) + 2048;
   if ((rc = ws_reserve(h, need))) return rc;
   double* base = (double*)ws_alloc(h, l * r * sizeof(double), st);
   if ((rc = run_classical(h, cp, data, dtype, ld, p, sample_idx, r, base, estimates, gof, status, st)))
@@ -646,10 +671,25 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
   if ((rc = launch_gower_context(h, data, dtype, ld, p, sample_idx, l, base, r, mean, M, v, S, q,
                                  cond, flag, st)))
     return rc;
+  // dense rows: bulk-copy stream with fused per-CTA column sums, landmark
+  // overwrite with a sum correction, one subtract pass (algorithms.py:264-274)
+  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r) + align_up(r * sizeof(double)), st);
+  double* corr = part + (size_t)recenter_ws_bytes(r) / sizeof(double);
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  if (ld == p && r <= 16 && ((size_t)p * es) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(data) & 15) == 0 && h->num_sms * r * sizeof(double) <= recenter_ws_bytes(r)) {
+    int nparts = 0;
+    if ((rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
+                                st)))
+      return rc;
+    if (nparts > 0) {
+      if ((rc = launch_landmark_overwrite(h, base, sample_idx, l, r, out, corr, st))) return rc;
+      return launch_subtract_mean(h, out, n, r, part, nparts, corr, st);
+    }
+  }
   if ((rc = launch_gower_affine(h, data, dtype, ld, n, p, r, mean, M, v, out, r, flag + 1, st)))
     return rc;
   if ((rc = launch_scatter(h, base, sample_idx, l, r, out, st))) return rc;
-  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
   if ((rc = launch_recenter(h, out, n, r, part, st))) return rc;
   return MDSX_OK;
 }

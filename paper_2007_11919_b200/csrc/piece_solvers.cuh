@@ -42,6 +42,16 @@ __device__ inline void full_jacobi_piece(const PieceDesc& d, int r, const double
   double* U = sm + kk * kk;
   const double* Ag = Aall + d.a_off;
 
+  if (status[pid].code == MDSX_INVALID_INPUT) {   // non-finite rows: nothing to solve
+    for (int e = tid; e < k * r; e += nt) Uout[d.u_off + e] = 0.0;
+    if (tid < r) {
+      estimates[(int64_t)pid * r + tid] = 0.0;
+      lam_out[(int64_t)pid * r + tid] = 0.0;
+    }
+    if (tid < 2) gof[2 * (int64_t)pid + tid] = 0.0;
+    return;
+  }
+
   double fro = 0.0;
   for (int e = tid; e < kk * kk; e += nt) {
     const int i = e / kk, j = e % kk;
@@ -82,6 +92,8 @@ __device__ inline void full_jacobi_piece(const PieceDesc& d, int r, const double
     __syncthreads();
   }
   const int triv = trivial;
+  for (int i = tid; i < k; i += nt) order[i] = i;   // valid indices even for NaN spectra
+  __syncthreads();
   if (tid < k && tid != triv) {
     const double lj = A[tid * kk + tid];
     int rank = 0;

@@ -13,6 +13,8 @@ from __future__ import annotations
 import json
 from dataclasses import dataclass, field
 
+import weakref
+
 import numpy as np
 
 from .errors import ParamError
@@ -275,6 +277,26 @@ def flatten_subsets(subsets) -> tuple[np.ndarray, np.ndarray]:
     off = np.zeros(len(subsets) + 1, dtype=np.int64)
     np.cumsum(sizes, out=off[1:])
     return np.concatenate(subsets).astype(np.int64, copy=False), off
+
+
+_FLAT_CACHE: dict = {}
+
+
+def flatten_subsets_cached(plan) -> tuple[np.ndarray, np.ndarray]:
+    """flatten_subsets(plan.subsets), memoised per plan object (a plan passed
+    explicitly to several calls is flattened once; plans are not mutated).
+    Keyed by identity; the entry is dropped when the plan is collected."""
+    key = id(plan)
+    hit = _FLAT_CACHE.get(key)
+    if hit is not None and hit[0]() is plan and hit[1] is plan.subsets:
+        return hit[2]
+    flat = flatten_subsets(plan.subsets)
+    try:
+        ref = weakref.ref(plan, lambda _r, k=key: _FLAT_CACHE.pop(k, None))
+    except TypeError:
+        return flat
+    _FLAT_CACHE[key] = (ref, plan.subsets, flat)
+    return flat
 
 
 @dataclass
