@@ -199,7 +199,8 @@ namespace mdsx {
 int lanczos_rmax();
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                        mdsx_piece_status* status, int full_basis, cudaStream_t st);
+                        mdsx_piece_status* status, int full_basis, int only_flagged,
+                       cudaStream_t st);
 void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t);
 
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -378,7 +379,7 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
     if ((rc = cuda_check(h, cudaMemsetAsync(sc_st, 0, n * sizeof(mdsx_piece_status), st), "memset")))
       return rc;
     if ((rc = launch_lanczos_smem(h, hpd, n, M, B, (const double*)h->ws, (double*)h->ws, theta,
-                                  sc_est, sc_gof, sc_st, 1, st)))
+                                  sc_est, sc_gof, sc_st, 1, 0, st)))
       return rc;
     if ((rc = launch_bgemm(h, dtasks, ditems, g7, st))) return rc;
     if ((rc = launch_bgemm(h, dtasks, ditems, g8, st))) return rc;

@@ -250,12 +250,22 @@ gram_piece_kernel(const T* __restrict__ X, int64_t ld, int p, int P,
   auto issue = [&](int c, int buf) {
     const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
     T* dst0 = stage + (size_t)buf * stage_elems;
-    for (int rr = warp; rr < nr; rr += GP_THREADS / 32) {
-      const char* src = reinterpret_cast<const char*>(X + ridx[r0 + rr] * ld);
-      char* dst = reinterpret_cast<char*>(dst0 + (size_t)rr * P);
-      for (int q = lane; q < pieces16; q += 32) {
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 16 * q);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * q));
+    // warp w copies rows w, w+4, ...: their indices are loaded in parallel
+    // (lane i holds row w + 4i) and broadcast, not chased one by one
+    constexpr int RPW = GP_KC / (GP_THREADS / 32);
+    const int myr = warp + (GP_THREADS / 32) * lane;
+    const int64_t myidx = (lane < RPW && myr < nr) ? ridx[r0 + myr] : 0;
+#pragma unroll 4
+    for (int i = 0; i < RPW; ++i) {
+      const int rr = warp + (GP_THREADS / 32) * i;
+      const int64_t gi = __shfl_sync(0xffffffffu, myidx, i);
+      if (rr < nr) {
+        const char* src = reinterpret_cast<const char*>(X + gi * ld);
+        char* dst = reinterpret_cast<char*>(dst0 + (size_t)rr * P);
+        for (int q = lane; q < pieces16; q += 32) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 16 * q);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * q));
+        }
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);

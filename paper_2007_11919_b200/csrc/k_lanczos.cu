@@ -45,17 +45,37 @@ __device__ __forceinline__ double hash_unit(uint64_t x) {
   return (double)(x >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
 }
 
-// number of eigenvalues of the m x m tridiagonal (al, be2 = beta^2) below x
-__device__ int sturm_below(const double* al, const double* be2, int m, double x, double pivmin) {
-  double q = al[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  int cnt = q < 0.0;
+// number of eigenvalues of the m x m tridiagonal (al, be2 = beta^2) below x:
+// sign changes of the leading-minor sequence p_i = det(T_i - x I),
+// p_i = (al_i - x) p_{i-1} - be2_{i-1} p_{i-2}  (division free; the pair is
+// rescaled when it leaves [1e-150, 1e150]; an exact zero counts as a change,
+// the limit of the LDL^T pivot rule).
+__device__ int sturm_below(const double* al, const double* be2, int m, double x) {
+  double pm = 1.0, pc = al[0] - x;
+  if (pc == 0.0) pc = -1e-300;
+  int cnt = pc < 0.0;
   for (int i = 1; i < m; ++i) {
-    q = (al[i] - x) - be2[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
+    double pn = fma(al[i] - x, pc, -be2[i - 1] * pm);
+    if (pn == 0.0) pn = pc < 0.0 ? 1e-300 : -1e-300;
+    cnt += (pn < 0.0) != (pc < 0.0);
+    pm = pc;
+    pc = pn;
+    const double ap = fabs(pc);
+    if (ap > 1e150) { pc *= 1e-150; pm *= 1e-150; }
+    else if (ap < 1e-150) { pc *= 1e150; pm *= 1e150; }
   }
   return cnt;
+}
+
+// 1/d to full double accuracy: single-precision seed + two Newton steps
+// (quadratic: 2^-23 -> 2^-92), exact division outside the float range.
+__device__ __forceinline__ double fast_rcp(double d) {
+  const double ad = fabs(d);
+  if (!(ad > 1e-30 && ad < 1e30)) return 1.0 / d;
+  double r = (double)__frcp_rn((float)d);
+  r = r * fma(-d, r, 2.0);
+  r = r * fma(-d, r, 2.0);
+  return r;
 }
 
 // Eigenvector of the m x m tridiagonal T (al, be) at its eigenvalue theta by a
@@ -69,13 +89,13 @@ __device__ void tri_twisted_vector(const double* al, const double* be, int m, do
   double t = al[0] - theta;
   d[0] = fabs(t) < pivmin ? -pivmin : t;
   for (int i = 1; i < m; ++i) {
-    t = (al[i] - theta) - be[i - 1] * be[i - 1] / d[i - 1];
+    t = (al[i] - theta) - be[i - 1] * be[i - 1] * fast_rcp(d[i - 1]);
     d[i] = fabs(t) < pivmin ? -pivmin : t;
   }
   t = al[m - 1] - theta;
   u[m - 1] = fabs(t) < pivmin ? -pivmin : t;
   for (int i = m - 2; i >= 0; --i) {
-    t = (al[i] - theta) - be[i] * be[i] / u[i + 1];
+    t = (al[i] - theta) - be[i] * be[i] * fast_rcp(u[i + 1]);
     u[i] = fabs(t) < pivmin ? -pivmin : t;
   }
   int kt = 0;
@@ -85,8 +105,8 @@ __device__ void tri_twisted_vector(const double* al, const double* be, int m, do
     if (g < best) { best = g; kt = i; }
   }
   z[kt] = 1.0;
-  for (int i = kt - 1; i >= 0; --i) z[i] = -(be[i] / d[i]) * z[i + 1];
-  for (int i = kt + 1; i < m; ++i) z[i] = -(be[i - 1] / u[i]) * z[i - 1];
+  for (int i = kt - 1; i >= 0; --i) z[i] = -(be[i] * fast_rcp(d[i])) * z[i + 1];
+  for (int i = kt + 1; i < m; ++i) z[i] = -(be[i - 1] * fast_rcp(u[i])) * z[i - 1];
   double nrm = 0.0;
   for (int i = 0; i < m; ++i) nrm = fma(z[i], z[i], nrm);
   nrm = 1.0 / sqrt(nrm);
@@ -104,29 +124,48 @@ __device__ double block_sum(double v, double* red) {
   return s;
 }
 
-// w -= Q[:, 0..nc) (Q[:, 0..nc)^T w): dot products one warp each (lanes split
-// the k entries, shuffle tree), then the update one row per thread.  Ends
-// with hv[0..nc) = the coefficients; caller syncs before reading wv.
+// w -= Q[:, 0..nc) (Q[:, 0..nc)^T w).  Dots: 4 threads per column (k split
+// in 4 contiguous parts, 2 accumulators each, 2-level shuffle); update: 2
+// threads per row (columns split in halves, 1 shuffle).  Ends with
+// hv[0..nc) = the coefficients and wv updated; caller syncs before reading wv.
 __device__ void cgs_project(const double* Q, int kq, int k, int nc, double* wv, double* hv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < nc; c += LT / 32) {
-    const double* qc = Q + (size_t)c * kq;
-    double h = 0.0;
-    for (int a = lane; a < k; a += 32) h = fma(qc[a], wv[a], h);
-    h = mdsx::warp_sum(h);
-    if (lane == 0) hv[c] = h;
+  const int tid = threadIdx.x;
+  const int part = tid & 3;
+  const int seg = (k + 3) >> 2;
+  for (int c = tid >> 2; c < ((nc + 7) & ~7); c += LT / 4) {     // warp-uniform trip count
+    double h0 = 0.0, h1 = 0.0;
+    if (c < nc) {
+      const double* qc = Q + (size_t)c * kq;
+      const int a1 = min(k, (part + 1) * seg);
+      int a = part * seg;
+      for (; a + 1 < a1; a += 2) {
+        h0 = fma(qc[a], wv[a], h0);
+        h1 = fma(qc[a + 1], wv[a + 1], h1);
+      }
+      if (a < a1) h0 = fma(qc[a], wv[a], h0);
+    }
+    double h = h0 + h1;
+    h += __shfl_xor_sync(0xffffffffu, h, 1);
+    h += __shfl_xor_sync(0xffffffffu, h, 2);
+    if (c < nc && part == 0) hv[c] = h;
   }
   __syncthreads();
-  const int tid = threadIdx.x;
-  if (tid < k) {
-    double s0 = wv[tid], s1 = 0.0;
-    int c = 0;
-    for (; c + 1 < nc; c += 2) {
-      s0 = fma(-Q[(size_t)c * kq + tid], hv[c], s0);
-      s1 = fma(-Q[(size_t)(c + 1) * kq + tid], hv[c + 1], s1);
+  const int hf = tid & 1;
+  const int cmid = (nc + 1) >> 1;
+  for (int a = tid >> 1; a < ((k + 15) & ~15); a += LT / 2) {
+    double s0 = 0.0, s1 = 0.0;
+    if (a < k) {
+      const int c1 = hf ? nc : cmid;
+      int c = hf ? cmid : 0;
+      for (; c + 1 < c1; c += 2) {
+        s0 = fma(Q[(size_t)c * kq + a], hv[c], s0);
+        s1 = fma(Q[(size_t)(c + 1) * kq + a], hv[c + 1], s1);
+      }
+      if (c < c1) s0 = fma(Q[(size_t)c * kq + a], hv[c], s0);
     }
-    if (c < nc) s0 = fma(-Q[(size_t)c * kq + tid], hv[c], s0);
-    wv[tid] = s0 + s1;
+    double t = s0 + s1;
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    if (a < k && hf == 0) wv[a] -= t;
   }
 }
 
@@ -135,7 +174,7 @@ __global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
 lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
                     double* __restrict__ Uout, double* __restrict__ lam_out,
                     double* __restrict__ estimates, double* __restrict__ gof,
-                    mdsx_piece_status* __restrict__ status, int qform_trivial) {
+                    mdsx_piece_status* __restrict__ status, int only_flagged) {
   extern __shared__ double sm[];
   __shared__ double alpha[QMAX], beta[QMAX], beta2[QMAX];
   __shared__ double wv[LMAX], hv[QMAX + 1];
@@ -149,6 +188,13 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   const int kq = k | 1;                        // odd leading dim of Q (conflict-free columns)
   const int tid = threadIdx.x;
   const double* Ag = Aall + d.a_off;
+  if (only_flagged) {           // fallback pass: only pieces the subspace kernel handed over
+    const mdsx_piece_status s0 = status[pid];
+    if (!(s0.code == MDSX_NUMERICAL && s0.value == -3.0)) return;
+    __syncthreads();
+    if (tid == 0) status[pid] = mdsx_piece_status{MDSX_OK, 0, 0.0};
+    __syncthreads();
+  }
   if (status[pid].code == MDSX_INVALID_INPUT) {   // non-finite rows: nothing to solve
     for (int e = tid; e < k * r; e += LT) Uout[d.u_off + e] = 0.0;
     if (tid < r) {
@@ -164,13 +210,27 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   const int qcap = min(QMAX, k);
 
   double fro = 0.0, tr = 0.0;
-  for (int i = 0; i < k; ++i) {                // packed copy, coalesced per row
-    const int off = i * k - i * (i - 1) / 2;
-    for (int a = i + tid; a < k; a += LT) {
-      const double v = Ag[(int64_t)i * k + a];
-      A[off + a - i] = v;
-      fro = fma((a == i ? 1.0 : 2.0) * v, v, fro);   // off-diagonal entries count twice
-      if (a == i) tr += v;
+  {                                            // packed copy: 4 independent loads in flight
+    const int kk2 = k * k;
+    for (int e0 = tid; e0 < kk2; e0 += 4 * LT) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * LT;
+        v[u] = e < kk2 ? Ag[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * LT;
+        if (e < kk2) {
+          const int i = e / k, a = e - i * k;
+          if (a >= i) {
+            A[i * k - i * (i - 1) / 2 + a - i] = v[u];
+            fro = fma((a == i ? 1.0 : 2.0) * v[u], v[u], fro);   // off-diagonal entries count twice
+            if (a == i) tr += v[u];
+          }
+        }
+      }
     }
   }
   fro = block_sum(fro, red);
@@ -182,29 +242,41 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   if (tid < k) Q[tid] = q0 / n0;
   __syncthreads();
   const double anorm = anorm_s;
-  const int row_off = tid < k ? tid * k - tid * (tid - 1) / 2 - tid : 0;   // packed row base
 
   int m = 0;                 // current Krylov dimension (columns 0..m-1 of Q valid)
   bool done = false, broke = false, capped = false;
   const int first_check = max(2 * r + 4, 24);
   while (!done) {
     const double* q = Q + (size_t)m * kq;
-    // w = A q with the packed symmetric A: row i = sum_{a<i} A[a][i] q_a + sum_{a>=i} A[i][a] q_a
-    if (tid < k) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int off = 0;
-      int a = 0;
-      for (; a < tid; ++a) {                   // column part (coalesced across threads)
-        a1 = fma(A[off + tid - a], q[a], a1);
-        off += k - a;
+    // w = A q with the packed symmetric A: row i = sum_{a<i} A[a][i] q_a + sum_{a>=i} A[i][a] q_a;
+    // two threads per row (a split in halves, 2 accumulators per part), one shuffle
+    {
+      const int i = tid >> 1, hf = tid & 1;
+      const int kh = (k + 1) >> 1;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (i < k) {
+        const int a0 = hf * kh, a1 = min(k, a0 + kh);
+        const int cend = min(a1, i);
+        int a = a0;
+        int off = a * k - a * (a - 1) / 2;      // packed offset of row a
+        for (; a + 1 < cend; a += 2) {          // column part
+          s0 = fma(A[off + i - a], q[a], s0);
+          off += k - a;
+          s1 = fma(A[off + i - a - 1], q[a + 1], s1);
+          off += k - a - 1;
+        }
+        if (a < cend) s0 = fma(A[off + i - a], q[a], s0);
+        const double* rowp = A + (i * k - i * (i - 1) / 2) - i;
+        a = max(a0, i);
+        for (; a + 1 < a1; a += 2) {            // own row part
+          s2 = fma(rowp[a], q[a], s2);
+          s3 = fma(rowp[a + 1], q[a + 1], s3);
+        }
+        if (a < a1) s2 = fma(rowp[a], q[a], s2);
       }
-      const double* rowp = A + row_off;
-      for (; a + 1 < k; a += 2) {              // own row part
-        a0 = fma(rowp[a], q[a], a0);
-        a2 = fma(rowp[a + 1], q[a + 1], a2);
-      }
-      if (a < k) a3 = fma(rowp[a], q[a], a3);
-      wv[tid] = (a0 + a1) + (a2 + a3);
+      double t = (s0 + s1) + (s2 + s3);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      if (i < k && hf == 0) wv[i] = t;
     }
     __syncthreads();
     double al = 0.0;
@@ -265,7 +337,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
         lo = lo_s[grp];
         hi = hi_s[grp];
         const double x = lo + (hi - lo) * (double)(sl + 1) / (double)(MS + 1);
-        below_ok = sturm_below(alpha, beta2, m, x, pivmin) <= m - 1 - grp;   // grp-th largest
+        below_ok = sturm_below(alpha, beta2, m, x) <= m - 1 - grp;   // grp-th largest
       }
       const unsigned okm = __ballot_sync(0xffffffffu, below_ok);
       // counts are monotone in x: points sl < c are below the eigenvalue
@@ -374,13 +446,14 @@ size_t lanczos_smem_bytes(int kmax) { return lanczos_bytes(kmax, LMAX); }
 // QCAP_PIECES (two CTAs / SM, capacity overflow -> Jacobi fallback).
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                        mdsx_piece_status* status, int full_basis, cudaStream_t st) {
+                        mdsx_piece_status* status, int full_basis, int only_flagged,
+                        cudaStream_t st) {
   if (npieces == 0) return MDSX_OK;
   auto go = [&](auto kern, int qmax) {
     const size_t smem = lanczos_bytes(kmax, qmax);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
-    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, 1);
+    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged);
     return launched(h, "lanczos_smem_kernel", st);
   };
   return full_basis ? go(lanczos_smem_kernel<LMAX>, LMAX)

@@ -1,6 +1,8 @@
 // C-ABI entry points and the handle runtime (workspace, staging, errors).
 #include "mdsx_common.cuh"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -46,14 +48,13 @@ int launch_double_center(mdsx_handle* h, const double* D, int64_t m, double* mu,
                          double* Q, cudaStream_t st);
 int launch_delta_check(mdsx_handle* h, const double* D, int64_t m, unsigned long long* mx,
                        int32_t* flags, cudaStream_t st);
-size_t subspace_smem_bytes(int kmax);
-int subspace_prof(long long* out, int n);
 int lanczos_kmax();
 int lanczos_rmax();
 size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                        mdsx_piece_status* status, int full_basis, cudaStream_t st);
+                        mdsx_piece_status* status, int full_basis, int only_flagged,
+                        cudaStream_t st);
 bool gram_piece_ok(const void* data, int dtype, int64_t ld, int p);
 int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                       const int64_t* row_idx, const PieceDesc* pd, int npieces, double* A,
@@ -69,10 +70,10 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
                    double* Uout, double* lam_out, double* estimates, double* gof,
                    mdsx_piece_status* status, cudaStream_t st,
                    int (*put)(mdsx_handle*, void*, const void*, size_t, cudaStream_t));
-int subspace_block();
-int launch_subspace_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
-                         const double* A, double* U, double* lam, double* estimates, double* gof,
-                         mdsx_piece_status* status, int qform_trivial, cudaStream_t st);
+int subspace_rmax();
+int launch_subspace(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
+                    const double* A, double* U, double* lam, double* estimates, double* gof,
+                    mdsx_piece_status* status, cudaStream_t st);
 
 int fail(mdsx_handle* h, int code, const std::string& msg) {
   if (h) h->err = msg;
@@ -308,8 +309,17 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
                           gof, status, 1, st)))
     return rc;
   if (!cp.pd_sub.empty()) {
+    // blocked subspace iteration on the tensor pipe; pieces without a gap
+    // after r fall through to Lanczos (flagged), capacity overflow to Jacobi
+    // solver choice (measured): Lanczos by default; MDSX_EIG=subspace
+    // selects the DMMA block iteration (same results within the tolerance)
+    const char* eig = getenv("MDSX_EIG");
+    const bool sub = r <= subspace_rmax() && eig && strcmp(eig, "subspace") == 0;
+    if (sub && (rc = launch_subspace(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
+                                     estimates, gof, status, st)))
+      return rc;
     if ((rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
-                                  estimates, gof, status, 0, st)))
+                                  estimates, gof, status, 0, sub ? 1 : 0, st)))
       return rc;
     if ((rc = launch_jacobi_fallback(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
                                      estimates, gof, status, st)))
@@ -329,9 +339,6 @@ using namespace mdsx;
 extern "C" {
 
 int mdsx_version(void) { return 1; }
-
-// diagnostics only (not in the public header): block-0 phase cycle counters
-int mdsx_debug_subspace_prof(long long* out, int n) { return mdsx::subspace_prof(out, n); }
 
 int mdsx_create(int device, mdsx_handle** out) {
   if (!out) return MDSX_PARAM;

@@ -31,7 +31,7 @@ for k_, (ms, c) in sorted(rep_t.items()):
 import ctypes
 from paper_2007_11919_b200 import _lib
 lib = _lib.load()
-buf = (ctypes.c_longlong * 16)()
-lib.mdsx_debug_subspace_prof(buf, 16)
-names = ["load", "loop-top", "mul_AV", "XtZ", "chol", "trsm", "RR-AV+XtZ", "symm", "jacobi32", "resid"]
-print({nm: buf[i] for i, nm in enumerate(names)})
+
+
+
+
