@@ -329,7 +329,7 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
       (rc = run_big_pieces(h, cp.pd_big, A, r, U, lam, estimates, gof, status, st, stage_put)))
     return rc;
   return launch_points(h, data, dtype, ld, p, ridx, dpd, np, cp.max_m, r, mu, U, lam, points,
-                       cand, st);
+                       cand, st, cp.pd_f1.empty());
 }
 
 }  // namespace mdsx

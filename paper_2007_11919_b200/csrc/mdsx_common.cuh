@@ -133,7 +133,7 @@ size_t points_ws_bytes(int npieces, int64_t max_m, int r);
 int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                   const int64_t* row_idx, const PieceDesc* pd, int npieces, int64_t max_m, int r,
                   const double* mu, const double* U, const double* lam, double* points,
-                  double2* cand, cudaStream_t st);
+                  double2* cand, cudaStream_t st, bool all_form0 = false);
 GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
                        const std::vector<GemmTask>& batch);
 int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_items,
