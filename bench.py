@@ -73,12 +73,16 @@ WORKLOADS = {
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
 TRAFFIC = {
-    ("dc2", "lanczos_smem_kernel"): {"bytes": (88.29 + 7.73) * 1e6,
-                                     "src": "profiles/r01_ncu_dc2_full.txt"},
-    ("dc2", "gram_dmma_kernel"): {"bytes": (887.46 + 70.59) * 1e6,
-                                  "src": "profiles/r01_ncu_dc2_full.txt"},
-    ("dc2", "points_kernel"): {"bytes": (896.65 + 89.09) * 1e6,
-                               "src": "profiles/r01_ncu_dc2_full.txt"},
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (84.195 + 5.184) * 1e6,
+                                     "src": "profiles/r01_ncu_full_dc2.txt"},
+    ("dc2", "gram_piece_kernel"): {"bytes": (878.910 + 72.684) * 1e6,
+                                   "src": "profiles/r01_ncu_full_dc2.txt"},
+    ("dc2", "points_rows_kernel"): {"bytes": (896.882 + 77.644) * 1e6,
+                                    "src": "profiles/r01_ncu_full_dc2.txt"},
+    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.048 + 785.069) * 1e6,
+                                       "src": "profiles/r01_ncu_full_interp4.txt"},
+    ("interp4", "subtract_mean_kernel"): {"bytes": (800.045 + 740.962) * 1e6,
+                                          "src": "profiles/r01_ncu_full_interp4.txt"},
 }
 
 
@@ -256,10 +260,10 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
     p, r = w["p"], w["r"]
     esize = 4 if w["dtype"] == "f32" else 8
     sizes = piece_sizes(w, plan)
-    if kernel in ("gram_dmma_kernel", "gram_kernel"):
+    if kernel in ("gram_dmma_kernel", "gram_piece_kernel", "gram_kernel"):
         fl = 0.0
         for m in sizes:
-            if (p < m) == (kernel == "gram_dmma_kernel"):
+            if (p < m) == (kernel != "gram_kernel"):
                 k, K = (p, m) if p < m else (m, p)
                 fl += K * k * (k + 1)          # symmetric rank-K update of a k x k Gram
         return {"bound": "tensor", "flops": fl, "model": "SYRK m*p*(p+1) per piece"}
@@ -279,7 +283,7 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
     if kernel == "subtract_mean_kernel":
         n = w["n"]
         return {"bound": "hbm", "bytes": 2 * n * r * 8, "model": "read + write of the n x r output"}
-    if kernel == "points_kernel":
+    if kernel in ("points_kernel", "points_rows_kernel"):
         tot = sum(sizes)
         return {"bound": "hbm", "bytes": tot * p * esize + tot * r * 8,
                 "model": "rows*p*sizeof(in) + rows*r*8"}
