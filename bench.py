@@ -18,12 +18,12 @@ separate flush is needed.  `e2e` repeats the measurement through the public
 API from pinned HOST memory: H2D of the input, the plan's index upload, the
 kernels, and the D2H of the n x r result and the fit figures, every step.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling.  D&C and
-interpolation run ONE global problem of N x the config's rows through
+Multi-GPU (torchrun, one process per GPU): weak scaling.  Every algorithm
+runs ONE global problem of N x the config's rows through
 paper_2007_11919_b200.distributed (input replicated on every GPU outside the
-timed region; each rank solves its contiguous share of subsets / rows; only
-per-subset sums and fit figures are exchanged — all-gathers over NCCL).  Fast
-MDS runs an independent config-sized problem per rank.  The timed region is
+timed region; each rank solves its contiguous share of subsets / rows /
+level-1 subtrees; only per-segment sums and fit figures are exchanged —
+all-gathers over NCCL).  The timed region is
 bracketed by barriers and the max over ranks is reported; the n x r result
 stays sharded on the devices (gathering it is not part of the metric).
 
@@ -215,7 +215,7 @@ class ShardedRun:
         from paper_2007_11919_b200 import AlgorithmParams
         from paper_2007_11919_b200 import distributed as dd
         self.dd, self.w = dd, w
-        self.be = dd.GpuBackend(x)
+        self.be = dd.GpuBackend(x, reuse=True)     # per-plan setup once, like the 1-GPU runners
         self.comm = dd.Comm(device=dev)
         self.plan = plan
         self.prm = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=0)
@@ -225,6 +225,8 @@ class ShardedRun:
         if self.w["algo"] == "divide":
             self.res = self.dd.sharded_divide_and_conquer(self.be, self.w["n"], self.prm, self.comm,
                                                           plan=self.plan)
+        elif self.w["algo"] == "fast":
+            self.res = self.dd.sharded_fast(self.be, self.w["n"], self.prm, self.comm, plan=self.plan)
         else:
             self.res = self.dd.sharded_interpolation(self.be, self.w["n"], self.prm, self.comm,
                                                      sample=self.plan)
@@ -400,7 +402,8 @@ def run_ours(args, w):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    force = os.environ.get("MDSX_BENCH_SHARDED") == "1"   # exercise the N>1 path on one GPU
+    if ws > 1 or force:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -409,13 +412,13 @@ def run_ours(args, w):
     from paper_2007_11919_b200 import _device as D
 
     peaks = measured_peaks(dev)
-    sharded = ws > 1 and w["algo"] in ("divide", "interpolate")
+    sharded = ws > 1 or force
     if sharded:
         # one global problem of ws x n rows, replicated input, same seed everywhere
         w = dict(w, n=w["n"] * ws)
         seed = 0
     else:
-        seed = rank                   # fast MDS at N>1: an independent problem per rank
+        seed = 0
     x = make_data(w, dev, seed)
     plan = make_plan(w, seed)
     if sharded:
@@ -590,7 +593,7 @@ def run_ours(args, w):
             "fit": {"g1": cfg_out.gof_g1, "estimates": [float(v) for v in cfg_out.eigenvalue_estimates]},
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if ws > 1 or force:
         dist.destroy_process_group()
     return 0
 

@@ -172,10 +172,11 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
  * (sums: nseg x r, device; seg_off: device).  Fixed-order reductions, so a
  * sharded run that sums the same segments in the same order is independent
  * of the number of ranks. */
+/* idx == NULL: the rows are the offsets themselves (contiguous segments). */
 int mdsx_segment_colsums(mdsx_handle* h, const double* points, const int64_t* idx,
                          const int64_t* seg_off, int32_t nseg, int32_t r, double* sums,
                          void* stream);
-/* points[idx[i]] -= shift (r doubles, device), i < n. */
+/* points[idx[i]] -= shift (r doubles, device), i < n; idx == NULL: rows 0..n-1. */
 int mdsx_shift_rows(mdsx_handle* h, double* points, const int64_t* idx, int64_t n, int32_t r,
                     const double* shift, void* stream);
 

@@ -153,10 +153,13 @@ class FastRun:
     (deepest first) one batched Procrustes fit + one batched in-place apply,
     then scatter to input order and re-centre."""
 
-    def __init__(self, x: torch.Tensor, plan: FastPlan, r: int):
-        self.x, self.plan, self.r = x, plan, r
+    def __init__(self, x: torch.Tensor, plan: FastPlan, r: int, flat=None, local: bool = False):
+        """`flat` (plans.flatten_fast_shard) + `local`: run one rank's share of
+        sharded fast MDS — no scatter to input order, no re-centring; the
+        rank's rows stay in `pts[:len(flat.order)]` (distributed.py)."""
+        self.x, self.plan, self.r, self.local = x, plan, r, local
         self.dev = dev = x.device
-        flat = self.flat = flatten_fast(plan)
+        flat = self.flat = flat if flat is not None else flatten_fast(plan)
         self.piece_rows = D.index_tensor(flat.piece_rows, dev)
         self.order = D.index_tensor(flat.order, dev)
         self.levels = []
@@ -174,7 +177,7 @@ class FastRun:
         self.est = D.empty((npc, r), dev)
         self.gof = D.empty((npc, 2), dev)
         self.status = D.status_tensor(npc, dev)
-        self.out = D.empty((plan.n, r), dev)
+        self.out = None if local else D.empty((plan.n, r), dev)
 
     def launch(self) -> None:
         x, r, dev = self.x, self.r, self.dev
@@ -191,6 +194,8 @@ class FastRun:
                    lv["trans"].data_ptr(), lv["loss"].data_ptr(), lv["deg"].data_ptr(), sp)
             h.call("mdsx_procrustes_apply", P, r, lv["start"].data_ptr(), lv["length"].data_ptr(),
                    lv["nj"], lv["max_len"], lv["rot"].data_ptr(), lv["trans"].data_ptr(), sp)
+        if self.local:
+            return
         h.call("mdsx_scatter_rows", P, self.order.data_ptr(), self.plan.n, r,
                self.out.data_ptr(), sp)
         h.call("mdsx_recenter", self.out.data_ptr(), self.plan.n, r, sp)

@@ -292,7 +292,7 @@ __global__ void seg_colsum_kernel(const double* __restrict__ X, const int64_t* _
   if (warp >= nseg * r) return;
   const int seg = warp / r, c = warp % r;
   double s = 0.0;
-  for (int64_t i = off[seg] + lane; i < off[seg + 1]; i += 32) s += X[idx[i] * r + c];
+  for (int64_t i = off[seg] + lane; i < off[seg + 1]; i += 32) s += X[(idx ? idx[i] : i) * r + c];
   s = mdsx::warp_sum(s);
   if (lane == 0) sums[(int64_t)seg * r + c] = s;
 }
@@ -303,7 +303,7 @@ __global__ void shift_rows_kernel(double* __restrict__ X, const int64_t* __restr
   if (e >= n * r) return;
   const int64_t i = e / r;
   const int c = (int)(e - i * r);
-  X[idx[i] * r + c] -= shift[c];
+  X[(idx ? idx[i] : i) * r + c] -= shift[c];
 }
 
 }  // namespace

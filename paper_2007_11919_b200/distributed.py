@@ -12,6 +12,13 @@ from the same seed), so the only exchanges are small:
   are all-gathered and combined in plan order, so the re-centring shift and
   G1/G2/estimates are identical on every rank and independent of the number
   of ranks.
+* fast: the root's level-1 subtrees are dealt to ranks (contiguous blocks);
+  every rank solves its subtrees completely (leaves, alignment sets, internal
+  alignments) and the root's alignment set (samples of ALL children, raw
+  rows — computed redundantly, no broadcast needed), aligns its children onto
+  their slices of it, and writes their rows.  Per-child column sums and fit
+  figures are all-gathered and combined in child order (the reference's
+  recursion, algorithms.py:314-320).
 * interpolation: rank 0 computes the landmark MDS and Gower context and
   broadcasts it (the north star's "computed once and broadcast"); each rank
   streams a contiguous block of rows; per-block column sums are all-gathered
@@ -25,14 +32,13 @@ rank 0 (outside the timed region in bench.py).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from .params import AlgorithmParams
-from .plans import DcPlan, flatten_subsets, interpolation_sample, plan_divide_conquer
+from .plans import (DcPlan, FastPlan, flatten_fast_shard, flatten_subsets, interpolation_sample,
+                    plan_divide_conquer, plan_fast)
 
 SUM_BLOCK = 65536      # canonical row block of the interpolation re-centring sums
 
@@ -44,18 +50,37 @@ def shard(count: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-@dataclass
 class ShardResult:
-    rows: np.ndarray            # global row indices this rank owns (input order)
-    out: object                 # backend buffer holding those rows (device tensor on GPU)
-    local: np.ndarray           # positions of `rows` inside `out`
-    estimates: np.ndarray
-    gof_g1: float
-    gof_g2: float
-    backend: object = None
+    """One rank's share of a sharded run.  `rows` (global row indices, input
+    order) and `local` (their positions in `out`) may be given as arrays or
+    as (lo, hi) ranges, materialised only when asked for (gather time)."""
+
+    def __init__(self, rows, out, local, estimates, gof_g1, gof_g2, backend=None):
+        self._rows, self._local = rows, local
+        self.out = out
+        self.estimates = estimates
+        self.gof_g1, self.gof_g2 = gof_g1, gof_g2
+        self.backend = backend
+
+    @staticmethod
+    def _arr(v):
+        if isinstance(v, tuple):
+            return np.arange(v[0], v[1], dtype=np.int64)
+        return v() if callable(v) else v
+
+    @property
+    def rows(self) -> np.ndarray:
+        return self._arr(self._rows)
+
+    @property
+    def local(self) -> np.ndarray:
+        return self._arr(self._local)
 
     def points(self) -> np.ndarray:
         """(len(rows), r) float64 on the host."""
+        if isinstance(self._local, tuple) and self._local[0] == 0 and \
+                self._local[1] == self.out.shape[0]:
+            return self.backend.take_all(self.out)
         return self.backend.take(self.out, self.local)
 
 
@@ -96,15 +121,26 @@ class Comm:
 class GpuBackend:
     """Per-rank compute on the rank's GPU through the C-ABI."""
 
-    def __init__(self, x: torch.Tensor):
+    def __init__(self, x: torch.Tensor, reuse: bool = False):
+        """reuse=True: keep the per-plan setup (flattened sub-plans, uploaded
+        index arrays, result buffers) across calls with the same plan, as the
+        single-GPU runners do (results of a call are overwritten by the next)."""
         from . import _device as D
         self.D = D
         self.x = x
         self.dev = x.device
+        self.reuse = reuse
+        self._cache = {}
 
-    def dc_subplan(self, subsets: list, c: int, r: int):
+    def dc_subplan(self, subsets: list, c: int, r: int, key=None):
         """D&C of a sub-plan (anchor first) without re-centring -> (out_dev, est, gof, status)."""
         D, x = self.D, self.x
+        ck = ("dc", key, c, r)
+        if self.reuse and key is not None and ck in self._cache:
+            ridx, off, out, est, gof, st, own = self._cache[ck]
+            out.zero_()
+            self._own = own
+            return self._run_dc(ridx, off, c, r, out, est, gof, st)
         rows, off = flatten_subsets(subsets)
         ridx = D.index_tensor(rows, self.dev)
         npc = len(subsets)
@@ -112,11 +148,78 @@ class GpuBackend:
         est = D.empty((npc, r), self.dev)
         gof = D.empty((npc, 2), self.dev)
         st = D.status_tensor(npc, self.dev)
+        # rows each subset contributes (anchor: all; others: own rows) as device
+        # index segments carved from the uploaded plan indices (no second upload)
+        keep = np.ones(int(off[-1]), dtype=bool)
+        for j in range(1, npc):
+            keep[off[j]:off[j] + c] = False
+        own = ridx[torch.from_numpy(keep).to(self.dev)]
+        sizes = np.diff(off) - np.r_[0, np.full(npc - 1, c)]
+        own_off = np.zeros(npc + 1, dtype=np.int64)
+        np.cumsum(sizes, out=own_off[1:])
+        self._own = (own, own_off)
+        if self.reuse and key is not None:
+            self._cache[ck] = (ridx, off, out, est, gof, st, self._own)
+        return self._run_dc(ridx, off, c, r, out, est, gof, st)
+
+    def _run_dc(self, ridx, off, c, r, out, est, gof, st):
+        D, x = self.D, self.x
+        npc = len(off) - 1
         D.handle(self.dev).call(
             "mdsx_divide_conquer_ex", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
             x.shape[1], ridx.data_ptr(), off.ctypes.data, npc, c, r, out.data_ptr(),
             est.data_ptr(), gof.data_ptr(), st.data_ptr(), 1, D.stream_ptr(self.dev))
         return out, est.cpu().numpy(), gof.cpu().numpy(), D.decode_status(st)
+
+    def own_segment_sums(self, out, r: int) -> np.ndarray:
+        """Column sums of each dc_subplan subset's own rows (fixed order)."""
+        own, own_off = self._own
+        return self._segsums(out, own.data_ptr(), own_off, r)
+
+    def shift_own(self, out, mean: np.ndarray) -> None:
+        own, _ = self._own
+        self._shift(out, own.data_ptr(), own.numel(), mean)
+
+    def range_sums(self, out, offsets: np.ndarray, r: int) -> np.ndarray:
+        """Column sums of the contiguous row ranges [offsets[j], offsets[j+1]) of out."""
+        return self._segsums(out, None, offsets, r)
+
+    def shift_all(self, out, mean: np.ndarray) -> None:
+        self._shift(out, None, out.shape[0], mean)
+
+    def _segsums(self, out, idx_ptr, offsets, r):
+        D = self.D
+        nseg = len(offsets) - 1
+        sums = D.empty((max(nseg, 1), r), self.dev)
+        if nseg > 0:
+            doff = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(self.dev)
+            D.handle(self.dev).call("mdsx_segment_colsums", out.data_ptr(), idx_ptr,
+                                    doff.data_ptr(), nseg, r, sums.data_ptr(),
+                                    D.stream_ptr(self.dev))
+        return sums.cpu().numpy()[:nseg]
+
+    def _shift(self, out, idx_ptr, n, mean):
+        D = self.D
+        m = torch.from_numpy(np.ascontiguousarray(mean, dtype=np.float64)).to(self.dev)
+        D.handle(self.dev).call("mdsx_shift_rows", out.data_ptr(), idx_ptr, n, out.shape[1],
+                                m.data_ptr(), D.stream_ptr(self.dev))
+
+    def fast_subtrees(self, plan: FastPlan, lo: int, hi: int, r: int, key=None):
+        """One rank's share of fast MDS (plans.flatten_fast_shard), aligned,
+        not re-centred -> (out_dev (rows in flat.order), flat, est, gof, status)."""
+        from .algorithms import FastRun
+        D = self.D
+        ck = ("fast", key, lo, hi, r)
+        run = self._cache.get(ck) if self.reuse and key is not None else None
+        if run is None:
+            flat = flatten_fast_shard(plan, lo, hi)
+            run = FastRun(self.x, plan, r, flat=flat, local=True)
+            if self.reuse and key is not None:
+                self._cache[ck] = run
+        flat = run.flat
+        run.launch()
+        out = run.pts[:len(flat.order)]
+        return out, flat, run.est.cpu().numpy(), run.gof.cpu().numpy(), D.decode_status(run.status)
 
     def segment_sums(self, out, segments: list, r: int) -> np.ndarray:
         D = self.D
@@ -138,6 +241,9 @@ class GpuBackend:
 
     def take(self, out, rows: np.ndarray) -> np.ndarray:
         return out[self.D.index_tensor(rows, self.dev)].cpu().numpy()
+
+    def take_all(self, out) -> np.ndarray:
+        return self.D.to_host(out)
 
     def place(self, out, local: np.ndarray, values: np.ndarray) -> None:
         """out[local[i]] = values[i] (mdsx_scatter_rows)."""
@@ -197,17 +303,19 @@ def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: C
     P, c, r = plan.p, prm.c, prm.r
     lo, hi = shard(P - 1, comm.world, comm.rank)
     mine = list(range(1 + lo, 1 + hi))                    # owned subsets besides the anchor
-    out, est, gof, st = backend.dc_subplan([plan.subsets[0]] + [plan.subsets[j] for j in mine], c, r)
+    out, est, gof, st = backend.dc_subplan([plan.subsets[0]] + [plan.subsets[j] for j in mine], c, r,
+                                           key=(id(plan), lo, hi))
     from .primitives import raise_piece_status
     if np.any(st["code"] == 3):
         from .errors import InvalidInputError
         raise InvalidInputError("data contains non-finite values")
     labels = [0] + mine
-    for rec, j in zip(st, labels):
-        raise_piece_status(rec, r, f"subset {j + 1}")
+    bad = np.flatnonzero(st["code"] != 0)
+    if bad.size:                                          # first failing subset in plan order
+        raise_piece_status(st[bad[0]], r, f"subset {labels[bad[0]] + 1}")
     # rows each subset contributes (anchor: all its rows; others: own rows)
     own = [plan.subsets[0]] + [plan.subsets[j][c:] for j in mine]
-    sums = backend.segment_sums(out, own, r)             # (1 + len(mine), r)
+    sums = backend.own_segment_sums(out, r)              # (1 + len(mine), r)
     # plan-order all-gather of per-subset sums and fit figures
     width = 3 + 2 * r                                    # [j, g1, g2, est(r), sums(r)]
     recs = np.zeros((len(mine), width))
@@ -223,9 +331,8 @@ def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: C
     for row in seg_sums:                                  # plan order
         total = total + row
     mean = total / n
-    rows = np.concatenate(own)
-    backend.shift(out, rows, mean)
-    sizes = np.array([len(q) for q in plan.subsets], dtype=np.float64)
+    backend.shift_own(out, mean)
+    sizes = np.fromiter((len(q) for q in plan.subsets), dtype=np.float64, count=P)
     weights = sizes.copy()
     weights[1:] -= c                                      # algorithms.py:158-166
     g1s = np.concatenate([gof[0:1, 0], allrecs[:, 1]])
@@ -233,10 +340,80 @@ def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: C
     ests = np.vstack([est[0:1], allrecs[:, 3:3 + r]])
     g1 = float(np.dot(weights, g1s) / n)
     g2 = float(np.dot(weights, g2s) / n)
-    per = np.stack([ests[j] * (sizes[j] / weights[j]) for j in range(P)])
-    if comm.rank != 0:                                    # the anchor's rows belong to rank 0
-        rows = np.concatenate(own[1:]) if len(own) > 1 else np.empty(0, np.int64)
+    per = ests * (sizes / weights)[:, None]
+    # the anchor's rows belong to rank 0; index lists built only when gathered
+    parts = own if comm.rank == 0 else own[1:]
+    rows = (lambda: np.concatenate(parts)) if parts else np.empty(0, np.int64)
     return ShardResult(rows, out, rows, per.mean(axis=0), g1, g2, backend)
+
+
+def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
+                 plan: FastPlan | None = None) -> ShardResult:
+    """fast_mds (algorithms.py:285-348) over comm.world ranks."""
+    from .errors import InvalidInputError
+    from .primitives import raise_piece_status
+    prm = params.resolved("fast")
+    r = prm.r
+    plan = plan if plan is not None else plan_fast(n, prm.l, prm.s, prm.seed)
+    if plan.root.is_leaf:                                 # n <= l: classical MDS (algorithms.py:337-338)
+        out, est, gof, st = backend.dc_subplan([plan.root.indices], 1, r)
+        raise_piece_status(st[0], r, "leaf 1")
+        rows = plan.root.indices if comm.rank == 0 else np.empty(0, np.int64)
+        return ShardResult(rows, out, rows, est[0], float(gof[0, 0]), float(gof[0, 1]), backend)
+    kids = plan.root.children
+    lo, hi = shard(len(kids), comm.world, comm.rank)
+    out, flat, est, gof, st = backend.fast_subtrees(plan, lo, hi, r, key=id(plan))
+    # failures: a consistent decision on every rank (all raise, no rank hangs)
+    root_pid = len(flat.piece_off) - 2                    # the root alignment set, evaluated last
+    first = next((k for k, pid in enumerate(flat.eval_order)
+                  if pid != root_pid and st[pid]["code"] != 0), -1)
+    flags = np.array([float(np.any(st["code"] == 3)), float(first >= 0)])
+    allflags = np.vstack(comm.allgather(flags)) if comm.world > 1 else flags[None]
+    if allflags[:, 0].any():
+        raise InvalidInputError("data contains non-finite values")
+    if allflags[:, 1].any():
+        culprit = int(np.flatnonzero(allflags[:, 1])[0])
+        if culprit == comm.rank:
+            pid = flat.eval_order[first]
+            raise_piece_status(st[pid], r, flat.labels[pid])
+        raise RuntimeError(f"fast MDS failed on rank {culprit}")
+    raise_piece_status(st[root_pid], r, flat.labels[root_pid])
+    # per-child aggregates of the owned subtrees (algorithms.py:289-320)
+    leaf = iter(range(flat.n_leaves))
+
+    def agg(node):
+        if node.is_leaf:
+            j = next(leaf)
+            return gof[j, 0], gof[j, 1], est[j], node.size
+        fits = [agg(ch) for ch in node.children]
+        sizes = np.array([f[3] for f in fits], dtype=np.float64)
+        tot = sizes.sum()
+        return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
+                float(np.dot(sizes, [f[1] for f in fits]) / tot),
+                np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
+
+    mine = kids[lo:hi]
+    fits = [agg(ch) for ch in mine]
+    starts = np.cumsum([0] + [ch.size for ch in mine]).astype(np.int64)
+    sums = backend.range_sums(out, starts, r)
+    width = 4 + 2 * r                                     # [i, g1, g2, size, est(r), sums(r)]
+    recs = np.zeros((len(mine), width))
+    for t, f in enumerate(fits):
+        recs[t, :4] = [lo + t, f[0], f[1], f[3]]
+        recs[t, 4:4 + r] = f[2]
+        recs[t, 4 + r:] = sums[t]
+    allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
+    allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
+    sizes = allrecs[:, 3]
+    tot = sizes.sum()
+    g1 = float(np.dot(sizes, allrecs[:, 1]) / tot)
+    g2 = float(np.dot(sizes, allrecs[:, 2]) / tot)
+    estimates = allrecs[:, 4:4 + r].mean(axis=0)
+    total = np.zeros(r)
+    for row in allrecs[:, 4 + r:]:                        # child order
+        total = total + row
+    backend.shift_all(out, total / n)
+    return ShardResult(flat.order, out, (0, len(flat.order)), estimates, g1, g2, backend)
 
 
 def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
@@ -262,17 +439,16 @@ def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
     # landmark rows inside the shard take the classical configuration
     in_shard = (sample >= lo) & (sample < hi)
     backend.place(out, (sample[in_shard] - lo).astype(np.int64), base[in_shard])
-    local = np.arange(hi - lo, dtype=np.int64)
-    segs = [local[s * SUM_BLOCK - lo:min(hi, (s + 1) * SUM_BLOCK) - lo] for s in range(b_lo, b_hi)]
-    sums = backend.segment_sums(out, segs, r) if segs else np.zeros((0, r))
+    bounds = np.array([min(hi, s * SUM_BLOCK) - lo for s in range(b_lo, b_hi + 1)], dtype=np.int64)
+    sums = backend.range_sums(out, bounds, r)
     recs = np.hstack([np.arange(b_lo, b_hi, dtype=np.float64)[:, None], sums])
     allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
     allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
     total = np.zeros(r)
     for row in allrecs[:, 1:]:                            # canonical block order
         total = total + row
-    backend.shift(out, local, total / n)
-    return ShardResult(np.arange(lo, hi, dtype=np.int64), out, local, est, g1, g2, backend)
+    backend.shift_all(out, total / n)
+    return ShardResult((lo, hi), out, (0, hi - lo), est, g1, g2, backend)
 
 
 def backend_context_len(backend, l: int, r: int) -> int:

@@ -338,6 +338,22 @@ class FastFlat:
 def flatten_fast(plan: FastPlan) -> FastFlat:
     """Walk the tree once: leaves in DFS order, alignment sets of every
     internal node, and per-depth Procrustes jobs (deepest first)."""
+    return _flatten_fast(plan.root, None)
+
+
+def flatten_fast_shard(plan: FastPlan, lo: int, hi: int) -> FastFlat:
+    """The share of one rank in sharded fast MDS: the level-1 subtrees
+    lo..hi-1 of the root (leaves, their alignment sets and internal jobs,
+    labelled as in the full tree), then the root's alignment set over ALL
+    children (computed redundantly by every rank) and the root-level jobs
+    aligning children lo..hi-1 onto their slices of it.  ``order`` = the
+    owned subtrees' rows; no other rank's rows appear."""
+    if plan.root.is_leaf:
+        raise ValueError("a single-leaf plan has no level-1 subtrees")
+    return _flatten_fast(plan.root, (lo, hi))
+
+
+def _flatten_fast(root: FastNode, span) -> FastFlat:
     leaves, aligns, labels_leaf, labels_align = [], [], [], []
     by_depth: dict = {}
     cursor = [0]
@@ -357,20 +373,34 @@ def flatten_fast(plan: FastPlan) -> FastFlat:
         post.append(("align", len(aligns)))
         aligns.append(samp)
         labels_align.append(f"{label or 'root'} alignment set")
-        by_depth.setdefault(depth, []).append((len(aligns) - 1, node, kid_starts))
+        by_depth.setdefault(depth, []).append((len(aligns) - 1, list(node.children), kid_starts, 0))
         return start
 
-    walk(plan.root, 0, "")
+    if span is None:
+        walk(root, 0, "")
+        order = root.indices
+    else:
+        lo, hi = span
+        kids = root.children[lo:hi]
+        kid_starts = [walk(ch, 1, f"branch {lo + i + 1}") for i, ch in enumerate(kids)]
+        samp = np.concatenate([ch.indices[ch.sampling_positions] for ch in root.children])
+        post.append(("align", len(aligns)))
+        aligns.append(samp)
+        labels_align.append("root alignment set")
+        off0 = int(sum(len(ch.sampling_positions) for ch in root.children[:lo]))
+        by_depth.setdefault(0, []).append((len(aligns) - 1, list(kids), kid_starts, off0))
+        order = (np.concatenate([ch.indices for ch in kids]) if kids
+                 else np.empty(0, dtype=np.int64))
     n_leaves = len(leaves)
     pieces = leaves + aligns
     piece_rows, piece_off = flatten_subsets(pieces)
     levels = []
     for depth in sorted(by_depth, reverse=True):
         tg, sr, jo, st, ln = [], [], [0], [], []
-        for a_idx, node, kid_starts in by_depth[depth]:
+        for a_idx, children, kid_starts, off0 in by_depth[depth]:
             a_base = piece_off[n_leaves + a_idx]
-            off = 0
-            for ch, ks in zip(node.children, kid_starts):
+            off = off0
+            for ch, ks in zip(children, kid_starts):
                 cnt = len(ch.sampling_positions)
                 tg.append(np.arange(a_base + off, a_base + off + cnt, dtype=np.int64))
                 sr.append(ks + ch.sampling_positions.astype(np.int64))
@@ -378,8 +408,10 @@ def flatten_fast(plan: FastPlan) -> FastFlat:
                 jo.append(jo[-1] + cnt)
                 st.append(ks)
                 ln.append(ch.size)
+        if len(st) == 0:
+            continue
         levels.append(FastLevel(np.concatenate(tg), np.concatenate(sr), np.asarray(jo, np.int64),
                                 np.asarray(st, np.int64), np.asarray(ln, np.int64)))
     eval_order = [i if kind == "leaf" else n_leaves + i for kind, i in post]
-    return FastFlat(plan.root.indices.astype(np.int64, copy=False), piece_rows, piece_off,
+    return FastFlat(np.asarray(order).astype(np.int64, copy=False), piece_rows, piece_off,
                     n_leaves, levels, labels_leaf + labels_align, eval_order)

@@ -30,7 +30,21 @@ class OracleBackend:
     def __init__(self, x):
         self.x = np.asarray(x, dtype=np.float64)
 
-    def dc_subplan(self, subsets, c, r):
+    def own_segment_sums(self, out, r):
+        return self.segment_sums(out, self._own, r)
+
+    def shift_own(self, out, mean):
+        self.shift(out, np.concatenate(self._own), mean)
+
+    def range_sums(self, out, offsets, r):
+        return np.stack([out[offsets[j]:offsets[j + 1]].sum(axis=0) for j in range(len(offsets) - 1)]) \
+            if len(offsets) > 1 else np.zeros((0, r))
+
+    def shift_all(self, out, mean):
+        out -= mean
+
+    def dc_subplan(self, subsets, c, r, key=None):
+        self._own = [subsets[0]] + [s[c:] for s in subsets[1:]]
         embs = [orc.mds_from_data(self.x[s], r) for s in subsets]
         out = np.zeros((self.x.shape[0], r))
         out[subsets[0]] = embs[0].points
@@ -41,6 +55,28 @@ class OracleBackend:
         gof = np.array([[e.g1, e.g2] for e in embs])
         return out, est, gof, np.zeros(len(subsets), dtype=STATUS)
 
+    def fast_subtrees(self, plan, lo, hi, r, key=None):
+        from paper_2007_11919_b200.plans import flatten_fast_shard
+        flat = flatten_fast_shard(plan, lo, hi)
+        off = flat.piece_off
+        npc = len(off) - 1
+        pts = np.zeros((int(off[-1]), r))
+        est = np.zeros((npc, r))
+        gof = np.zeros((npc, 2))
+        for j in range(npc):
+            e = orc.mds_from_data(self.x[flat.piece_rows[off[j]:off[j + 1]]], r)
+            pts[off[j]:off[j + 1]] = e.points
+            est[j] = e.estimates
+            gof[j] = [e.g1, e.g2]
+        for lv in flat.levels:
+            for t in range(len(lv.start)):
+                a, b = lv.job_off[t], lv.job_off[t + 1]
+                T = orc.procrustes_fit(pts[lv.tgt_rows[a:b]], pts[lv.src_rows[a:b]])
+                s0, ln = lv.start[t], lv.length[t]
+                pts[s0:s0 + ln] = orc.procrustes_apply(pts[s0:s0 + ln], T)
+        out = pts[:len(flat.order)]
+        return out, flat, est, gof, np.zeros(npc, dtype=STATUS)
+
     def segment_sums(self, out, segments, r):
         return np.stack([out[s].sum(axis=0) for s in segments])
 
@@ -49,6 +85,9 @@ class OracleBackend:
 
     def take(self, out, rows):
         return out[rows].copy()
+
+    def take_all(self, out):
+        return np.array(out, copy=True)
 
     def place(self, out, local, values):
         out[local] = values
@@ -84,6 +123,9 @@ def _worker(rank, world, port, algo, path):
         if algo == "divide":
             prm = AlgorithmParams(r=4, l=300, c=10, seed=2)
             res = dd.sharded_divide_and_conquer(be, x.shape[0], prm, comm)
+        elif algo == "fast":
+            prm = AlgorithmParams(r=4, l=300, s=8, seed=2)
+            res = dd.sharded_fast(be, x.shape[0], prm, comm)
         else:
             prm = AlgorithmParams(r=4, l=400, seed=2)
             dd.SUM_BLOCK = 256                     # several blocks per rank at test size
@@ -110,11 +152,13 @@ def _run(world, algo):
     return out
 
 
-@pytest.mark.parametrize("algo", ["divide", "interpolate"])
+@pytest.mark.parametrize("algo", ["divide", "interpolate", "fast"])
 def test_sharded_matches_reference_and_is_world_size_independent(algo):
     x = scenario(2600, 8, 4, seed=9)
     if algo == "divide":
         ref = orc.divide_conquer(x, 4, l=300, c=10, seed=2, threads=1)
+    elif algo == "fast":
+        ref = orc.run("fast", x, 4, l=300, s=8, seed=2, threads=1)
     else:
         ref = orc.interpolation(x, 4, l=400, seed=2, threads=1)
     one = _run(1, algo)
