@@ -396,7 +396,13 @@ constexpr int GB_MAX_STAGES = 4;
 // header: full[4], empty[4] mbarriers [0, 64), c0 [64, 192), v [192, 320)
 constexpr int GB_HEADER = 512;
 
-template <typename T, int RM, int TPR, int CPS>
+// N32 (fp32 rows, fused interpolation only): the squared norm |x - xbar|^2 is
+// accumulated on the fp32 pipe.  It enters the result only through
+// -|x - xbar|^2 v with v = S^-1 (1^T X1) / (2l), and X1 (the landmarks'
+// classical configuration) has zero column sums up to rounding, so its 1e-7
+// relative error reaches the output at ~1e-22; the fp64 pipe keeps the linear
+// term (11 instead of 13 fp64 operations per row-feature).
+template <typename T, int RM, int TPR, int CPS, bool N32>
 __global__ void __launch_bounds__(GB_CTA, CPS)
 gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
                   const double* __restrict__ ctx_mean, const double* __restrict__ ctx_M,
@@ -459,7 +465,8 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
         v2.y = c + 1 < r ? ctx_M[(int64_t)a * r + c + 1] : 0.0;
       } else {
         v2.x = ctx_mean[a];
-        v2.y = 1.0;                          // feature mask
+        v2.y = N32 ? __hiloint2double(__float_as_int(1.0f), __float_as_int((float)ctx_mean[a]))
+                   : 1.0;                   // feature mask (N32: packed with the fp32 mean)
       }
     }
     rec[e] = v2;
@@ -491,9 +498,11 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
     const int64_t r0 = t * TR;
     const int nr = (int)min((int64_t)TR, m - r0);
     double acc[R][RMP], nrm[R];
+    float nrm32[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       nrm[q] = 0.0;
+      nrm32[q] = 0.0f;
 #pragma unroll
       for (int c = 0; c < RMP; ++c) acc[q][c] = 0.0;
     }
@@ -532,8 +541,15 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
           // linear term on the raw value (its centring is the constant c0);
           // the squared norm on the centred value (fma(x, 1, -mu) == x - mu)
           const double xq = xv[q][u];
-          const double y = fma(xq, msk, -mu);
-          nrm[q] = fma(y, y, nrm[q]);
+          if constexpr (N32) {
+            const float xf = (float)xq;                      // exact: the input is fp32
+            const float y32 = (xf - __int_as_float(__double2loint(msk))) *
+                              __int_as_float(__double2hiint(msk));
+            nrm32[q] = fmaf(y32, y32, nrm32[q]);
+          } else {
+            const double y = fma(xq, msk, -mu);
+            nrm[q] = fma(y, y, nrm[q]);
+          }
 #pragma unroll
           for (int w = 0; w < RM / 2; ++w) {
             acc[q][2 * w] = fma(xq, mw[w].x, acc[q][2 * w]);
@@ -547,17 +563,26 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
     bool rescan = false;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
+      if constexpr (N32) nrm[q] = (double)nrm32[q];
 #pragma unroll
       for (int o = TPR / 2; o > 0; o >>= 1) nrm[q] += __shfl_xor_sync(0xffffffffu, nrm[q], o);
       rescan |= (g + q * G < nr) && !isfinite(nrm[q]);
     }
-    if (rescan && j == 0)
+    if (rescan)
 #pragma unroll
       for (int q = 0; q < R; ++q)
         if (g + q * G < nr && !isfinite(nrm[q])) {
-          // a squared norm can overflow on finite fp64 data: decide on the values
+          // a squared norm can overflow on finite data (fp64 rows; fp32 norms of
+          // |x| > 1e19): decide on the values, recompute the norm in fp64
           const T* xr = xs + (size_t)(g + q * G) * p;
-          for (int a = 0; a < p; ++a) bad |= !isfinite((double)xr[a]);
+          double s2 = 0.0;
+          for (int a = 0; a < p; ++a) {
+            const double xa = (double)xr[a];
+            bad |= !isfinite(xa);
+            const double ya = xa - ctx_mean[a];
+            s2 = fma(ya, ya, s2);
+          }
+          nrm[q] = s2;
         }
     __syncwarp();
     if (lane == 0) bulk::arrive(&empty[s]);
@@ -646,7 +671,8 @@ int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t*
 // not fit, in which case nothing is launched).
 int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
                       const double* mean, const double* M, const double* v, double* out,
-                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st) {
+                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
+                      bool norm32) {
   *nparts = 0;
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
   const int VW = (int)(16 / es);
@@ -683,7 +709,9 @@ int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p
     using T = decltype(tag);
     constexpr int RMc = decltype(rm)::value;
     constexpr int TPRc = decltype(tpr)::value;
-    auto kern = gower_bulk_kernel<T, RMc, TPRc, 1>;
+    auto kern = gower_bulk_kernel<T, RMc, TPRc, 1, false>;
+    if constexpr (sizeof(T) == 4)
+      if (norm32) kern = gower_bulk_kernel<T, RMc, TPRc, 1, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t TR = 2 * GB_THREADS / TPRc;
     const int64_t ntiles = (m + TR - 1) / TR;
@@ -780,7 +808,7 @@ int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, in
       (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
     int launched_parts = 0;
     int rc = launch_gower_bulk(h, X, dtype, m, p, r, mean, M, v, out, nullptr, nonfinite,
-                               &launched_parts, st);
+                               &launched_parts, st, false);
     if (rc || launched_parts) return rc;
     rc = launch_gower_stream(h, X, dtype, m, p, r, mean, M, v, out, nonfinite, st);
     if (rc >= 0) return rc;                       // -1: shape does not fit the staged kernel

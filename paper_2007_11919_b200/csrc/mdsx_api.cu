@@ -33,7 +33,8 @@ int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t*
                               int r, double* out, double* corr, cudaStream_t st);
 int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
                       const double* mean, const double* M, const double* v, double* out,
-                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st);
+                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
+                      bool norm32 = false);
 int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
                          const int64_t* idx, int64_t l, const double* X1, int r, double* mean,
                          double* M, double* v, double* S, double* q, double* cond, int32_t* flag,
@@ -686,8 +687,9 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
   if (ld == p && r <= 16 && ((size_t)p * es) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(data) & 15) == 0 && h->num_sms * r * sizeof(double) <= recenter_ws_bytes(r)) {
     int nparts = 0;
+    // the landmark configuration is centred -> v ~ 0: fp32 norms are exact enough
     if ((rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
-                                st)))
+                                st, dtype == MDSX_F32 && !getenv("MDSX_GOWER_NORM64"))))
       return rc;
     if (nparts > 0) {
       if ((rc = launch_landmark_overwrite(h, base, sample_idx, l, r, out, corr, st))) return rc;
