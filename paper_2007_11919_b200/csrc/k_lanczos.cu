@@ -28,6 +28,14 @@
 #include "mdsx_common.cuh"
 #include "piece_solvers.cuh"
 
+#ifdef MDSX_LZ_PROF
+#define LZ_T0(v) long long v = clock64()
+#define LZ_ACC(slot, v) if (blockIdx.x == 0 && threadIdx.x == 0) lzp[slot] += clock64() - v
+#else
+#define LZ_T0(v)
+#define LZ_ACC(slot, v)
+#endif
+
 namespace {
 
 constexpr int LT = 256;          // threads per CTA
@@ -82,35 +90,51 @@ __device__ __forceinline__ double fast_rcp(double d) {
 // twisted factorisation of T - theta I: top-down LDL^T pivots d, bottom-up
 // UDU^T pivots u, twist index with the smallest |d_k + u_k - (al_k - theta)|,
 // then the vector outward from the twist (z_k = 1).  O(m), no pivoting needed.
-template <int QMAX>
-__device__ void tri_twisted_vector(const double* al, const double* be, int m, double theta,
-                                   double pivmin, double* z /* m, out, unit norm */) {
-  double d[QMAX], u[QMAX];
+// Twisted factorisation of T - theta I (T: m x m tridiagonal, al / be) with
+// the pivots in shared-memory columns (stride RMAX, one column per calling
+// thread): top-down LDL^T pivots d (in zc), bottom-up UDU^T pivots u (in uc),
+// twist kt = argmin |gamma_k|, gamma_k = d_k + u_k - (al_k - theta); then the
+// vector outward from the twist (z_kt = 1) overwrites zc.  Returns gamma_kt
+// and |z|^2 (z is left unnormalised): (T - theta I) z = gamma_kt e_kt, so
+// theta + gamma_kt / |z|^2 is the Rayleigh quotient of z.  O(m).
+__device__ void tri_twisted(const double* al, const double* be, int m, double theta,
+                            double pivmin, double* zc, double* uc, double& gamma, double& nrm2) {
   double t = al[0] - theta;
-  d[0] = fabs(t) < pivmin ? -pivmin : t;
+  double dprev = fabs(t) < pivmin ? -pivmin : t;
+  zc[0] = dprev;
   for (int i = 1; i < m; ++i) {
-    t = (al[i] - theta) - be[i - 1] * be[i - 1] * fast_rcp(d[i - 1]);
-    d[i] = fabs(t) < pivmin ? -pivmin : t;
+    t = (al[i] - theta) - be[i - 1] * be[i - 1] * fast_rcp(dprev);
+    dprev = fabs(t) < pivmin ? -pivmin : t;
+    zc[i * RMAX] = dprev;
   }
   t = al[m - 1] - theta;
-  u[m - 1] = fabs(t) < pivmin ? -pivmin : t;
+  double unext = fabs(t) < pivmin ? -pivmin : t;
+  uc[(m - 1) * RMAX] = unext;
+  int kt = m - 1;
+  double best = fabs(zc[(m - 1) * RMAX] + unext - t), gk = zc[(m - 1) * RMAX] + unext - t;
   for (int i = m - 2; i >= 0; --i) {
-    t = (al[i] - theta) - be[i] * be[i] * fast_rcp(u[i + 1]);
-    u[i] = fabs(t) < pivmin ? -pivmin : t;
+    const double ai = al[i] - theta;
+    t = ai - be[i] * be[i] * fast_rcp(unext);
+    unext = fabs(t) < pivmin ? -pivmin : t;
+    uc[i * RMAX] = unext;
+    const double g = zc[i * RMAX] + unext - ai;
+    if (fabs(g) < best) { best = fabs(g); gk = g; kt = i; }
   }
-  int kt = 0;
-  double best = 1e308;
-  for (int i = 0; i < m; ++i) {
-    const double g = fabs(d[i] + u[i] - (al[i] - theta));
-    if (g < best) { best = g; kt = i; }
+  double n2 = 1.0, zp = 1.0;
+  for (int i = kt - 1; i >= 0; --i) {            // reads d_i, writes z_i in place
+    zp = -(be[i] * fast_rcp(zc[i * RMAX])) * zp;
+    zc[i * RMAX] = zp;
+    n2 = fma(zp, zp, n2);
   }
-  z[kt] = 1.0;
-  for (int i = kt - 1; i >= 0; --i) z[i] = -(be[i] * fast_rcp(d[i])) * z[i + 1];
-  for (int i = kt + 1; i < m; ++i) z[i] = -(be[i - 1] * fast_rcp(u[i])) * z[i - 1];
-  double nrm = 0.0;
-  for (int i = 0; i < m; ++i) nrm = fma(z[i], z[i], nrm);
-  nrm = 1.0 / sqrt(nrm);
-  for (int i = 0; i < m; ++i) z[i] *= nrm;
+  zc[kt * RMAX] = 1.0;
+  zp = 1.0;
+  for (int i = kt + 1; i < m; ++i) {
+    zp = -(be[i - 1] * fast_rcp(uc[i * RMAX])) * zp;
+    zc[i * RMAX] = zp;
+    n2 = fma(zp, zp, n2);
+  }
+  gamma = gk;
+  nrm2 = n2;
 }
 
 __device__ double block_sum(double v, double* red) {
@@ -207,6 +231,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   double* A = sm;                              // packed upper: row i = A[i][i..k)
   double* Q = A + (size_t)k * (k + 1) / 2;     // column j at Q + j*kq, j < QMAX
   double* S = Q + (size_t)QMAX * kq;           // Ritz coefficients, S[c*RMAX + i]
+  double* U2 = S + (size_t)QMAX * RMAX;        // twisted-factorisation scratch, same layout
   const int qcap = min(QMAX, k);
 
   double fro = 0.0, tr = 0.0;
@@ -246,8 +271,13 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   int m = 0;                 // current Krylov dimension (columns 0..m-1 of Q valid)
   bool done = false, broke = false, capped = false;
   const int first_check = max(2 * r + 4, 24);
+#ifdef MDSX_LZ_PROF
+  long long lzp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  LZ_T0(t_all);
+#endif
   while (!done) {
     const double* q = Q + (size_t)m * kq;
+    LZ_T0(t_mv);
     // w = A q with the packed symmetric A: row i = sum_{a<i} A[a][i] q_a + sum_{a>=i} A[i][a] q_a;
     // two threads per row (a split in halves, 2 accumulators per part), one shuffle
     {
@@ -268,23 +298,32 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
         if (a < cend) s0 = fma(A[off + i - a], q[a], s0);
         const double* rowp = A + (i * k - i * (i - 1) / 2) - i;
         a = max(a0, i);
-        for (; a + 1 < a1; a += 2) {            // own row part
+        double s4 = 0.0, s5 = 0.0;
+        for (; a + 3 < a1; a += 4) {            // own row part, 4 chains
           s2 = fma(rowp[a], q[a], s2);
           s3 = fma(rowp[a + 1], q[a + 1], s3);
+          s4 = fma(rowp[a + 2], q[a + 2], s4);
+          s5 = fma(rowp[a + 3], q[a + 3], s5);
         }
-        if (a < a1) s2 = fma(rowp[a], q[a], s2);
+        for (; a < a1; ++a) s2 = fma(rowp[a], q[a], s2);
+        s2 += s4;
+        s3 += s5;
       }
       double t = (s0 + s1) + (s2 + s3);
       t += __shfl_xor_sync(0xffffffffu, t, 1);
       if (i < k && hf == 0) wv[i] = t;
     }
     __syncthreads();
+    LZ_ACC(0, t_mv);
+    LZ_T0(t_cgs);
     double al = 0.0;
     for (int pass = 0; pass < 2; ++pass) {     // CGS2 against Q[:, 0..m]
       cgs_project(Q, kq, k, m + 1, wv, hv);
       al += hv[m];
       __syncthreads();
     }
+    LZ_ACC(1, t_cgs);
+    LZ_T0(t_b);
     const double b = sqrt(block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red));
     if (tid == 0) {
       alpha[m] = al;
@@ -293,6 +332,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     }
     m += 1;
     const bool full = (m >= k);
+    LZ_ACC(2, t_b);
     broke = false;
     if (!full && m < qcap) {
       if (b > 1e-13 * anorm) {
@@ -316,6 +356,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     capped = !full && m >= qcap;
     if (!(full || capped || (!broke && m >= first_check && m % CHECK_EVERY == 0))) continue;
 
+    LZ_T0(t_ck);
     // ---- top-r eigenpairs of T_m: multisection (16 threads per eigenvalue)
     const int rr = r < m ? r : m;
     double gl = 1e308, gu = -1e308, bmax = 0.0;
@@ -329,36 +370,69 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     const int grp = tid / MS, sl = tid % MS;
     if (tid < RMAX && tid < rr) { lo_s[tid] = gl; hi_s[tid] = gu; }
     __syncthreads();
-    for (int it = 0; it < 14; ++it) {              // 17^14 > 1e17: interval at fp resolution
-      const bool active = grp < rr;
-      double lo = 0.0, hi = 0.0;
-      bool below_ok = false;
-      if (active) {
-        lo = lo_s[grp];
-        hi = hi_s[grp];
-        const double x = lo + (hi - lo) * (double)(sl + 1) / (double)(MS + 1);
-        below_ok = sturm_below(alpha, beta2, m, x) <= m - 1 - grp;   // grp-th largest
+    // multisection rounds: 6 bring each bracket to ~1e-7 of the Gershgorin
+    // width; one Rayleigh-quotient step from the twisted factorisation then
+    // lands at working precision (cubic).  A quotient outside its bracket (a
+    // cluster tighter than the bracket) falls back to 8 more rounds.
+    auto msect = [&](int rounds) {
+      for (int it = 0; it < rounds; ++it) {
+        const bool active = grp < rr;
+        double lo = 0.0, hi = 0.0;
+        bool below_ok = false;
+        if (active) {
+          lo = lo_s[grp];
+          hi = hi_s[grp];
+          const double x = lo + (hi - lo) * (double)(sl + 1) / (double)(MS + 1);
+          below_ok = sturm_below(alpha, beta2, m, x) <= m - 1 - grp;   // grp-th largest
+        }
+        const unsigned okm = __ballot_sync(0xffffffffu, below_ok);
+        // counts are monotone in x: points sl < c are below the eigenvalue
+        const int c = __popc((okm >> ((threadIdx.x & 31) & ~(MS - 1))) & 0xFFFFu);
+        __syncthreads();
+        if (active && sl == 0) {
+          lo_s[grp] = c > 0 ? lo + (hi - lo) * (double)c / (double)(MS + 1) : lo;
+          hi_s[grp] = c < MS ? lo + (hi - lo) * (double)(c + 1) / (double)(MS + 1) : hi;
+        }
+        __syncthreads();
       }
-      const unsigned okm = __ballot_sync(0xffffffffu, below_ok);
-      // counts are monotone in x: points sl < c are below the eigenvalue
-      const int c = __popc((okm >> ((threadIdx.x & 31) & ~(MS - 1))) & 0xFFFFu);
-      __syncthreads();
-      if (active && sl == 0) {
-        lo_s[grp] = c > 0 ? lo + (hi - lo) * (double)c / (double)(MS + 1) : lo;
-        hi_s[grp] = c < MS ? lo + (hi - lo) * (double)(c + 1) / (double)(MS + 1) : hi;
-      }
-      __syncthreads();
-    }
-    if (tid < rr) theta[tid] = 0.5 * (lo_s[tid] + hi_s[tid]);
-    __syncthreads();
-    // eigenvectors of T_m (one thread per eigenvalue), S[c*RMAX + i]
+    };
+    LZ_T0(t_ms6);
+    msect(6);
+    LZ_ACC(5, t_ms6);
+    LZ_T0(t_rq);
+    int rq_bad = 0;
     if (tid < rr) {
-      double z[QMAX];
-      tri_twisted_vector<QMAX>(alpha, beta, m, theta[tid], pivmin + 1e-300, z);
-      for (int c = 0; c < m; ++c) S[c * RMAX + tid] = z[c];
+      const double lo = lo_s[tid], hi = hi_s[tid], th0 = 0.5 * (lo + hi);
+      double gam, n2;
+      tri_twisted(alpha, beta, m, th0, pivmin + 1e-300, S + tid, U2 + tid, gam, n2);
+      const double th1 = th0 + gam / n2;
+      if (th1 >= lo && th1 <= hi) theta[tid] = th1;
+      else rq_bad = 1;
+    }
+    const int any_bad = __syncthreads_or(rq_bad);
+    LZ_ACC(6, t_rq);
+#ifdef MDSX_LZ_PROF
+    if (blockIdx.x == 0 && tid == 0) { lzp[8] += any_bad; lzp[9] += 1; }
+#endif
+    if (any_bad) {
+      msect(8);                                    // 17^14 > 1e17: bracket at fp resolution
+      if (tid < rr) theta[tid] = 0.5 * (lo_s[tid] + hi_s[tid]);
     }
     __syncthreads();
-    if (tid < 32) {            // MGS inside eigenvalue clusters only (fixed order, warp 0)
+    // eigenvectors of T_m at the final theta (one thread per eigenvalue), S[c*RMAX + i]
+    if (tid < rr) {
+      double gam, n2;
+      tri_twisted(alpha, beta, m, theta[tid], pivmin + 1e-300, S + tid, U2 + tid, gam, n2);
+      const double sc = 1.0 / sqrt(n2);
+      for (int c = 0; c < m; ++c) S[c * RMAX + tid] *= sc;
+    }
+    __syncthreads();
+    LZ_ACC(3, t_ck);
+    LZ_T0(t_mgs);
+    // clusters are runs of adjacent Ritz values (theta is descending): skip the
+    // MGS pass entirely when no neighbours are within the cluster tolerance
+    const int adj = tid >= 1 && tid < rr && fabs(theta[tid - 1] - theta[tid]) <= 1e-3 * fabs(theta[0]);
+    if (__syncthreads_or(adj) && tid < 32) {   // MGS inside eigenvalue clusters only (fixed order, warp 0)
       const int lane = tid;
       const double ctol = 1e-3 * fabs(theta[0]);
       for (int i = 1; i < rr; ++i) {
@@ -391,7 +465,14 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     }
     __syncthreads();
     done = conv_s != 0;
+    LZ_ACC(4, t_mgs);
   }
+#ifdef MDSX_LZ_PROF
+  LZ_ACC(7, t_all);
+  if (blockIdx.x == 0 && tid == 0)
+    printf("lz prof m=%d matvec %lld cgs %lld beta+norm %lld check %lld (msect6 %lld rq %lld fallbacks %lld/%lld) mgs+resid %lld total %lld\n", m,
+           lzp[0], lzp[1], lzp[2], lzp[3], lzp[5], lzp[6], lzp[8], lzp[9], lzp[4], lzp[7]);
+#endif
   if (conv_s == 2) {          // basis capacity exhausted: the full Jacobi kernel takes over
     if (tid == 0 && status[pid].code == MDSX_OK) status[pid] = mdsx_piece_status{MDSX_NUMERICAL, 0, -2.0};
     return;
@@ -435,7 +516,7 @@ int lanczos_kmax() { return LMAX; }
 int lanczos_rmax() { return RMAX; }
 
 static size_t lanczos_bytes(int kmax, int qmax) {
-  return ((size_t)kmax * (kmax + 1) / 2 + (size_t)qmax * (kmax | 1) + (size_t)qmax * RMAX) *
+  return ((size_t)kmax * (kmax + 1) / 2 + (size_t)qmax * (kmax | 1) + 2 * (size_t)qmax * RMAX) *
          sizeof(double);
 }
 
