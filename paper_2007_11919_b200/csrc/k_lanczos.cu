@@ -28,6 +28,9 @@
 #include "mdsx_common.cuh"
 #include "piece_solvers.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 #ifdef MDSX_LZ_PROF
 #define LZ_T0(v) long long v = clock64()
 #define LZ_ACC(slot, v) if (blockIdx.x == 0 && threadIdx.x == 0) lzp[slot] += clock64() - v
@@ -75,16 +78,10 @@ __device__ int sturm_below(const double* al, const double* be2, int m, double x)
   return cnt;
 }
 
-// 1/d to full double accuracy: single-precision seed + two Newton steps
-// (quadratic: 2^-23 -> 2^-92), exact division outside the float range.
-__device__ __forceinline__ double fast_rcp(double d) {
-  const double ad = fabs(d);
-  if (!(ad > 1e-30 && ad < 1e30)) return 1.0 / d;
-  double r = (double)__frcp_rn((float)d);
-  r = r * fma(-d, r, 2.0);
-  r = r * fma(-d, r, 2.0);
-  return r;
-}
+// Reciprocal for the serial recurrences.  Measured on B200 (tools/lat_micro.cu):
+// a dependent DDIV costs ~60 clk, a float-seeded Newton reciprocal ~130 clk
+// (two F2F conversions + MUFU on the chain), so plain division wins.
+__device__ __forceinline__ double fast_rcp(double d) { return 1.0 / d; }
 
 // Eigenvector of the m x m tridiagonal T (al, be) at its eigenvalue theta by a
 // twisted factorisation of T - theta I: top-down LDL^T pivots d, bottom-up
@@ -531,7 +528,8 @@ int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int km
                         cudaStream_t st) {
   if (npieces == 0) return MDSX_OK;
   auto go = [&](auto kern, int qmax) {
-    const size_t smem = lanczos_bytes(kmax, qmax);
+    size_t smem = lanczos_bytes(kmax, qmax);
+    if (getenv("MDSX_LZ_ONE")) smem = std::max<size_t>(smem, 120 * 1024);   // experiment: 1 CTA/SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
     kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged);

@@ -90,15 +90,10 @@ __device__ __forceinline__ void gram16(const double* Bt, int nk4, double* G, int
   G[(8 * ib + gid) * SB + 8 * jb + 2 * tig + 1] = c1;
 }
 
-// 1/d to full double accuracy: single-precision seed + two Newton steps.
-__device__ __forceinline__ double fast_rcp(double d) {
-  const double ad = fabs(d);
-  if (!(ad > 1e-30 && ad < 1e30)) return 1.0 / d;
-  double r = (double)__frcp_rn((float)d);
-  r = r * fma(-d, r, 2.0);
-  r = r * fma(-d, r, 2.0);
-  return r;
-}
+// Reciprocal for the serial recurrences.  Measured on B200 (tools/lat_micro.cu):
+// a dependent DDIV costs ~60 clk, a float-seeded Newton reciprocal ~130 clk
+// (two F2F conversions + MUFU on the chain), so plain division wins.
+__device__ __forceinline__ double fast_rcp(double d) { return 1.0 / d; }
 
 // Cholesky G = L L^T of the 16 x 16 Gram in G (symmetrised on the fly) by one
 // warp: lane i holds row i in registers, column j's pivot and entries are
@@ -118,9 +113,7 @@ __device__ __forceinline__ void chol16_warp(double* G, double* rinv, int lane, i
     ok = ok && piv > 0.0;
     // 1/sqrt(piv): single-precision seed, two Newton steps (full double accuracy)
     const double pv = fmax(piv, 1e-300);
-    double rs = (pv > 1e-30 && pv < 1e30) ? (double)rsqrtf((float)pv) : rsqrt(pv);
-    rs = rs * fma(-0.5 * pv * rs, rs, 1.5);
-    rs = rs * fma(-0.5 * pv * rs, rs, 1.5);
+    const double rs = 1.0 / sqrt(pv);
     const double lij = i > j ? g[j] * rs : (i == j ? pv * rs : 0.0);
     g[j] = lij;
 #pragma unroll
@@ -157,20 +150,7 @@ __device__ int jacobi16_warp(double* H, double* Z, double floor_abs, int lane, i
         const double app = H[p * SB + p], aqq = H[q * SB + q], apq = H[p * SB + q];
         double c = 1.0, sv = 0.0, t = 0.0;
         if (fabs(apq) > floor_abs && apq * apq > eps * eps * fabs(app * aqq)) {
-          // Rutishauser rotation with Newton-refined reciprocals / square roots
-          const double tau = (aqq - app) * fast_rcp(2.0 * apq);
-          const double w = fma(tau, tau, 1.0);
-          double rs = (w < 1e30) ? (double)rsqrtf((float)w) : rsqrt(w);
-          rs = rs * fma(-0.5 * w * rs, rs, 1.5);
-          rs = rs * fma(-0.5 * w * rs, rs, 1.5);
-          const double tt = (tau >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(tau) + w * rs);
-          const double w2 = fma(tt, tt, 1.0);
-          double rc = (double)rsqrtf((float)w2);
-          rc = rc * fma(-0.5 * w2 * rc, rc, 1.5);
-          rc = rc * fma(-0.5 * w2 * rc, rc, 1.5);
-          c = rc;
-          sv = tt * rc;
-          t = tt;
+          mdsx::sym_rotation(app, aqq, apq, c, sv, t);
           rot = 1;
         }
         cs[lane] = c; sn[lane] = sv; pq[lane] = p | (q << 8);
