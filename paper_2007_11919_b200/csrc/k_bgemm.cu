@@ -5,6 +5,7 @@
 // fixed reduction order (deterministic).
 #include "mdsx_common.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 namespace {
@@ -71,6 +72,108 @@ bgemm_kernel(const GemmTask* __restrict__ tasks, const int4* __restrict__ items)
     }
 }
 
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Same contract on the fp64 tensor pipe (DMMA m8n8k4): the CTA tile BM x BN is
+// split over 8 warps in a (BM/WM) x (BN/WN) grid, each warp holding MI x NI
+// 8x8 accumulator blocks; K staged BK at a time with register prefetch of the
+// next panel; shared-memory pitches == 4 (mod 16) doubles make the fragment
+// loads conflict-free.
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(GT_THREADS)
+bgemm_dmma_kernel(const GemmTask* __restrict__ tasks, const int4* __restrict__ items) {
+  constexpr int MI = WM / 8, NI = WN / 8;
+  constexpr int WGN = BN / WN;                       // warps along n
+  constexpr int PA = BM + 4, PB = BN + 4;
+  constexpr int EA = BK * BM / GT_THREADS, EB = (BK * BN + GT_THREADS - 1) / GT_THREADS;
+  __shared__ __align__(16) double sa[BK][PA];
+  __shared__ __align__(16) double sb[BK][PB];
+  const int4 it = items[blockIdx.x];
+  const GemmTask t = tasks[it.x];
+  if (t.skip && *t.skip) return;
+  const int m0 = it.y * BM, n0 = it.z * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = (warp / WGN) * WM, wn = (warp % WGN) * WN;
+  double acc[MI][NI][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double pa[EA], pb[EB];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < EA; ++q) {
+      const int e = tid + q * GT_THREADS;
+      int kk, mm;
+      if (t.transA) { kk = e / BM; mm = e % BM; }
+      else { mm = e / BK; kk = e % BK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      pa[q] = (gm < t.M && gk < t.K)
+                  ? (t.transA ? t.A[(int64_t)gk * t.lda + gm] : t.A[(int64_t)gm * t.lda + gk])
+                  : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < EB; ++q) {
+      const int e = tid + q * GT_THREADS;
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      pb[q] = (e < BK * BN && gk < t.K && gn < t.N) ? t.B[(int64_t)gk * t.ldb + gn] : 0.0;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < EA; ++q) {
+      const int e = tid + q * GT_THREADS;
+      int kk, mm;
+      if (t.transA) { kk = e / BM; mm = e % BM; }
+      else { mm = e / BK; kk = e % BK; }
+      sa[kk][mm] = pa[q];
+    }
+#pragma unroll
+    for (int q = 0; q < EB; ++q) {
+      const int e = tid + q * GT_THREADS;
+      if (e < BK * BN) sb[e / BN][e % BN] = pb[q];
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < t.K; k0 += BK) {
+    stash();
+    __syncthreads();
+    if (k0 + BK < t.K) fetch(k0 + BK);              // next panel in flight during the DMMAs
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double af[MI], bf[NI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) af[i] = sa[4 * ks + tig][wm + 8 * i + gid];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) bf[j] = sb[4 * ks + tig][wn + 8 * j + gid];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int gm = m0 + wm + 8 * i + gid, gn = n0 + wn + 8 * j + 2 * tig + v;
+        if (gm < t.M && gn < t.N) {
+          const double dv = t.beta == 0.0 ? 0.0 : t.beta * t.D[(int64_t)gm * t.ldd + gn];
+          t.C[(int64_t)gm * t.ldc + gn] = fma(t.alpha, acc[i][j][v], dv);
+        }
+      }
+}
+
 }  // namespace
 
 namespace mdsx {
@@ -99,11 +202,18 @@ int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_item
                  const GemmBatch& b, cudaStream_t st) {
   if (b.nitems == 0) return MDSX_OK;
   mdsx::pre(h, st);
+  if (getenv("MDSX_BGEMM_FMA")) {                 // the CUDA-core variant, for comparison
+    if (b.narrow)
+      bgemm_kernel<128, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+    else
+      bgemm_kernel<64, 64><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+    return launched(h, "bgemm_kernel", st);
+  }
   if (b.narrow)
-    bgemm_kernel<128, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+    bgemm_dmma_kernel<128, 16, 16, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
   else
-    bgemm_kernel<64, 64><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
-  return launched(h, "bgemm_kernel", st);
+    bgemm_dmma_kernel<64, 64, 32, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+  return launched(h, "bgemm_dmma_kernel", st);
 }
 
 }  // namespace mdsx
