@@ -58,19 +58,44 @@ __global__ void bk_init_kernel(const BigDesc* __restrict__ bd) {
 __global__ void __launch_bounds__(KT)
 bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int col) {
   __shared__ double G[B * B];
+  __shared__ double Gp[KT / 32][B * B];
+  __shared__ double rinv[B];
   const BigDesc d = bd[blockIdx.x];
   if (done[blockIdx.x]) return;
   double* W = d.Q + col;
   const int tid = threadIdx.x;
   for (int pass = 0; pass < 2; ++pass) {
-    {  // G = W^T W (B x B): thread per entry, fixed order over rows
-      const int i = tid / B, j = tid % B;
-      double acc = 0.0;
-      for (int a = 0; a < d.k; ++a) acc = fma(W[(int64_t)a * M + i], W[(int64_t)a * M + j], acc);
-      G[tid] = acc;
+    {  // G = W^T W (B x B) on DMMA: warp w takes the k4 row steps w, w+8, ...
+       // (fragments straight from global/L2), partials summed in warp order
+      const int lane = tid & 31, warp = tid >> 5, gid = lane >> 2, tig = lane & 3;
+      double c[2][2][2] = {};
+      const int nk4 = (d.k + 3) / 4;
+      for (int kb = warp; kb < nk4; kb += KT / 32) {
+        const int a = 4 * kb + tig;
+        const double* row = W + (int64_t)a * M;
+        const double f0 = a < d.k ? row[gid] : 0.0, f1 = a < d.k ? row[8 + gid] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[0][0][0]), "+d"(c[0][0][1]) : "d"(f0), "d"(f0));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[0][1][0]), "+d"(c[0][1][1]) : "d"(f0), "d"(f1));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[1][0][0]), "+d"(c[1][0][1]) : "d"(f1), "d"(f0));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[1][1][0]), "+d"(c[1][1][1]) : "d"(f1), "d"(f1));
+      }
+#pragma unroll
+      for (int ib = 0; ib < 2; ++ib)
+#pragma unroll
+        for (int jb = 0; jb < 2; ++jb)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            Gp[warp][(8 * ib + gid) * B + 8 * jb + 2 * tig + v] = c[ib][jb][v];
+      __syncthreads();
+      double g = 0.0;
+      for (int w = 0; w < KT / 32; ++w) g += Gp[w][tid];
+      G[tid] = g;
     }
-    __syncthreads();
-    if (tid < 32) {  // shifted upper Cholesky G + delta I = R^T R (warp 0)
+    __syncthreads();    if (tid < 32) {  // shifted upper Cholesky G + delta I = R^T R (warp 0)
       double tr = 0.0;
       for (int i = 0; i < B; ++i) tr += G[i * B + i];
       const double delta = (pass == 0 ? 1e-13 : 1e-15) * tr + 1e-300;
@@ -80,7 +105,7 @@ bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int
         const double rjj = sqrt(piv > 0.0 ? piv : delta);
         __syncwarp();
         if (l > j && l < B) G[j * B + l] /= rjj;
-        if (l == j) G[j * B + j] = rjj;
+        if (l == j) { G[j * B + j] = rjj; rinv[j] = 1.0 / rjj; }
         __syncwarp();
         if (l > j && l < B) {
           const double rjl = G[j * B + l];
@@ -98,7 +123,7 @@ bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int
         double s = w[j];
 #pragma unroll
         for (int i = 0; i < j; ++i) s = fma(-x[i], G[i * B + j], s);
-        x[j] = s / G[j * B + j];
+        x[j] = s * rinv[j];
       }
 #pragma unroll
       for (int j = 0; j < B; ++j) w[j] = x[j];
