@@ -6,10 +6,9 @@
 #include "mdsx_common.cuh"
 
 #include <algorithm>
+#include <vector>
 
 namespace {
-
-constexpr int DT = 32;  // distance tile
 
 template <typename T>
 __global__ void rownorm_kernel(const T* __restrict__ X, int64_t ld, int64_t m, int p,
@@ -24,45 +23,78 @@ __global__ void rownorm_kernel(const T* __restrict__ X, int64_t ld, int64_t m, i
   nrm[i] = s;
 }
 
-// out_ij = max(na_i + nb_j - 2 a_i.b_j, 0); self: exact-zero diagonal.
-// For self distances d_ij and d_ji are computed from identical products and
-// sums (commutative), so the matrix is exactly symmetric and the reference's
-// 0.5 (d + d^T) step is the identity.
+// K1 on the fp64 tensor pipe: the cross term A B^T of a 64 x 64 output tile by
+// DMMA m8n8k4 (8 warps as 2 x 4, each 32 x 16 = 4 x 2 blocks), rows staged
+// 16 features at a time in shared memory with pitches == 4 (mod 16) doubles
+// (conflict-free fragments).  Self distances: only tiles on and below the
+// diagonal are computed and mirrored, so D is exactly symmetric (the
+// reference's (D + D^T)/2 is the identity) with half the work.
+constexpr int QT = 64, QK = 16, QP = QT + 4;
+
 template <typename T>
-__global__ void __launch_bounds__(DT * 8)
-sqdist_kernel(const T* __restrict__ A, int64_t lda, int64_t ma, const T* __restrict__ B,
-              int64_t ldb, int64_t mb, int p, const double* __restrict__ na,
-              const double* __restrict__ nb, double* __restrict__ out, int64_t ldo, int self) {
-  __shared__ double sa[DT][DT + 1];
-  __shared__ double sb[DT][DT + 1];
-  const int tx = threadIdx.x % DT, ty = threadIdx.x / DT;  // 32 x 8
-  const int64_t i0 = (int64_t)blockIdx.y * DT, j0 = (int64_t)blockIdx.x * DT;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int k0 = 0; k0 < p; k0 += DT) {
-    for (int e = threadIdx.x; e < DT * DT; e += DT * 8) {
-      const int rr = e / DT, kk = e % DT;
-      const int64_t ia = i0 + rr, jb = j0 + rr;
-      sa[rr][kk] = (ia < ma && k0 + kk < p) ? mdsx::ld_val(A + ia * lda + k0 + kk) : 0.0;
-      sb[rr][kk] = (jb < mb && k0 + kk < p) ? mdsx::ld_val(B + jb * ldb + k0 + kk) : 0.0;
+__global__ void __launch_bounds__(256)
+sqdist_dmma_kernel(const T* __restrict__ A, int64_t lda, int64_t ma, const T* __restrict__ B,
+                   int64_t ldb, int64_t mb, int p, const double* __restrict__ na,
+                   const double* __restrict__ nb, double* __restrict__ out, int64_t ldo, int self,
+                   const int2* __restrict__ tiles) {
+  __shared__ __align__(16) double sa[QK][QP];
+  __shared__ __align__(16) double sb[QK][QP];
+  const int2 tl = tiles ? tiles[blockIdx.x] : make_int2(blockIdx.y, blockIdx.x);
+  const int64_t i0 = (int64_t)tl.x * QT, j0 = (int64_t)tl.y * QT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < p; k0 += QK) {
+    // 64 rows x 16 features of each operand: thread -> (row, 4 features)
+    {
+      const int rr = tid >> 2, kq = (tid & 3) * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = kq + u;
+        const int64_t ia = i0 + rr, jb = j0 + rr;
+        sa[kk][rr] = (ia < ma && k0 + kk < p) ? mdsx::ld_val(A + ia * lda + k0 + kk) : 0.0;
+        sb[kk][rr] = (jb < mb && k0 + kk < p) ? mdsx::ld_val(B + jb * ldb + k0 + kk) : 0.0;
+      }
     }
     __syncthreads();
-    for (int kk = 0; kk < DT; ++kk) {
-      const double b = sb[tx][kk];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(sa[ty + 8 * u][kk], b, acc[u]);
+    for (int ks = 0; ks < QK / 4; ++ks) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = sa[4 * ks + tig][wm + 8 * i + gid];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = sb[4 * ks + tig][wn + 8 * j + gid];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]) : "d"(af[i]), "d"(bf[j]));
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int64_t i = i0 + ty + 8 * u, j = j0 + tx;
-    if (i < ma && j < mb) {
-      double d;
-      if (self) d = (i == j) ? 0.0 : fmax((na[i] + nb[j]) - 2.0 * acc[u], 0.0);
-      else d = fmax((-2.0 * acc[u] + na[i]) + nb[j], 0.0);
-      out[i * ldo + j] = d;
-    }
-  }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int64_t gi = i0 + wm + 8 * i + gid, gj = j0 + wn + 8 * j + 2 * tig + v;
+        if (gi >= ma || gj >= mb) continue;
+        if (self) {
+          if (gj > gi) continue;                       // lower triangle, mirrored
+          const double d = gi == gj ? 0.0 : fmax((na[gi] + nb[gj]) - 2.0 * acc[i][j][v], 0.0);
+          out[gi * ldo + gj] = d;
+          out[gj * ldo + gi] = d;
+        } else {
+          out[gi * ldo + gj] = fmax((-2.0 * acc[i][j][v] + na[gi]) + nb[gj], 0.0);
+        }
+      }
 }
 
 __global__ void rowmean_kernel(const double* __restrict__ D, int64_t m, double* __restrict__ mu) {
@@ -151,11 +183,24 @@ int launch_sqdist(mdsx_handle* h, const void* A, int64_t lda, int64_t ma, const 
       rc = launched(h, "rownorm_kernel", st);
       if (rc) return rc;
     }
-    dim3 grid((unsigned)((mb + DT - 1) / DT), (unsigned)((ma + DT - 1) / DT));
-    mdsx::pre(h, st);
-    sqdist_kernel<T><<<grid, DT * 8, 0, st>>>((const T*)A, lda, ma, (const T*)B, ldb, mb, p, na,
-                                                self ? na : nb, out, ldo, self);
-    return launched(h, "sqdist_kernel", st);
+    const int64_t ta = (ma + QT - 1) / QT, tb = (mb + QT - 1) / QT;
+    if (self) {                        // lower-triangle tile list (ti >= tj)
+      std::vector<int2> tl;
+      for (int64_t a = 0; a < ta; ++a)
+        for (int64_t b = 0; b <= a; ++b) tl.push_back(make_int2((int)a, (int)b));
+      int2* dt = (int2*)ws_alloc(h, tl.size() * sizeof(int2), st);
+      if (!dt) return (int)MDSX_CUDA;
+      if ((rc = upload(h, dt, tl.data(), tl.size() * sizeof(int2), st))) return rc;
+      mdsx::pre(h, st);
+      sqdist_dmma_kernel<T><<<(unsigned)tl.size(), 256, 0, st>>>(
+          (const T*)A, lda, ma, (const T*)B, ldb, mb, p, na, na, out, ldo, 1, dt);
+    } else {
+      dim3 grid((unsigned)tb, (unsigned)ta);
+      mdsx::pre(h, st);
+      sqdist_dmma_kernel<T><<<grid, 256, 0, st>>>((const T*)A, lda, ma, (const T*)B, ldb, mb, p,
+                                                  na, nb, out, ldo, 0, nullptr);
+    }
+    return launched(h, "sqdist_dmma_kernel", st);
   };
   return dtype == MDSX_F64 ? go(double{}) : go(float{});
 }

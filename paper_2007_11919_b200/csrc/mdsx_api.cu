@@ -171,6 +171,10 @@ static int stage_put(mdsx_handle* h, void* dst, const void* src, size_t bytes, c
   return sg.end();
 }
 
+int upload(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  return stage_put(h, dst, src, bytes, st);
+}
+
 // ------------------------------------------------------ classical pipeline
 struct ClassicalPlan {
   std::vector<PieceDesc> pd;
@@ -406,7 +410,8 @@ int mdsx_sqdist_self(mdsx_handle* h, const void* x, int dtype, int64_t ld, int64
                      double* out, int64_t ldo, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (m < 1 || p < 1) return fail(h, MDSX_INVALID_INPUT, "data must be non-empty");
-  int rc = ws_reserve(h, align_up(m * sizeof(double)));
+  const int64_t ta = (m + 63) / 64;                      // lower-triangle 64 x 64 tiles
+  int rc = ws_reserve(h, align_up(m * sizeof(double)) + align_up(ta * (ta + 1) / 2 * 8) + 512);
   if (rc) return rc;
   double* na = (double*)ws_alloc(h, m * sizeof(double), st);
   return launch_sqdist(h, x, ld, m, x, ld, m, dtype, p, na, na, out, ldo, 1, st);

@@ -51,6 +51,22 @@ class TestDistances:
         d = mds.euclidean_distance_matrix(np.random.default_rng(1).standard_normal((40, 6)))
         assert np.array_equal(d, d.T) and np.all(np.diagonal(d) == 0.0) and d.min() >= 0.0
 
+    @pytest.mark.parametrize("m,mb,p,dtype", [(200, 130, 37, np.float64), (65, 64, 16, np.float64),
+                                              (300, 77, 100, np.float32), (1, 129, 5, np.float64)])
+    def test_tensor_tiles_ragged(self, mds, m, mb, p, dtype):
+        """DMMA distance tiles: ragged rows / features, fp32 storage, several
+        tiles; self distances exactly symmetric (mirrored lower triangle)."""
+        rng = np.random.default_rng(m + p)
+        a = rng.standard_normal((m, p)).astype(dtype)
+        b = rng.standard_normal((mb, p)).astype(dtype)
+        a64, b64 = a.astype(np.float64), b.astype(np.float64)
+        ref = np.maximum((a64 * a64).sum(1)[:, None] + (b64 * b64).sum(1)[None, :] - 2 * a64 @ b64.T, 0)
+        got = mds.cross_squared_distances(a, b)
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+        d = mds.euclidean_distance_matrix(a)
+        assert np.array_equal(d, d.T) and np.all(np.diagonal(d) == 0.0)
+        assert np.abs(d - naive_sq(a64)).max() <= 1e-12 * max(1.0, d.max())
+
     def test_non_finite_and_guard(self, mds):
         with pytest.raises(mds.InvalidInputError):
             mds.euclidean_distance_matrix([[1.0, np.nan]])
