@@ -56,14 +56,49 @@ __global__ void bk_init_kernel(const BigDesc* __restrict__ bd) {
 // Cholesky-QR with a small diagonal shift (keeps rank-deficient blocks finite;
 // an all-zero column stays zero and only contributes a zero Ritz value).
 __global__ void __launch_bounds__(KT)
-bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int col) {
+bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int col,
+               int* __restrict__ noamp, int reorth) {
   __shared__ double G[B * B];
   __shared__ double Gp[KT / 32][B * B];
   __shared__ double rinv[B];
+  __shared__ double floor2[B];
   const BigDesc d = bd[blockIdx.x];
-  if (done[blockIdx.x]) return;
+  if (reorth) {                         // second normalisation: flagged pieces only
+    if (done[blockIdx.x] || noamp[blockIdx.x]) return;
+  } else {
+    __syncthreads();
+    if (noamp && threadIdx.x == 0) noamp[blockIdx.x] = 1;
+    if (done[blockIdx.x]) return;
+  }
   double* W = d.Q + col;
   const int tid = threadIdx.x;
+  __shared__ int amp;
+  if (tid == 0) amp = 0;
+  // Breakdown guard.  A block of Q beyond the first was produced from
+  // Z_s = A Q_s (columns col - B ..) by projecting out all previous blocks
+  // (CGS2).  A column whose residual keeps less than 1e-14 of its Z_s norm is
+  // rounding noise (rank-deficient / exhausted Krylov space) and is zeroed
+  // (a zero column stays zero and only adds zero Ritz values).  A column that
+  // kept less than 1e-4 is normalised but flags the piece (noamp = 0): the
+  // amplified rounding is not orthogonal to the previous blocks, so the caller
+  // projects the block once more and re-normalises it.
+  if (tid < B) floor2[tid] = 0.0;
+  if (col > 0) {
+    const int j = tid & (B - 1), part = tid >> 4;            // 16 columns x 16 row parts
+    double z2 = 0.0;
+    for (int a = part; a < d.k; a += KT / B) {
+      const double z = d.Z[(int64_t)a * M + (col - B) + j];
+      z2 = fma(z, z, z2);
+    }
+    Gp[0][tid] = z2;
+    __syncthreads();
+    if (tid < B) {
+      double t = 0.0;
+      for (int q = 0; q < KT / B; ++q) t += Gp[0][q * B + tid];
+      floor2[tid] = t;
+    }
+    __syncthreads();
+  }
   for (int pass = 0; pass < 2; ++pass) {
     {  // G = W^T W (B x B) on DMMA: warp w takes the k4 row steps w, w+8, ...
        // (fragments straight from global/L2), partials summed in warp order
@@ -95,17 +130,21 @@ bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int
       for (int w = 0; w < KT / 32; ++w) g += Gp[w][tid];
       G[tid] = g;
     }
-    __syncthreads();    if (tid < 32) {  // shifted upper Cholesky G + delta I = R^T R (warp 0)
-      double tr = 0.0;
-      for (int i = 0; i < B; ++i) tr += G[i * B + i];
-      const double delta = (pass == 0 ? 1e-13 : 1e-15) * tr + 1e-300;
+    __syncthreads();    if (tid < 32) {  // upper Cholesky G = R^T R with breakdown columns dropped (warp 0)
+      double mx = 0.0;
+      for (int i = 0; i < B; ++i) mx = fmax(mx, G[i * B + i]);
       const int l = tid;
       for (int j = 0; j < B; ++j) {
-        const double piv = G[j * B + j] + delta;
-        const double rjj = sqrt(piv > 0.0 ? piv : delta);
+        const double piv = G[j * B + j];
+        // pass 0: below the Z_s-relative floor (or 1e-20 of the block for the
+        // first block); pass 1 (unit / zero columns): plain zero test
+        const double fl = pass == 0 ? fmax(1e-28 * floor2[j], 1e-20 * mx) : 1e-20 * fmax(mx, 1e-300);
+        const bool dead = !(piv > fl);
+        if (pass == 0 && l == 0 && !dead && piv < 1e-8 * floor2[j]) amp = 1;
+        const double rjj = dead ? 0.0 : sqrt(piv);
         __syncwarp();
-        if (l > j && l < B) G[j * B + l] /= rjj;
-        if (l == j) { G[j * B + j] = rjj; rinv[j] = 1.0 / rjj; }
+        if (l > j && l < B) G[j * B + l] = dead ? 0.0 : G[j * B + l] / rjj;
+        if (l == j) { G[j * B + j] = dead ? 1.0 : rjj; rinv[j] = dead ? 0.0 : 1.0 / rjj; }
         __syncwarp();
         if (l > j && l < B) {
           const double rjl = G[j * B + l];
@@ -130,6 +169,7 @@ bk_orth_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done, int
     }
     __syncthreads();
   }
+  if (!reorth && noamp && tid == 0 && amp) noamp[blockIdx.x] = 0;
 }
 
 __global__ void bk_sym_kernel(const BigDesc* __restrict__ bd, const int* __restrict__ done) {
@@ -234,14 +274,14 @@ size_t bk_ws_bytes(const std::vector<PieceDesc>& big) {
   size_t n = big.size(), tot = 0;
   for (const auto& d : big) tot += al((size_t)d.k * (2 * M + 2 * B) * sizeof(double));
   tot += n * al((size_t)(M * M + M * B) * sizeof(double));
-  tot += al(n * sizeof(BigDesc)) + al(n * sizeof(int)) + al(n * B * sizeof(double)) * 2 +
+  tot += al(n * sizeof(BigDesc)) + 2 * al(n * sizeof(int)) + al(n * B * sizeof(double)) * 2 +
          al(n * 2 * sizeof(double)) + al(n * sizeof(mdsx_piece_status)) +
          al(n * sizeof(PieceDesc));
   // GEMM tasks / work items of one cycle (see run_big_pieces)
-  size_t ntask = n * (S + 4 * (S - 1) + 3), nitem = 0;
+  size_t ntask = n * (S + 6 * (S - 1) + 3), nitem = 0;
   for (const auto& d : big) {
     const size_t kt = (d.k + 127) / 128;
-    nitem += (S + 2 * (S - 1) + 2) * kt + 2 * (S - 1) * ((M + 127) / 128) +
+    nitem += (S + 3 * (S - 1) + 2) * kt + 3 * (S - 1) * ((M + 127) / 128) +
              ((M + 63) / 64) * ((M + 63) / 64);
   }
   tot += al(ntask * sizeof(GemmTask)) + al((nitem + n * 64) * sizeof(int4));
@@ -276,6 +316,7 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
   }
   BigDesc* dbd = (BigDesc*)ws_alloc(h, n * sizeof(BigDesc), st);
   int* done = (int*)ws_alloc(h, n * sizeof(int), st);
+  int* noamp = (int*)ws_alloc(h, n * sizeof(int), st);
   double* theta = (double*)ws_alloc(h, (size_t)n * B * sizeof(double), st);
   double* sc_est = (double*)ws_alloc(h, (size_t)n * B * sizeof(double), st);
   double* sc_gof = (double*)ws_alloc(h, (size_t)n * 2 * sizeof(double), st);
@@ -299,7 +340,7 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
   // all GEMM tasks of one cycle
   std::vector<GemmTask> tasks;
   std::vector<int4> items;
-  std::vector<GemmBatch> g1(S), g2(S), g3(S), g4(S), g5(S);
+  std::vector<GemmBatch> g1(S), g2(S), g3(S), g4(S), g5(S), g4r(S), g5r(S);
   GemmBatch g6, g7, g8;
   auto base = [&](int q) {
     GemmTask t{};
@@ -342,6 +383,12 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
       }
       (pass == 0 ? g2 : g4)[s] = append_bgemm(tasks, items, proj);
       (pass == 0 ? g3 : g5)[s] = append_bgemm(tasks, items, upd);
+      if (pass == 1) {               // re-projection after an amplifying normalisation
+        for (auto& t : proj) t.skip = noamp + (&t - proj.data());
+        for (auto& t : upd) t.skip = noamp + (&t - upd.data());
+        g4r[s] = append_bgemm(tasks, items, proj);
+        g5r[s] = append_bgemm(tasks, items, upd);
+      }
     }
   }
   {
@@ -384,7 +431,7 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
   std::vector<int> hdone(n, 0);
   for (int cyc = 0; cyc < MAX_CYCLES; ++cyc) {
     mdsx::pre(h, st);
-    bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, 0);
+    bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, 0, noamp, 0);
     if ((rc = launched(h, "bk_orth_kernel", st))) return rc;
     for (int s = 0; s < S; ++s) {
       if ((rc = launch_bgemm(h, dtasks, ditems, g1[s], st))) return rc;
@@ -394,7 +441,13 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
       if ((rc = launch_bgemm(h, dtasks, ditems, g4[s], st))) return rc;
       if ((rc = launch_bgemm(h, dtasks, ditems, g5[s], st))) return rc;
       mdsx::pre(h, st);
-      bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, (s + 1) * B);
+      bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, (s + 1) * B, noamp, 0);
+      if ((rc = launched(h, "bk_orth_kernel", st))) return rc;
+      // flagged pieces only (skip flags): project the new block once more, renormalise
+      if ((rc = launch_bgemm(h, dtasks, ditems, g4r[s], st))) return rc;
+      if ((rc = launch_bgemm(h, dtasks, ditems, g5r[s], st))) return rc;
+      mdsx::pre(h, st);
+      bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, (s + 1) * B, noamp, 1);
       if ((rc = launched(h, "bk_orth_kernel", st))) return rc;
     }
     if ((rc = launch_bgemm(h, dtasks, ditems, g6, st))) return rc;

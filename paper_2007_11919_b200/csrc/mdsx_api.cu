@@ -455,14 +455,17 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
   if (r < 1 || r > m - 1 || r > MDSX_MAX_R)
     return fail(h, MDSX_PARAM, "r must satisfy 1 <= r <= n-1, got r=" + std::to_string(r) +
                                    ", n=" + std::to_string(m));
-  if (m > MDSX_JACOBI_KMAX)
-    return fail(h, MDSX_UNSUPPORTED, "classical_mds(delta) on the GPU handles n <= " +
-                                         std::to_string(MDSX_JACOBI_KMAX));
+  const bool big = m > MDSX_JACOBI_KMAX;     // top-r by block Krylov (full spectrum: caller)
+  if (big && r > 12)
+    return fail(h, MDSX_UNSUPPORTED, "classical_mds(delta) with n > " +
+                                         std::to_string(MDSX_JACOBI_KMAX) + " handles r <= 12");
   PieceDesc d{};
   d.m = (int)m; d.k = (int)m; d.form = 1;
+  const std::vector<PieceDesc> bigv(big ? 1 : 0, d);
   const size_t need = align_up(sizeof(PieceDesc)) + align_up(m * m * sizeof(double)) * 2 +
                       align_up(m * r * sizeof(double)) + align_up(r * sizeof(double)) +
-                      align_up(m * sizeof(double)) + align_up(points_ws_bytes(1, m, r)) + 512 + 256;
+                      align_up(m * sizeof(double)) + align_up(points_ws_bytes(1, m, r)) + 512 + 256 +
+                      (big ? bk_ws_bytes(bigv) : 0);
   int rc = ws_reserve(h, need);
   if (rc) return rc;
   PieceDesc* dpd = (PieceDesc*)ws_alloc(h, sizeof(PieceDesc), st);
@@ -479,7 +482,16 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
   if ((rc = launch_double_center(h, delta, m, mu, g, Q, st))) return rc;
   if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, sizeof(mdsx_piece_status), st), "memset")))
     return rc;
-  if ((rc = launch_jacobi(h, dpd, 1, (int)m, r, Q, U, lam, estimates, gof, status, 1, st))) return rc;
+  if (big) {
+    // largest algebraic eigenpairs of the (possibly indefinite) Q; the trivial
+    // mode (Q 1 = 0) sits at eigenvalue 0 and is never among them unless the
+    // spectrum is degenerate.  G1/G2 here are trace-based: the Python layer
+    // replaces them (and the DegenerateRank decision) from the full spectrum.
+    if ((rc = run_big_pieces(h, bigv, Q, r, U, lam, estimates, gof, status, st, stage_put)))
+      return rc;
+  } else if ((rc = launch_jacobi(h, dpd, 1, (int)m, r, Q, U, lam, estimates, gof, status, 1, st))) {
+    return rc;
+  }
   return launch_points(h, nullptr, MDSX_F64, 0, 0, nullptr, dpd, 1, m, r, nullptr, U, lam, points,
                        cand, st);
 }

@@ -22,8 +22,10 @@ from . import _device as D
 from . import _lib
 from .errors import (DegenerateRankError, InvalidInputError, NumericalError, ParamError,
                      ShapeError)
-from .params import EXACT_SIZE_GUARD
+from .params import EIGENVALUE_ZERO_TOL, EXACT_SIZE_GUARD
 from .results import GofBreakdown, GowerContext, MdsConfiguration, ProcrustesTransform
+
+JACOBI_KMAX = 112        # mdsx_common.cuh MDSX_JACOBI_KMAX: largest in-kernel full spectrum
 
 
 # ---------------------------------------------------------------- distances
@@ -191,13 +193,36 @@ def classical_mds(delta, r: int, *, exact_guard: int = EXACT_SIZE_GUARD, device=
                          "use one of the partition-based algorithms instead")
     d = _delta_tensor(arr, dev)
     _validate_delta(d)
+    spectrum = None
+    if n > JACOBI_KMAX:
+        # beyond the in-kernel full-spectrum solver: the top-r pairs come from
+        # the block-Krylov kernels below; the full spectrum that G1/G2 and the
+        # DegenerateRank rule need (classical.py:88-150) from cuSOLVER's
+        # eigenvalue-only routine on the device (a library call, off the hot path)
+        q = D.empty((n, n), dev)
+        D.handle(dev).call("mdsx_double_center", d.data_ptr(), n, q.data_ptr(), D.stream_ptr(dev))
+        ev = torch.linalg.eigvalsh(q).cpu().numpy()[::-1].copy()
+        del q
+        ev = np.delete(ev, int(np.argmin(np.abs(ev))))          # the structural zero (Q 1 = 0)
+        ev[np.abs(ev) <= EIGENVALUE_ZERO_TOL * float(np.abs(ev).max(initial=0.0))] = 0.0
+        bad = np.nonzero(ev[:r] <= 0.0)[0]
+        if bad.size:
+            raise DegenerateRankError(f"eigenvalue {bad[0] + 1} of {r} is not positive "
+                                      f"({ev[bad[0]]:.3e}); reduce r")
+        spectrum = ev
     pts = D.empty((n, r), dev)
     est = D.empty((1, r), dev)
     gof = D.empty((1, 2), dev)
     st = D.status_tensor(1, dev)
     D.handle(dev).call("mdsx_classical_delta", d.data_ptr(), n, r, pts.data_ptr(), est.data_ptr(),
                        gof.data_ptr(), st.data_ptr(), D.stream_ptr(dev))
-    raise_piece_status(D.decode_status(st)[0], r)
+    rec = D.decode_status(st)[0]
+    if spectrum is not None:
+        if int(rec["code"]) != _lib.DEGENERATE:                # the host spectrum decided that
+            raise_piece_status(rec, r)
+        g1, g2 = goodness_of_fit(spectrum, r)
+        return MdsConfiguration(pts.cpu().numpy(), est.cpu().numpy()[0], g1, g2)
+    raise_piece_status(rec, r)
     g = gof.cpu().numpy()[0]
     return MdsConfiguration(pts.cpu().numpy(), est.cpu().numpy()[0], float(g[0]), float(g[1]))
 
