@@ -21,7 +21,7 @@ namespace {
 constexpr int B = 16;          // block width
 constexpr int S = 6;           // blocks per cycle
 constexpr int M = B * S;       // Krylov dimension per cycle (= Rayleigh-Ritz size, <= 104)
-constexpr int MAX_CYCLES = 8;
+constexpr int MAX_CYCLES = 24;
 constexpr int KT = 256;
 
 struct BigDesc {
@@ -295,8 +295,8 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
                    int (*put)(mdsx_handle*, void*, const void*, size_t, cudaStream_t)) {
   const int n = (int)big.size();
   if (n == 0) return MDSX_OK;
-  if (r > B - 4)
-    return fail(h, MDSX_UNSUPPORTED, "r > 12 with pieces larger than 104 (block Krylov needs b >= r+4)");
+  if (r > B)
+    return fail(h, MDSX_UNSUPPORTED, "r > 16 with pieces larger than 112 (block Krylov block width 16)");
   std::vector<BigDesc> bd(n);
   for (int q = 0; q < n; ++q) {
     const PieceDesc& d = big[q];
