@@ -71,9 +71,11 @@ __device__ int sturm_below(const double* al, const double* be2, int m, double x)
     cnt += (pn < 0.0) != (pc < 0.0);
     pm = pc;
     pc = pn;
-    const double ap = fabs(pc);
-    if (ap > 1e150) { pc *= 1e-150; pm *= 1e-150; }
-    else if (ap < 1e-150) { pc *= 1e150; pm *= 1e150; }
+    if (i & 1) {                        // rescale every other step (off the per-step chain)
+      const double ap = fabs(pc);
+      if (ap > 1e100) { pc *= 1e-100; pm *= 1e-100; }
+      else if (ap < 1e-100) { pc *= 1e100; pm *= 1e100; }
+    }
   }
   return cnt;
 }
@@ -96,40 +98,48 @@ __device__ __forceinline__ double fast_rcp(double d) { return 1.0 / d; }
 // theta + gamma_kt / |z|^2 is the Rayleigh quotient of z.  O(m).
 __device__ void tri_twisted(const double* al, const double* be, int m, double theta,
                             double pivmin, double* zc, double* uc, double& gamma, double& nrm2) {
+  // forward LDL^T pivots d (into zc) and backward UDU^T pivots u (into uc):
+  // two independent chains, interleaved to overlap their divide latencies
   double t = al[0] - theta;
   double dprev = fabs(t) < pivmin ? -pivmin : t;
   zc[0] = dprev;
-  for (int i = 1; i < m; ++i) {
-    t = (al[i] - theta) - be[i - 1] * be[i - 1] * fast_rcp(dprev);
-    dprev = fabs(t) < pivmin ? -pivmin : t;
-    zc[i * RMAX] = dprev;
-  }
   t = al[m - 1] - theta;
   double unext = fabs(t) < pivmin ? -pivmin : t;
   uc[(m - 1) * RMAX] = unext;
+  for (int i = 1, j = m - 2; i < m; ++i, --j) {
+    const double td = (al[i] - theta) - be[i - 1] * be[i - 1] * fast_rcp(dprev);
+    const double tu = (al[j] - theta) - be[j] * be[j] * fast_rcp(unext);
+    dprev = fabs(td) < pivmin ? -pivmin : td;
+    unext = fabs(tu) < pivmin ? -pivmin : tu;
+    zc[i * RMAX] = dprev;
+    uc[j * RMAX] = unext;
+  }
+  // twist: argmin |gamma_k|, gamma_k = d_k + u_k - (al_k - theta)
   int kt = m - 1;
-  double best = fabs(zc[(m - 1) * RMAX] + unext - t), gk = zc[(m - 1) * RMAX] + unext - t;
+  double gk = zc[(m - 1) * RMAX] + uc[(m - 1) * RMAX] - (al[m - 1] - theta);
+  double best = fabs(gk);
   for (int i = m - 2; i >= 0; --i) {
-    const double ai = al[i] - theta;
-    t = ai - be[i] * be[i] * fast_rcp(unext);
-    unext = fabs(t) < pivmin ? -pivmin : t;
-    uc[i * RMAX] = unext;
-    const double g = zc[i * RMAX] + unext - ai;
+    const double g = zc[i * RMAX] + uc[i * RMAX] - (al[i] - theta);
     if (fabs(g) < best) { best = fabs(g); gk = g; kt = i; }
   }
-  double n2 = 1.0, zp = 1.0;
-  for (int i = kt - 1; i >= 0; --i) {            // reads d_i, writes z_i in place
-    zp = -(be[i] * fast_rcp(zc[i * RMAX])) * zp;
-    zc[i * RMAX] = zp;
-    n2 = fma(zp, zp, n2);
+  // vector outward from the twist (z_kt = 1): both directions interleaved
+  double n2 = 1.0, zl = 1.0, zr = 1.0;
+  int il = kt - 1, ir = kt + 1;
+  while (il >= 0 || ir < m) {
+    if (il >= 0) {                              // reads d_il, writes z_il in place
+      zl = -(be[il] * fast_rcp(zc[il * RMAX])) * zl;
+      zc[il * RMAX] = zl;
+      n2 = fma(zl, zl, n2);
+      --il;
+    }
+    if (ir < m) {
+      zr = -(be[ir - 1] * fast_rcp(uc[ir * RMAX])) * zr;
+      zc[ir * RMAX] = zr;
+      n2 = fma(zr, zr, n2);
+      ++ir;
+    }
   }
   zc[kt * RMAX] = 1.0;
-  zp = 1.0;
-  for (int i = kt + 1; i < m; ++i) {
-    zp = -(be[i - 1] * fast_rcp(uc[i * RMAX])) * zp;
-    zc[i * RMAX] = zp;
-    n2 = fma(zp, zp, n2);
-  }
   gamma = gk;
   nrm2 = n2;
 }
