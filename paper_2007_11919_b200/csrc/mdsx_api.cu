@@ -31,6 +31,10 @@ int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const doub
                          int nparts, const double* corr, cudaStream_t st);
 int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
                               int r, double* out, double* corr, cudaStream_t st);
+int launch_gower_tma(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
+                     const double* mean, const double* M, const double* v, double* out,
+                     double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
+                     bool norm32);
 int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
                       const double* mean, const double* M, const double* v, double* out,
                       double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
@@ -705,8 +709,13 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
       (reinterpret_cast<uintptr_t>(data) & 15) == 0 && h->num_sms * r * sizeof(double) <= recenter_ws_bytes(r)) {
     int nparts = 0;
     // the landmark configuration is centred -> v ~ 0: fp32 norms are exact enough
-    if ((rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
-                                st, dtype == MDSX_F32 && !getenv("MDSX_GOWER_NORM64"))))
+    const bool n32 = dtype == MDSX_F32 && !getenv("MDSX_GOWER_NORM64");
+    if ((rc = launch_gower_tma(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
+                               st, n32)))
+      return rc;
+    if (nparts == 0 &&
+        (rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
+                                st, n32)))
       return rc;
     if (nparts > 0) {
       if ((rc = launch_landmark_overwrite(h, base, sample_idx, l, r, out, corr, st))) return rc;
