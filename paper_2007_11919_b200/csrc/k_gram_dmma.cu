@@ -11,6 +11,7 @@
 // mirrored to the upper -> exactly symmetric; fixed reduction order.
 #include "mdsx_common.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace {
@@ -154,6 +155,165 @@ gram_dmma_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __re
   }
 }
 
+
+// ---- large k (config 5, p = 784): 64 x 64 output tiles of the Gram, rows
+// gathered with cp.async into a 3-deep ring of raw column slices (the row
+// indices of a chunk are loaded in parallel and broadcast), converted and
+// shifted by x0 at fragment-load time.  Same arithmetic and outputs as
+// gram_dmma_kernel, without its dependent index -> value load chains.
+constexpr int TS_KC = 32;                 // rows per chunk
+constexpr int TS_NS = 3;                  // ring depth
+
+template <typename T>
+struct TsPitch {                          // conflict-free fragment pitch (elements)
+  static constexpr int value = sizeof(T) == 4 ? 72 : 68;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NT)
+gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
+                       const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
+                       const int4* __restrict__ tiles, double* __restrict__ A,
+                       double* __restrict__ mu_all, mdsx_piece_status* __restrict__ status) {
+  constexpr int P = TsPitch<T>::value;
+  constexpr int SLICE = TS_KC * P;                       // elements per slice per stage
+  extern __shared__ __align__(16) unsigned char ts_smem[];
+  T* ring = reinterpret_cast<T*>(ts_smem);               // TS_NS x 2 slices
+  __shared__ double x0a[TT], x0b[TT], sa[TT], sb[TT];
+  __shared__ int bad;
+  const int4 tl = tiles[blockIdx.x];
+  const PieceDesc d = pd[tl.x];
+  const int ti = tl.y, tj = tl.z, k = d.k, m = d.m;
+  const bool diag = ti == tj;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 1, wc = warp & 1;              // warp sub-tile: rows 16*wr.., cols 32*wc..
+  const int64_t* ridx = row_idx + d.row_off;
+  const int ca = ti * TT, cb = tj * TT;
+  const int na = min(TT, k - ca), nb = min(TT, k - cb);  // valid columns of each slice
+  const int pa16 = (int)((size_t)na * sizeof(T) / 16), pb16 = (int)((size_t)nb * sizeof(T) / 16);
+  const int nchunks = (m + TS_KC - 1) / TS_KC;
+
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      const int r0 = c * TS_KC, nr = min(TS_KC, m - r0);
+      T* dst_a = ring + (size_t)(c % TS_NS) * 2 * SLICE;
+      T* dst_b = dst_a + SLICE;
+      // warp w copies rows w, w+8, w+16, w+24; their indices loaded in parallel
+      const int myr = warp + 8 * lane;
+      const int64_t myidx = (lane < TS_KC / 8 && myr < nr) ? ridx[r0 + myr] : 0;
+#pragma unroll
+      for (int i = 0; i < TS_KC / 8; ++i) {
+        const int rr = warp + 8 * i;
+        const int64_t gi = __shfl_sync(0xffffffffu, myidx, i);
+        if (rr < nr) {
+          const char* src = reinterpret_cast<const char*>(X + gi * ld);
+          for (int q = lane; q < pa16 + (diag ? 0 : pb16); q += 32) {
+            const bool second = q >= pa16;
+            const int qq = second ? q - pa16 : q;
+            const char* s16 = src + (size_t)(second ? cb : ca) * sizeof(T) + 16 * qq;
+            char* d16 = reinterpret_cast<char*>((second ? dst_b : dst_a) + (size_t)rr * P) + 16 * qq;
+            const unsigned sa_ = (unsigned)__cvta_generic_to_shared(d16);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa_), "l"(s16));
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+#pragma unroll
+  for (int c = 0; c < TS_NS - 1; ++c) issue(c);
+  if (tid == 0) bad = 0;
+  if (tid < TT) {
+    const T* r0p = X + ridx[0] * ld;
+    x0a[tid] = tid < na ? (double)r0p[ca + tid] : 0.0;
+    x0b[tid] = tid < nb ? (double)r0p[cb + tid] : 0.0;
+    sa[tid] = 0.0;
+    sb[tid] = 0.0;
+  }
+  __syncthreads();
+  double xa4[2], xb4[4];                                   // per-lane shifts of the fragment columns
+#pragma unroll
+  for (int i = 0; i < 2; ++i) xa4[i] = x0a[wr * 16 + i * 8 + gid];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) xb4[j] = diag ? x0a[wc * 32 + j * 8 + gid] : x0b[wc * 32 + j * 8 + gid];
+  bool oka[2], okb[4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) oka[i] = wr * 16 + i * 8 + gid < na;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) okb[j] = wc * 32 + j * 8 + gid < (diag ? na : nb);
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int c = 0; c < nchunks; ++c) {
+    issue(c + TS_NS - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(TS_NS - 1));
+    __syncthreads();
+    const T* sta = ring + (size_t)(c % TS_NS) * 2 * SLICE;
+    const T* stb = diag ? sta : sta + SLICE;
+    const int nr = min(TS_KC, m - c * TS_KC);
+    if (tid < TT) {                                        // column sums of the centred chunk
+      double s = 0.0;
+      if (tid < na)
+        for (int rr = 0; rr < nr; ++rr) s += (double)sta[rr * P + tid] - x0a[tid];
+      sa[tid] += s;
+    } else if (tid < 2 * TT && !diag) {
+      const int cc = tid - TT;
+      double s = 0.0;
+      if (cc < nb)
+        for (int rr = 0; rr < nr; ++rr) s += (double)stb[rr * P + cc] - x0b[cc];
+      sb[cc] += s;
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < TS_KC; k4 += 4) {
+      const int row = k4 + tig;
+      const bool rok = row < nr;
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double v = (rok && oka[i]) ? (double)sta[row * P + wr * 16 + i * 8 + gid] : 0.0;
+        af[i] = (rok && oka[i]) ? v - xa4[i] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double v = (rok && okb[j]) ? (double)stb[row * P + wc * 32 + j * 8 + gid] : 0.0;
+        bf[j] = (rok && okb[j]) ? v - xb4[j] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();                                       // slot refilled next iteration
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  if (diag && tid < TT) sb[tid] = sa[tid];
+  if (tid < TT && tid < na && !isfinite(sa[tid])) bad = 1;
+  __syncthreads();
+  const double inv_m = 1.0 / (double)m;
+  double* out = A + d.a_off;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int li = wr * 16 + i * 8 + gid, lj = wc * 32 + j * 8 + 2 * tig + v;
+        const int gi = ca + li, gj = cb + lj;
+        if (gi < k && gj < k && (!diag || gi >= gj)) {
+          const double cv = fma(-sa[li] * inv_m, sb[lj], acc[i][j][v]);
+          out[(int64_t)gi * k + gj] = cv;
+          out[(int64_t)gj * k + gi] = cv;
+        }
+      }
+  if (diag) {
+    if (tid < TT && ca + tid < k) mu_all[(int64_t)d.id * p + ca + tid] = x0a[tid] + sa[tid] * inv_m;
+    if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
+  }
+}
 
 // ---- one CTA per piece for k <= 104 (the config 2/3 shape).  The lower
 // triangle of the k x k Gram in 8x8 blocks (NB*(NB+1)/2 block pairs) is split
@@ -379,6 +539,21 @@ int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, in
                      const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
                      double* A, double* mu, mdsx_piece_status* status, cudaStream_t st) {
   if (ntiles == 0) return MDSX_OK;
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  if (((size_t)p * es) % 16 == 0 && ((size_t)ld * es) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(data) & 15) == 0 && !getenv("MDSX_GRAM_TILED_SYNC")) {
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      const size_t smem = (size_t)TS_NS * 2 * TS_KC * TsPitch<T>::value * sizeof(T);
+      cudaFuncSetAttribute(gram_tile_async_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      mdsx::pre(h, st);
+      gram_tile_async_kernel<T><<<ntiles, NT, smem, st>>>((const T*)data, ld, p, row_idx, pd, tiles,
+                                                          A, mu, status);
+      return launched(h, "gram_tile_async_kernel", st);
+    };
+    return dtype == MDSX_F64 ? go(double{}) : go(float{});
+  }
   mdsx::pre(h, st);
   if (dtype == MDSX_F64)
     gram_dmma_kernel<double><<<ntiles, NT, 0, st>>>((const double*)data, ld, p, row_idx, pd, tiles,
