@@ -12,6 +12,8 @@
 // as classical.py:75-85.  The sign rule of linalg.py:139-146 is applied to
 // the output columns.
 #include "mdsx_common.cuh"
+
+#include <cstdlib>
 #include "piece_solvers.cuh"
 
 #include <algorithm>
@@ -152,6 +154,129 @@ gram_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restric
     }
 }
 
+
+// ---- form 1 on the fp64 tensor pipe: 64 x 64 tiles of Q = Y Y^T (Y = the
+// piece's rows centred by the piece means), K = features in chunks of 32
+// staged by cp.async into a 3-deep ring (each thread copies fixed rows, so the
+// row indices are read once), converted and centred at fragment-load time.
+// 8 warps as 2 x 4, 32 x 16 outputs each (m8n8k4, 4 A + 2 B fragments per
+// 8 DMMA).  Pitch 36 elements: conflict-free fragment loads (fp32 and fp64).
+constexpr int RA_FC = 32;                 // features per chunk
+constexpr int RA_NS = 3;
+constexpr int RA_P = 36;
+
+__device__ __forceinline__ void dmma_r(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+gram_rows_async_kernel(const T* __restrict__ X, int64_t ld, int p,
+                       const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
+                       const double* __restrict__ mu_all, const int4* __restrict__ tiles,
+                       double* __restrict__ A) {
+  constexpr int SLICE = GT * RA_P;
+  extern __shared__ __align__(16) unsigned char ra_smem[];
+  T* ring = reinterpret_cast<T*>(ra_smem);            // RA_NS x 2 slices
+  const int4 tl = tiles[blockIdx.x];
+  const PieceDesc d = pd[tl.x];
+  const int ti = tl.y, tj = tl.z, k = d.k;
+  const bool diag = ti == tj;
+  const double* mu = mu_all + (int64_t)d.id * p;
+  const int64_t* ridx = row_idx + d.row_off;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;            // warp sub-tile: rows 32*wr.., cols 16*wc..
+  const int nchunks = (p + RA_FC - 1) / RA_FC;
+  // copy duty: thread t handles row (t >> 1) of the tile pair (0..63: block ti,
+  // 64..127: block tj) and every other 16-byte piece of it, starting at (t & 1)
+  const int crow = tid >> 1, cpart = tid & 1;          // 128 rows x 2 halves
+  const bool second = crow >= GT;
+  const int lrow = second ? crow - GT : crow;
+  const int grow = (second ? tj : ti) * GT + lrow;     // row within the piece
+  const bool active = (!second || !diag) && grow < k;
+  const char* src = active ? reinterpret_cast<const char*>(X + ridx[grow] * ld) : nullptr;
+  constexpr int PCS = RA_FC * (int)sizeof(T) / 16;     // 16-byte pieces per row per chunk
+  auto issue = [&](int c) {
+    if (c < nchunks && active) {
+      T* dst = ring + (size_t)(c % RA_NS) * 2 * SLICE + (second ? SLICE : 0) + (size_t)lrow * RA_P;
+      const int f0 = c * RA_FC;
+      const int nbytes = min(RA_FC, p - f0) * (int)sizeof(T);
+      for (int q = cpart; q < PCS; q += 2) {
+        if (16 * q < nbytes) {
+          const unsigned sa_ = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + 16 * q);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa_),
+                       "l"(src + (size_t)f0 * sizeof(T) + 16 * q));
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+#pragma unroll
+  for (int c = 0; c < RA_NS - 1; ++c) issue(c);
+  bool oka[4], okb[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) oka[i] = ti * GT + wr * 32 + i * 8 + gid < k;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) okb[j] = tj * GT + wc * 16 + j * 8 + gid < k;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    issue(c + RA_NS - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(RA_NS - 1));
+    __syncthreads();
+    const T* sta = ring + (size_t)(c % RA_NS) * 2 * SLICE;
+    const T* stb = diag ? sta : sta + SLICE;
+    const int f0 = c * RA_FC;
+    double mr[RA_FC / 4];                                // this lane's chunk means, loaded together
+#pragma unroll
+    for (int ks = 0; ks < RA_FC / 4; ++ks) mr[ks] = f0 + 4 * ks + tig < p ? mu[f0 + 4 * ks + tig] : 0.0;
+#pragma unroll
+    for (int ks = 0; ks < RA_FC / 4; ++ks) {
+      const int f = 4 * ks + tig;
+      const bool fok = f0 + f < p;
+      const double m = mr[ks];
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = fok && oka[i];
+        const double v = ok ? (double)sta[(wr * 32 + i * 8 + gid) * RA_P + f] : 0.0;
+        af[i] = ok ? v - m : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool ok = fok && okb[j];
+        const double v = ok ? (double)stb[(wc * 16 + j * 8 + gid) * RA_P + f] : 0.0;
+        bf[j] = ok ? v - m : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_r(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  double* out = A + d.a_off;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int x = ti * GT + wr * 32 + i * 8 + gid, y = tj * GT + wc * 16 + j * 8 + 2 * tig + v;
+        if (x < k && y < k) {
+          out[(int64_t)x * k + y] = acc[i][j][v];
+          if (!diag) out[(int64_t)y * k + x] = acc[i][j][v];
+        }
+      }
+}
+
 // ------------------------------------------------------------- K3 Jacobi
 // Re-solve, with the full Jacobi method, the pieces the Lanczos kernel flagged
 // (status NUMERICAL with value -2: Krylov basis capacity exhausted).
@@ -217,6 +342,21 @@ int launch_gram(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                 const int64_t* row_idx, const PieceDesc* pd, const double* mu, const int4* tiles,
                 int ntiles, double* A, cudaStream_t st) {
   if (ntiles == 0) return MDSX_OK;
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  if (((size_t)p * es) % 16 == 0 && ((size_t)ld * es) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(data) & 15) == 0 && !getenv("MDSX_GRAM_ROWS_FMA")) {
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      const size_t smem = (size_t)RA_NS * 2 * GT * RA_P * sizeof(T);
+      cudaFuncSetAttribute(gram_rows_async_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      mdsx::pre(h, st);
+      gram_rows_async_kernel<T><<<ntiles, 256, smem, st>>>((const T*)data, ld, p, row_idx, pd, mu,
+                                                           tiles, A);
+      return launched(h, "gram_rows_async_kernel", st);
+    };
+    return dtype == MDSX_F64 ? go(double{}) : go(float{});
+  }
   mdsx::pre(h, st);
   if (dtype == MDSX_F64)
     gram_kernel<double><<<ntiles, 256, 0, st>>>((const double*)data, ld, p, row_idx, pd, mu, tiles, A);
