@@ -63,13 +63,19 @@ procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict_
       for (int j = i + 1; j < r; ++j) {
         const double x = lane < r ? B[lane * r + i] : 0.0;
         const double y = lane < r ? B[lane * r + j] : 0.0;
-        const double al = mdsx::warp_sum(x * x);
-        const double be = mdsx::warp_sum(y * y);
-        const double ga = mdsx::warp_sum(x * y);
-        if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        // the three column dots reduced together (interleaved shuffle trees)
+        double al = x * x, be = y * y, ga = x * y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga != 0.0 && ga * ga > 1e-30 * (al * be)) {
+          // t = tan of the rotation angle, |t| <= 1 (one sqrt, one divide, one rsqrt)
+          const double h = 0.5 * (be - al);
+          const double t = ga / (h + copysign(sqrt(fma(h, h, ga * ga)), h == 0.0 ? 1.0 : h));
+          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
           if (lane < r) {
             B[lane * r + i] = c * x - s * y;
             B[lane * r + j] = s * x + c * y;
