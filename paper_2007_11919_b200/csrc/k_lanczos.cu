@@ -154,6 +154,24 @@ __device__ void tri_twisted(const double* al, const double* be, int m, double th
   nrm2 = n2;
 }
 
+// three sums over the CTA at once (fixed order), results in every thread
+__device__ void block_sum3(double (&v)[3], double* red3) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) v[c] = mdsx::warp_sum(v[c]);
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) red3[c * (LT / 32) + warp] = v[c];
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double s = 0.0;
+    for (int w = 0; w < LT / 32; ++w) s += red3[c * (LT / 32) + w];
+    v[c] = s;
+  }
+  __syncthreads();
+}
+
 __device__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = mdsx::warp_sum(v);
@@ -223,7 +241,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   __shared__ double as_[QMAX + 8], bs_[QMAX + 8], bq_[QMAX + 8], ar_[QMAX + 8], br_[QMAX + 8];
   __shared__ double gl_s, gu_s;
   __shared__ int rounds_s;
-  __shared__ double red[LT / 32];
+  __shared__ double red[LT / 32], red3[3 * (LT / 32)];
   __shared__ double trace_s, anorm_s;
   __shared__ int conv_s;
 
@@ -337,15 +355,37 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     __syncthreads();
     LZ_ACC(0, t_mv);
     LZ_T0(t_cgs);
-    double al = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {     // CGS2 against Q[:, 0..m]
+    // three-term part first (alpha = q_j.y, gamma = q_{j-1}.y, |y|^2 in one
+    // reduction), then ONE classical Gram-Schmidt pass against Q[:, 0..m];
+    // a second pass only when the first removed more than half of the norm
+    // (DGKS, "twice is enough") or the three-term estimate is unreliable
+    double al, nw0;
+    {
+      const double yv = tid < k ? wv[tid] : 0.0;
+      const double qv = tid < k ? q[tid] : 0.0;
+      const double pv = (tid < k && m > 0) ? Q[(size_t)(m - 1) * kq + tid] : 0.0;
+      double s3[3] = {qv * yv, pv * yv, yv * yv};
+      block_sum3(s3, red3);
+      al = s3[0];
+      const double ga = s3[1];
+      nw0 = s3[2] - al * al - ga * ga;
+      if (!(nw0 > 1e-4 * s3[2])) nw0 = 1e308;        // cancellation: force the second pass
+      if (tid < k) wv[tid] = fma(-al, qv, fma(-ga, pv, yv));
+      __syncthreads();
+    }
+    cgs_project(Q, kq, k, m + 1, wv, hv);
+    al += hv[m];
+    __syncthreads();
+    double nw = block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red);
+    if (nw < 0.5 * nw0) {
       cgs_project(Q, kq, k, m + 1, wv, hv);
       al += hv[m];
       __syncthreads();
+      nw = block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red);
     }
     LZ_ACC(1, t_cgs);
     LZ_T0(t_b);
-    const double b = sqrt(block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red));
+    const double b = sqrt(nw);
     if (tid == 0) {
       alpha[m] = al;
       beta[m] = b;
@@ -905,27 +945,7 @@ __device__ __noinline__ void tw_charpoly(const double* as, const double* bs, con
 // its bracket take the robust path: multisection to full precision and the
 // residual from the twisted eigenvectors.
 __device__ __noinline__ void rg_checker(RgShared& sh, double* S, double* U2, double* U3, int k, int r, int lane) {
-#ifdef MDSX_LZ_PROF
-  for (int rep = 0; rep < 2; ++rep) {
-    long long g0 = clock64();
-    double gl = 1e308, gu = -1e308, bmax = 0.0;
-    const int m = 24;
-    for (int i = lane; i < m; i += 32) {
-      const double off = (i > 0 ? fabs(sh.beta[i - 1]) : 0.0) + (i + 1 < m ? fabs(sh.beta[i]) : 0.0);
-      gl = fmin(gl, sh.alpha[i] - off);
-      gu = fmax(gu, sh.alpha[i] + off);
-      if (i + 1 < m) bmax = fmax(bmax, sh.beta2[i]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
-      gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
-      bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-    }
-    long long g1 = clock64();
-    if (blockIdx.x == 0 && lane == 0) printf("early gersh rep %d: %lld (%g)\n", rep, g1 - g0, gl + gu + bmax);
-  }
-#endif
+
   int cp = max(2 * r + 4, 24);
   int last = 0;
   bool have_prev = false;
@@ -954,13 +974,7 @@ __device__ __noinline__ void rg_checker(RgShared& sh, double* S, double* U2, dou
     const double* be = sh.beta;
     const double* be2 = sh.beta2;
     const int rr = r < m ? r : m;
-    double gl, gu, bmax;
-#ifdef MDSX_LZ_PROF
-    long long tg[3];
-    for (int rep = 0; rep < 2; ++rep) {
-      tg[rep] = clock64();
-#endif
-    gl = 1e308; gu = -1e308; bmax = 0.0;
+    double gl = 1e308, gu = -1e308, bmax = 0.0;
     for (int i = lane; i < m; i += 32) {
       const double off = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < m ? fabs(be[i]) : 0.0);
       gl = fmin(gl, al[i] - off);
@@ -973,11 +987,6 @@ __device__ __noinline__ void rg_checker(RgShared& sh, double* S, double* U2, dou
       gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
       bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
     }
-#ifdef MDSX_LZ_PROF
-    }
-    tg[2] = clock64();
-    if (blockIdx.x == 0 && lane == 0) printf("gersh rep0 %lld rep1 %lld\n", tg[1] - tg[0], tg[2] - tg[1]);
-#endif
     // exact power-of-two scaling of T into [-1, 1]
     int ex;
     frexp(fmax(fmax(fabs(gl), fabs(gu)), 1e-300), &ex);
