@@ -298,6 +298,48 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   if ((rc = sg.end())) return rc;
   if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, np * sizeof(mdsx_piece_status), st), "memset")))
     return rc;
+  // Piece pipeline (the BASELINE D&C / fast shapes: every piece form 0 with
+  // k <= 104, Lanczos route): chunks of pieces alternate between the caller's
+  // stream and a second one, so one chunk's latency-bound eigensolver runs
+  // next to another chunk's HBM / tensor-bound Gram and points kernels.
+  // Same kernels and per-piece arithmetic, so results are unchanged.
+  {
+    const char* eig = getenv("MDSX_EIG");
+    const char* pc = getenv("MDSX_PIPE_CHUNKS");
+    const bool simple = piece_gram && cp.pd_jac.empty() && cp.pd_big.empty() && cp.pd_f1.empty() &&
+                        (int)cp.pd_g.size() == np && (int)cp.pd_sub.size() == np &&
+                        !(eig && strcmp(eig, "subspace") == 0);
+    int nc = pc ? atoi(pc) : 2;                       // measured best on dc2 / fast3
+    nc = std::min(nc, np / (2 * h->num_sms));          // >= two waves of pieces per chunk
+    if (simple && nc > 1) {
+      if (!h->aux) {
+        if ((rc = cuda_check(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking), "stream")))
+          return rc;
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+      }
+      cudaEventRecord(h->ev_fork, st);
+      cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
+      for (int c = 0; c < nc; ++c) {
+        const int j0 = (int)((int64_t)np * c / nc), j1 = (int)((int64_t)np * (c + 1) / nc);
+        const int n = j1 - j0;
+        cudaStream_t s = (c & 1) ? h->aux : st;
+        if ((rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd + j0, n, A, mu, status, s)))
+          return rc;
+        if ((rc = launch_lanczos_smem(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
+                                      status, 0, 0, s)))
+          return rc;
+        if ((rc = launch_jacobi_fallback(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
+                                         status, s)))
+          return rc;
+        if ((rc = launch_points(h, data, dtype, ld, p, ridx, dpd + j0, n, cp.max_m, r, mu, U, lam,
+                                points, cand, s, true)))
+          return rc;
+      }
+      cudaEventRecord(h->ev_join, h->aux);
+      return cuda_check(h, cudaStreamWaitEvent(st, h->ev_join, 0), "pipeline join");
+    }
+  }
   // form 0: DMMA Gram with fused shifted means;  form 1: means pass + row Gram
   if (piece_gram && (rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd_g, (int)cp.pd_g.size(),
                                             A, mu, status, st)))
@@ -370,6 +412,9 @@ void mdsx_destroy(mdsx_handle* h) {
   if (h->pinned_free) cudaEventDestroy(h->pinned_free);
   for (auto& t : h->timed) { cudaEventDestroy(t.second.first); cudaEventDestroy(t.second.second); }
   for (auto e : h->event_pool) cudaEventDestroy(e);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 

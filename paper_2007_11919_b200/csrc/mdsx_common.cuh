@@ -31,6 +31,9 @@ struct mdsx_handle {
   std::vector<cudaEvent_t> event_pool;
   std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> timed;
   std::vector<std::pair<std::string, std::pair<double, int64_t>>> report;
+  // second stream for the piece pipeline (run_classical), created on first use
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace mdsx {
