@@ -73,16 +73,16 @@ WORKLOADS = {
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
 TRAFFIC = {
-    ("dc2", "lanczos_smem_kernel"): {"bytes": (84.195 + 5.184) * 1e6,
-                                     "src": "profiles/r01_ncu_full_dc2.txt"},
-    ("dc2", "gram_piece_kernel"): {"bytes": (878.910 + 72.684) * 1e6,
-                                   "src": "profiles/r01_ncu_full_dc2.txt"},
-    ("dc2", "points_rows_kernel"): {"bytes": (896.882 + 77.644) * 1e6,
-                                    "src": "profiles/r01_ncu_full_dc2.txt"},
-    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.048 + 785.069) * 1e6,
-                                       "src": "profiles/r01_ncu_full_interp4.txt"},
-    ("interp4", "subtract_mean_kernel"): {"bytes": (800.045 + 740.962) * 1e6,
-                                          "src": "profiles/r01_ncu_full_interp4.txt"},
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (40.937 + 0.073) * 1e6,
+                                     "src": "profiles/r01b_ncu_full_dc2.txt"},
+    ("dc2", "gram_piece_kernel"): {"bytes": (439.812 + 29.598) * 1e6,
+                                   "src": "profiles/r01b_ncu_full_dc2.txt"},
+    ("dc2", "points_rows_kernel"): {"bytes": (448.773 + 35.181) * 1e6,
+                                    "src": "profiles/r01b_ncu_full_dc2.txt"},
+    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.050 + 784.856) * 1e6,
+                                       "src": "profiles/r01b_ncu_full_interp4.txt"},
+    ("interp4", "subtract_mean_kernel"): {"bytes": (800.045 + 741.575) * 1e6,
+                                          "src": "profiles/r01b_ncu_full_interp4.txt"},
 }
 
 
@@ -275,9 +275,10 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
             k = min(m, p)
             if steps > 0:
                 j = np.arange(int(steps))
-                fl += float(np.sum(2.0 * k * k + 8.0 * k * (j + 1)))
+                fl += float(np.sum(2.0 * k * k + 4.0 * k * (j + 1) + 6.0 * k))
         return {"bound": "tensor", "flops": fl,
-                "model": "sum over Krylov steps of 2k^2 (matvec) + 8k(j+1) (CGS2)"}
+                "model": "sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
+                         "+ 6k (three-term part)"}
     if kernel in ("gower_affine_kernel", "gower_stream_kernel", "gower_bulk_kernel"):
         n = w["n"]
         return {"bound": "hbm", "bytes": n * p * esize + n * r * 8,
@@ -491,6 +492,9 @@ def run_ours(args, w):
                     "work_model": work["model"]}
         if roof is not None:
             roof["share_of_kernel_time"] = ms_k / total_k
+            if w["algo"] in ("divide", "fast"):
+                roof["note"] = ("two-stream piece pipeline: launch durations include time "
+                                "shared with the other stream's kernels")
             roof["avg_launch_ms"] = per_launch_ms
             traffic = TRAFFIC.get((args.workload, dom))
             if traffic:
