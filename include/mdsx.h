@@ -47,7 +47,8 @@ enum mdsx_status {
   MDSX_NUMERICAL = 4,      /* NumericalError */
   MDSX_DEGENERATE = 5,     /* DegenerateRankError */
   MDSX_CUDA = 6,           /* CUDA runtime failure */
-  MDSX_UNSUPPORTED = 7     /* shape outside what this build handles */
+  MDSX_UNSUPPORTED = 7,    /* shape outside what this build handles */
+  MDSX_FORMAT = 8          /* FormatError: a file does not match its declared format */
 };
 
 /* Element type of data matrices: the reference coerces to float64
@@ -190,6 +191,37 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
                        double* out, double* estimates, double* gof,
                        mdsx_piece_status* status, double* cond, int32_t* flags,
                        void* stream);
+
+/* ---- file ingestion (replaces dataio.py:42-58, 68-82, 102-130) ----------
+ * Host-side parsing; no device is needed except for mdsx_idx_load_images.
+ * On failure `msg` (msg_len bytes, NUL-terminated) carries the reference's
+ * FormatError text. */
+
+/* IDX header check: expect_kind 3 = images (magic 0x00000803, dims count,
+ * height, width; dataio.py:42-58) or 1 = labels (magic 0x00000801, dim count;
+ * dataio.py:68-82).  Validates the magic and the payload size against the file
+ * size.  height/width are set to 1 for labels. */
+int mdsx_idx_probe(const char* path, int32_t expect_kind, int64_t* count, int32_t* height,
+                   int32_t* width, char* msg, int64_t msg_len);
+
+/* Stream an IDX image payload straight into a device matrix `out`
+ * (count x height*width, row-major, dtype MDSX_F64 / MDSX_F32), each element
+ * scale * pixel: the file is read in chunks into two pinned buffers, the
+ * unsigned bytes cross PCIe (1/8 of the float64 volume) and a kernel widens
+ * them on the device; reads of chunk i+1 overlap the copy and kernel of chunk i.
+ * Synchronises `stream` before returning (the pinned buffers are released). */
+int mdsx_idx_load_images(mdsx_handle* h, const char* path, void* out, int dtype, double scale,
+                         void* stream);
+
+/* Numeric CSV (dataio.py:102-130), two calls: with out == NULL it counts the
+ * data rows and the fields of the first data row (rows, cols); with out (rows x
+ * cols doubles, host) it parses every field (correctly rounded, Python float()
+ * syntax: surrounding whitespace and double quotes stripped, inf/nan accepted,
+ * no hexadecimal) with `threads` host threads and reports the FIRST bad line in
+ * file order: "ragged row at line N: expected W fields, got K" / "invalid
+ * number at line N: ..." / "no data rows" (MDSX_FORMAT). */
+int mdsx_csv_read(const char* path, int32_t has_header, int32_t threads, double* out,
+                  int64_t* rows, int64_t* cols, char* msg, int64_t msg_len);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,10 @@ names, arguments and exceptions; all arithmetic runs in libmdsx.so
 
 from .algorithms import (DivideRun, FastRun, InterpolationRun, divide_and_conquer_mds,
                          fast_mds, interpolation_mds, run_algorithm)
+from .dataio import (IdxImageSet, RunManifest, load_idx_images, pair_images_labels,
+                     read_csv_matrix, read_idx_images, read_idx_labels, read_manifest,
+                     write_configuration, write_csv_matrix, write_idx_images, write_idx_labels,
+                     write_manifest)
 from .errors import (DegenerateRankError, FormatError, InvalidInputError, JoinError, MdsError,
                      MetricError, NumericalError, ParamError, ShapeError, UsageError)
 from .params import (ALGORITHM_NAMES, EXACT_SIZE_GUARD, AlgorithmParams)
@@ -33,4 +37,7 @@ __all__ = [
     "fast_stats", "fit_procrustes", "gof_breakdown", "goodness_of_fit", "gower_context",
     "gower_interpolate", "interpolation_mds", "plan_divide_conquer", "plan_fast",
     "plan_interpolation", "run_algorithm", "spawned_generator", "sub_seed",
+    "IdxImageSet", "RunManifest", "load_idx_images", "pair_images_labels", "read_csv_matrix",
+    "read_idx_images", "read_idx_labels", "read_manifest", "write_configuration",
+    "write_csv_matrix", "write_idx_images", "write_idx_labels", "write_manifest",
 ]

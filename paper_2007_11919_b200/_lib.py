@@ -10,12 +10,12 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-from .errors import (DegenerateRankError, InvalidInputError, MdsError, NumericalError,
-                     ParamError, ShapeError)
+from .errors import (DegenerateRankError, FormatError, InvalidInputError, MdsError,
+                     NumericalError, ParamError, ShapeError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libmdsx.so"
 
-OK, PARAM, SHAPE, INVALID, NUMERICAL, DEGENERATE, CUDA, UNSUPPORTED = range(8)
+OK, PARAM, SHAPE, INVALID, NUMERICAL, DEGENERATE, CUDA, UNSUPPORTED, FORMAT = range(9)
 F64, F32 = 0, 1
 
 
@@ -62,6 +62,11 @@ SIGNATURES = {
     "mdsx_shift_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_idx_probe": (_int, [C.c_char_p, _i32, C.POINTER(_i64), C.POINTER(_i32),
+                              C.POINTER(_i32), C.c_char_p, _i64]),
+    "mdsx_idx_load_images": (_int, [_vp, C.c_char_p, _vp, _int, C.c_double, _vp]),
+    "mdsx_csv_read": (_int, [C.c_char_p, _i32, _i32, _vp, C.POINTER(_i64), C.POINTER(_i64),
+                             C.c_char_p, _i64]),
 }
 
 _lib = None
@@ -137,7 +142,7 @@ class Handle:
 def status_error(code: int, msg: str) -> Exception:
     return {
         PARAM: ParamError, SHAPE: ShapeError, INVALID: InvalidInputError,
-        NUMERICAL: NumericalError, DEGENERATE: DegenerateRankError,
+        NUMERICAL: NumericalError, DEGENERATE: DegenerateRankError, FORMAT: FormatError,
     }.get(code, MdsError if code == UNSUPPORTED else RuntimeError)(msg)
 
 
