@@ -192,6 +192,20 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
                        mdsx_piece_status* status, double* cond, int32_t* flags,
                        void* stream);
 
+/* ---- harness metric (simulation.py:83-108) --------------------------------
+ * aligned_correlations: Procrustes-align the configuration `points` (n x r,
+ * f64, device) onto `dominant` (n x r, dtype, row stride ld, device: e.g. the
+ * first r columns of the data matrix) and return the per-column Pearson
+ * correlations corr (r, device).  One pass over the rows (shifted column sums
+ * and the 2r x 2r Gram, fixed-order reductions), then the rotation from the
+ * centred cross-product by the warp SVD of the Procrustes kernels; the aligned
+ * matrix is never formed.  rotation (r x r, device) may be NULL; zero_var
+ * (1 int32, device) is set to 1 when a column has zero variance (the caller
+ * raises MetricError).  1 <= r <= 16. */
+int mdsx_aligned_correlations(mdsx_handle* h, const double* points, int64_t n, int32_t r,
+                              const void* dominant, int32_t dtype, int64_t ld, double* corr,
+                              double* rotation, int32_t* zero_var, void* stream);
+
 /* ---- file ingestion (replaces dataio.py:42-58, 68-82, 102-130) ----------
  * Host-side parsing; no device is needed except for mdsx_idx_load_images.
  * On failure `msg` (msg_len bytes, NUL-terminated) carries the reference's

@@ -21,6 +21,9 @@ from .primitives import (apply_procrustes, classical_mds, classical_mds_from_dat
                          cross_squared_distances, double_center, euclidean_distance_matrix,
                          fit_procrustes, gof_breakdown, goodness_of_fit, gower_context,
                          gower_interpolate)
+from .simulation import (DEFAULT_DOMINANT_SD, STUDY_COLUMNS, ScenarioMetrics, ScenarioSpec,
+                         aligned_correlations, eigenvalue_error_stats, g1_curve,
+                         generate_scenario, gof_sweep, run_cell, run_study)
 from .results import (EigenSystem, GofBreakdown, GowerContext, MdsConfiguration,
                       ProcrustesTransform)
 
@@ -40,4 +43,7 @@ __all__ = [
     "IdxImageSet", "RunManifest", "load_idx_images", "pair_images_labels", "read_csv_matrix",
     "read_idx_images", "read_idx_labels", "read_manifest", "write_configuration",
     "write_csv_matrix", "write_idx_images", "write_idx_labels", "write_manifest",
+    "DEFAULT_DOMINANT_SD", "STUDY_COLUMNS", "ScenarioMetrics", "ScenarioSpec",
+    "aligned_correlations", "eigenvalue_error_stats", "g1_curve", "generate_scenario",
+    "gof_sweep", "run_cell", "run_study",
 ]

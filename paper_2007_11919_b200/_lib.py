@@ -62,6 +62,8 @@ SIGNATURES = {
     "mdsx_shift_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,
                                   _vp, _vp, _vp, _vp, _vp]),
+    "mdsx_aligned_correlations": (_int, [_vp, _vp, _i64, _i32, _vp, _i32, _i64, _vp, _vp, _vp,
+                                         _vp]),
     "mdsx_idx_probe": (_int, [C.c_char_p, _i32, C.POINTER(_i64), C.POINTER(_i32),
                               C.POINTER(_i32), C.c_char_p, _i64]),
     "mdsx_idx_load_images": (_int, [_vp, C.c_char_p, _vp, _int, C.c_double, _vp]),

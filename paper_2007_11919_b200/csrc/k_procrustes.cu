@@ -16,46 +16,14 @@ namespace {
 
 constexpr int FIT_WARPS = 4;
 
-__global__ void __launch_bounds__(FIT_WARPS * 32)
-procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
-                      const double* __restrict__ src, const int64_t* __restrict__ src_rows,
-                      const int64_t* __restrict__ job_off, int njobs, int r,
-                      double* __restrict__ rot, double* __restrict__ trans,
-                      double* __restrict__ loss, int32_t* __restrict__ degenerate) {
-  extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int job = blockIdx.x * FIT_WARPS + warp;
-  if (job >= njobs) return;
-  double* B = sm + (size_t)warp * (2 * r * r + 3 * r);
-  double* V = B + r * r;
-  double* mt = V + r * r;
-  double* ms = mt + r;
-  double* sg = ms + r;
-  const int64_t o = job_off[job];
-  const int K = (int)(job_off[job + 1] - o);
-  const int64_t* tr = tgt_rows + o;
-  const int64_t* sr = src_rows + o;
-
-  if (lane < r) {
-    double a = 0.0, b = 0.0;
-    for (int t = 0; t < K; ++t) {
-      a += tgt[tr[t] * r + lane];
-      b += src[sr[t] * r + lane];
-    }
-    mt[lane] = a / K;
-    ms[lane] = b / K;
-  }
-  __syncwarp();
-  for (int e = lane; e < r * r; e += 32) {
-    const int a = e / r, b = e % r;
-    double s = 0.0;
-    for (int t = 0; t < K; ++t)
-      s = fma(tgt[tr[t] * r + a] - mt[a], src[sr[t] * r + b] - ms[b], s);
-    B[e] = s;
-    V[e] = (a == b) ? 1.0 : 0.0;
-  }
-  __syncwarp();
-
+// Rotation of the orthogonal Procrustes problem from the r x r cross-product
+// B (procrustes.py:46-50): one-sided (Hestenes) Jacobi SVD on the columns of B
+// (lane a owns row a; B and V in shared memory, V starts as the identity),
+// rank-deficient left bases completed by Gram-Schmidt, T = V L^T written to T
+// (row-major, may be global memory).  One warp; smin / smax are the extreme
+// singular values (the degenerate flag, procrustes.py:48).
+__device__ void rotation_from_cross(double* B, double* V, double* sg, int r, int lane, double* T,
+                                    double& smin_out, double& smax_out) {
   // one-sided Jacobi on the columns of B (lane a owns row a)
   for (int sweep = 0; sweep < 60; ++sweep) {
     int nrot = 0;
@@ -127,13 +95,59 @@ procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict_
     __syncwarp();
   }
   // T = V L^T  (row a of T on lane a)
-  double* T = rot + (size_t)job * r * r;
   if (lane < r)
     for (int b = 0; b < r; ++b) {
       double s = 0.0;
       for (int i = 0; i < r; ++i) s = fma(V[lane * r + i], B[b * r + i], s);
       T[lane * r + b] = s;
     }
+  smin_out = smin;
+  smax_out = smax;
+}
+
+__global__ void __launch_bounds__(FIT_WARPS * 32)
+procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
+                      const double* __restrict__ src, const int64_t* __restrict__ src_rows,
+                      const int64_t* __restrict__ job_off, int njobs, int r,
+                      double* __restrict__ rot, double* __restrict__ trans,
+                      double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * FIT_WARPS + warp;
+  if (job >= njobs) return;
+  double* B = sm + (size_t)warp * (2 * r * r + 3 * r);
+  double* V = B + r * r;
+  double* mt = V + r * r;
+  double* ms = mt + r;
+  double* sg = ms + r;
+  const int64_t o = job_off[job];
+  const int K = (int)(job_off[job + 1] - o);
+  const int64_t* tr = tgt_rows + o;
+  const int64_t* sr = src_rows + o;
+
+  if (lane < r) {
+    double a = 0.0, b = 0.0;
+    for (int t = 0; t < K; ++t) {
+      a += tgt[tr[t] * r + lane];
+      b += src[sr[t] * r + lane];
+    }
+    mt[lane] = a / K;
+    ms[lane] = b / K;
+  }
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {
+    const int a = e / r, b = e % r;
+    double s = 0.0;
+    for (int t = 0; t < K; ++t)
+      s = fma(tgt[tr[t] * r + a] - mt[a], src[sr[t] * r + b] - ms[b], s);
+    B[e] = s;
+    V[e] = (a == b) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+
+  double smin, smax;
+  double* T = rot + (size_t)job * r * r;
+  rotation_from_cross(B, V, sg, r, lane, T, smin, smax);
   __syncwarp();
   // translation t = mean(tgt) - mean(src) T ; loss
   double* tv = trans + (size_t)job * r;
@@ -312,6 +326,124 @@ __global__ void shift_rows_kernel(double* __restrict__ X, const int64_t* __restr
   X[(idx ? idx[i] : i) * r + c] -= shift[c];
 }
 
+// ---- harness metric (simulation.py:83-108): aligned_correlations on the device.
+// U = [X | D] (n x 2r: the configuration and the dominant columns).  Pass 1:
+// each CTA owns a contiguous row range, stages rows shifted by row 0 into a
+// shared tile and accumulates the shifted column sums and the upper triangle
+// of U'U (one value per thread slot, fixed order); pass 2 (one CTA): the
+// partials reduced in block order, centred (P - s s^T / n), the Procrustes
+// rotation of the dominant onto X from the cross-product D~'X~ (the warp SVD
+// above), then per column corr_j = (X~T)_j . D~_j / (|X~T_j| |D~_j|), all from
+// the 2r x 2r Gram: the n x r aligned matrix is never formed.
+constexpr int AC_T = 256;
+constexpr int AC_TILE = 64;
+
+template <typename T>
+__global__ void __launch_bounds__(AC_T)
+corr_partial_kernel(const double* __restrict__ X, int64_t n, int r, const T* __restrict__ Dm,
+                    int64_t ld, double* __restrict__ part, int nq) {
+  __shared__ double tile[AC_TILE * 32];
+  __shared__ double u0[32];
+  __shared__ unsigned char pa[560], pb[560];
+  const int w = 2 * r, tid = threadIdx.x;
+  if (tid < w) u0[tid] = tid < r ? X[tid] : (double)Dm[tid - r];
+  if (tid == 0) {
+    int q = w;
+    for (int a = 0; a < w; ++a)
+      for (int b = a; b < w; ++b) { pa[q] = (unsigned char)a; pb[q] = (unsigned char)b; ++q; }
+  }
+  __syncthreads();
+  const int64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t t0 = r0; t0 < r1; t0 += AC_TILE) {
+    const int rows = (int)(r1 - t0 < AC_TILE ? r1 - t0 : AC_TILE);
+    for (int e = tid; e < rows * w; e += AC_T) {
+      const int i = e / w, c = e - i * w;
+      const int64_t row = t0 + i;
+      const double v = c < r ? X[row * r + c] : (double)Dm[row * ld + (c - r)];
+      tile[i * w + c] = v - u0[c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int q = tid + k * AC_T;
+      if (q < nq) {
+        double s = 0.0;
+        if (q < w) {
+          for (int i = 0; i < rows; ++i) s += tile[i * w + q];
+        } else {
+          const int a = pa[q], b = pb[q];
+          for (int i = 0; i < rows; ++i) s = fma(tile[i * w + a], tile[i * w + b], s);
+        }
+        acc[k] += s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int q = tid + k * AC_T;
+    if (q < nq) part[(size_t)blockIdx.x * nq + q] = acc[k];
+  }
+}
+
+__global__ void __launch_bounds__(AC_T)
+corr_finish_kernel(const double* __restrict__ part, int nparts, int nq, int64_t n, int r,
+                   double* __restrict__ corr, double* __restrict__ rot_out,
+                   int32_t* __restrict__ zero_var) {
+  __shared__ double val[560];
+  __shared__ double C[32 * 32];
+  __shared__ double B[16 * 16], V[16 * 16], Tm[16 * 16], sg[16];
+  const int w = 2 * r, tid = threadIdx.x;
+  for (int q = tid; q < nq; q += AC_T) {
+    double s = 0.0;
+    for (int g = 0; g < nparts; ++g) s += part[(size_t)g * nq + q];   // fixed order
+    val[q] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {                                  // centred Gram C = P - s s^T / n
+    const double dn = (double)n;
+    int q = w;
+    for (int a = 0; a < w; ++a)
+      for (int b = a; b < w; ++b, ++q) {
+        const double c = val[q] - val[a] * val[b] / dn;
+        C[a * w + b] = c;
+        C[b * w + a] = c;
+      }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int lane = tid;
+    for (int e = lane; e < r * r; e += 32) {       // B = D~' X~ (target = dominant, source = X)
+      const int a = e / r, b = e % r;
+      B[e] = C[(r + a) * w + b];
+      V[e] = a == b ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    double smin, smax;
+    rotation_from_cross(B, V, sg, r, lane, Tm, smin, smax);
+    __syncwarp();
+    int zero = 0;
+    if (lane < r) {
+      const int j = lane;
+      double num = 0.0, da = 0.0;
+      for (int a = 0; a < r; ++a) {
+        num = fma(Tm[a * r + j], C[a * w + (r + j)], num);
+        double t = 0.0;
+        for (int b = 0; b < r; ++b) t = fma(C[a * w + b], Tm[b * r + j], t);
+        da = fma(Tm[a * r + j], t, da);
+      }
+      const double dd = C[(r + j) * w + (r + j)];
+      zero = !(da > 0.0) || !(dd > 0.0);
+      corr[j] = zero ? 0.0 : num / (sqrt(da) * sqrt(dd));
+    }
+    zero = __any_sync(0xffffffffu, zero);
+    if (lane == 0) *zero_var = zero;
+    if (rot_out)
+      for (int e = lane; e < r * r; e += 32) rot_out[e] = Tm[e];
+  }
+}
+
 }  // namespace
 
 namespace mdsx {
@@ -407,6 +539,29 @@ int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const doub
   mdsx::pre(h, st);
   subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, nparts, corr);
   return launched(h, "subtract_mean_kernel", st);
+}
+
+int corr_ws_doubles(int64_t n, int r, int num_sms) {
+  const int nq = 2 * r + (2 * r) * (2 * r + 1) / 2;
+  const int64_t g = std::max<int64_t>(1, std::min<int64_t>((n + AC_TILE - 1) / AC_TILE, 2 * num_sms));
+  return (int)(g * nq);
+}
+
+int launch_aligned_corr(mdsx_handle* h, const double* X, int64_t n, int r, const void* D,
+                        int dtype, int64_t ld, double* part, double* corr, double* rot,
+                        int32_t* zero_var, cudaStream_t st) {
+  const int nq = 2 * r + (2 * r) * (2 * r + 1) / 2;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + AC_TILE - 1) / AC_TILE, 2 * h->num_sms));
+  mdsx::pre(h, st);
+  if (dtype == MDSX_F32)
+    corr_partial_kernel<float><<<g, AC_T, 0, st>>>(X, n, r, (const float*)D, ld, part, nq);
+  else
+    corr_partial_kernel<double><<<g, AC_T, 0, st>>>(X, n, r, (const double*)D, ld, part, nq);
+  int rc = launched(h, "corr_partial_kernel", st);
+  if (rc) return rc;
+  mdsx::pre(h, st);
+  corr_finish_kernel<<<1, AC_T, 0, st>>>(part, g, nq, n, r, corr, rot, zero_var);
+  return launched(h, "corr_finish_kernel", st);
 }
 
 }  // namespace mdsx

@@ -25,6 +25,10 @@ int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const
                       int nseg, int r, double* sums, cudaStream_t st);
 int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, int r,
                       const double* shift, cudaStream_t st);
+int corr_ws_doubles(int64_t n, int r, int num_sms);
+int launch_aligned_corr(mdsx_handle* h, const double* X, int64_t n, int r, const void* D,
+                        int dtype, int64_t ld, double* part, double* corr, double* rot,
+                        int32_t* zero_var, cudaStream_t st);
 size_t recenter_ws_bytes(int r);
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st);
 int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
@@ -775,3 +779,22 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
 }
 
 }  // extern "C"
+
+extern "C" int mdsx_aligned_correlations(mdsx_handle* h, const double* points, int64_t n,
+                                         int32_t r, const void* dominant, int32_t dtype,
+                                         int64_t ld, double* corr, double* rotation,
+                                         int32_t* zero_var, void* stream) {
+  using namespace mdsx;
+  if (!h) return MDSX_PARAM;
+  if (r < 1 || r > 16) return fail(h, MDSX_UNSUPPORTED, "aligned correlations need 1 <= r <= 16");
+  if (n < 2) return fail(h, MDSX_SHAPE, "need at least 2 rows");
+  if (dtype != MDSX_F64 && dtype != MDSX_F32) return fail(h, MDSX_PARAM, "bad dtype");
+  cudaStream_t st = as_stream(stream);
+  const size_t nd = (size_t)corr_ws_doubles(n, r, h->num_sms);
+  int rc = ws_reserve(h, align_up(nd * sizeof(double)) + 256);
+  if (rc) return rc;
+  double* part = (double*)ws_alloc(h, nd * sizeof(double), st);
+  if (!part) return MDSX_CUDA;
+  return launch_aligned_corr(h, points, n, r, dominant, dtype, ld, part, corr, rotation, zero_var,
+                             st);
+}

@@ -28,16 +28,21 @@ def _gen(seed: int, *path: int) -> np.random.Generator:
         np.random.SeedSequence(entropy=seed, spawn_key=tuple(path))))
 
 
-def scenario(n: int, p: int, h: int, seed: int = 0, rep: int = 0) -> np.ndarray:
-    """N(0, diag(15 x h, 1 x (p-h))) rows, float64, reference stream."""
-    g = _gen(seed, rep)
-    total = n * p
+def normal_matrix(g: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+    """Box-Muller normals from the generator's uniform doubles (rng.py:26-41):
+    radius sqrt(-2 log1p(-u1)), angle 2 pi u2, cosines then sines."""
+    total = rows * cols
     half = (total + 1) // 2
     u = g.random(half)
     v = g.random(half)
     rad = np.sqrt(-2.0 * np.log1p(-u))
     ang = (2.0 * np.pi) * v
-    out = np.concatenate([rad * np.cos(ang), rad * np.sin(ang)])[:total].reshape(n, p)
+    return np.concatenate([rad * np.cos(ang), rad * np.sin(ang)])[:total].reshape(rows, cols)
+
+
+def scenario(n: int, p: int, h: int, seed: int = 0, rep: int = 0) -> np.ndarray:
+    """N(0, diag(15 x h, 1 x (p-h))) rows, float64, reference stream."""
+    out = normal_matrix(_gen(seed, rep), n, p)
     out[:, :h] *= np.sqrt(15.0)
     return out
 
