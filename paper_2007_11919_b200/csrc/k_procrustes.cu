@@ -11,6 +11,8 @@
 #include "mdsx_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 namespace {
 
@@ -75,23 +77,36 @@ __device__ void rotation_from_cross(double* B, double* V, double* sg, int r, int
   for (int i = 0; i < r; ++i) {
     const double s = sg[i];
     if (s > 1e-15 * smax && s > 0.0) continue;
-    // rank-deficient: complete the left basis by Gram-Schmidt on e_q
-    for (int q = 0; q < r; ++q) {
-      double v = (lane == q) ? 1.0 : 0.0;
+    // rank-deficient: complete the left basis by Gram-Schmidt on the e_q that
+    // leaves the largest remainder (lane q's squared row norm over the basis)
+    double n2 = 1.0;
+    for (int l = 0; l < r; ++l) {
+      if (l == i) continue;
+      const bool good = sg[l] > 1e-15 * smax && sg[l] > 0.0;
+      if (!good && l > i) continue;
+      const double ll = lane < r ? B[lane * r + l] : 0.0;
+      n2 -= ll * ll;
+    }
+    double best = lane < r ? n2 : -2.0;
+    int qb = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int q2 = __shfl_xor_sync(0xffffffffu, qb, o);
+      if (b2 > best || (b2 == best && q2 < qb)) { best = b2; qb = q2; }
+    }
+    double v = (lane == qb) ? 1.0 : 0.0;
+    for (int pass = 0; pass < 2; ++pass)
       for (int l = 0; l < r; ++l) {
         if (l == i) continue;
         const bool good = sg[l] > 1e-15 * smax && sg[l] > 0.0;
         if (!good && l > i) continue;
         const double ll = lane < r ? B[lane * r + l] : 0.0;
-        const double dot = __shfl_sync(0xffffffffu, ll, q);
+        const double dot = mdsx::warp_sum(ll * v);
         v -= dot * ll;
       }
-      const double nv = sqrt(mdsx::warp_sum(lane < r ? v * v : 0.0));
-      if (nv > 0.5) {
-        if (lane < r) B[lane * r + i] = v / nv;
-        break;
-      }
-    }
+    const double nv = sqrt(mdsx::warp_sum(lane < r ? v * v : 0.0));
+    if (lane < r) B[lane * r + i] = v / nv;
     __syncwarp();
   }
   // T = V L^T  (row a of T on lane a)
@@ -169,6 +184,291 @@ procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict_
   }
   ls = mdsx::warp_sum(ls);
   if (lane == 0) {
+    loss[job] = ls;
+    degenerate[job] = (r == 0 || smin <= 1e-12 * smax) ? 1 : 0;
+  }
+}
+
+// ---- register-resident fit for r <= 16: a group of P = ceil(r/2) lanes per
+// fit, 32/P fits per warp.  Lane l of a group holds two columns of B (and of
+// V) in registers, so the three column dots of a Jacobi rotation are local
+// FMAs (no shuffle trees); the P lanes rotate P disjoint column pairs at once
+// and then pass columns along a round-robin (Brent-Luk tournament) ordering,
+// so one sweep visits every pair in 2P-1 rounds.  A sweep with no rotation
+// ends the fit (further sweeps are no-ops, so groups of one warp simply run
+// until the slowest converges).  T = V L^T, t, loss and the degenerate flag
+// as procrustes_fit_kernel (the same rule for rank-deficient left bases).
+constexpr int FR_WARPS = 2;
+
+template <int RM>
+__global__ void __launch_bounds__(FR_WARPS * 32)
+procrustes_fit_reg_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
+                          const double* __restrict__ src, const int64_t* __restrict__ src_rows,
+                          const int64_t* __restrict__ job_off, int njobs, int r,
+                          double* __restrict__ rot, double* __restrict__ trans,
+                          double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+  extern __shared__ double sm[];
+  const int P = (r + 1) >> 1;                  // lanes per fit
+  const int FPW = 32 / P;                      // fits per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / P, l = lane - g * P;
+  const int gbase = g * P;
+  const int job = (blockIdx.x * FR_WARPS + warp) * FPW + g;
+  const bool act = g < FPW && job < njobs;
+  // per-fit shared area: L, V (r x r, column-major), T (r x r, row-major), ms (r)
+  double* Ls = sm + ((size_t)warp * FPW + (g < FPW ? g : 0)) * (3 * r * r + r);
+  double* Vs = Ls + r * r;
+  double* Ts = Vs + r * r;
+  double* mss = Ts + r * r;
+
+  int64_t o = 0;
+  int K = 0;
+  if (act) {
+    o = job_off[job];
+    K = (int)(job_off[job + 1] - o);
+  }
+  const int64_t* tr = tgt_rows + o;
+  const int64_t* sr = src_rows + o;
+  int ct = 2 * l, cb = 2 * l + 1;              // column indices held (>= r: zero dummy)
+  // means: all r target columns, the two source columns this lane owns
+  double mt[RM], bt[RM], bb[RM], vt[RM], vb[RM];
+#pragma unroll
+  for (int a = 0; a < RM; ++a) mt[a] = 0.0;
+  double mst = 0.0, msb = 0.0;
+#pragma unroll 4
+  for (int t = 0; t < K; ++t) {
+    const double* xr = tgt + tr[t] * r;
+    const double* yr = src + sr[t] * r;
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+      if (a < r) mt[a] += xr[a];
+    if (ct < r) mst += yr[ct];
+    if (cb < r) msb += yr[cb];
+  }
+  const double iK = K > 0 ? 1.0 / K : 0.0;
+#pragma unroll
+  for (int a = 0; a < RM; ++a) mt[a] *= iK;
+  mst *= iK;
+  msb *= iK;
+  if (act) {
+    if (ct < r) mss[ct] = mst;
+    if (cb < r) mss[cb] = msb;
+  }
+  // B[:, c] = sum_t (x_t - mt)(y_t[c] - ms[c]); V = I
+#pragma unroll
+  for (int a = 0; a < RM; ++a) {
+    bt[a] = 0.0;
+    bb[a] = 0.0;
+    vt[a] = (a == ct) ? 1.0 : 0.0;
+    vb[a] = (a == cb) ? 1.0 : 0.0;
+  }
+#pragma unroll 4
+  for (int t = 0; t < K; ++t) {
+    const double* xr = tgt + tr[t] * r;
+    const double* yr = src + sr[t] * r;
+    const double yt = ct < r ? yr[ct] - mst : 0.0;
+    const double yb = cb < r ? yr[cb] - msb : 0.0;
+#pragma unroll
+    for (int a = 0; a < RM; ++a) {
+      const double x = a < r ? xr[a] - mt[a] : 0.0;
+      bt[a] = fma(x, yt, bt[a]);
+      bb[a] = fma(x, yb, bb[a]);
+    }
+  }
+  // one-sided Jacobi sweeps, P disjoint pairs per round, tournament ordering
+  const unsigned gmask = (P == 32 ? 0xffffffffu : ((1u << P) - 1u)) << gbase;
+  const int src_top = l == 0 ? lane : lane - 1;           // top' source lane
+  const int src_bot = l == P - 1 ? lane : (lane + 1) & 31;  // bot' source lane
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int nrot = 0;
+    for (int round = 0; round < 2 * P - 1; ++round) {
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int a = 0; a < RM; ++a) {
+        al = fma(bt[a], bt[a], al);
+        be = fma(bb[a], bb[a], be);
+        ga = fma(bt[a], bb[a], ga);
+      }
+      if (ga != 0.0 && ga * ga > 1e-30 * (al * be)) {
+        const double h = 0.5 * (be - al);
+        const double t = ga / (h + copysign(sqrt(fma(h, h, ga * ga)), h == 0.0 ? 1.0 : h));
+        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+#pragma unroll
+        for (int a = 0; a < RM; ++a) {
+          const double x = bt[a], y = bb[a];
+          bt[a] = c * x - s * y;
+          bb[a] = s * x + c * y;
+          const double vx = vt[a], vy = vb[a];
+          vt[a] = c * vx - s * vy;
+          vb[a] = s * vx + c * vy;
+        }
+        ++nrot;
+      }
+      if (P > 1) {
+        // top'_0 = top_0, top'_1 = bot_0, top'_l = top_{l-1};  bot'_l = bot_{l+1},
+        // bot'_{P-1} = top_{P-1}.  The SENDER picks the value: on the top channel
+        // lane 0 sends its bottom column, every other lane its top column.
+#pragma unroll
+        for (int a = 0; a < RM; ++a) {
+          const double ntb = __shfl_sync(0xffffffffu, l == 0 ? bb[a] : bt[a], src_top);
+          const double ntv = __shfl_sync(0xffffffffu, l == 0 ? vb[a] : vt[a], src_top);
+          const double nbb = __shfl_sync(0xffffffffu, bb[a], src_bot);
+          const double nbv = __shfl_sync(0xffffffffu, vb[a], src_bot);
+          if (l == P - 1) { bb[a] = bt[a]; vb[a] = vt[a]; }
+          else { bb[a] = nbb; vb[a] = nbv; }
+          if (l != 0) { bt[a] = ntb; vt[a] = ntv; }
+        }
+        const int nct = __shfl_sync(0xffffffffu, l == 0 ? cb : ct, src_top);
+        const int ncb = __shfl_sync(0xffffffffu, cb, src_bot);
+        if (l == P - 1) cb = ct;
+        else cb = ncb;
+        if (l != 0) ct = nct;
+      }
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, act && nrot > 0);
+    if (any == 0u) break;
+  }
+  // singular values, extreme ones over the group, normalised left vectors
+  double st2 = 0.0, sb2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < RM; ++a) {
+    st2 = fma(bt[a], bt[a], st2);
+    sb2 = fma(bb[a], bb[a], sb2);
+  }
+  const double sgt = sqrt(st2), sgb = sqrt(sb2);
+  double smax = fmax(ct < r ? sgt : 0.0, cb < r ? sgb : 0.0);
+  double smin = fmin(ct < r ? sgt : 1e308, cb < r ? sgb : 1e308);
+  for (int q = 0; q < P; ++q) {
+    const double a1 = __shfl_sync(0xffffffffu, smax, gbase + q);
+    const double a2 = __shfl_sync(0xffffffffu, smin, gbase + q);
+    if (q != l) { smax = fmax(smax, a1); smin = fmin(smin, a2); }
+  }
+  const bool okt = sgt > 1e-15 * smax && sgt > 0.0, okb = sgb > 1e-15 * smax && sgb > 0.0;
+  if (act) {
+#pragma unroll
+    for (int a = 0; a < RM; ++a) {
+      if (a < r && ct < r) {
+        Ls[ct * r + a] = okt ? bt[a] / sgt : 0.0;
+        Vs[ct * r + a] = vt[a];
+      }
+      if (a < r && cb < r) {
+        Ls[cb * r + a] = okb ? bb[a] / sgb : 0.0;
+        Vs[cb * r + a] = vb[a];
+      }
+    }
+  }
+  // rank-deficient left bases: complete by Gram-Schmidt on e_q (group lane 0,
+  // columns in index order as procrustes_fit_kernel)
+  const bool bad = act && ((ct < r && !okt) || (cb < r && !okb));
+  const unsigned badm = __ballot_sync(0xffffffffu, bad) & gmask;
+  __syncwarp();
+
+  if (badm != 0u && l == 0) {
+    bool good[RM];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+      double s2 = 0.0;
+      if (i < r)
+        for (int a = 0; a < r; ++a) s2 = fma(Ls[i * r + a], Ls[i * r + a], s2);
+      good[i] = s2 > 0.5;                       // normalised columns have norm 1, the rest 0
+    }
+    for (int i = 0; i < r; ++i) {
+      if (good[i]) continue;
+      // e_q minus its projection on the basis so far, for the q that leaves the
+      // largest remainder (>= 1/sqrt(r): a fixed acceptance threshold can fail
+      // for every q once r > 4)
+      int qb = 0;
+      double nb = -1.0;
+      for (int q = 0; q < r; ++q) {
+        double n2 = 1.0;
+        for (int c = 0; c < r; ++c) {
+          if (c == i || (!good[c] && c > i)) continue;
+          const double d = Ls[c * r + q];
+          n2 -= d * d;
+        }
+        if (n2 > nb) { nb = n2; qb = q; }
+      }
+      double v[RM];
+#pragma unroll
+      for (int a = 0; a < RM; ++a) v[a] = (a == qb) ? 1.0 : 0.0;
+      for (int pass = 0; pass < 2; ++pass)         // twice: orthogonal to working precision
+        for (int c = 0; c < r; ++c) {
+          if (c == i || (!good[c] && c > i)) continue;
+          double dot = 0.0;
+#pragma unroll
+          for (int a = 0; a < RM; ++a)
+            if (a < r) dot = fma(Ls[c * r + a], v[a], dot);
+#pragma unroll
+          for (int a = 0; a < RM; ++a)
+            if (a < r) v[a] -= dot * Ls[c * r + a];
+        }
+      double nv = 0.0;
+#pragma unroll
+      for (int a = 0; a < RM; ++a)
+        if (a < r) nv = fma(v[a], v[a], nv);
+      nv = sqrt(nv);
+#pragma unroll
+      for (int a = 0; a < RM; ++a)
+        if (a < r) Ls[i * r + a] = v[a] / nv;
+      good[i] = true;
+    }
+  }
+  __syncwarp();
+  // T = V L^T (rows a = 2l, 2l+1 on lane l), t = mt - ms T, loss
+  double* T = rot + (size_t)job * r * r;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int a = 2 * l + h;
+    if (act && a < r)
+      for (int b = 0; b < r; ++b) {
+        double s = 0.0;
+        for (int i = 0; i < r; ++i) s = fma(Vs[i * r + a], Ls[i * r + b], s);
+        Ts[a * r + b] = s;
+        T[a * r + b] = s;
+      }
+  }
+  __syncwarp();
+  // translation: lane l owns entries b = 2l, 2l+1 of t (written to Vs[0..r), free now)
+  double* tv = trans + (size_t)job * r;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int b = 2 * l + h;
+    if (act && b < r) {
+      double s = 0.0;
+      for (int a = 0; a < r; ++a) s = fma(mss[a], Ts[a * r + b], s);
+      double mtb = 0.0;
+#pragma unroll
+      for (int a = 0; a < RM; ++a)
+        if (a == b) mtb = mt[a];
+      tv[b] = mtb - s;
+      Ls[b] = mtb - s;
+    }
+  }
+  __syncwarp();
+  // loss: lane l takes rows t = l, l+P, ...
+  double ls = 0.0;
+  if (act)
+#pragma unroll 2
+    for (int t = l; t < K; t += P) {
+      const double* xr = tgt + tr[t] * r;
+      const double* yr = src + sr[t] * r;
+      double y[RM];
+#pragma unroll
+      for (int a = 0; a < RM; ++a) y[a] = a < r ? yr[a] : 0.0;
+      for (int b = 0; b < r; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < RM; ++a)
+          if (a < r) s = fma(y[a], Ts[a * r + b], s);
+        const double e = xr[b] - s - Ls[b];
+        ls = fma(e, e, ls);
+      }
+    }
+  for (int q = 1; q < P; ++q) {
+    const double v = __shfl_sync(0xffffffffu, ls, gbase + q);
+    if (l == 0) ls += v;
+  }
+  if (act && l == 0) {
     loss[job] = ls;
     degenerate[job] = (r == 0 || smin <= 1e-12 * smax) ? 1 : 0;
   }
@@ -471,6 +771,26 @@ int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_
                           int njobs, int r, double* rot, double* trans, double* loss,
                           int32_t* degenerate, cudaStream_t st) {
   if (njobs == 0) return MDSX_OK;
+  if (r <= 16 && !getenv("MDSX_FIT_WARP")) {
+    const int P = (r + 1) / 2, fpw = 32 / P;
+    const size_t sm2 = (size_t)FR_WARPS * fpw * (3 * r * r + r) * sizeof(double);
+    const int blocks = (int)((njobs + (int64_t)FR_WARPS * fpw - 1) / ((int64_t)FR_WARPS * fpw));
+    auto go = [&](auto rm) {
+      constexpr int RMc = decltype(rm)::value;
+      auto kern = procrustes_fit_reg_kernel<RMc>;
+      if (sm2 > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      mdsx::pre(h, st);
+      kern<<<blocks, FR_WARPS * 32, sm2, st>>>(tgt, tgt_rows, src, src_rows, job_off_dev, njobs, r,
+                                                rot, trans, loss, degenerate);
+      return launched(h, "procrustes_fit_kernel", st);
+    };
+    if (r <= 4) return go(std::integral_constant<int, 4>{});
+    if (r <= 8) return go(std::integral_constant<int, 8>{});
+    if (r <= 10) return go(std::integral_constant<int, 10>{});
+    if (r <= 12) return go(std::integral_constant<int, 12>{});
+    return go(std::integral_constant<int, 16>{});
+  }
   const size_t smem = (size_t)FIT_WARPS * (2 * r * r + 3 * r) * sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(procrustes_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -364,3 +364,63 @@ class TestAlgorithms:
         assert isinstance(cfg.points, torch.Tensor) and cfg.points.is_cuda
         host = mds.divide_and_conquer_mds(scenario_data, mds.AlgorithmParams(r=5, l=400, c=10, seed=3))
         assert np.array_equal(cfg.points.cpu().numpy(), host.points)
+
+
+class TestProcrustesBatched:
+    """The batched fit kernels (lane-group register kernel for r <= 16, the
+    warp kernel above) against the oracle restatement of procrustes.py:46-78
+    on many jobs at once: every r up to 16, uneven job sizes, rank-deficient
+    cross products (collinear / constant sources)."""
+
+    @staticmethod
+    def _batch(mds, tgts, srcs, r):
+        import torch
+        from paper_2007_11919_b200 import _device as D
+        dev = D.require_device(None)
+        sizes = [len(t) for t in tgts]
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        tt = torch.from_numpy(np.ascontiguousarray(np.concatenate(tgts))).to(dev)
+        ss = torch.from_numpy(np.ascontiguousarray(np.concatenate(srcs))).to(dev)
+        rows = torch.arange(int(off[-1]), dtype=torch.int64, device=dev)
+        nj = len(tgts)
+        rot, tr = D.empty((nj, r, r), dev), D.empty((nj, r), dev)
+        loss, deg = D.empty((nj,), dev), torch.empty(nj, dtype=torch.int32, device=dev)
+        D.handle(dev).call("mdsx_procrustes_fit", tt.data_ptr(), rows.data_ptr(), ss.data_ptr(),
+                           rows.data_ptr(), off.ctypes.data, nj, r, rot.data_ptr(), tr.data_ptr(),
+                           loss.data_ptr(), deg.data_ptr(), D.stream_ptr(dev))
+        return rot.cpu().numpy(), tr.cpu().numpy(), loss.cpu().numpy(), deg.cpu().numpy()
+
+    @pytest.mark.parametrize("r", list(range(1, 17)))
+    def test_matches_oracle(self, mds, r, monkeypatch):
+        from oracle import mds_oracle as orc
+        rng = np.random.default_rng(100 + r)
+        tgts, srcs = [], []
+        for j in range(77):
+            k = int(rng.integers(max(2, r), 3 * r + 4))
+            t = rng.standard_normal((k, r)) * rng.uniform(0.1, 20.0)
+            if j % 11 == 3 and r > 1:      # rank-deficient source: one column repeated
+                s = rng.standard_normal((k, r))
+                s[:, -1] = s[:, 0]
+            elif j % 11 == 7:              # constant source: zero cross product
+                s = np.ones((k, r))
+            else:
+                q, _ = np.linalg.qr(rng.standard_normal((r, r)))
+                s = t @ q + rng.standard_normal((k, r)) * 0.1 + rng.standard_normal(r)
+            tgts.append(t)
+            srcs.append(s)
+        rot, tr, loss, deg = self._batch(mds, tgts, srcs, r)
+        monkeypatch.setenv("MDSX_FIT_WARP", "1")
+        rot_w, tr_w, loss_w, deg_w = self._batch(mds, tgts, srcs, r)
+        for j, (t, s) in enumerate(zip(tgts, srcs)):
+            ref = orc.procrustes_fit(t, s)
+            assert bool(deg[j]) == ref.degenerate == bool(deg_w[j])
+            scale = max(1.0, np.abs(t).max())
+            # orthogonality and the optimal loss hold whatever completion a degenerate fit takes
+            assert np.abs(rot[j] @ rot[j].T - np.eye(r)).max() <= 1e-10
+            assert abs(loss[j] - ref.loss) <= 1e-9 * max(ref.loss, scale ** 2 * len(t))
+            res = t - s @ rot[j] - tr[j]
+            assert abs(np.sum(res * res) - loss[j]) <= 1e-9 * max(loss[j], scale ** 2)
+            if not ref.degenerate:
+                assert np.abs(rot[j] - ref.rotation).max() <= 1e-9
+                assert np.abs(rot[j] - rot_w[j]).max() <= 1e-12
+                assert np.abs(tr[j] - ref.translation).max() <= 1e-9 * scale
