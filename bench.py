@@ -286,7 +286,7 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
     if kernel == "subtract_mean_kernel":
         n = w["n"]
         return {"bound": "hbm", "bytes": 2 * n * r * 8, "model": "read + write of the n x r output"}
-    if kernel in ("points_kernel", "points_rows_kernel"):
+    if kernel in ("points_kernel", "points_rows_kernel", "points_piece_kernel"):
         tot = sum(sizes)
         return {"bound": "hbm", "bytes": tot * p * esize + tot * r * 8,
                 "model": "rows*p*sizeof(in) + rows*r*8"}

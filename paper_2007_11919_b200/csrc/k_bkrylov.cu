@@ -265,7 +265,7 @@ int lanczos_rmax();
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int full_basis, int only_flagged,
-                       cudaStream_t st);
+                       cudaStream_t st, const PtsEpi* epi = nullptr);
 void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t);
 
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }

@@ -27,9 +27,11 @@
 // Euclidean data: Sum|lambda| = trace, G1 == G2 bitwise, classical.py:75-85).
 #include "mdsx_common.cuh"
 #include "piece_solvers.cuh"
+#include "points_stream.cuh"
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #ifdef MDSX_LZ_PROF
 #define LZ_T0(v) long long v = clock64()
@@ -228,12 +230,28 @@ __device__ void cgs_project(const double* Q, int kq, int k, int nc, double* wv, 
   }
 }
 
+template <typename T>
+__device__ __noinline__ void lz_points(const PtsEpi& epi, const PieceDesc& d, int r,
+                                       const double* Uout, unsigned char* smem) {
+  auto go = [&](auto rm) {
+    constexpr int RM = decltype(rm)::value;
+    mdsx::PieceStream<T, RM> ps(smem, (const T*)epi.X, epi.ld, epi.row_idx + d.row_off, epi.p, d.m);
+    ps.prologue();
+    mdsx::ps_load_records<RM>(smem, Uout + d.u_off, epi.mu + (int64_t)d.id * epi.p, epi.p, r);
+    __syncthreads();
+    ps.run(smem, r, epi.points + d.pt_off * r);
+  };
+  if (r <= 4) go(std::integral_constant<int, 4>{});
+  else if (r <= 8) go(std::integral_constant<int, 8>{});
+  else go(std::integral_constant<int, 10>{});
+}
+
 template <int QMAX>
 __global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
 lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
                     double* __restrict__ Uout, double* __restrict__ lam_out,
                     double* __restrict__ estimates, double* __restrict__ gof,
-                    mdsx_piece_status* __restrict__ status, int only_flagged) {
+                    mdsx_piece_status* __restrict__ status, int only_flagged, const PtsEpi epi) {
   extern __shared__ double sm[];
   __shared__ double alpha[QMAX], beta[QMAX], beta2[QMAX];
   __shared__ double wv[LMAX], hv[QMAX + 1];
@@ -258,6 +276,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     __syncthreads();
   }
   if (status[pid].code == MDSX_INVALID_INPUT) {   // non-finite rows: nothing to solve
+    if (epi.pending && tid == 0) epi.pending[pid] = 1;
     for (int e = tid; e < k * r; e += LT) Uout[d.u_off + e] = 0.0;
     if (tid < r) {
       estimates[(int64_t)pid * r + tid] = 0.0;
@@ -591,6 +610,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
 #endif
   if (conv_s == 2) {          // basis capacity exhausted: the full Jacobi kernel takes over
     if (tid == 0 && status[pid].code == MDSX_OK) status[pid] = mdsx_piece_status{MDSX_NUMERICAL, 0, -2.0};
+    if (epi.pending && tid == 0) epi.pending[pid] = 1;
     return;
   }
 
@@ -621,6 +641,14 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     const double g = st.code == MDSX_OK ? kept / trace_s : 0.0;
     gof[2 * (int64_t)pid] = g;
     gof[2 * (int64_t)pid + 1] = g;
+  }
+  if (epi.points) {
+    // points epilogue: the CTA streams its piece's rows while the SM's other
+    // CTA is (typically) still in its latency-bound Krylov phase
+    __syncthreads();                          // U in global (L1-hot), A / Q smem free
+    if (tid == 0) epi.pending[pid] = 0;
+    if (epi.f32) lz_points<float>(epi, d, r, Uout, reinterpret_cast<unsigned char*>(sm));
+    else lz_points<double>(epi, d, r, Uout, reinterpret_cast<unsigned char*>(sm));
   }
 }
 
@@ -1502,14 +1530,18 @@ size_t lanczos_smem_bytes(int kmax) { return lanczos_bytes(kmax, LMAX); }
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int full_basis, int only_flagged,
-                        cudaStream_t st) {
+                        cudaStream_t st, const PtsEpi* epi) {
+  if (epi && (full_basis || only_flagged || r > 10 || getenv("MDSX_LZ_REG"))) epi = nullptr;
   if (npieces == 0) return MDSX_OK;
+  PtsEpi e{};
+  if (epi) e = *epi;
   auto go = [&](auto kern, int qmax) {
     size_t smem = lanczos_bytes(kmax, qmax);
+    if (epi) smem = std::max(smem, mdsx::ps_smem_bytes<10>(epi->p));
     if (getenv("MDSX_LZ_ONE")) smem = std::max<size_t>(smem, 120 * 1024);   // experiment: 1 CTA/SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
-    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged);
+    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged, e);
     return launched(h, "lanczos_smem_kernel", st);
   };
   if (!full_basis && kmax <= RG_KP && getenv("MDSX_LZ_REG")) {

@@ -9,6 +9,7 @@
 // sign_kernel: one CTA per piece reduces the candidates in fixed order and
 // flips the piece's columns.
 #include "mdsx_common.cuh"
+#include "points_stream.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -171,132 +172,23 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
 }
 
 
-// ---- form 0, 16-byte aligned rows: each thread owns one row of a 256-row
-// chunk and streams that row through a private 4-deep cp.async ring of
-// 64-byte feature blocks in shared memory (its own cp.async groups: no block
-// barrier in the loop).  The per-feature records (U row, mean) are read as
-// warp broadcasts; all r outputs are accumulated in registers.
-constexpr int PR_NS = 4;          // ring depth (64-byte blocks in flight per row)
-constexpr int PR_PITCH = 80;      // bytes per row slot (64 + 16: conflict-free 16-byte reads)
-
+// ---- form 0, 16-byte aligned rows: one CTA per piece (points_stream.cuh).
+// `pending` (optional): only pieces with pending[id] != 0 -- the ones whose
+// points the fused Lanczos epilogue did not produce.
 template <typename T, int RM>
-__global__ void __launch_bounds__(PT, 2)
-points_rows_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
-                   const PieceDesc* __restrict__ pd, int r, const double* __restrict__ mu_all,
-                   const double* __restrict__ Uall, double* __restrict__ points,
-                   double2* __restrict__ cand, int maxch) {
-  constexpr int FB = 64 / (int)sizeof(T);                 // features per block
-  constexpr int W = RM / 2 + 1;                           // record: U pairs, (mean, 0)
+__global__ void __launch_bounds__(mdsx::PS_T, 2)
+points_piece_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
+                    const PieceDesc* __restrict__ pd, int r, const double* __restrict__ mu_all,
+                    const double* __restrict__ Uall, double* __restrict__ points,
+                    const int* __restrict__ pending) {
   extern __shared__ __align__(16) unsigned char pr_smem[];
-  double2* rec = reinterpret_cast<double2*>(pr_smem);     // p x W
-  const PieceDesc d = pd[blockIdx.y];
-  const int chunk = blockIdx.x;
-  const int r0 = chunk * CH;
-  if (r0 >= d.m) return;
-  const int rows = min(CH, d.m - r0);
-  const int tid = threadIdx.x;
-  // ring slot b of thread t at ring + b * PT * PR_PITCH + t * PR_PITCH: lanes
-  // 80 bytes apart -> 16-byte reads of 8 lanes hit distinct bank quads
-  unsigned char* ring = pr_smem + (size_t)p * W * sizeof(double2) + (size_t)tid * PR_PITCH;
-  const bool live = tid < rows;
-  const int nblk = (p + FB - 1) / FB;
-  const char* src = live ? reinterpret_cast<const char*>(X + row_idx[d.row_off + r0 + tid] * ld)
-                         : nullptr;
-  auto issue = [&](int b) {
-    if (live && b < nblk) {
-      const int nbytes = min(64, (int)((p - b * FB) * (int)sizeof(T)));
-      unsigned char* dst = ring + (size_t)(b % PR_NS) * PT * PR_PITCH;
-      for (int o = 0; o < nbytes; o += 16) {
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + o);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 64 * b + o));
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-#pragma unroll
-  for (int b = 0; b < PR_NS - 1; ++b) issue(b);
-  const double* Ug = Uall + d.u_off;
-  const double* mu = mu_all + (int64_t)d.id * p;
-  for (int e = tid; e < p * W; e += PT) {
-    const int a = e / W, w = e % W;
-    double2 v = make_double2(0.0, 0.0);
-    if (w < RM / 2) {
-      v.x = 2 * w < r ? Ug[(int64_t)a * r + 2 * w] : 0.0;
-      v.y = 2 * w + 1 < r ? Ug[(int64_t)a * r + 2 * w + 1] : 0.0;
-    } else {
-      v.x = mu[a];
-    }
-    rec[e] = v;
-  }
+  const PieceDesc d = pd[blockIdx.x];
+  if (pending && !pending[d.id]) return;
+  mdsx::PieceStream<T, RM> ps(pr_smem, X, ld, row_idx + d.row_off, p, d.m);
+  ps.prologue();
+  mdsx::ps_load_records<RM>(pr_smem, Uall + d.u_off, mu_all + (int64_t)d.id * p, p, r);
   __syncthreads();
-  double acc[RM];
-#pragma unroll
-  for (int c = 0; c < RM; ++c) acc[c] = 0.0;
-  for (int b = 0; b < nblk; ++b) {
-    issue(b + PR_NS - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(PR_NS - 1));
-    const unsigned char* xb = ring + (size_t)(b % PR_NS) * PT * PR_PITCH;
-    const int a0 = b * FB;
-    const int nf = min(FB, p - a0);
-    constexpr int VW = 16 / (int)sizeof(T);
-#pragma unroll
-    for (int v4 = 0; v4 < 4; ++v4) {
-      if (v4 * VW >= nf) break;                     // the last block may be short
-      double xv[VW];
-      if constexpr (sizeof(T) == 4) {
-        const float4 f = *reinterpret_cast<const float4*>(xb + 16 * v4);
-        xv[0] = f.x; xv[1] = f.y; xv[2] = f.z; xv[3] = f.w;
-      } else {
-        const double2 f = *reinterpret_cast<const double2*>(xb + 16 * v4);
-        xv[0] = f.x; xv[1] = f.y;
-      }
-#pragma unroll
-      for (int u = 0; u < VW; ++u) {
-        const double2* rp = rec + (size_t)(a0 + v4 * VW + u) * W;
-        const double y = xv[u] - rp[W - 1].x;
-#pragma unroll
-        for (int w = 0; w < RM / 2; ++w) {
-          const double2 uu = rp[w];
-          acc[2 * w] = fma(y, uu.x, acc[2 * w]);
-          acc[2 * w + 1] = fma(y, uu.y, acc[2 * w + 1]);
-        }
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  double* out = points + (d.pt_off + r0) * r;
-  if (live)
-#pragma unroll
-    for (int c = 0; c < RM; ++c)
-      if (c < r) out[(int64_t)tid * r + c] = acc[c];
-  // per-CTA argmax candidates per column (ties -> lowest row), fixed order
-  __shared__ double wv_s[PT / 32][MDSX_MAX_R];
-  __shared__ int wi_s[PT / 32][MDSX_MAX_R];
-  const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-  for (int c = 0; c < RM; ++c) {
-    if (c >= r) break;
-    double v = live ? fabs(acc[c]) : -1.0;
-    int ix = live ? r0 + tid : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-      if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
-    }
-    if (lane == 0) { wv_s[warp][c] = v; wi_s[warp][c] = ix; }
-  }
-  __syncthreads();
-  if (tid < r) {
-    double v = -1.0;
-    int ix = 0x7fffffff;
-    for (int w = 0; w < PT / 32; ++w) {
-      const double v2 = wv_s[w][tid];
-      const int i2 = wi_s[w][tid];
-      if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
-    }
-    cand[((size_t)d.id * maxch + chunk) * r + tid] = make_double2(v, (double)ix);
-  }
+  ps.run(pr_smem, r, points + d.pt_off * r);
 }
 
 __global__ void __launch_bounds__(PT)
@@ -338,7 +230,7 @@ size_t points_ws_bytes(int npieces, int64_t max_m, int r) {
 int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                   const int64_t* row_idx, const PieceDesc* pd, int npieces, int64_t max_m, int r,
                   const double* mu, const double* U, const double* lam, double* points,
-                  double2* cand, cudaStream_t st, bool all_form0) {
+                  double2* cand, cudaStream_t st, bool all_form0, const int* pending) {
   const int maxch = (int)((max_m + CH - 1) / CH);
   const int G = (r + 3) / 4, rp = 4 * G;
   // tile rows: 32 (one per lane) unless the double buffer would not fit
@@ -358,16 +250,16 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
                        !getenv("MDSX_POINTS_TILED");
   if (rows_ok && all_form0) {
     const int RM = r <= 4 ? 4 : r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : 16;
-    const size_t smem2 = (size_t)p * (RM / 2 + 1) * 16 + (size_t)PT * PR_NS * PR_PITCH;
     auto go = [&](auto tag, auto rm) {
       using T = decltype(tag);
       constexpr int RMc = decltype(rm)::value;
-      auto kern = points_rows_kernel<T, RMc>;
+      const size_t smem2 = mdsx::ps_smem_bytes<RMc>(p);
+      auto kern = points_piece_kernel<T, RMc>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       mdsx::pre(h, st);
-      kern<<<grid, PT, smem2, st>>>((const T*)data, ld, p, row_idx, pd, r, mu, U, points, cand,
-                                    maxch);
-      return launched(h, "points_rows_kernel", st);
+      kern<<<npieces, mdsx::PS_T, smem2, st>>>((const T*)data, ld, p, row_idx, pd, r, mu, U, points,
+                                                pending);
+      return launched(h, "points_piece_kernel", st);
     };
     auto by_rm = [&](auto tag) {
       switch (RM) {
@@ -378,10 +270,7 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
         default: return go(tag, std::integral_constant<int, 16>{});
       }
     };
-    if ((rc = dtype == MDSX_F32 ? by_rm(float{}) : by_rm(double{}))) return rc;
-    mdsx::pre(h, st);
-    sign_kernel<<<npieces, PT, 0, st>>>(pd, r, cand, maxch, points);
-    return launched(h, "sign_kernel", st);
+    return dtype == MDSX_F32 ? by_rm(float{}) : by_rm(double{});
   }
   if (dtype == MDSX_F32) {
     cudaFuncSetAttribute(points_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -63,7 +63,7 @@ size_t lanczos_smem_bytes(int kmax);
 int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int full_basis, int only_flagged,
-                        cudaStream_t st);
+                        cudaStream_t st, const PtsEpi* epi = nullptr);
 bool gram_piece_ok(const void* data, int dtype, int64_t ld, int p);
 int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                       const int64_t* row_idx, const PieceDesc* pd, int npieces, double* A,
@@ -259,7 +259,7 @@ static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
          align_up(cp.tiles1.size() * sizeof(int4)) +
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
          align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double)) +
-         align_up(points_ws_bytes((int)np, cp.max_m, r)) +
+         align_up(points_ws_bytes((int)np, cp.max_m, r)) + align_up(np * sizeof(int)) +
          (cp.pd_big.empty() ? 0 : bk_ws_bytes(cp.pd_big));
 }
 
@@ -315,6 +315,17 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
                         !(eig && strcmp(eig, "subspace") == 0);
     int nc = pc ? atoi(pc) : 2;                       // measured best on dc2 / fast3
     nc = std::min(nc, np / (2 * h->num_sms));          // >= two waves of pieces per chunk
+    // fused points epilogue in the Lanczos kernel (aligned rows, r <= 10): each
+    // CTA streams its piece's rows right after its eigenvectors, next to the
+    // other CTA's Krylov phase; the points kernel then only takes the pieces
+    // the epilogue left pending (Jacobi fallback / non-finite input)
+    const size_t es = dtype == MDSX_F32 ? 4 : 8;
+    const bool fuse = simple && r <= 10 && data != nullptr && ((size_t)p * es) % 16 == 0 &&
+                      ((size_t)ld * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(data) & 15) == 0 &&
+                      !getenv("MDSX_POINTS_TILED") && !getenv("MDSX_NO_FUSE");
+    int* pending = fuse ? (int*)ws_alloc(h, (size_t)np * sizeof(int), st) : nullptr;
+    if (fuse && !pending) return MDSX_CUDA;
+    PtsEpi epi{data, dtype == MDSX_F32 ? 1 : 0, ld, p, ridx, mu, points, pending};
     if (simple && nc > 1) {
       if (!h->aux) {
         if ((rc = cuda_check(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking), "stream")))
@@ -331,13 +342,13 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
         if ((rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd + j0, n, A, mu, status, s)))
           return rc;
         if ((rc = launch_lanczos_smem(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
-                                      status, 0, 0, s)))
+                                      status, 0, 0, s, fuse ? &epi : nullptr)))
           return rc;
         if ((rc = launch_jacobi_fallback(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
                                          status, s)))
           return rc;
         if ((rc = launch_points(h, data, dtype, ld, p, ridx, dpd + j0, n, cp.max_m, r, mu, U, lam,
-                                points, cand, s, true)))
+                                points, cand, s, true, pending)))
           return rc;
       }
       cudaEventRecord(h->ev_join, h->aux);

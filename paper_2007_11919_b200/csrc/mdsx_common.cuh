@@ -102,6 +102,22 @@ struct PieceDesc {
   int32_t m, k, form, id;   // id: global piece index (output slot)
 };
 
+// Points epilogue of the Lanczos kernel (form-0 pieces, 16-byte aligned rows,
+// r <= 10): after the eigenvectors, the same CTA streams the piece's rows and
+// writes its signed points (points_stream.cuh); pending[id] = 0 marks pieces
+// done, 1 the ones left to the separate points kernel (Jacobi fallback,
+// non-finite input).
+struct PtsEpi {
+  const void* X;
+  int f32;
+  int64_t ld;
+  int p;
+  const int64_t* row_idx;
+  const double* mu;
+  double* points;
+  int* pending;
+};
+
 // One batched-GEMM task: C = alpha * op(A) B + beta * D  (row-major, op(A) = A
 // (M x K, lda) or A^T with A stored K x M); skipped when *skip != 0.
 struct GemmTask {
@@ -136,7 +152,8 @@ size_t points_ws_bytes(int npieces, int64_t max_m, int r);
 int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                   const int64_t* row_idx, const PieceDesc* pd, int npieces, int64_t max_m, int r,
                   const double* mu, const double* U, const double* lam, double* points,
-                  double2* cand, cudaStream_t st, bool all_form0 = false);
+                  double2* cand, cudaStream_t st, bool all_form0 = false,
+                  const int* pending = nullptr);
 GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
                        const std::vector<GemmTask>& batch);
 int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_items,
