@@ -500,35 +500,130 @@ apply_kernel(double* __restrict__ buf, int r, const int64_t* __restrict__ start,
 }
 
 // D&C stitch (algorithms.py:151-156): piece 0 verbatim, piece j>0 rows c..
-// through fit j-1, scattered to original rows.
+// through fit j-1, scattered to original rows, minus the final column mean
+// (algorithms.py:122-125) when `mean` is given.  One CTA per piece: T, t and
+// the mean staged in shared memory, one row per thread per pass.
 template <int RM>
 __global__ void __launch_bounds__(256)
 dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_idx,
                  const int64_t* __restrict__ off, int c, int r, const double* __restrict__ rot,
-                 const double* __restrict__ trans, double* __restrict__ out) {
-  const int j = blockIdx.y;
+                 const double* __restrict__ trans, const double* __restrict__ mean,
+                 double* __restrict__ out) {
+  __shared__ double Ts[RM * RM], ts[RM], ms[RM];
+  const int j = blockIdx.x;
   const int64_t o = off[j], m = off[j + 1] - o;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (j == 0 ? 0 : c);
-  if (i >= m) return;
-  const double* src = P + (o + i) * r;
-  double* dst = out + row_idx[o + i] * r;
-  if (j == 0) {
-    for (int b = 0; b < r; ++b) dst[b] = src[b];
-    return;
+  for (int e = threadIdx.x; e < RM * RM; e += blockDim.x) {
+    const int a = e / RM, b = e % RM;
+    Ts[e] = (a < r && b < r) ? (j == 0 ? (a == b ? 1.0 : 0.0) : rot[(size_t)(j - 1) * r * r + a * r + b])
+                             : 0.0;
   }
-  const double* T = rot + (size_t)(j - 1) * r * r;
-  const double* tv = trans + (size_t)(j - 1) * r;
-  double x[RM];
+  if (threadIdx.x < RM) {
+    const int b = threadIdx.x;
+    ts[b] = (j == 0 || b >= r) ? 0.0 : trans[(size_t)(j - 1) * r + b];
+    ms[b] = (mean && b < r) ? mean[b] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x + (j == 0 ? 0 : c); i < m; i += blockDim.x) {
+    const double* src = P + (o + i) * r;
+    double* dst = out + row_idx[o + i] * r;
+    double x[RM];
 #pragma unroll
-  for (int a = 0; a < RM; ++a) x[a] = a < r ? src[a] : 0.0;
+    for (int a = 0; a < RM; ++a) x[a] = a < r ? src[a] : 0.0;
+    if (j == 0) {
+#pragma unroll
+      for (int b = 0; b < RM; ++b)
+        if (b < r) dst[b] = x[b] - ms[b];
+      continue;
+    }
+#pragma unroll
+    for (int b = 0; b < RM; ++b) {
+      if (b >= r) break;
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < RM; ++a) s = fma(x[a], Ts[a * RM + b], s);
+      dst[b] = (s + ts[b]) - ms[b];
+    }
+  }
+}
+
+// Column sums of each piece's OWN rows of the piece points P (piece 0: all
+// rows, piece j > 0: rows c..), fixed-order block reduction.
+template <int RM>
+__global__ void __launch_bounds__(256)
+dc_own_sums_kernel(const double* __restrict__ P, const int64_t* __restrict__ off, int c, int r,
+                   const double* __restrict__ rot, const double* __restrict__ trans,
+                   double* __restrict__ sums) {
+  __shared__ double red[8][RM];
+  const int j = blockIdx.x;
+  const int64_t o = off[j], m = off[j + 1] - o;
+  double acc[RM];
+#pragma unroll
+  for (int a = 0; a < RM; ++a) acc[a] = 0.0;
+  for (int64_t i = threadIdx.x + (j == 0 ? 0 : c); i < m; i += 256) {
+    const double* src = P + (o + i) * r;
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+      if (a < r) acc[a] += src[a];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < RM; ++a) {
+    double v = acc[a];
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+    if (lane == 0) red[warp][a] = v;
+  }
+  __syncthreads();
+  // contribution of the piece to the stitched column sums: S (piece 0) or
+  // S T_{j-1} + n_j t_{j-1}
+  if (threadIdx.x < r) {
+    const int b = threadIdx.x;
+    double v;
+    if (j == 0) {
+      v = 0.0;
+      for (int w = 0; w < 8; ++w) v += red[w][b];
+    } else {
+      const double* T = rot + (size_t)(j - 1) * r * r;
+      v = (double)(m - c) * trans[(size_t)(j - 1) * r + b];
+      for (int a = 0; a < r; ++a) {
+        double sa = 0.0;
+        for (int w = 0; w < 8; ++w) sa += red[w][a];
+        v = fma(sa, T[a * r + b], v);
+      }
+    }
+    sums[(size_t)j * r + b] = v;
+  }
+}
+
+// Final column mean of the stitched configuration from the per-piece
+// contributions (dc_own_sums_kernel): thread t adds pieces t, t+256, ... in
+// order (independent loads, unrolled), then a fixed tree.
+template <int RM>
+__global__ void __launch_bounds__(256)
+dc_mean_kernel(const double* __restrict__ sums, int npieces, int r, int64_t n,
+               double* __restrict__ mean) {
+  __shared__ double red[256];
+  double acc[RM];
+#pragma unroll
+  for (int b = 0; b < RM; ++b) acc[b] = 0.0;
+#pragma unroll 4
+  for (int j = threadIdx.x; j < npieces; j += 256) {
+    const double* S = sums + (size_t)j * r;
+#pragma unroll
+    for (int b = 0; b < RM; ++b)
+      if (b < r) acc[b] += S[b];
+  }
 #pragma unroll
   for (int b = 0; b < RM; ++b) {
     if (b >= r) break;
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < RM; ++a)
-      if (a < r) s = fma(x[a], T[a * r + b], s);
-    dst[b] = s + tv[b];
+    red[threadIdx.x] = acc[b];
+    __syncthreads();
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+      if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) mean[b] = red[0] / (double)n;
+    __syncthreads();
   }
 }
 
@@ -817,14 +912,36 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
 
 int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
                      int npieces, int64_t max_m, int c, int r, const double* rot,
-                     const double* trans, double* out, cudaStream_t st) {
-  dim3 grid((unsigned)((max_m + 255) / 256), (unsigned)npieces);
-  if (r <= 4) { mdsx::pre(h, st); dc_stitch_kernel<4><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
-  else if (r <= 8) { mdsx::pre(h, st); dc_stitch_kernel<8><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
-  else if (r <= 16) { mdsx::pre(h, st); dc_stitch_kernel<16><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
-  else { mdsx::pre(h, st); dc_stitch_kernel<32><<<grid, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, out); }
-  return launched(h, "dc_stitch_kernel", st);
+                     const double* trans, double* out, cudaStream_t st, int64_t n_recenter,
+                     double* ws) {
+  (void)max_m;
+  auto go = [&](auto rm) {
+    constexpr int RM = decltype(rm)::value;
+    const double* mean = nullptr;
+    if (n_recenter > 0) {
+      double* sums = ws;
+      double* mn = ws + (size_t)npieces * r;
+      mdsx::pre(h, st);
+      dc_own_sums_kernel<RM><<<npieces, 256, 0, st>>>(P, off, c, r, rot, trans, sums);
+      int rc = launched(h, "dc_own_sums_kernel", st);
+      if (rc) return rc;
+      mdsx::pre(h, st);
+      dc_mean_kernel<RM><<<1, 256, 0, st>>>(sums, npieces, r, n_recenter, mn);
+      if ((rc = launched(h, "dc_mean_kernel", st))) return rc;
+      mean = mn;
+    }
+    mdsx::pre(h, st);
+    dc_stitch_kernel<RM><<<npieces, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, mean, out);
+    return launched(h, "dc_stitch_kernel", st);
+  };
+  if (r <= 4) return go(std::integral_constant<int, 4>{});
+  if (r <= 8) return go(std::integral_constant<int, 8>{});
+  if (r <= 10) return go(std::integral_constant<int, 10>{});
+  if (r <= 16) return go(std::integral_constant<int, 16>{});
+  return go(std::integral_constant<int, 32>{});
 }
+
+size_t dc_stitch_ws_bytes(int npieces, int r) { return ((size_t)npieces * r + 32) * sizeof(double); }
 
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st) {

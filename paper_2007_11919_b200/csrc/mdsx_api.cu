@@ -18,7 +18,9 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
                  cudaStream_t st);
 int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
                      int npieces, int64_t max_m, int c, int r, const double* rot,
-                     const double* trans, double* out, cudaStream_t st);
+                     const double* trans, double* out, cudaStream_t st, int64_t n_recenter,
+                     double* ws);
+size_t dc_stitch_ws_bytes(int npieces, int r);
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st);
 int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const int64_t* off,
@@ -684,7 +686,7 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                       align_up((size_t)(npieces + 1) * sizeof(int64_t)) +
                       align_up((size_t)nj * r * r * sizeof(double)) +
                       align_up((size_t)nj * r * sizeof(double)) + align_up(nj * sizeof(double)) +
-                      align_up(nj * sizeof(int32_t)) + recenter_ws_bytes(r) + 4096;
+                      align_up(nj * sizeof(int32_t)) + align_up(dc_stitch_ws_bytes(npieces, r)) + 4096;
   if ((rc = ws_reserve(h, need))) return rc;
   double* P = (double*)ws_alloc(h, cp.total * r * sizeof(double), st);
   if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, P, estimates, gof, status, st)))
@@ -722,11 +724,13 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
     if ((rc = sg.put(toff, piece_off, (npieces + 1) * sizeof(int64_t)))) return rc;
     if ((rc = sg.end())) return rc;
   }
-  if ((rc = launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st)))
-    return rc;
-  if (flags & MDSX_NO_RECENTER) return MDSX_OK;
-  double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
-  return launch_recenter(h, out, n, r, part, st);
+  // stitch + final re-centring in one pass over P: the column mean comes from
+  // per-piece sums of P pushed through each fit (no second pass over out)
+  const bool rec = !(flags & MDSX_NO_RECENTER);
+  double* sws = rec ? (double*)ws_alloc(h, dc_stitch_ws_bytes(npieces, r), st) : nullptr;
+  if (rec && !sws) return MDSX_CUDA;
+  return launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st,
+                          rec ? n : 0, sws);
 }
 
 int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
