@@ -73,16 +73,14 @@ WORKLOADS = {
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
 TRAFFIC = {
-    ("dc2", "lanczos_smem_kernel"): {"bytes": (40.937 + 0.073) * 1e6,
-                                     "src": "profiles/r01b_ncu_full_dc2.txt"},
-    ("dc2", "gram_piece_kernel"): {"bytes": (439.812 + 29.598) * 1e6,
-                                   "src": "profiles/r01b_ncu_full_dc2.txt"},
-    ("dc2", "points_rows_kernel"): {"bytes": (448.773 + 35.181) * 1e6,
-                                    "src": "profiles/r01b_ncu_full_dc2.txt"},
-    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.050 + 784.856) * 1e6,
-                                       "src": "profiles/r01b_ncu_full_interp4.txt"},
-    ("interp4", "subtract_mean_kernel"): {"bytes": (800.045 + 741.575) * 1e6,
-                                          "src": "profiles/r01b_ncu_full_interp4.txt"},
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (501.808 + 67.287) * 1e6,
+                                     "src": "profiles/r01c_ncu_full_dc2.txt"},
+    ("dc2", "gram_piece_kernel"): {"bytes": (439.715 + 27.654) * 1e6,
+                                   "src": "profiles/r01c_ncu_full_dc2.txt"},
+    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.103 + 786.258) * 1e6,
+                                       "src": "profiles/r01c_ncu_full_interp4.txt"},
+    ("interp4", "subtract_mean_kernel"): {"bytes": (800.045 + 741.213) * 1e6,
+                                          "src": "profiles/r01c_ncu_full_interp4.txt"},
 }
 
 
@@ -256,6 +254,13 @@ def piece_sizes(w: dict, plan) -> list:
     return [w["l"]]
 
 
+def fused_points(w: dict) -> bool:
+    """The piece pipeline computes points inside the Lanczos kernel (mdsx_api.cu
+    run_classical): form-0 pieces with k <= 104, r <= 10, aligned rows."""
+    return (w["algo"] in ("divide", "fast") and w["p"] <= 104 and w["r"] <= 10
+            and not os.environ.get("MDSX_NO_FUSE"))
+
+
 def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
     """Work of ONE launch of `kernel` in one step (DESIGN.md §3 work models):
     flops for compute-bound kernels (fp64), bytes for streaming ones."""
@@ -276,9 +281,17 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
             if steps > 0:
                 j = np.arange(int(steps))
                 fl += float(np.sum(2.0 * k * k + 4.0 * k * (j + 1) + 6.0 * k))
-        return {"bound": "tensor", "flops": fl,
-                "model": "sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
-                         "+ 6k (three-term part)"}
+        krylov_model = ("sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
+                        "+ 6k (three-term part)")
+        if fused_points(w):
+            # the piece pipeline's Lanczos kernel also streams every piece's rows
+            # for its points (points_stream.cuh): its algorithmic traffic
+            tot = sum(sizes)
+            by = tot * p * esize + tot * r * 8 + sum(min(m, p) ** 2 * 8 for m in sizes)
+            return {"bound": "hbm", "bytes": by, "flops": fl,
+                    "model": "rows*p*sizeof(in) (points stream) + rows*r*8 (points) + k^2*8 "
+                             "per piece (Gram read); Krylov phase: " + krylov_model}
+        return {"bound": "tensor", "flops": fl, "model": krylov_model}
     if kernel in ("gower_affine_kernel", "gower_stream_kernel", "gower_bulk_kernel"):
         n = w["n"]
         return {"bound": "hbm", "bytes": n * p * esize + n * r * 8,
@@ -510,6 +523,9 @@ def run_ours(args, w):
         if wk["bound"] == "hbm":
             per_kernel[kname] = {"GB/s": wk["bytes"] / lps / t / 1e9,
                                  "frac_hbm": wk["bytes"] / lps / t / 1e9 / peaks["hbm_gbs"]}
+            if "flops" in wk:
+                per_kernel[kname]["TFLOP/s"] = wk["flops"] / lps / t / 1e12
+                per_kernel[kname]["frac_fp64"] = wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]
         else:
             per_kernel[kname] = {"TFLOP/s": wk["flops"] / lps / t / 1e12,
                                  "frac_fp64": wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]}

@@ -172,23 +172,31 @@ points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restr
 }
 
 
-// ---- form 0, 16-byte aligned rows: one CTA per piece (points_stream.cuh).
-// `pending` (optional): only pieces with pending[id] != 0 -- the ones whose
-// points the fused Lanczos epilogue did not produce.
+// ---- form 0, 16-byte aligned rows (points_stream.cuh).  Grid (chunks, pieces):
+// chunks == 1 -> one CTA per piece, signs applied in the CTA; otherwise each
+// CTA takes CH rows and leaves its column candidates for sign_kernel (few
+// pieces: spread one piece over several SMs).  `pending` (optional): only
+// pieces with pending[id] != 0 -- the ones whose points the fused Lanczos
+// epilogue did not produce.
 template <typename T, int RM>
 __global__ void __launch_bounds__(mdsx::PS_T, 2)
 points_piece_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
                     const PieceDesc* __restrict__ pd, int r, const double* __restrict__ mu_all,
                     const double* __restrict__ Uall, double* __restrict__ points,
-                    const int* __restrict__ pending) {
+                    const int* __restrict__ pending, double2* __restrict__ cand, int maxch) {
   extern __shared__ __align__(16) unsigned char pr_smem[];
-  const PieceDesc d = pd[blockIdx.x];
+  const PieceDesc d = pd[blockIdx.y];
   if (pending && !pending[d.id]) return;
-  mdsx::PieceStream<T, RM> ps(pr_smem, X, ld, row_idx + d.row_off, p, d.m);
+  const bool chunked = gridDim.x > 1;
+  const int r0 = chunked ? blockIdx.x * CH : 0;
+  if (r0 >= d.m) return;
+  const int rows = chunked ? min(CH, d.m - r0) : d.m;
+  mdsx::PieceStream<T, RM> ps(pr_smem, X, ld, row_idx + d.row_off + r0, p, rows);
   ps.prologue();
   mdsx::ps_load_records<RM>(pr_smem, Uall + d.u_off, mu_all + (int64_t)d.id * p, p, r);
   __syncthreads();
-  ps.run(pr_smem, r, points + d.pt_off * r);
+  ps.run(pr_smem, r, points + (d.pt_off + r0) * r,
+         chunked ? cand + ((size_t)d.id * maxch + blockIdx.x) * r : nullptr, r0);
 }
 
 __global__ void __launch_bounds__(PT)
@@ -214,6 +222,39 @@ sign_kernel(const PieceDesc* __restrict__ pd, int r, const double2* __restrict__
   __syncthreads();
   for (int64_t e = threadIdx.x; e < (int64_t)d.m * r; e += PT) {
     const int c = (int)(e % r);
+    if (sgn[c] < 0.0) out[e] = -out[e];
+  }
+}
+
+// Signs for the chunked points_piece_kernel: candidates hold the SIGNED value
+// of each chunk's largest |entry| (x) and its row (y); grid (chunks, pieces),
+// every CTA reduces the piece's candidates (fixed order, lowest row on ties)
+// and flips its own chunk's rows.
+__global__ void __launch_bounds__(PT)
+sign_chunk_kernel(const PieceDesc* __restrict__ pd, int r, const double2* __restrict__ cand,
+                  int maxch, double* __restrict__ points) {
+  __shared__ double sgn[MDSX_MAX_R];
+  const PieceDesc d = pd[blockIdx.y];
+  const int r0 = blockIdx.x * CH;
+  if (r0 >= d.m) return;
+  const int nch = (d.m + CH - 1) / CH;
+  if (threadIdx.x < r) {
+    const int c = threadIdx.x;
+    double bv = -1.0, bs = 1.0;
+    int bi = 0x7fffffff;
+    for (int ch = 0; ch < nch; ++ch) {
+      const double2 e = cand[((size_t)d.id * maxch + ch) * r + c];
+      const int i = (int)e.y;
+      const double a = fabs(e.x);
+      if (a > bv || (a == bv && i < bi)) { bv = a; bi = i; bs = e.x < 0.0 ? -1.0 : 1.0; }
+    }
+    sgn[c] = bs;
+  }
+  __syncthreads();
+  double* out = points + (d.pt_off + r0) * r;
+  const int rows = min(CH, d.m - r0);
+  for (int e = threadIdx.x; e < rows * r; e += PT) {
+    const int c = e % r;
     if (sgn[c] < 0.0) out[e] = -out[e];
   }
 }
@@ -249,6 +290,9 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
                        ((size_t)ld * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(data) & 15) == 0 &&
                        !getenv("MDSX_POINTS_TILED");
   if (rows_ok && all_form0) {
+    // few pieces (e.g. the landmark set of interpolation): CH-row chunks over
+    // several CTAs + sign_kernel; many pieces: one CTA per piece
+    const int chunks = (npieces < 2 * h->num_sms && !pending) ? maxch : 1;
     const int RM = r <= 4 ? 4 : r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : 16;
     auto go = [&](auto tag, auto rm) {
       using T = decltype(tag);
@@ -257,8 +301,8 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
       auto kern = points_piece_kernel<T, RMc>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
       mdsx::pre(h, st);
-      kern<<<npieces, mdsx::PS_T, smem2, st>>>((const T*)data, ld, p, row_idx, pd, r, mu, U, points,
-                                                pending);
+      kern<<<dim3(chunks, npieces), mdsx::PS_T, smem2, st>>>((const T*)data, ld, p, row_idx, pd, r,
+                                                             mu, U, points, pending, cand, maxch);
       return launched(h, "points_piece_kernel", st);
     };
     auto by_rm = [&](auto tag) {
@@ -270,7 +314,11 @@ int launch_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p
         default: return go(tag, std::integral_constant<int, 16>{});
       }
     };
-    return dtype == MDSX_F32 ? by_rm(float{}) : by_rm(double{});
+    int rc2 = dtype == MDSX_F32 ? by_rm(float{}) : by_rm(double{});
+    if (rc2 || chunks == 1) return rc2;
+    mdsx::pre(h, st);
+    sign_chunk_kernel<<<dim3(chunks, npieces), PT, 0, st>>>(pd, r, cand, maxch, points);
+    return launched(h, "sign_chunk_kernel", st);
   }
   if (dtype == MDSX_F32) {
     cudaFuncSetAttribute(points_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -61,6 +61,7 @@ struct PieceStream {
   const char* src_cur;
   int64_t nxt_idx;
 
+  // rows [0, m) of ridx_ (callers offset ridx_ to a chunk of the piece)
   __device__ PieceStream(unsigned char* smem, const T* X_, int64_t ld_, const int64_t* ridx_, int p_,
                          int m)
       : X(X_), ld(ld_), ridx(ridx_), p(p_) {
@@ -101,8 +102,12 @@ struct PieceStream {
     for (int b = 0; b < PS_NS - 1; ++b) issue();
   }
 
-  // points of the piece into out (m x r rows, row-major), signs applied
-  __device__ void run(const unsigned char* smem, int r, double* out) {
+  // points of the rows into out (m x r, row-major).  cand == nullptr: the rows
+  // are the whole piece and the column signs are applied here; otherwise the
+  // per-column (signed value, row0 + row) of the largest |value| go to
+  // cand[0..r) for sign_chunk_kernel.
+  __device__ void run(const unsigned char* smem, int r, double* out, double2* cand = nullptr,
+                      int row0 = 0) {
     constexpr int W = ps_rec_width<RM>();
     const double2* rec = reinterpret_cast<const double2*>(smem);
     const int tid = threadIdx.x;
@@ -200,7 +205,9 @@ struct PieceStream {
         }
       }
       ps_sgn[tid] = v < 0.0 ? -1.0 : 1.0;
+      if (cand) cand[tid] = make_double2(v, (double)(ix == 0x7fffffff ? ix : row0 + ix));
     }
+    if (cand) return;
     __syncthreads();
     bool any = false;
     double sg[RM];

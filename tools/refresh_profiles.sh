@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $o/${tag}_ncu_launch.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $o/${tag}_launches_interp4.csv \
     python bench.py --workload interp4 --steps 2 --warmup 3 --no-e2e --no-cpu > $o/${tag}_ncu_launch4.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"lanczos|gram_piece|points_rows|procrustes_fit|dc_stitch" -c 5 \
+ncu --set full --import-source on --clock-control none -k regex:"lanczos|gram_piece|procrustes_fit|dc_stitch|points_piece" -c 5 \
     -o $o/${tag}_dc2_full python tools/profile_run.py dc2 > $o/${tag}_ncu_full.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"gower_bulk|subtract_mean" -c 2 \
     -o $o/${tag}_interp4_full python tools/profile_run.py interp4 > $o/${tag}_ncu_full4.log 2>&1
