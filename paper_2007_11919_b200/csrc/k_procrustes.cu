@@ -474,42 +474,71 @@ procrustes_fit_reg_kernel(const double* __restrict__ tgt, const int64_t* __restr
   }
 }
 
+// X[start_j + i] <- X[start_j + i] T_j + t_j for the rows of job j (in place);
+// grid (row chunks of AP_ROWS, jobs).  The chunk is contiguous (rows x r
+// doubles): it is staged through shared memory with coalesced 16-byte loads,
+// and every thread then produces flat output elements (row, column) that are
+// stored coalesced -- a thread-per-row walk over 80-byte rows would touch ~20
+// L1 lines per warp instruction.
+template <int RM>
+__host__ __device__ constexpr int ap_rows() { return RM <= 16 ? 256 : 128; }
+
 template <int RM>
 __global__ void __launch_bounds__(256)
 apply_kernel(double* __restrict__ buf, int r, const int64_t* __restrict__ start,
              const int64_t* __restrict__ len, const double* __restrict__ rot,
              const double* __restrict__ trans) {
+  __shared__ double Ts[RM * RM], ts[RM];
+  constexpr int AP_ROWS = ap_rows<RM>();
+  __shared__ __align__(16) double xs[AP_ROWS * RM];
   const int job = blockIdx.y;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= len[job]) return;
-  const double* T = rot + (size_t)job * r * r;
-  const double* tv = trans + (size_t)job * r;
-  double* row = buf + (start[job] + i) * r;
-  double x[RM];
-#pragma unroll
-  for (int a = 0; a < RM; ++a) x[a] = a < r ? row[a] : 0.0;
-#pragma unroll
-  for (int b = 0; b < RM; ++b) {
-    if (b >= r) break;
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < RM; ++a)
-      if (a < r) s = fma(x[a], T[a * r + b], s);
-    row[b] = s + tv[b];
+  const int64_t n = len[job];
+  const int64_t i0 = (int64_t)blockIdx.x * AP_ROWS;
+  if (i0 >= n) return;
+  const int rows = (int)min((int64_t)AP_ROWS, n - i0);
+  for (int e = threadIdx.x; e < RM * RM; e += blockDim.x) {
+    const int a = e / RM, b = e % RM;
+    Ts[e] = (a < r && b < r) ? rot[(size_t)job * r * r + a * r + b] : 0.0;
+  }
+  if (threadIdx.x < RM) ts[threadIdx.x] = threadIdx.x < r ? trans[(size_t)job * r + threadIdx.x] : 0.0;
+  double* base = buf + (start[job] + i0) * r;
+  const int ne = rows * r;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+    const double2* b2 = reinterpret_cast<const double2*>(base);
+    for (int e = threadIdx.x; e < ne / 2; e += blockDim.x) reinterpret_cast<double2*>(xs)[e] = b2[e];
+    if ((ne & 1) && threadIdx.x == 0) xs[ne - 1] = base[ne - 1];
+  } else {
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) xs[e] = base[e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int row = e / r, b = e - row * r;
+    const double* xr = xs + row * r;
+    double s2 = 0.0;
+    for (int a = 0; a < r; ++a) s2 = fma(xr[a], Ts[a * RM + b], s2);
+    base[e] = s2 + ts[b];
   }
 }
 
 // D&C stitch (algorithms.py:151-156): piece 0 verbatim, piece j>0 rows c..
 // through fit j-1, scattered to original rows, minus the final column mean
 // (algorithms.py:122-125) when `mean` is given.  One CTA per piece: T, t and
-// the mean staged in shared memory, one row per thread per pass.
+// the mean in shared memory; the piece's rows (contiguous in P) are staged in
+// ST_ROWS-row chunks with coalesced loads, then every thread produces flat
+// (row, column) elements, so a warp store covers ~3 output rows' contiguous
+// 80-byte segments instead of 32 scattered rows.
+constexpr int ST_ROWS = 256;
+
 template <int RM>
 __global__ void __launch_bounds__(256)
 dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_idx,
                  const int64_t* __restrict__ off, int c, int r, const double* __restrict__ rot,
                  const double* __restrict__ trans, const double* __restrict__ mean,
                  double* __restrict__ out) {
+  constexpr int SR = RM <= 16 ? ST_ROWS : ST_ROWS / 2;
   __shared__ double Ts[RM * RM], ts[RM], ms[RM];
+  __shared__ double xs[SR * RM];
+  __shared__ int64_t dsts[SR];
   const int j = blockIdx.x;
   const int64_t o = off[j], m = off[j + 1] - o;
   for (int e = threadIdx.x; e < RM * RM; e += blockDim.x) {
@@ -522,56 +551,61 @@ dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_i
     ts[b] = (j == 0 || b >= r) ? 0.0 : trans[(size_t)(j - 1) * r + b];
     ms[b] = (mean && b < r) ? mean[b] : 0.0;
   }
-  __syncthreads();
-  for (int64_t i = threadIdx.x + (j == 0 ? 0 : c); i < m; i += blockDim.x) {
-    const double* src = P + (o + i) * r;
-    double* dst = out + row_idx[o + i] * r;
-    double x[RM];
-#pragma unroll
-    for (int a = 0; a < RM; ++a) x[a] = a < r ? src[a] : 0.0;
-    if (j == 0) {
-#pragma unroll
-      for (int b = 0; b < RM; ++b)
-        if (b < r) dst[b] = x[b] - ms[b];
-      continue;
-    }
-#pragma unroll
-    for (int b = 0; b < RM; ++b) {
-      if (b >= r) break;
-      double s = 0.0;
-#pragma unroll
-      for (int a = 0; a < RM; ++a) s = fma(x[a], Ts[a * RM + b], s);
-      dst[b] = (s + ts[b]) - ms[b];
+  const int64_t first = (j == 0 ? 0 : c);
+  for (int64_t i0 = first; i0 < m; i0 += SR) {
+    const int rows = (int)min((int64_t)SR, m - i0);
+    __syncthreads();                                  // previous chunk consumed
+    const double* src = P + (o + i0) * r;
+    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) xs[e] = src[e];
+    for (int q = threadIdx.x; q < rows; q += blockDim.x) dsts[q] = row_idx[o + i0 + q] * r;
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {
+      const int row = e / r, b = e - row * r;
+      const double* xr = xs + row * r;
+      double v;
+      if (j == 0) {
+        v = xr[b];
+      } else {
+        double s2 = 0.0;
+        for (int a2 = 0; a2 < r; ++a2) s2 = fma(xr[a2], Ts[a2 * RM + b], s2);
+        v = s2 + ts[b];
+      }
+      out[dsts[row] + b] = v - ms[b];
     }
   }
 }
 
 // Column sums of each piece's OWN rows of the piece points P (piece 0: all
-// rows, piece j > 0: rows c..), fixed-order block reduction.
+// rows, piece j > 0: rows c..), pushed through the piece's fit; coalesced:
+// thread (g, col) of RG = 256 / r row groups walks rows g, g + RG, ...
 template <int RM>
 __global__ void __launch_bounds__(256)
 dc_own_sums_kernel(const double* __restrict__ P, const int64_t* __restrict__ off, int c, int r,
                    const double* __restrict__ rot, const double* __restrict__ trans,
                    double* __restrict__ sums) {
-  __shared__ double red[8][RM];
+  __shared__ double red[256];
+  __shared__ double colsum[RM];
   const int j = blockIdx.x;
   const int64_t o = off[j], m = off[j + 1] - o;
-  double acc[RM];
+  const int RG = 256 / r;
+  const int g = threadIdx.x / r, col = threadIdx.x - g * r;
+  double acc = 0.0;
+  if (g < RG) {
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};          // four loads in flight, fixed combine order
+    int64_t i = (j == 0 ? 0 : c) + g;
+    for (; i + 3 * RG < m; i += 4 * RG) {
 #pragma unroll
-  for (int a = 0; a < RM; ++a) acc[a] = 0.0;
-  for (int64_t i = threadIdx.x + (j == 0 ? 0 : c); i < m; i += 256) {
-    const double* src = P + (o + i) * r;
-#pragma unroll
-    for (int a = 0; a < RM; ++a)
-      if (a < r) acc[a] += src[a];
+      for (int u = 0; u < 4; ++u) a4[u] += P[(o + i + u * RG) * r + col];
+    }
+    for (; i < m; i += RG) a4[0] += P[(o + i) * r + col];
+    acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int a = 0; a < RM; ++a) {
-    double v = acc[a];
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-    if (lane == 0) red[warp][a] = v;
+  red[threadIdx.x] = g < RG ? acc : 0.0;
+  __syncthreads();
+  if (threadIdx.x < r) {
+    double v = 0.0;
+    for (int gg = 0; gg < RG; ++gg) v += red[gg * r + threadIdx.x];   // fixed order
+    colsum[threadIdx.x] = v;
   }
   __syncthreads();
   // contribution of the piece to the stitched column sums: S (piece 0) or
@@ -580,16 +614,11 @@ dc_own_sums_kernel(const double* __restrict__ P, const int64_t* __restrict__ off
     const int b = threadIdx.x;
     double v;
     if (j == 0) {
-      v = 0.0;
-      for (int w = 0; w < 8; ++w) v += red[w][b];
+      v = colsum[b];
     } else {
       const double* T = rot + (size_t)(j - 1) * r * r;
       v = (double)(m - c) * trans[(size_t)(j - 1) * r + b];
-      for (int a = 0; a < r; ++a) {
-        double sa = 0.0;
-        for (int w = 0; w < 8; ++w) sa += red[w][a];
-        v = fma(sa, T[a * r + b], v);
-      }
+      for (int a2 = 0; a2 < r; ++a2) v = fma(colsum[a2], T[a2 * r + b], v);
     }
     sums[(size_t)j * r + b] = v;
   }
@@ -902,11 +931,17 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
                  int njobs, int64_t max_len, const double* rot, const double* trans,
                  cudaStream_t st) {
   if (njobs == 0 || max_len == 0) return MDSX_OK;
-  dim3 grid((unsigned)((max_len + 255) / 256), (unsigned)njobs);
-  if (r <= 4) { mdsx::pre(h, st); apply_kernel<4><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
-  else if (r <= 8) { mdsx::pre(h, st); apply_kernel<8><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
-  else if (r <= 16) { mdsx::pre(h, st); apply_kernel<16><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
-  else { mdsx::pre(h, st); apply_kernel<32><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans); }
+  auto go = [&](auto rm) {
+    constexpr int RM = decltype(rm)::value;
+    dim3 grid((unsigned)((max_len + ap_rows<RM>() - 1) / ap_rows<RM>()), (unsigned)njobs);
+    mdsx::pre(h, st);
+    apply_kernel<RM><<<grid, 256, 0, st>>>(buf, r, start, len, rot, trans);
+  };
+  if (r <= 4) go(std::integral_constant<int, 4>{});
+  else if (r <= 8) go(std::integral_constant<int, 8>{});
+  else if (r <= 10) go(std::integral_constant<int, 10>{});
+  else if (r <= 16) go(std::integral_constant<int, 16>{});
+  else go(std::integral_constant<int, 32>{});
   return launched(h, "apply_kernel", st);
 }
 
