@@ -156,6 +156,11 @@ __device__ void tri_twisted(const double* al, const double* be, int m, double th
   nrm2 = n2;
 }
 
+// index of the stored upper tile (I, J), I <= J, of an nbk x nbk block grid
+__device__ __forceinline__ int lz_tile(int I, int J, int nbk) {
+  return I * nbk - (I * (I - 1)) / 2 + (J - I);
+}
+
 // three sums over the CTA at once (fixed order), results in every thread
 __device__ void block_sum3(double (&v)[3], double* red3) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -265,7 +270,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
 
   const PieceDesc d = pd[blockIdx.x];
   const int pid = d.id, k = d.k;
-  const int kq = k | 1;                        // odd leading dim of Q (conflict-free columns)
+  const int kq = (8 * ((k + 7) >> 3)) | 1;    // odd leading dim of Q, >= the tiled width (zero rows past k)
   const int tid = threadIdx.x;
   const double* Ag = Aall + d.a_off;
   if (only_flagged) {           // fallback pass: only pieces the subspace kernel handed over
@@ -285,15 +290,24 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     if (tid < 2) gof[2 * (int64_t)pid + tid] = 0.0;
     return;
   }
-  double* A = sm;                              // packed upper: row i = A[i][i..k)
-  double* Q = A + (size_t)k * (k + 1) / 2;     // column j at Q + j*kq, j < QMAX
+  // A in 8x8 tiles of its upper block triangle: tile (I, J), I <= J < nbk, at
+  // At + 64 * tidx(I, J), row-major inside the tile, zero-padded past k
+  // (diagonal tiles hold both triangles).  One LDS.128 per lane reads a whole
+  // tile, and the matvec needs no per-element index arithmetic.
+  const int nbk = (k + 7) >> 3;
+  const int ntile = nbk * (nbk + 1) / 2;
+  double* At = sm;
+  double* Q = At + (size_t)64 * ntile;         // column j at Q + j*kq, j < QMAX
   double* S = Q + (size_t)QMAX * kq;           // Ritz coefficients, S[c*RMAX + i]
   double* U2 = S + (size_t)QMAX * RMAX;        // twisted-factorisation pivots, same layout
   double* U3 = U2 + (size_t)QMAX * RMAX;
   const int qcap = min(QMAX, k);
 
   double fro = 0.0, tr = 0.0;
-  {                                            // packed copy: 4 independent loads in flight
+  for (int e = tid; e < 64 * ntile; e += LT) At[e] = 0.0;
+  for (int e = tid; e < QMAX * kq; e += LT) Q[e] = 0.0;     // rows past k stay zero
+  __syncthreads();
+  {                                            // tiled copy: 4 independent loads in flight
     const int kk2 = k * k;
     for (int e0 = tid; e0 < kk2; e0 += 4 * LT) {
       double v[4];
@@ -307,8 +321,9 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
         const int e = e0 + u * LT;
         if (e < kk2) {
           const int i = e / k, a = e - i * k;
+          const int I = i >> 3, J = a >> 3;
+          if (I <= J) At[64 * lz_tile(I, J, nbk) + 8 * (i & 7) + (a & 7)] = v[u];
           if (a >= i) {
-            A[i * k - i * (i - 1) / 2 + a - i] = v[u];
             fro = fma((a == i ? 1.0 : 2.0) * v[u], v[u], fro);   // off-diagonal entries count twice
             if (a == i) tr += v[u];
           }
@@ -336,40 +351,44 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   while (!done) {
     const double* q = Q + (size_t)m * kq;
     LZ_T0(t_mv);
-    // w = A q with the packed symmetric A: row i = sum_{a<i} A[a][i] q_a + sum_{a>=i} A[i][a] q_a;
-    // two threads per row (a split in halves, 2 accumulators per part), one shuffle
+    // w = A q over the tiles: warp w owns block rows I = w, w + 8; lane (i =
+    // lane / 4, c = lane % 4) reads A_IJ[i][2c..2c+1] of the stored tile (I, J)
+    // (J >= I: direct, y_I[i] += A_IJ[i][.] q_J[.]) or of tile (J, I) (J < I:
+    // transposed, y_I[2c+v] += A_JI[i][2c+v] q_J[i]); both partial sums stay
+    // in registers over the block row and are reduced once (4 and 8 lanes).
     {
-      const int i = tid >> 1, hf = tid & 1;
-      const int kh = (k + 1) >> 1;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      if (i < k) {
-        const int a0 = hf * kh, a1 = min(k, a0 + kh);
-        const int cend = min(a1, i);
-        int a = a0;
-        int off = a * k - a * (a - 1) / 2;      // packed offset of row a
-        for (; a + 1 < cend; a += 2) {          // column part
-          s0 = fma(A[off + i - a], q[a], s0);
-          off += k - a;
-          s1 = fma(A[off + i - a - 1], q[a + 1], s1);
-          off += k - a - 1;
+      const int lane = tid & 31, warp = tid >> 5;
+      const int ti = lane >> 2, tc = lane & 3;
+      for (int I = warp; I < nbk; I += LT / 32) {
+        double dsum = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll 4
+        for (int J = 0; J < nbk; ++J) {
+          const bool dir = J >= I;
+          const double2 a2 = *reinterpret_cast<const double2*>(
+              At + 64 * (dir ? lz_tile(I, J, nbk) : lz_tile(J, I, nbk)) + 8 * ti + 2 * tc);
+          const double* qJ = q + 8 * J;
+          if (dir) {
+            dsum = fma(a2.x, qJ[2 * tc], dsum);
+            dsum = fma(a2.y, qJ[2 * tc + 1], dsum);
+          } else {
+            const double qi = qJ[ti];
+            t0 = fma(a2.x, qi, t0);
+            t1 = fma(a2.y, qi, t1);
+          }
         }
-        if (a < cend) s0 = fma(A[off + i - a], q[a], s0);
-        const double* rowp = A + (i * k - i * (i - 1) / 2) - i;
-        a = max(a0, i);
-        double s4 = 0.0, s5 = 0.0;
-        for (; a + 3 < a1; a += 4) {            // own row part, 4 chains
-          s2 = fma(rowp[a], q[a], s2);
-          s3 = fma(rowp[a + 1], q[a + 1], s3);
-          s4 = fma(rowp[a + 2], q[a + 2], s4);
-          s5 = fma(rowp[a + 3], q[a + 3], s5);
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
         }
-        for (; a < a1; ++a) s2 = fma(rowp[a], q[a], s2);
-        s2 += s4;
-        s3 += s5;
+        // lane (ti, 0) owns row 8I + ti of the direct part; lane (0, tc) rows 8I + 2tc, +1
+        // of the transposed part: gather both into row-owner lanes, one store each
+        const double tt0 = __shfl_sync(0xffffffffu, t0, (ti >> 1) & 3);   // lane (0, ti/2)
+        const double tt1 = __shfl_sync(0xffffffffu, t1, (ti >> 1) & 3);
+        if (tc == 0 && 8 * I + ti < k) wv[8 * I + ti] = dsum + ((ti & 1) ? tt1 : tt0);
       }
-      double t = (s0 + s1) + (s2 + s3);
-      t += __shfl_xor_sync(0xffffffffu, t, 1);
-      if (i < k && hf == 0) wv[i] = t;
     }
     __syncthreads();
     LZ_ACC(0, t_mv);
@@ -1518,7 +1537,8 @@ int lanczos_kmax() { return LMAX; }
 int lanczos_rmax() { return RMAX; }
 
 static size_t lanczos_bytes(int kmax, int qmax) {
-  return ((size_t)kmax * (kmax + 1) / 2 + (size_t)qmax * (kmax | 1) + 3 * (size_t)qmax * RMAX) *
+  const size_t nbk = (size_t)(kmax + 7) / 8;
+  return (64 * nbk * (nbk + 1) / 2 + (size_t)qmax * ((8 * nbk) | 1) + 3 * (size_t)qmax * RMAX) *
          sizeof(double);
 }
 
