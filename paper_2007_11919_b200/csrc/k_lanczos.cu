@@ -396,14 +396,29 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     // three-term part first (alpha = q_j.y, gamma = q_{j-1}.y, |y|^2 in one
     // reduction), then ONE classical Gram-Schmidt pass against Q[:, 0..m];
     // a second pass only when the first removed more than half of the norm
-    // (DGKS, "twice is enough") or the three-term estimate is unreliable
+    // (DGKS, "twice is enough") or the three-term estimate is unreliable.
+    // Barriers: partial sums (1), w (1), CGS coefficients (1), projected w and
+    // its norm (1), next basis vector (1); each reduction buffer is written
+    // once per step, so one barrier per reduction suffices.
+    const int lane = tid & 31, wrp = tid >> 5;
     double al, nw0;
     {
       const double yv = tid < k ? wv[tid] : 0.0;
       const double qv = tid < k ? q[tid] : 0.0;
       const double pv = (tid < k && m > 0) ? Q[(size_t)(m - 1) * kq + tid] : 0.0;
       double s3[3] = {qv * yv, pv * yv, yv * yv};
-      block_sum3(s3, red3);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s3[c] = mdsx::warp_sum(s3[c]);
+        if (lane == 0) red3[c * (LT / 32) + wrp] = s3[c];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < LT / 32; ++w2) t += red3[c * (LT / 32) + w2];   // fixed order
+        s3[c] = t;
+      }
       al = s3[0];
       const double ga = s3[1];
       nw0 = s3[2] - al * al - ga * ga;
@@ -411,15 +426,68 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       if (tid < k) wv[tid] = fma(-al, qv, fma(-ga, pv, yv));
       __syncthreads();
     }
-    cgs_project(Q, kq, k, m + 1, wv, hv);
-    al += hv[m];
-    __syncthreads();
-    double nw = block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red);
-    if (nw < 0.5 * nw0) {
-      cgs_project(Q, kq, k, m + 1, wv, hv);
-      al += hv[m];
+    // one CGS pass: coefficients h = Q^T w (4 threads per column), then
+    // w -= Q h by row pairs with the squared norm of the result reduced in the
+    // same phase; the row owner keeps its projected entry in wreg
+    const int nc = m + 1;
+    double wreg = 0.0, nw = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      {
+        const int part = tid & 3;
+        const int seg = (k + 3) >> 2;
+        for (int c = tid >> 2; c < ((nc + 7) & ~7); c += LT / 4) {     // warp-uniform trip count
+          double h0 = 0.0, h1 = 0.0;
+          if (c < nc) {
+            const double* qc = Q + (size_t)c * kq;
+            const int a1 = min(k, (part + 1) * seg);
+            int a = part * seg;
+            for (; a + 1 < a1; a += 2) {
+              h0 = fma(qc[a], wv[a], h0);
+              h1 = fma(qc[a + 1], wv[a + 1], h1);
+            }
+            if (a < a1) h0 = fma(qc[a], wv[a], h0);
+          }
+          double h = h0 + h1;
+          h += __shfl_xor_sync(0xffffffffu, h, 1);
+          h += __shfl_xor_sync(0xffffffffu, h, 2);
+          if (c < nc && part == 0) hv[c] = h;
+        }
+      }
       __syncthreads();
-      nw = block_sum(tid < k ? wv[tid] * wv[tid] : 0.0, red);
+      al += hv[m];
+      {
+        const int hf = tid & 1;
+        const int cmid = (nc + 1) >> 1;
+        double sq = 0.0;
+        for (int a = tid >> 1; a < ((k + 15) & ~15); a += LT / 2) {
+          double s0 = 0.0, s1 = 0.0;
+          if (a < k) {
+            const int c1 = hf ? nc : cmid;
+            int c = hf ? cmid : 0;
+            for (; c + 1 < c1; c += 2) {
+              s0 = fma(Q[(size_t)c * kq + a], hv[c], s0);
+              s1 = fma(Q[(size_t)(c + 1) * kq + a], hv[c + 1], s1);
+            }
+            if (c < c1) s0 = fma(Q[(size_t)c * kq + a], hv[c], s0);
+          }
+          double t = s0 + s1;
+          t += __shfl_xor_sync(0xffffffffu, t, 1);
+          if (a < k && hf == 0) {
+            wreg = wv[a] - t;                        // LT / 2 >= k: one row per pair
+            sq = wreg * wreg;
+          }
+        }
+        sq = mdsx::warp_sum(sq);
+        if (lane == 0) red[wrp] = sq;
+        // the projected entries go back to wv only after everyone has read the
+        // old ones (the barrier below): kept in wreg meanwhile
+        __syncthreads();
+        nw = 0.0;
+        for (int w2 = 0; w2 < LT / 32; ++w2) nw += red[w2];                  // fixed order
+        if ((tid >> 1) < k && (tid & 1) == 0) wv[tid >> 1] = wreg;
+      }
+      if (!(nw < 0.5 * nw0) || pass == 1) break;
+      __syncthreads();                              // second pass reads the new wv
     }
     LZ_ACC(1, t_cgs);
     LZ_T0(t_b);
@@ -435,11 +503,12 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     broke = false;
     if (!full && m < qcap) {
       if (b > 1e-13 * anorm) {
-        if (tid < k) Q[(size_t)m * kq + tid] = wv[tid] / b;
+        if ((tid >> 1) < k && (tid & 1) == 0) Q[(size_t)m * kq + (tid >> 1)] = wreg / b;
       } else {
         // invariant subspace: continue from a fresh direction orthogonal to Q
         // (finds further copies of repeated eigenvalues)
         broke = true;
+        __syncthreads();
         if (tid == 0) { beta[m - 1] = 0.0; beta2[m - 1] = 0.0; }
         if (tid < k) wv[tid] = hash_unit(((uint64_t)m << 20) ^ (uint64_t)tid);
         __syncthreads();
