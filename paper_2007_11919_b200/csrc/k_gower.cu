@@ -83,6 +83,47 @@ __global__ void ctx_qdiag_kernel(const T* __restrict__ X, int64_t ld, const int6
   q[j] = s;
 }
 
+// S = X1c^T X1c / l for r <= RM: every thread walks rows tid, tid + nt, ...
+// with the centred row and the whole upper triangle in registers; warp
+// shuffles, then the per-warp partials in `scr` (>= RM(RM+1)/2 x nw) summed
+// in fixed order.
+template <int RM>
+__device__ void ctx_S_upper(const double* __restrict__ X1, int64_t l, int r, const double* m1,
+                            double* scr, double* Ssh, double* S, int tid, int lane, int warp, int nw) {
+  constexpr int NE = RM * (RM + 1) / 2;
+  double ac[NE];
+#pragma unroll
+  for (int u = 0; u < NE; ++u) ac[u] = 0.0;
+  for (int64_t j = tid; j < l; j += blockDim.x) {
+    double xr[RM];
+#pragma unroll
+    for (int c = 0; c < RM; ++c) xr[c] = c < r ? X1[j * r + c] - m1[c] : 0.0;
+#pragma unroll
+    for (int a = 0, u = 0; a < RM; ++a)
+#pragma unroll
+      for (int b = a; b < RM; ++b, ++u) ac[u] = fma(xr[a], xr[b], ac[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < NE; ++u) {
+    const double t = mdsx::warp_sum(ac[u]);
+    if (lane == 0) scr[u * nw + warp] = t;
+  }
+  __syncthreads();
+  for (int u = tid; u < NE; u += blockDim.x) {
+    int a = 0, rem = u;
+    while (rem >= RM - a) { rem -= RM - a; ++a; }
+    const int b = a + rem;
+    if (a < r && b < r) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) t += scr[u * nw + w2];
+      t /= (double)l;
+      Ssh[a * r + b] = Ssh[b * r + a] = t;
+      S[a * r + b] = S[b * r + a] = t;
+    }
+  }
+  __syncthreads();
+}
+
 // ---- S, s, eigen-condition, Cholesky, M, v (one block)
 __global__ void __launch_bounds__(256)
 ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
@@ -91,67 +132,115 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
   __shared__ double m1[MDSX_MAX_R], s1[MDSX_MAX_R];
   __shared__ double Ssh[MDSX_MAX_R * MDSX_MAX_R], E[MDSX_MAX_R * MDSX_MAX_R];
   __shared__ double L[MDSX_MAX_R * MDSX_MAX_R];
+  __shared__ double scr[136 * 8];                 // S partials (16 * 17 / 2 entries x 8 warps)
   __shared__ int ok;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // column sums / means of X1: warp per column, lanes split the l rows (fixed order)
-  for (int c = warp; c < r; c += nw) {
-    double s = 0.0;
-    for (int64_t j = lane; j < l; j += 32) s += X1[j * r + c];
-    s = mdsx::warp_sum(s);
-    if (lane == 0) { s1[c] = s; m1[c] = s / (double)l; }
+  // column sums / means of X1, then S = X1c^T X1c / l: every thread walks
+  // rows tid, tid + 256, ... with the row in registers (coalesced-by-row
+  // loads, no strided column walks), then fixed-order warp + block trees
+  {
+    double cs[MDSX_MAX_R];
+    for (int c = 0; c < r; ++c) cs[c] = 0.0;
+    for (int64_t j = tid; j < l; j += blockDim.x)
+      for (int c = 0; c < r; ++c) cs[c] += X1[j * r + c];
+    for (int c = 0; c < r; ++c) {
+      const double t = mdsx::warp_sum(cs[c]);
+      if (lane == 0) E[c * nw + warp] = t;            // E as scratch (r x nw <= 32 x 32)
+    }
+    __syncthreads();
+    if (tid < r) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) t += E[tid * nw + w2];
+      s1[tid] = t;
+      m1[tid] = t / (double)l;
+    }
+    __syncthreads();
   }
+  if (r <= 10) ctx_S_upper<10>(X1, l, r, m1, scr, Ssh, S, tid, lane, warp, nw);
+
+  else {
+    // upper-triangle entries in chunks of 32, same walk (r > 16)
+    const int ne = r * (r + 1) / 2;
+    for (int e0 = 0; e0 < ne; e0 += 32) {
+      double ac[32];
+      int ea[32], eb[32];
+      int cnt = 0;
+      for (int a = 0, e = 0; a < r; ++a)
+        for (int b = a; b < r; ++b, ++e)
+          if (e >= e0 && e < e0 + 32) { ea[cnt] = a; eb[cnt] = b; ++cnt; }
+      for (int u = 0; u < 32; ++u) ac[u] = 0.0;
+      for (int64_t j = tid; j < l; j += blockDim.x) {
+        double xr[MDSX_MAX_R];
+        for (int c = 0; c < r; ++c) xr[c] = X1[j * r + c] - m1[c];
+        for (int u = 0; u < cnt; ++u) ac[u] = fma(xr[ea[u]], xr[eb[u]], ac[u]);
+      }
+      for (int u = 0; u < cnt; ++u) {
+        const double t = mdsx::warp_sum(ac[u]);
+        if (lane == 0) L[u * nw + warp] = t;          // L as scratch (32 x nw)
+      }
+      __syncthreads();
+      if (tid < cnt) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < nw; ++w2) t += L[tid * nw + w2];
+        t /= (double)l;
+        const int a = ea[tid], b = eb[tid];
+        Ssh[a * r + b] = Ssh[b * r + a] = t;
+        S[a * r + b] = S[b * r + a] = t;
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < r * r; e += blockDim.x) E[e] = Ssh[e];
   __syncthreads();
-  // S = X1c^T X1c / l: warp per entry (a <= b), mirrored
-  for (int e = warp; e < r * r; e += nw) {
-    const int a = e / r, b = e % r;
-    if (a > b) continue;
-    double s = 0.0;
-    for (int64_t j = lane; j < l; j += 32) s = fma(X1[j * r + a] - m1[a], X1[j * r + b] - m1[b], s);
-    s = mdsx::warp_sum(s) / (double)l;
+  if (warp == 0) {
+    // eigenvalues of the symmetric PSD S for the condition test
+    // (algorithms.py:209-216) as the singular values of S: one-sided Jacobi on
+    // its columns, lane a owns row a, the three column dots of a pair reduced
+    // by one interleaved shuffle tree (a serial one-thread Jacobi cost ~0.15 ms)
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      int nrot = 0;
+      for (int i = 0; i < r - 1; ++i)
+        for (int j = i + 1; j < r; ++j) {
+          const double x = lane < r ? E[lane * r + i] : 0.0;
+          const double y = lane < r ? E[lane * r + j] : 0.0;
+          double al = x * x, be = y * y, ga = x * y;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          if (ga != 0.0 && ga * ga > 1e-30 * (al * be)) {
+            const double h = 0.5 * (be - al);
+            const double t = ga / (h + copysign(sqrt(fma(h, h, ga * ga)), h == 0.0 ? 1.0 : h));
+            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+            if (lane < r) {
+              E[lane * r + i] = c * x - sn * y;
+              E[lane * r + j] = sn * x + c * y;
+            }
+            ++nrot;
+          }
+          __syncwarp();
+        }
+      if (nrot == 0) break;
+    }
+    double lo = 1e308, hi = 0.0;
+    for (int i = 0; i < r; ++i) {
+      const double x = lane < r ? E[lane * r + i] : 0.0;
+      const double sv = sqrt(mdsx::warp_sum(x * x));
+      lo = fmin(lo, sv);
+      hi = fmax(hi, sv);
+    }
     if (lane == 0) {
-      Ssh[a * r + b] = Ssh[b * r + a] = s;
-      S[a * r + b] = S[b * r + a] = s;
-      E[a * r + b] = E[b * r + a] = s;
+      const double cd = lo <= 0.0 ? INFINITY : hi / lo;
+      cond[0] = cd;
+      ok = cd <= 1e12 ? 1 : 0;
     }
   }
   __syncthreads();
   if (tid == 0) {
-    // cyclic Jacobi for the r x r eigenvalues (condition estimate, algorithms.py:209-216)
-    double fro = 0.0;
-    for (int e = 0; e < r * r; ++e) fro += E[e] * E[e];
-    for (int sweep = 0; sweep < 40; ++sweep) {
-      double off = 0.0;
-      for (int i = 0; i < r; ++i)
-        for (int j = i + 1; j < r; ++j) off += E[i * r + j] * E[i * r + j];
-      // |offdiag|_F <= 1e-14 |S|_F: eigenvalues to 1e-14 |S|, far inside what
-      // the 1e12 condition test resolves (rotations leave ~eps|S| residues,
-      // so a tighter stop would only spin)
-      if (off <= 1e-28 * fro) break;
-      for (int pp = 0; pp < r - 1; ++pp)
-        for (int qq = pp + 1; qq < r; ++qq) {
-          const double apq = E[pp * r + qq];
-          if (apq == 0.0) continue;
-          double c, s, t;
-          mdsx::sym_rotation(E[pp * r + pp], E[qq * r + qq], apq, c, s, t);
-          for (int k = 0; k < r; ++k) {
-            const double ekp = E[k * r + pp], ekq = E[k * r + qq];
-            E[k * r + pp] = c * ekp - s * ekq;
-            E[k * r + qq] = s * ekp + c * ekq;
-          }
-          for (int k = 0; k < r; ++k) {
-            const double epk = E[pp * r + k], eqk = E[qq * r + k];
-            E[pp * r + k] = c * epk - s * eqk;
-            E[qq * r + k] = s * epk + c * eqk;
-          }
-          E[pp * r + qq] = 0.0;
-          E[qq * r + pp] = 0.0;
-        }
-    }
-    double lo = 1e308, hi = -1e308;
-    for (int i = 0; i < r; ++i) { lo = fmin(lo, E[i * r + i]); hi = fmax(hi, E[i * r + i]); }
-    const double cd = lo <= 0.0 ? INFINITY : hi / lo;
-    cond[0] = cd;
-    int good = cd <= 1e12 ? 1 : 0;
+    int good = ok;
+    const double cd = cond[0];
     // Cholesky S = L L^T (scipy cho_factor lower)
     for (int j = 0; j < r && good; ++j) {
       double d = Ssh[j * r + j];
@@ -629,28 +718,39 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
 
 // Interpolation's landmark overwrite (algorithms.py:264-268) fused with the
 // correction of the column sums: out[idx[i]] = base[i]; corr = sum(base - old).
+// landmark rows <- the classical configuration; per CTA (256 landmark rows)
+// the column sums of (base - old) go to corr_part[blockIdx.x] (fed to the
+// re-centring as extra partials; fixed-order tree).  Rows in registers.
+template <int RM>
 __global__ void __launch_bounds__(256)
 landmark_overwrite_kernel(const double* __restrict__ base, const int64_t* __restrict__ idx,
-                          int64_t l, int r, double* __restrict__ out, double* __restrict__ corr) {
+                          int64_t l, int r, double* __restrict__ out, double* __restrict__ corr_part) {
   __shared__ double red[256];
-  double acc[MDSX_MAX_R];
-  for (int c = 0; c < r; ++c) acc[c] = 0.0;
-  for (int64_t i = threadIdx.x; i < l; i += 256) {
+  double acc[RM];
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+#pragma unroll
+  for (int c = 0; c < RM; ++c) acc[c] = 0.0;
+  if (i < l) {
     double* o = out + idx[i] * r;
-    for (int c = 0; c < r; ++c) {
-      const double b = base[i * r + c];
-      acc[c] += b - o[c];
-      o[c] = b;
+#pragma unroll
+    for (int c = 0; c < RM; ++c) {
+      if (c < r) {
+        const double bv = base[i * r + c];
+        acc[c] = bv - o[c];
+        o[c] = bv;
+      }
     }
   }
-  for (int c = 0; c < r; ++c) {
+#pragma unroll
+  for (int c = 0; c < RM; ++c) {
+    if (c >= r) break;
     red[threadIdx.x] = acc[c];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int i = 0; i < 256; ++i) s += red[i];
-      corr[c] = s;
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+      if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+      __syncthreads();
     }
+    if (threadIdx.x == 0) corr_part[(size_t)blockIdx.x * r + c] = red[0];
     __syncthreads();
   }
 }
@@ -662,7 +762,15 @@ namespace mdsx {
 int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
                               int r, double* out, double* corr, cudaStream_t st) {
   mdsx::pre(h, st);
-  landmark_overwrite_kernel<<<1, 256, 0, st>>>(base, idx, l, r, out, corr);
+  const unsigned nb = (unsigned)((l + 255) / 256);
+  auto go = [&](auto rm) {
+    constexpr int RM = decltype(rm)::value;
+    landmark_overwrite_kernel<RM><<<nb, 256, 0, st>>>(base, idx, l, r, out, corr);
+  };
+  if (r <= 4) go(std::integral_constant<int, 4>{});
+  else if (r <= 10) go(std::integral_constant<int, 10>{});
+  else if (r <= 16) go(std::integral_constant<int, 16>{});
+  else go(std::integral_constant<int, 32>{});
   return launched(h, "landmark_overwrite_kernel", st);
 }
 

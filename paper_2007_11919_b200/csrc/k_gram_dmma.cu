@@ -492,9 +492,82 @@ gram_piece_kernel(const T* __restrict__ X, int64_t ld, int p, int P,
   if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
 }
 
+// Combine the centred Grams of a piece's row ranges (parallel-variance
+// formula): mu = sum_q m_q mu_q / m,  C = sum_q C_q + m_q (mu_q - mu)(mu_q - mu)^T;
+// splits in fixed order (deterministic).  Grid (entry blocks of 256, pieces);
+// every CTA stages the split sizes and means and forms mu itself.
+constexpr int GC_SMAX = 32;
+
+__global__ void __launch_bounds__(256)
+gram_combine_kernel(const PieceDesc* __restrict__ pd, const int4* __restrict__ rng,
+                    const PieceDesc* __restrict__ pds, const double* __restrict__ As,
+                    const double* __restrict__ mus, const mdsx_piece_status* __restrict__ sts, int p,
+                    double* __restrict__ A, double* __restrict__ mu_all,
+                    mdsx_piece_status* __restrict__ status) {
+  __shared__ double mu[104], dm[GC_SMAX][104], mq_s[GC_SMAX];
+  __shared__ int64_t aoff[GC_SMAX];
+  const int4 g = rng[blockIdx.y];
+  const int q0 = g.x, S = g.y;
+  const PieceDesc d = pd[blockIdx.y];
+  const int k = d.k;
+  if (threadIdx.x < S) {
+    const PieceDesc v = pds[q0 + threadIdx.x];
+    mq_s[threadIdx.x] = (double)v.m;
+    aoff[threadIdx.x] = v.a_off;
+  }
+  for (int e = threadIdx.x; e < S * k; e += blockDim.x) {
+    const int q = e / k, a = e - q * k;
+    dm[q][a] = mus[(int64_t)(q0 + q) * p + a];
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < S; ++q) s = fma(mq_s[q], dm[q][a], s);
+    mu[a] = s / (double)d.m;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * k; e += blockDim.x) {
+    const int q = e / k, a = e - q * k;
+    dm[q][a] -= mu[a];
+  }
+  __syncthreads();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * k) {
+    const int a = e / k, b = e - a * k;
+    if (b <= a) {
+      double c = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < S; ++q) c += As[aoff[q] + e] + mq_s[q] * (dm[q][a] * dm[q][b]);
+      double* out = A + d.a_off;
+      out[(int64_t)a * k + b] = c;
+      out[(int64_t)b * k + a] = c;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int a = threadIdx.x; a < k; a += blockDim.x) mu_all[(int64_t)d.id * p + a] = mu[a];
+    if (threadIdx.x == 0) {
+      bool bad = false;
+      for (int q = 0; q < S; ++q) bad = bad || sts[q0 + q].code == MDSX_INVALID_INPUT;
+      if (bad) status[d.id].code = MDSX_INVALID_INPUT;
+    }
+  }
+}
+
 }  // namespace
 
 namespace mdsx {
+
+int launch_gram_combine(mdsx_handle* h, const PieceDesc* pd, const int4* rng, int npieces,
+                        const PieceDesc* pd_split, const double* A_split, const double* mu_split,
+                        const mdsx_piece_status* st_split, int p, double* A, double* mu,
+                        mdsx_piece_status* status, cudaStream_t st) {
+  if (npieces == 0) return MDSX_OK;
+  mdsx::pre(h, st);
+  gram_combine_kernel<<<dim3((104 * 104 + 255) / 256, npieces), 256, 0, st>>>(
+      pd, rng, pd_split, A_split, mu_split, st_split, p, A, mu, status);
+  return launched(h, "gram_combine_kernel", st);
+}
+
 
 // Pitch (elements) of a staged row: >= p, 16-byte multiple, and congruent so
 // that the 32 lanes of an m8n8k4 fragment load hit distinct banks.

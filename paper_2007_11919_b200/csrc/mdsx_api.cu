@@ -70,6 +70,10 @@ bool gram_piece_ok(const void* data, int dtype, int64_t ld, int p);
 int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                       const int64_t* row_idx, const PieceDesc* pd, int npieces, double* A,
                       double* mu, mdsx_piece_status* status, cudaStream_t st);
+int launch_gram_combine(mdsx_handle* h, const PieceDesc* pd, const int4* rng, int npieces,
+                        const PieceDesc* pd_split, const double* A_split, const double* mu_split,
+                        const mdsx_piece_status* st_split, int p, double* A, double* mu,
+                        mdsx_piece_status* status, cudaStream_t st);
 int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                      const int64_t* row_idx, const PieceDesc* pd, const int4* tiles, int ntiles,
                      double* A, double* mu, mdsx_piece_status* status, cudaStream_t st);
@@ -200,6 +204,11 @@ struct ClassicalPlan {
   int64_t total = 0;
   size_t a_doubles = 0, u_doubles = 0;
   int64_t max_m = 0;
+  // few large form-0 pieces (e.g. the landmark set of interpolation): each is
+  // split into row ranges whose centred Grams are combined (gram_combine)
+  std::vector<PieceDesc> pd_split;                 // virtual pieces (row sub-ranges)
+  std::vector<int4> split_rng;                     // real piece j: (first split, count, j, 0)
+  size_t split_a_doubles = 0;
 };
 
 static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int npieces, int r,
@@ -251,6 +260,30 @@ static int plan_classical(mdsx_handle* h, int p, const int64_t* piece_off, int n
   cp.total = piece_off[npieces] - piece_off[0];
   cp.a_doubles = (size_t)a_off;
   cp.u_doubles = (size_t)u_off;
+  // one CTA per piece leaves most SMs idle when there are only a few pieces:
+  // split each into row ranges of >= 128 rows (two 64-row stages each)
+  if (!cp.pd_g.empty() && (int)cp.pd_g.size() * 4 <= h->num_sms && !getenv("MDSX_NO_GRAM_SPLIT")) {
+    bool big = true;
+    for (const PieceDesc& d : cp.pd_g) big = big && d.m >= 512;
+    if (big) {
+      int64_t a2 = 0;
+      for (const PieceDesc& d : cp.pd_g) {
+        const int S = std::min(std::max(1, h->num_sms / (int)cp.pd_g.size()), std::min(32, d.m / 128));
+        cp.split_rng.push_back(make_int4((int)cp.pd_split.size(), S, d.id, 0));
+        for (int q = 0; q < S; ++q) {
+          const int r0 = (int)((int64_t)d.m * q / S), r1 = (int)((int64_t)d.m * (q + 1) / S);
+          PieceDesc v = d;
+          v.row_off = d.row_off + r0;
+          v.m = r1 - r0;
+          v.a_off = a2;
+          v.id = (int)cp.pd_split.size();
+          a2 += (int64_t)d.k * d.k;
+          cp.pd_split.push_back(v);
+        }
+      }
+      cp.split_a_doubles = (size_t)a2;
+    }
+  }
   return MDSX_OK;
 }
 
@@ -262,7 +295,13 @@ static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
          align_up(np * p * sizeof(double)) + align_up(cp.a_doubles * sizeof(double)) +
          align_up(cp.u_doubles * sizeof(double)) + align_up(np * r * sizeof(double)) +
          align_up(points_ws_bytes((int)np, cp.max_m, r)) + align_up(np * sizeof(int)) +
-         (cp.pd_big.empty() ? 0 : bk_ws_bytes(cp.pd_big));
+         (cp.pd_big.empty() ? 0 : bk_ws_bytes(cp.pd_big)) +
+         (cp.pd_split.empty() ? 0
+                              : align_up(cp.split_a_doubles * sizeof(double)) +
+                                    align_up(cp.pd_split.size() * (size_t)p * sizeof(double)) +
+                                    align_up(cp.pd_split.size() * sizeof(mdsx_piece_status)) +
+                                    align_up(cp.pd_split.size() * sizeof(PieceDesc)) +
+                                    align_up(cp.split_rng.size() * sizeof(int4)));
 }
 
 // Runs K2 -> K1 -> K3 -> points for all pieces.  Workspace must be reserved.
@@ -287,11 +326,25 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   double* lam = (double*)ws_alloc(h, (size_t)np * r * sizeof(double), st);
   double2* cand = (double2*)ws_alloc(h, points_ws_bytes(np, cp.max_m, r), st);
   if (!dpd || !dtiles || !mu || !A || !U || !lam || !cand) return MDSX_CUDA;
+  const int nsplit = (int)cp.pd_split.size();
+  double* A_sp = nullptr;
+  double* mu_sp = nullptr;
+  mdsx_piece_status* st_sp = nullptr;
+  PieceDesc* dpd_sp = nullptr;
+  int4* drng = nullptr;
+  if (nsplit) {
+    A_sp = (double*)ws_alloc(h, cp.split_a_doubles * sizeof(double), st);
+    mu_sp = (double*)ws_alloc(h, (size_t)nsplit * p * sizeof(double), st);
+    st_sp = (mdsx_piece_status*)ws_alloc(h, nsplit * sizeof(mdsx_piece_status), st);
+    dpd_sp = (PieceDesc*)ws_alloc(h, nsplit * sizeof(PieceDesc), st);
+    drng = (int4*)ws_alloc(h, cp.split_rng.size() * sizeof(int4), st);
+    if (!A_sp || !mu_sp || !st_sp || !dpd_sp || !drng) return MDSX_CUDA;
+  }
   const std::vector<PieceDesc>& pd = cp.pd;  // row_off indexes row_idx directly
   const int64_t* ridx = row_idx;
   Stager sg(h, st);
   int rc = sg.begin(6 * np * sizeof(PieceDesc) + (tiles0.size() + cp.tiles1.size()) * sizeof(int4) +
-                    4096);
+                    nsplit * sizeof(PieceDesc) + cp.split_rng.size() * sizeof(int4) + 8192);
   if (rc) return rc;
   if ((rc = sg.put(dpd, pd.data(), np * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dpd_jac, cp.pd_jac.data(), cp.pd_jac.size() * sizeof(PieceDesc)))) return rc;
@@ -301,6 +354,10 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     return rc;
   if ((rc = sg.put(dpd_f1, cp.pd_f1.data(), cp.pd_f1.size() * sizeof(PieceDesc)))) return rc;
   if ((rc = sg.put(dtiles1, cp.tiles1.data(), cp.tiles1.size() * sizeof(int4)))) return rc;
+  if (nsplit) {
+    if ((rc = sg.put(dpd_sp, cp.pd_split.data(), nsplit * sizeof(PieceDesc)))) return rc;
+    if ((rc = sg.put(drng, cp.split_rng.data(), cp.split_rng.size() * sizeof(int4)))) return rc;
+  }
   if ((rc = sg.end())) return rc;
   if ((rc = cuda_check(h, cudaMemsetAsync(status, 0, np * sizeof(mdsx_piece_status), st), "memset")))
     return rc;
@@ -358,9 +415,20 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     }
   }
   // form 0: DMMA Gram with fused shifted means;  form 1: means pass + row Gram
-  if (piece_gram && (rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd_g, (int)cp.pd_g.size(),
-                                            A, mu, status, st)))
+  if (piece_gram && nsplit) {
+    // row-split Grams of the few large pieces, combined (Chan et al.) in fixed order
+    if ((rc = cuda_check(h, cudaMemsetAsync(st_sp, 0, nsplit * sizeof(mdsx_piece_status), st),
+                         "memset")))
+      return rc;
+    if ((rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd_sp, nsplit, A_sp, mu_sp, st_sp, st)))
+      return rc;
+    if ((rc = launch_gram_combine(h, dpd_g, drng, (int)cp.split_rng.size(), dpd_sp, A_sp, mu_sp,
+                                  st_sp, p, A, mu, status, st)))
+      return rc;
+  } else if (piece_gram && (rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd_g,
+                                                   (int)cp.pd_g.size(), A, mu, status, st))) {
     return rc;
+  }
   if ((rc = launch_gram_dmma(h, data, dtype, ld, p, ridx, dpd, dtiles, (int)tiles0.size(), A, mu,
                              status, st)))
     return rc;
@@ -767,7 +835,6 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
   // dense rows: bulk-copy stream with fused per-CTA column sums, landmark
   // overwrite with a sum correction, one subtract pass (algorithms.py:264-274)
   double* part = (double*)ws_alloc(h, recenter_ws_bytes(r) + align_up(r * sizeof(double)), st);
-  double* corr = part + (size_t)recenter_ws_bytes(r) / sizeof(double);
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
   if (ld == p && r <= 16 && ((size_t)p * es) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(data) & 15) == 0 && h->num_sms * r * sizeof(double) <= recenter_ws_bytes(r)) {
@@ -781,9 +848,17 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
         (rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
                                 st, n32)))
       return rc;
-    if (nparts > 0) {
-      if ((rc = launch_landmark_overwrite(h, base, sample_idx, l, r, out, corr, st))) return rc;
-      return launch_subtract_mean(h, out, n, r, part, nparts, corr, st);
+    const int lparts = (int)((l + 255) / 256);
+    if (nparts > 0 && (size_t)(nparts + lparts) * r * sizeof(double) <= recenter_ws_bytes(r)) {
+      // landmark overwrite: its per-CTA corrections are extra column-sum partials
+      if ((rc = launch_landmark_overwrite(h, base, sample_idx, l, r, out,
+                                          part + (size_t)nparts * r, st)))
+        return rc;
+      return launch_subtract_mean(h, out, n, r, part, nparts + lparts, nullptr, st);
+    }
+    if (nparts > 0) {             // too many landmarks for the partials buffer: rewrite by scatter
+      if ((rc = launch_scatter(h, base, sample_idx, l, r, out, st))) return rc;
+      return launch_recenter(h, out, n, r, part, st);
     }
   }
   if ((rc = launch_gower_affine(h, data, dtype, ld, n, p, r, mean, M, v, out, r, flag + 1, st)))
