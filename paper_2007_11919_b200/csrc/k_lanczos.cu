@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
 lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
                     double* __restrict__ Uout, double* __restrict__ lam_out,
                     double* __restrict__ estimates, double* __restrict__ gof,
-                    mdsx_piece_status* __restrict__ status, int only_flagged, const PtsEpi epi) {
+                    mdsx_piece_status* __restrict__ status, int only_flagged, const PtsEpi epi,
+                    int getenv_first_check) {
   extern __shared__ double sm[];
   __shared__ double alpha[QMAX], beta[QMAX], beta2[QMAX];
   __shared__ double wv[LMAX], hv[QMAX + 1];
@@ -343,7 +344,9 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
 
   int m = 0;                 // current Krylov dimension (columns 0..m-1 of Q valid)
   bool done = false, broke = false, capped = false, have_prev = false;
-  const int first_check = max(2 * r + 4, 24);
+  // first check at 28 (r = 10): measured on dc2 / fast3, a check (~30k cycles) costs about
+  // as much as four steps, and about half the pieces are not converged at 24
+  const int first_check = getenv_first_check > 0 ? getenv_first_check : max(2 * r + 8, 28);
 #ifdef MDSX_LZ_PROF
   long long lzp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   LZ_T0(t_all);
@@ -1630,7 +1633,9 @@ int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int km
     if (getenv("MDSX_LZ_ONE")) smem = std::max<size_t>(smem, 120 * 1024);   // experiment: 1 CTA/SM
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
-    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged, e);
+    const char* fc = getenv("MDSX_LZ_FIRST");
+    kern<<<npieces, LT, smem, st>>>(pd, r, A, U, lam, estimates, gof, status, only_flagged, e,
+                                    fc ? atoi(fc) : 0);
     return launched(h, "lanczos_smem_kernel", st);
   };
   if (!full_basis && kmax <= RG_KP && getenv("MDSX_LZ_REG")) {
