@@ -25,9 +25,12 @@
  *   mdsx_interpolation      <- interpolation_mds (algorithms.py:245-274)
  *   mdsx_recenter           <- _recentered (algorithms.py:122-125)
  *   mdsx_scatter_rows       <- points[root.indices] = block (algorithms.py:341-342)
+ *   mdsx_fast_finish        <- the root's child alignment (algorithms.py:310-311) +
+ *                              points[root.indices] = block (:341-342) + _recentered
+ *                              (:122-125) in one pass
  * fast_mds (algorithms.py:323-348) is composed from mdsx_classical_pieces,
- * mdsx_procrustes_fit/apply, mdsx_scatter_rows and mdsx_recenter by the host
- * (see INTEGRATION.md).
+ * mdsx_procrustes_fit/apply and mdsx_fast_finish (or mdsx_scatter_rows +
+ * mdsx_recenter) by the host.
  */
 #ifndef MDSX_H
 #define MDSX_H
@@ -148,6 +151,12 @@ int mdsx_scatter_rows(mdsx_handle* h, const double* src, const int64_t* idx, int
                       int32_t r, double* out, void* stream);
 /* points (n x r) -= column means (fixed-order, deterministic reduction). */
 int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* stream);
+/* out[order[i]] = P[i] @ rot_j + trans_j - mean for the rows i of job j
+ * (HOST job_off: njobs+1 offsets covering 0..n), mean = the column mean of
+ * the result (from per-job sums pushed through each fit; fixed order). */
+int mdsx_fast_finish(mdsx_handle* h, const double* P, int32_t r, const int64_t* job_off,
+                     int32_t njobs, const double* rot, const double* trans,
+                     const int64_t* order, int64_t n, double* out, void* stream);
 
 /* ---- whole algorithms ------------------------------------------------------ */
 /* divide_and_conquer_mds with an explicit plan (partition.py:184-214 layout:

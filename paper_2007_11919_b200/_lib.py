@@ -54,6 +54,7 @@ SIGNATURES = {
     "mdsx_procrustes_apply": (_int, [_vp, _vp, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
     "mdsx_scatter_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_recenter": (_int, [_vp, _vp, _i64, _i32, _vp]),
+    "mdsx_fast_finish": (_int, [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp]),
     "mdsx_divide_conquer": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
                                    _vp, _vp, _vp, _vp, _vp]),
     "mdsx_divide_conquer_ex": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,

@@ -178,6 +178,17 @@ class FastRun:
         self.gof = D.empty((npc, 2), dev)
         self.status = D.status_tensor(npc, dev)
         self.out = None if local else D.empty((plan.n, r), dev)
+        # the shallowest level's jobs tile rows 0..n of the working buffer
+        # contiguously: its apply, the scatter and the re-centring run as one
+        # pass (mdsx_fast_finish)
+        self.finish_off = None
+        if not local and flat.levels:
+            top = flat.levels[-1]
+            st_, ln_ = np.asarray(top.start, np.int64), np.asarray(top.length, np.int64)
+            off = np.concatenate([st_, [st_[-1] + ln_[-1]]]) if len(st_) else None
+            if (off is not None and off[0] == 0 and off[-1] == plan.n
+                    and np.array_equal(off[1:-1], st_[:-1] + ln_[:-1])):
+                self.finish_off = np.ascontiguousarray(off)
 
     def launch(self) -> None:
         x, r, dev = self.x, self.r, self.dev
@@ -188,13 +199,21 @@ class FastRun:
                self.pts.data_ptr(), self.est.data_ptr(), self.gof.data_ptr(),
                self.status.data_ptr(), sp)
         P = self.pts.data_ptr()
-        for lv in self.levels:
+        for li, lv in enumerate(self.levels):
             h.call("mdsx_procrustes_fit", P, lv["tgt"].data_ptr(), P, lv["src"].data_ptr(),
                    lv["job_off"].ctypes.data, lv["nj"], r, lv["rot"].data_ptr(),
                    lv["trans"].data_ptr(), lv["loss"].data_ptr(), lv["deg"].data_ptr(), sp)
+            if li == len(self.levels) - 1 and self.finish_off is not None:
+                break                       # applied by mdsx_fast_finish below
             h.call("mdsx_procrustes_apply", P, r, lv["start"].data_ptr(), lv["length"].data_ptr(),
                    lv["nj"], lv["max_len"], lv["rot"].data_ptr(), lv["trans"].data_ptr(), sp)
         if self.local:
+            return
+        if self.finish_off is not None:
+            lv = self.levels[-1]
+            h.call("mdsx_fast_finish", P, r, self.finish_off.ctypes.data, lv["nj"],
+                   lv["rot"].data_ptr(), lv["trans"].data_ptr(), self.order.data_ptr(),
+                   self.plan.n, self.out.data_ptr(), sp)
             return
         h.call("mdsx_scatter_rows", P, self.order.data_ptr(), self.plan.n, r,
                self.out.data_ptr(), sp)

@@ -528,32 +528,40 @@ apply_kernel(double* __restrict__ buf, int r, const int64_t* __restrict__ start,
 // (row, column) elements, so a warp store covers ~3 output rows' contiguous
 // 80-byte segments instead of 32 scattered rows.
 constexpr int ST_ROWS = 256;
+constexpr int ST_CR = 1024;       // rows per CTA of the stitch (multiple of ST_ROWS)
+constexpr int OS_CR = 2048;       // rows per CTA of the per-job sums
 
 template <int RM>
 __global__ void __launch_bounds__(256)
 dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_idx,
                  const int64_t* __restrict__ off, int c, int r, const double* __restrict__ rot,
                  const double* __restrict__ trans, const double* __restrict__ mean,
-                 double* __restrict__ out) {
+                 double* __restrict__ out, int first_identity) {
   constexpr int SR = RM <= 16 ? ST_ROWS : ST_ROWS / 2;
   __shared__ double Ts[RM * RM], ts[RM], ms[RM];
   __shared__ double xs[SR * RM];
   __shared__ int64_t dsts[SR];
-  const int j = blockIdx.x;
+  // D&C (first_identity): piece 0 verbatim, fit j-1 for piece j, own rows from c;
+  // fast MDS finish: fit j for job j, all rows
+  const int j = blockIdx.y;
+  const bool ident = first_identity && j == 0;
+  const int fj = first_identity ? j - 1 : j;
   const int64_t o = off[j], m = off[j + 1] - o;
   for (int e = threadIdx.x; e < RM * RM; e += blockDim.x) {
     const int a = e / RM, b = e % RM;
-    Ts[e] = (a < r && b < r) ? (j == 0 ? (a == b ? 1.0 : 0.0) : rot[(size_t)(j - 1) * r * r + a * r + b])
+    Ts[e] = (a < r && b < r) ? (ident ? (a == b ? 1.0 : 0.0) : rot[(size_t)fj * r * r + a * r + b])
                              : 0.0;
   }
   if (threadIdx.x < RM) {
     const int b = threadIdx.x;
-    ts[b] = (j == 0 || b >= r) ? 0.0 : trans[(size_t)(j - 1) * r + b];
+    ts[b] = (ident || b >= r) ? 0.0 : trans[(size_t)fj * r + b];
     ms[b] = (mean && b < r) ? mean[b] : 0.0;
   }
-  const int64_t first = (j == 0 ? 0 : c);
-  for (int64_t i0 = first; i0 < m; i0 += SR) {
-    const int rows = (int)min((int64_t)SR, m - i0);
+  const int64_t first = (ident || !first_identity) ? 0 : c;
+  // blockIdx.x: this CTA's range of ST_CR rows of the job (long jobs over many CTAs)
+  const int64_t lo = first + (int64_t)blockIdx.x * ST_CR, hi = min(m, lo + ST_CR);
+  for (int64_t i0 = lo; i0 < hi; i0 += SR) {
+    const int rows = (int)min((int64_t)SR, hi - i0);
     __syncthreads();                                  // previous chunk consumed
     const double* src = P + (o + i0) * r;
     for (int e = threadIdx.x; e < rows * r; e += blockDim.x) xs[e] = src[e];
@@ -563,7 +571,7 @@ dc_stitch_kernel(const double* __restrict__ P, const int64_t* __restrict__ row_i
       const int row = e / r, b = e - row * r;
       const double* xr = xs + row * r;
       double v;
-      if (j == 0) {
+      if (ident) {
         v = xr[b];
       } else {
         double s2 = 0.0;
@@ -582,22 +590,27 @@ template <int RM>
 __global__ void __launch_bounds__(256)
 dc_own_sums_kernel(const double* __restrict__ P, const int64_t* __restrict__ off, int c, int r,
                    const double* __restrict__ rot, const double* __restrict__ trans,
-                   double* __restrict__ sums) {
+                   double* __restrict__ sums, int first_identity) {
   __shared__ double red[256];
   __shared__ double colsum[RM];
-  const int j = blockIdx.x;
+  const int j = blockIdx.y;
   const int64_t o = off[j], m = off[j + 1] - o;
   const int RG = 256 / r;
   const int g = threadIdx.x / r, col = threadIdx.x - g * r;
   double acc = 0.0;
+  const bool ident = first_identity && j == 0;
+  const int fj = first_identity ? j - 1 : j;
+  const int64_t first = (ident || !first_identity) ? 0 : c;
+  // blockIdx.x: this CTA's range of OS_CR rows of the job
+  const int64_t lo = min(m, first + (int64_t)blockIdx.x * OS_CR), hi = min(m, lo + OS_CR);
   if (g < RG) {
     double a4[4] = {0.0, 0.0, 0.0, 0.0};          // four loads in flight, fixed combine order
-    int64_t i = (j == 0 ? 0 : c) + g;
-    for (; i + 3 * RG < m; i += 4 * RG) {
+    int64_t i = lo + g;
+    for (; i + 3 * RG < hi; i += 4 * RG) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) a4[u] += P[(o + i + u * RG) * r + col];
     }
-    for (; i < m; i += RG) a4[0] += P[(o + i) * r + col];
+    for (; i < hi; i += RG) a4[0] += P[(o + i) * r + col];
     acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
   red[threadIdx.x] = g < RG ? acc : 0.0;
@@ -613,14 +626,14 @@ dc_own_sums_kernel(const double* __restrict__ P, const int64_t* __restrict__ off
   if (threadIdx.x < r) {
     const int b = threadIdx.x;
     double v;
-    if (j == 0) {
+    if (ident) {
       v = colsum[b];
     } else {
-      const double* T = rot + (size_t)(j - 1) * r * r;
-      v = (double)(m - c) * trans[(size_t)(j - 1) * r + b];
+      const double* T = rot + (size_t)fj * r * r;
+      v = (double)(hi - lo) * trans[(size_t)fj * r + b];
       for (int a2 = 0; a2 < r; ++a2) v = fma(colsum[a2], T[a2 * r + b], v);
     }
-    sums[(size_t)j * r + b] = v;
+    sums[((size_t)j * gridDim.x + blockIdx.x) * r + b] = v;
   }
 }
 
@@ -948,25 +961,28 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
 int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
                      int npieces, int64_t max_m, int c, int r, const double* rot,
                      const double* trans, double* out, cudaStream_t st, int64_t n_recenter,
-                     double* ws) {
-  (void)max_m;
+                     double* ws, int first_identity) {
+  const unsigned nch_s = (unsigned)std::max<int64_t>(1, (max_m + OS_CR - 1) / OS_CR);
+  const unsigned nch_t = (unsigned)std::max<int64_t>(1, (max_m + ST_CR - 1) / ST_CR);
   auto go = [&](auto rm) {
     constexpr int RM = decltype(rm)::value;
     const double* mean = nullptr;
     if (n_recenter > 0) {
       double* sums = ws;
-      double* mn = ws + (size_t)npieces * r;
+      double* mn = ws + (size_t)npieces * nch_s * r;
       mdsx::pre(h, st);
-      dc_own_sums_kernel<RM><<<npieces, 256, 0, st>>>(P, off, c, r, rot, trans, sums);
+      dc_own_sums_kernel<RM><<<dim3(nch_s, npieces), 256, 0, st>>>(P, off, c, r, rot, trans, sums,
+                                                                   first_identity);
       int rc = launched(h, "dc_own_sums_kernel", st);
       if (rc) return rc;
       mdsx::pre(h, st);
-      dc_mean_kernel<RM><<<1, 256, 0, st>>>(sums, npieces, r, n_recenter, mn);
+      dc_mean_kernel<RM><<<1, 256, 0, st>>>(sums, npieces * (int)nch_s, r, n_recenter, mn);
       if ((rc = launched(h, "dc_mean_kernel", st))) return rc;
       mean = mn;
     }
     mdsx::pre(h, st);
-    dc_stitch_kernel<RM><<<npieces, 256, 0, st>>>(P, row_idx, off, c, r, rot, trans, mean, out);
+    dc_stitch_kernel<RM><<<dim3(nch_t, npieces), 256, 0, st>>>(P, row_idx, off, c, r, rot, trans,
+                                                                mean, out, first_identity);
     return launched(h, "dc_stitch_kernel", st);
   };
   if (r <= 4) return go(std::integral_constant<int, 4>{});
@@ -976,7 +992,10 @@ int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, co
   return go(std::integral_constant<int, 32>{});
 }
 
-size_t dc_stitch_ws_bytes(int npieces, int r) { return ((size_t)npieces * r + 32) * sizeof(double); }
+size_t dc_stitch_ws_bytes(int npieces, int r, int64_t max_m) {
+  const size_t nch = (size_t)std::max<int64_t>(1, (max_m + OS_CR - 1) / OS_CR);
+  return ((size_t)npieces * nch * r + 32) * sizeof(double);
+}
 
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st) {

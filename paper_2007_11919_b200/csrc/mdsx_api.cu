@@ -19,8 +19,8 @@ int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const
 int launch_dc_stitch(mdsx_handle* h, const double* P, const int64_t* row_idx, const int64_t* off,
                      int npieces, int64_t max_m, int c, int r, const double* rot,
                      const double* trans, double* out, cudaStream_t st, int64_t n_recenter,
-                     double* ws);
-size_t dc_stitch_ws_bytes(int npieces, int r);
+                     double* ws, int first_identity = 1);
+size_t dc_stitch_ws_bytes(int npieces, int r, int64_t max_m);
 int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int r,
                    double* out, cudaStream_t st);
 int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const int64_t* off,
@@ -754,7 +754,7 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                       align_up((size_t)(npieces + 1) * sizeof(int64_t)) +
                       align_up((size_t)nj * r * r * sizeof(double)) +
                       align_up((size_t)nj * r * sizeof(double)) + align_up(nj * sizeof(double)) +
-                      align_up(nj * sizeof(int32_t)) + align_up(dc_stitch_ws_bytes(npieces, r)) + 4096;
+                      align_up(nj * sizeof(int32_t)) + align_up(dc_stitch_ws_bytes(npieces, r, cp.max_m)) + 4096;
   if ((rc = ws_reserve(h, need))) return rc;
   double* P = (double*)ws_alloc(h, cp.total * r * sizeof(double), st);
   if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, P, estimates, gof, status, st)))
@@ -795,7 +795,7 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
   // stitch + final re-centring in one pass over P: the column mean comes from
   // per-piece sums of P pushed through each fit (no second pass over out)
   const bool rec = !(flags & MDSX_NO_RECENTER);
-  double* sws = rec ? (double*)ws_alloc(h, dc_stitch_ws_bytes(npieces, r), st) : nullptr;
+  double* sws = rec ? (double*)ws_alloc(h, dc_stitch_ws_bytes(npieces, r, cp.max_m), st) : nullptr;
   if (rec && !sws) return MDSX_CUDA;
   return launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st,
                           rec ? n : 0, sws);
@@ -869,6 +869,29 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
 }
 
 }  // extern "C"
+
+// fast_mds finish (algorithms.py:310-311, 341-342, 122-125): the shallowest
+// level's in-place apply, the scatter to input order and the re-centring in
+// one pass over P (mean from per-job sums pushed through each fit).
+extern "C" int mdsx_fast_finish(mdsx_handle* h, const double* P, int32_t r, const int64_t* job_off,
+                                int32_t njobs, const double* rot, const double* trans,
+                                const int64_t* order, int64_t n, double* out, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (njobs < 1 || r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad fast finish shape");
+  if (job_off[0] != 0 || job_off[njobs] != n)
+    return fail(h, MDSX_PARAM, "fast finish jobs must cover rows 0..n");
+  int64_t max_m = 0;
+  for (int j = 0; j < njobs; ++j) max_m = std::max<int64_t>(max_m, job_off[j + 1] - job_off[j]);
+  const size_t need = align_up((size_t)(njobs + 1) * sizeof(int64_t)) +
+                      align_up(dc_stitch_ws_bytes(njobs, r, max_m)) + 4096;
+  int rc;
+  if ((rc = ws_reserve(h, need))) return rc;
+  int64_t* doff = (int64_t*)ws_alloc(h, (size_t)(njobs + 1) * sizeof(int64_t), st);
+  double* sws = (double*)ws_alloc(h, dc_stitch_ws_bytes(njobs, r, max_m), st);
+  if (!doff || !sws) return MDSX_CUDA;
+  if ((rc = upload(h, doff, job_off, (size_t)(njobs + 1) * sizeof(int64_t), st))) return rc;
+  return launch_dc_stitch(h, P, order, doff, njobs, max_m, 0, r, rot, trans, out, st, n, sws, 0);
+}
 
 extern "C" int mdsx_aligned_correlations(mdsx_handle* h, const double* points, int64_t n,
                                          int32_t r, const void* dominant, int32_t dtype,
