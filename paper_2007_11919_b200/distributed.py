@@ -138,8 +138,7 @@ class GpuBackend:
         ck = ("dc", key, c, r)
         if self.reuse and key is not None and ck in self._cache:
             ridx, off, out, est, gof, st, own = self._cache[ck]
-            out.zero_()
-            self._own = own
+            self._own = own                 # every owned row is rewritten: no clearing pass
             return self._run_dc(ridx, off, c, r, out, est, gof, st)
         rows, off = flatten_subsets(subsets)
         ridx = D.index_tensor(rows, self.dev)
@@ -157,7 +156,8 @@ class GpuBackend:
         sizes = np.diff(off) - np.r_[0, np.full(npc - 1, c)]
         own_off = np.zeros(npc + 1, dtype=np.int64)
         np.cumsum(sizes, out=own_off[1:])
-        self._own = (own, own_off)
+        self._own = (own, own_off,
+                     torch.from_numpy(np.ascontiguousarray(own_off)).to(self.dev))
         if self.reuse and key is not None:
             self._cache[ck] = (ridx, off, out, est, gof, st, self._own)
         return self._run_dc(ridx, off, c, r, out, est, gof, st)
@@ -173,11 +173,11 @@ class GpuBackend:
 
     def own_segment_sums(self, out, r: int) -> np.ndarray:
         """Column sums of each dc_subplan subset's own rows (fixed order)."""
-        own, own_off = self._own
-        return self._segsums(out, own.data_ptr(), own_off, r)
+        own, own_off, own_off_dev = self._own
+        return self._segsums(out, own.data_ptr(), own_off, r, own_off_dev)
 
     def shift_own(self, out, mean: np.ndarray) -> None:
-        own, _ = self._own
+        own = self._own[0]
         self._shift(out, own.data_ptr(), own.numel(), mean)
 
     def range_sums(self, out, offsets: np.ndarray, r: int) -> np.ndarray:
@@ -187,12 +187,13 @@ class GpuBackend:
     def shift_all(self, out, mean: np.ndarray) -> None:
         self._shift(out, None, out.shape[0], mean)
 
-    def _segsums(self, out, idx_ptr, offsets, r):
+    def _segsums(self, out, idx_ptr, offsets, r, doff=None):
         D = self.D
         nseg = len(offsets) - 1
         sums = D.empty((max(nseg, 1), r), self.dev)
         if nseg > 0:
-            doff = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(self.dev)
+            if doff is None:
+                doff = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(self.dev)
             D.handle(self.dev).call("mdsx_segment_colsums", out.data_ptr(), idx_ptr,
                                     doff.data_ptr(), nseg, r, sums.data_ptr(),
                                     D.stream_ptr(self.dev))
@@ -295,6 +296,15 @@ class GpuBackend:
 
 
 # ------------------------------------------------------------------ algorithms
+def fold_rows(rows: np.ndarray, r: int) -> np.ndarray:
+    """Left fold (((0 + s_0) + s_1) + ...) of the rows in the given order: a
+    sequential running sum, identical on every rank and for every world size
+    (np.add.reduce would pair them up instead)."""
+    if len(rows) == 0:
+        return np.zeros(r)
+    return np.cumsum(np.asarray(rows, dtype=np.float64), axis=0)[-1]
+
+
 def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: Comm,
                                plan: DcPlan | None = None) -> ShardResult:
     """divide_and_conquer_mds (algorithms.py:128-172) over comm.world ranks."""
@@ -319,17 +329,14 @@ def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: C
     # plan-order all-gather of per-subset sums and fit figures
     width = 3 + 2 * r                                    # [j, g1, g2, est(r), sums(r)]
     recs = np.zeros((len(mine), width))
-    for t, j in enumerate(mine):
-        recs[t, 0] = j
-        recs[t, 1:3] = gof[1 + t]
-        recs[t, 3:3 + r] = est[1 + t]
-        recs[t, 3 + r:3 + 2 * r] = sums[1 + t]
+    recs[:, 0] = mine
+    recs[:, 1:3] = gof[1:1 + len(mine)]
+    recs[:, 3:3 + r] = est[1:1 + len(mine)]
+    recs[:, 3 + r:3 + 2 * r] = sums[1:1 + len(mine)]
     allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
     allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
     seg_sums = np.vstack([sums[0:1], allrecs[:, 3 + r:3 + 2 * r]])
-    total = np.zeros(r)
-    for row in seg_sums:                                  # plan order
-        total = total + row
+    total = fold_rows(seg_sums, r)                        # plan order
     mean = total / n
     backend.shift_own(out, mean)
     sizes = np.fromiter((len(q) for q in plan.subsets), dtype=np.float64, count=P)
@@ -365,8 +372,9 @@ def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
     out, flat, est, gof, st = backend.fast_subtrees(plan, lo, hi, r, key=id(plan))
     # failures: a consistent decision on every rank (all raise, no rank hangs)
     root_pid = len(flat.piece_off) - 2                    # the root alignment set, evaluated last
-    first = next((k for k, pid in enumerate(flat.eval_order)
-                  if pid != root_pid and st[pid]["code"] != 0), -1)
+    ev = np.asarray(flat.eval_order, dtype=np.int64)
+    bad = np.flatnonzero((ev != root_pid) & (st["code"][ev] != 0))
+    first = int(bad[0]) if bad.size else -1
     flags = np.array([float(np.any(st["code"] == 3)), float(first >= 0)])
     allflags = np.vstack(comm.allgather(flags)) if comm.world > 1 else flags[None]
     if allflags[:, 0].any():
@@ -378,14 +386,25 @@ def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
             raise_piece_status(st[pid], r, flat.labels[pid])
         raise RuntimeError(f"fast MDS failed on rank {culprit}")
     raise_piece_status(st[root_pid], r, flat.labels[root_pid])
-    # per-child aggregates of the owned subtrees (algorithms.py:289-320)
-    leaf = iter(range(flat.n_leaves))
+    # per-child aggregates of the owned subtrees (algorithms.py:289-320); a node
+    # whose children are all leaves is reduced with array ops over its leaf range
+    leaf = [0]
 
     def agg(node):
         if node.is_leaf:
-            j = next(leaf)
+            j = leaf[0]
+            leaf[0] += 1
             return gof[j, 0], gof[j, 1], est[j], node.size
-        fits = [agg(ch) for ch in node.children]
+        kids_ = node.children
+        if all(ch.is_leaf for ch in kids_):
+            j0 = leaf[0]
+            leaf[0] += len(kids_)
+            sizes = np.array([ch.size for ch in kids_], dtype=np.float64)
+            tot = sizes.sum()
+            return (float(np.dot(sizes, gof[j0:leaf[0], 0]) / tot),
+                    float(np.dot(sizes, gof[j0:leaf[0], 1]) / tot),
+                    est[j0:leaf[0]].mean(axis=0), int(tot))
+        fits = [agg(ch) for ch in kids_]
         sizes = np.array([f[3] for f in fits], dtype=np.float64)
         tot = sizes.sum()
         return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
@@ -393,15 +412,28 @@ def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
                 np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
 
     mine = kids[lo:hi]
-    fits = [agg(ch) for ch in mine]
+    shape = _fast_shape(plan, mine, backend)
+    if shape is not None:                                 # two-level subtrees: array ops only
+        owner, lsize = shape
+        starts_l = np.searchsorted(owner, np.arange(len(mine) + 1))
+        g1c, g2c = np.ascontiguousarray(gof[:, 0]), np.ascontiguousarray(gof[:, 1])
+        fits = [(float(np.dot(lsize[a:b], g1c[a:b]) / lsize[a:b].sum()),
+                 float(np.dot(lsize[a:b], g2c[a:b]) / lsize[a:b].sum()),
+                 est[a:b].mean(axis=0), int(lsize[a:b].sum()))
+                for a, b in zip(starts_l[:-1], starts_l[1:])]
+    else:
+        fits = [agg(ch) for ch in mine]
     starts = np.cumsum([0] + [ch.size for ch in mine]).astype(np.int64)
     sums = backend.range_sums(out, starts, r)
     width = 4 + 2 * r                                     # [i, g1, g2, size, est(r), sums(r)]
     recs = np.zeros((len(mine), width))
-    for t, f in enumerate(fits):
-        recs[t, :4] = [lo + t, f[0], f[1], f[3]]
-        recs[t, 4:4 + r] = f[2]
-        recs[t, 4 + r:] = sums[t]
+    if fits:
+        recs[:, 0] = np.arange(lo, lo + len(mine))
+        recs[:, 1] = [f[0] for f in fits]
+        recs[:, 2] = [f[1] for f in fits]
+        recs[:, 3] = [f[3] for f in fits]
+        recs[:, 4:4 + r] = np.stack([f[2] for f in fits])
+        recs[:, 4 + r:] = sums[:len(mine)]
     allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
     allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
     sizes = allrecs[:, 3]
@@ -409,11 +441,29 @@ def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
     g1 = float(np.dot(sizes, allrecs[:, 1]) / tot)
     g2 = float(np.dot(sizes, allrecs[:, 2]) / tot)
     estimates = allrecs[:, 4:4 + r].mean(axis=0)
-    total = np.zeros(r)
-    for row in allrecs[:, 4 + r:]:                        # child order
-        total = total + row
+    total = fold_rows(allrecs[:, 4 + r:], r)              # child order
     backend.shift_all(out, total / n)
     return ShardResult(flat.order, out, (0, len(flat.order)), estimates, g1, g2, backend)
+
+
+def _fast_shape(plan, mine, backend):
+    """For subtrees whose children are all leaves (the BASELINE fast plans):
+    (child index of every leaf in DFS order, leaf sizes), cached per plan on
+    the backend; None for deeper trees."""
+    cache = getattr(backend, "_fast_shape_cache", None)
+    if cache is None:
+        cache = backend._fast_shape_cache = {}
+    key = (id(plan), id(mine[0]) if mine else 0, len(mine))
+    if key not in cache:
+        if not mine or not all(not ch.is_leaf and all(g.is_leaf for g in ch.children)
+                               for ch in mine):
+            cache[key] = None
+        else:
+            owner = np.concatenate([np.full(len(ch.children), t, np.int64)
+                                    for t, ch in enumerate(mine)])
+            lsize = np.array([g.size for ch in mine for g in ch.children], dtype=np.float64)
+            cache[key] = (owner, lsize)
+    return cache[key]
 
 
 def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
@@ -444,9 +494,7 @@ def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
     recs = np.hstack([np.arange(b_lo, b_hi, dtype=np.float64)[:, None], sums])
     allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
     allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
-    total = np.zeros(r)
-    for row in allrecs[:, 1:]:                            # canonical block order
-        total = total + row
+    total = fold_rows(allrecs[:, 1:], r)                  # canonical block order
     backend.shift_all(out, total / n)
     return ShardResult((lo, hi), out, (0, hi - lo), est, g1, g2, backend)
 
