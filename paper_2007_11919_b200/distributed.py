@@ -489,7 +489,7 @@ def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
     # landmark rows inside the shard take the classical configuration
     in_shard = (sample >= lo) & (sample < hi)
     backend.place(out, (sample[in_shard] - lo).astype(np.int64), base[in_shard])
-    bounds = np.array([min(hi, s * SUM_BLOCK) - lo for s in range(b_lo, b_hi + 1)], dtype=np.int64)
+    bounds = np.minimum(hi, np.arange(b_lo, b_hi + 1, dtype=np.int64) * SUM_BLOCK) - lo
     sums = backend.range_sums(out, bounds, r)
     recs = np.hstack([np.arange(b_lo, b_hi, dtype=np.float64)[:, None], sums])
     allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
