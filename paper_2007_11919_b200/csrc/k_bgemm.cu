@@ -186,7 +186,14 @@ GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
   GemmBatch b{(int64_t)items.size(), 0, 0};
   if (batch.empty()) return b;
   b.narrow = batch[0].N <= 16 ? 1 : 0;
-  const int BM = b.narrow ? 128 : 64, BN = b.narrow ? 16 : 64;
+  if (b.narrow) {
+    // few large-M tasks (e.g. the single landmark piece of interpolation):
+    // 32-row tiles so the product spreads over 4x more CTAs
+    int64_t tiles128 = 0;
+    for (const auto& t : batch) tiles128 += (t.M + 127) / 128;
+    if (tiles128 < 64 && !getenv("MDSX_BGEMM_NO_SMALL")) b.narrow = 2;
+  }
+  const int BM = b.narrow == 2 ? 32 : b.narrow ? 128 : 64, BN = b.narrow ? 16 : 64;
   for (const auto& t : batch) {
     const int id = (int)tasks.size();
     tasks.push_back(t);
@@ -203,13 +210,17 @@ int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_item
   if (b.nitems == 0) return MDSX_OK;
   mdsx::pre(h, st);
   if (getenv("MDSX_BGEMM_FMA")) {                 // the CUDA-core variant, for comparison
-    if (b.narrow)
+    if (b.narrow == 2)
+      bgemm_kernel<32, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+    else if (b.narrow)
       bgemm_kernel<128, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
     else
       bgemm_kernel<64, 64><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
     return launched(h, "bgemm_kernel", st);
   }
-  if (b.narrow)
+  if (b.narrow == 2)
+    bgemm_dmma_kernel<32, 16, 8, 8><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
+  else if (b.narrow)
     bgemm_dmma_kernel<128, 16, 16, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
   else
     bgemm_dmma_kernel<64, 64, 32, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
