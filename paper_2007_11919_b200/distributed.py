@@ -280,6 +280,61 @@ class GpuBackend:
         return (np.concatenate([ctx.cpu().numpy(), pts.cpu().numpy().ravel()]),
                 est.cpu().numpy()[0], float(g[0]), float(g[1]))
 
+    def _cached_index(self, key, arr: np.ndarray):
+        ck = ("idx", key)
+        if ck not in self._cache:
+            self._cache[ck] = self.D.index_tensor(arr, self.dev)
+        return self._cache[ck]
+
+    def landmark_context_dev(self, sample: np.ndarray, r: int):
+        """landmark_context kept on the device: (head, check) with head =
+        [g1, g2, est(r), context, landmark configuration] as one device vector
+        (broadcast as is) and check() raising the deferred failures."""
+        from .primitives import classical_pieces, raise_piece_status
+        D, x = self.D, self.x
+        idx = self._cached_index(("sample", id(sample)), sample)
+        pts, est, gof, st = classical_pieces(x, idx, np.array([0, len(sample)], np.int64), r)
+        h = D.handle(self.dev)
+        l, p = len(sample), x.shape[1]
+        size = int(h.lib.mdsx_gower_context_size(l, p, r))
+        head = D.empty((2 + r + size + l * r,), self.dev)
+        cond = D.empty((1,), self.dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        h.call("mdsx_gower_context", x.data_ptr(), D.dtype_code(x), p, p, idx.data_ptr(), l,
+               pts.data_ptr(), r, head[2 + r:].data_ptr(), cond.data_ptr(), flag.data_ptr(),
+               D.stream_ptr(self.dev))
+        head[0:2] = gof[0]
+        head[2:2 + r] = est[0]
+        head[2 + r + size:] = pts.reshape(-1)
+
+        def check():
+            raise_piece_status(D.decode_status(st)[0], r, "sample subset")
+            if int(flag.item()):
+                from .errors import NumericalError
+                raise NumericalError("base covariance is ill-conditioned or not positive definite")
+        return head, check
+
+    def gower_rows_dev(self, head, l: int, r: int, lo: int, hi: int):
+        D, x = self.D, self.x
+        p = x.shape[1]
+        h = D.handle(self.dev)
+        rows = x[lo:hi]
+        out = D.empty((hi - lo, r), self.dev)
+        nf = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        h.call("mdsx_gower_interpolate", head[2 + r:].data_ptr(), l, p, r, rows.data_ptr(),
+               D.dtype_code(x), p, hi - lo, out.data_ptr(), r, nf.data_ptr(),
+               D.stream_ptr(self.dev))
+        return out
+
+    def place_dev(self, out, key, local: np.ndarray, values_dev) -> None:
+        """out[local[i]] = values_dev[i] with the index upload cached under key."""
+        if len(local) == 0:
+            return
+        D = self.D
+        li = self._cached_index(key, local)
+        D.handle(self.dev).call("mdsx_scatter_rows", values_dev.data_ptr(), li.data_ptr(),
+                                len(local), out.shape[1], out.data_ptr(), D.stream_ptr(self.dev))
+
     def gower_rows(self, packed: np.ndarray, l: int, r: int, lo: int, hi: int):
         D, x = self.D, self.x
         p = x.shape[1]
@@ -473,22 +528,47 @@ def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
     r, l = prm.r, prm.l
     sample = sample if sample is not None else interpolation_sample(n, l, prm.seed)
     l = len(sample)
-    if comm.rank == 0:
-        packed, est, g1, g2 = backend.landmark_context(sample, r)
-        head = np.concatenate([[g1, g2], est, packed])
-    else:
-        size = backend_context_len(backend, l, r) + 2 + r
-        head = np.zeros(size)
-    head = comm.broadcast(head, src=0) if comm.world > 1 else head
-    g1, g2, est, packed = float(head[0]), float(head[1]), head[2:2 + r], head[2 + r:]
-    base = packed[-l * r:].reshape(l, r)
     blocks = (n + SUM_BLOCK - 1) // SUM_BLOCK
     b_lo, b_hi = shard(blocks, comm.world, comm.rank)
     lo, hi = b_lo * SUM_BLOCK, min(n, b_hi * SUM_BLOCK)
-    out = backend.gower_rows(packed, l, r, lo, hi)        # (hi - lo) x r, shard-local rows
-    # landmark rows inside the shard take the classical configuration
     in_shard = (sample >= lo) & (sample < hi)
-    backend.place(out, (sample[in_shard] - lo).astype(np.int64), base[in_shard])
+    if hasattr(backend, "landmark_context_dev"):
+        # device-resident: the context is computed on rank 0 and broadcast as a
+        # device vector (no host round trip inside the step)
+        check = None
+        if comm.rank == 0:
+            head_dev, check = backend.landmark_context_dev(sample, r)
+        else:
+            size = backend_context_len(backend, l, r) + 2 + r
+            head_dev = torch.zeros(size, dtype=torch.float64, device=backend.dev)
+        if comm.world > 1:
+            dist.broadcast(head_dev, src=0, group=comm.group)
+        out = backend.gower_rows_dev(head_dev, l, r, lo, hi)
+        base_dev = head_dev[-l * r:].reshape(l, r)
+        if in_shard.all():
+            vals = base_dev
+        else:
+            sel = backend._cached_index(("insel", id(sample), lo, hi), np.flatnonzero(in_shard))
+            vals = base_dev.index_select(0, sel)
+        backend.place_dev(out, ("local", id(sample), lo, hi), (sample[in_shard] - lo).astype(np.int64),
+                          vals)
+        if check is not None:
+            check()
+        head_small = head_dev[:2 + r].cpu().numpy()
+        g1, g2, est = float(head_small[0]), float(head_small[1]), head_small[2:2 + r]
+    else:
+        if comm.rank == 0:
+            packed, est, g1, g2 = backend.landmark_context(sample, r)
+            head = np.concatenate([[g1, g2], est, packed])
+        else:
+            size = backend_context_len(backend, l, r) + 2 + r
+            head = np.zeros(size)
+        head = comm.broadcast(head, src=0) if comm.world > 1 else head
+        g1, g2, est, packed = float(head[0]), float(head[1]), head[2:2 + r], head[2 + r:]
+        base = packed[-l * r:].reshape(l, r)
+        out = backend.gower_rows(packed, l, r, lo, hi)        # (hi - lo) x r, shard-local rows
+        # landmark rows inside the shard take the classical configuration
+        backend.place(out, (sample[in_shard] - lo).astype(np.int64), base[in_shard])
     bounds = np.minimum(hi, np.arange(b_lo, b_hi + 1, dtype=np.int64) * SUM_BLOCK) - lo
     sums = backend.range_sums(out, bounds, r)
     recs = np.hstack([np.arange(b_lo, b_hi, dtype=np.float64)[:, None], sums])
