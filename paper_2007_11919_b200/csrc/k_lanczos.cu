@@ -364,20 +364,27 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
       const int ti = lane >> 2, tc = lane & 3;
       for (int I = warp; I < nbk; I += LT / 32) {
         double dsum = 0.0, t0 = 0.0, t1 = 0.0;
+        const int lofs = 8 * ti + 2 * tc;
+        // transposed part, J < I: tile (J, I); its index grows by nbk - J - 1 per J
+        const double* tp = At + 64 * (I) + lofs;           // tile (0, I)
 #pragma unroll 4
-        for (int J = 0; J < nbk; ++J) {
-          const bool dir = J >= I;
-          const double2 a2 = *reinterpret_cast<const double2*>(
-              At + 64 * (dir ? lz_tile(I, J, nbk) : lz_tile(J, I, nbk)) + 8 * ti + 2 * tc);
-          const double* qJ = q + 8 * J;
-          if (dir) {
-            dsum = fma(a2.x, qJ[2 * tc], dsum);
-            dsum = fma(a2.y, qJ[2 * tc + 1], dsum);
-          } else {
-            const double qi = qJ[ti];
-            t0 = fma(a2.x, qi, t0);
-            t1 = fma(a2.y, qi, t1);
-          }
+        for (int J = 0; J < I; ++J) {
+          const double2 a2 = *reinterpret_cast<const double2*>(tp);
+          const double qi = q[8 * J + ti];
+          t0 = fma(a2.x, qi, t0);
+          t1 = fma(a2.y, qi, t1);
+          tp += 64 * (nbk - J - 1);
+        }
+        // direct part, J >= I: tiles (I, I), (I, I+1), ... are consecutive
+        const double* dp = At + 64 * lz_tile(I, I, nbk) + lofs;
+        const double* qd = q + 8 * I + 2 * tc;
+#pragma unroll 4
+        for (int J = I; J < nbk; ++J) {
+          const double2 a2 = *reinterpret_cast<const double2*>(dp);
+          dsum = fma(a2.x, qd[0], dsum);
+          dsum = fma(a2.y, qd[1], dsum);
+          dp += 64;
+          qd += 8;
         }
         dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
         dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
