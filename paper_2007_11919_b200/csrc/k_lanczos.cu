@@ -443,9 +443,10 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
     double wreg = 0.0, nw = 0.0;
     for (int pass = 0; pass < 2; ++pass) {
       {
-        const int part = tid & 3;
-        const int seg = (k + 3) >> 2;
-        for (int c = tid >> 2; c < ((nc + 7) & ~7); c += LT / 4) {     // warp-uniform trip count
+        // 8 threads per column (k split in 8 contiguous parts), 3-level shuffle
+        const int part = tid & 7;
+        const int seg = (k + 7) >> 3;
+        for (int c = tid >> 3; c < ((nc + 3) & ~3); c += LT / 8) {     // warp-uniform trip count
           double h0 = 0.0, h1 = 0.0;
           if (c < nc) {
             const double* qc = Q + (size_t)c * kq;
@@ -460,6 +461,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
           double h = h0 + h1;
           h += __shfl_xor_sync(0xffffffffu, h, 1);
           h += __shfl_xor_sync(0xffffffffu, h, 2);
+          h += __shfl_xor_sync(0xffffffffu, h, 4);
           if (c < nc && part == 0) hv[c] = h;
         }
       }
