@@ -73,9 +73,9 @@ WORKLOADS = {
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
 TRAFFIC = {
-    ("dc2", "lanczos_smem_kernel"): {"bytes": (499.866 + 68.592) * 1e6,
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (500.035 + 68.574) * 1e6,
                                      "src": "profiles/r01g_ncu_full_dc2.txt"},
-    ("dc2", "gram_piece_kernel"): {"bytes": (439.717 + 27.759) * 1e6,
+    ("dc2", "gram_piece_kernel"): {"bytes": (439.716 + 27.652) * 1e6,
                                    "src": "profiles/r01g_ncu_full_dc2.txt"},
     ("interp4", "gower_bulk_kernel"): {"bytes": (4000.516 + 784.652) * 1e6,
                                        "src": "profiles/r01e_ncu_full_interp4.txt"},
