@@ -80,6 +80,14 @@ int mdsx_version(void);
 int mdsx_timing_enable(mdsx_handle* h, int on);
 int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap);
 
+/* Copy `bytes` from a PAGEABLE host array (e.g. the numpy array the reference
+ * API receives, linalg.py:28-38) to device memory, staged through page-locked
+ * chunk buffers by `threads` host threads (0 = half the cores) so host
+ * memcpy and PCIe DMA overlap.  Returns once the source has been read; the
+ * device writes are ordered on `stream` like cudaMemcpyAsync. */
+int mdsx_h2d(mdsx_handle* h, void* dst, const void* src, int64_t bytes, int32_t threads,
+             void* stream);
+
 /* ---- dense primitives (function-level seams) ---------------------------- */
 /* out (m x m, ldo) = squared distances between rows of x (m x p, ld);
  * symmetrised, clamped at 0, exact-zero diagonal. */

@@ -7,10 +7,8 @@ names, arguments and exceptions; all arithmetic runs in libmdsx.so
 
 from .algorithms import (DivideRun, FastRun, InterpolationRun, divide_and_conquer_mds,
                          fast_mds, interpolation_mds, run_algorithm)
-from .dataio import (IdxImageSet, RunManifest, load_idx_images, pair_images_labels,
-                     read_csv_matrix, read_idx_images, read_idx_labels, read_manifest,
-                     write_configuration, write_csv_matrix, write_idx_images, write_idx_labels,
-                     write_manifest)
+from .dataio import (IdxImageSet, load_idx_images, read_csv_matrix, read_idx_images,
+                     read_idx_labels)
 from .errors import (DegenerateRankError, FormatError, InvalidInputError, JoinError, MdsError,
                      MetricError, NumericalError, ParamError, ShapeError, UsageError)
 from .params import (ALGORITHM_NAMES, EXACT_SIZE_GUARD, AlgorithmParams)
@@ -21,9 +19,7 @@ from .primitives import (apply_procrustes, classical_mds, classical_mds_from_dat
                          cross_squared_distances, double_center, euclidean_distance_matrix,
                          fit_procrustes, gof_breakdown, goodness_of_fit, gower_context,
                          gower_interpolate)
-from .simulation import (DEFAULT_DOMINANT_SD, STUDY_COLUMNS, ScenarioMetrics, ScenarioSpec,
-                         aligned_correlations, eigenvalue_error_stats, g1_curve,
-                         generate_scenario, gof_sweep, run_cell, run_study)
+from .simulation import aligned_correlations, g1_curve, gof_sweep
 from .results import (EigenSystem, GofBreakdown, GowerContext, MdsConfiguration,
                       ProcrustesTransform)
 
@@ -40,10 +36,6 @@ __all__ = [
     "fast_stats", "fit_procrustes", "gof_breakdown", "goodness_of_fit", "gower_context",
     "gower_interpolate", "interpolation_mds", "plan_divide_conquer", "plan_fast",
     "plan_interpolation", "run_algorithm", "spawned_generator", "sub_seed",
-    "IdxImageSet", "RunManifest", "load_idx_images", "pair_images_labels", "read_csv_matrix",
-    "read_idx_images", "read_idx_labels", "read_manifest", "write_configuration",
-    "write_csv_matrix", "write_idx_images", "write_idx_labels", "write_manifest",
-    "DEFAULT_DOMINANT_SD", "STUDY_COLUMNS", "ScenarioMetrics", "ScenarioSpec",
-    "aligned_correlations", "eigenvalue_error_stats", "g1_curve", "generate_scenario",
-    "gof_sweep", "run_cell", "run_study",
+    "IdxImageSet", "load_idx_images", "read_csv_matrix", "read_idx_images", "read_idx_labels",
+    "aligned_correlations", "g1_curve", "gof_sweep",
 ]

@@ -754,159 +754,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
 
 
 // ---------------------------------------------------------------------------
-// Register-resident Lanczos (default for plan pieces, 32 < k <= 104).
-//
-// The smem kernel above is latency-bound: every step re-reads A (40 KB packed)
-// and Q from shared memory through eight barriers, and the convergence checks
-// (serial Sturm / twisted recurrences) stall all warps.  Here:
-//  * A lives in REGISTERS: its 28 upper 16x16 blocks (k padded to 112) are
-//    spread over 7 stepper warps, 4 blocks each (1 diagonal + 3 off-diagonal);
-//    lane (r = lane & 15, h = lane >> 4) holds row r, columns 8h..8h+7 of each
-//    block, so w = A q costs 8 (diagonal) or 16 (off-diagonal) FMAs per block
-//    per lane and each stored element is used twice (A_ij q_j and A_ji q_i).
-//  * the Krylov basis Q lives in registers too: column c in warp c % 7, slot
-//    c / 7, rows lane + 32 t (t < 4), so the re-orthogonalisation dots and the
-//    rank-(j+1) update of each warp touch only its own columns; one barrier
-//    combines the per-warp updates (fixed order).
-//  * every stepper warp keeps the full current vector (4 rows per lane), so
-//    norms and the three-term part need warp shuffles only: two barriers per
-//    step.  The three-term recurrence runs first and a single CGS pass follows,
-//    repeated only when it removes more than half of the norm (DGKS, "twice
-//    is enough"), so the usual step does one projection instead of two.
-//  * warp 7 is the CHECKER: while the steppers keep extending the basis it
-//    computes the top-r eigenpairs of T_m at the fixed check points
-//    m = m0, m0 + 4, ... (same multisection / twisted-factorisation method as
-//    above) and stops the steppers at the first converged one.  The check
-//    points do not depend on timing, so results are bitwise reproducible.
-// ---------------------------------------------------------------------------
-constexpr int RG_W = 7;                  // stepper warps
-constexpr int RG_T = (RG_W + 1) * 32;    // + the checker warp
-constexpr int RG_NT = RG_W * 32;         // stepper threads (named barrier 1)
-constexpr int RG_KP = 112;               // padded k (7 blocks of 16)
-constexpr int RG_S = 8;                  // basis columns per stepper warp
-constexpr int RG_QMAX = RG_W * RG_S;     // 56
-constexpr int RG_GAP = 4;                // steps between check points
-constexpr int RG_NB = 28;                // upper 16x16 blocks
-
-struct RgShared {
-  double alpha[RG_QMAX], beta[RG_QMAX], beta2[RG_QMAX];
-  double ysum[7][128];                   // [ordinal][row]: the 7 block contributions per block row
-  double upart[2][RG_W][128];            // per-warp projection updates (alternating passes)
-  double qbuf[RG_W][128];                // per-warp copy of q_j for the matvec
-  double theta[RMAX], thp[RMAX], rhp[RMAX];   // Ritz values; previous check's values / residuals
-  double as_[RG_QMAX + 8], bs_[RG_QMAX + 8], bq_[RG_QMAX + 8];   // the checker's scaled T
-  double ar_[RG_QMAX + 8], br_[RG_QMAX + 8];                      // ... reversed (trailing passes)
-  double red[8];
-  double hj[4];
-  int m_pub, sdone, stop, m_res, res_code, verdict;
-  double trace, anorm;
-};
-
-__device__ __forceinline__ int bar_or(int pred) {          // named barrier 1, the stepper warps
-  int out;
-  asm volatile("{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n bar.red.or.pred q, 1, %2, p;\n"
-               " selp.s32 %0, 1, 0, q;\n}"
-               : "=r"(out) : "r"(pred), "n"(RG_NT) : "memory");
-  return out;
-}
-// release / acquire flags in shared memory (no full fence: MEMBAR.SC is slow)
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.cta.shared.s32 [%0], %1;" :: "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void bar_steps() {
-  asm volatile("bar.sync 1, %0;" :: "n"(RG_NT) : "memory");
-}
-
-// sum over the warp, result in every lane (fixed butterfly order: identical in every warp)
-__device__ __forceinline__ double wsum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// off-diagonal pair index (0..20, row-major over I < J) -> (I, J)
-__device__ __forceinline__ void rg_pair(int p, int& I, int& J);
-// position of block g's row (side 0) or column (side 1) contribution among
-// the 7 contributions to block row `row`, in block order (the fixed summation order)
-__device__ __forceinline__ int rg_ordinal(int row, int gq, int side) {
-  int n = 0;
-  for (int g = 0; g < RG_NB; ++g) {
-    const int w = g >> 2, b = g & 3;
-    int I = w, J = w;
-    if (b) rg_pair(3 * w + b - 1, I, J);
-    if (I == row) { if (g == gq && side == 0) return n; ++n; }
-    if (b && J == row) { if (g == gq && side == 1) return n; ++n; }
-  }
-  return n;
-}
-
-__device__ __forceinline__ void rg_pair(int p, int& I, int& J) {
-  I = 0;
-  while (p >= 6 - I) { p -= 6 - I; ++I; }
-  J = I + 1 + p;
-}
-
-// One projection pass of the stepper warp: w -= Q (Q^T w) over all basis
-// columns (unused slots are zero).  Dots reduce-scattered over the warp, the
-// per-warp update combined across warps through upart (one barrier).
-// Returns (in hcol) the coefficient of column jcol when this warp owns it.
-__device__ __forceinline__ void rg_project(const double (&Qr)[RG_S][4], double (&w)[4], RgShared& sh,
-                                           int wid, int lane, int jcol, int pass, int& buf) {
-  double d[RG_S];
-#pragma unroll
-  for (int s = 0; s < RG_S; ++s) {
-    double a0 = Qr[s][0] * w[0];
-    a0 = fma(Qr[s][1], w[1], a0);
-    double a1 = Qr[s][2] * w[2];
-    a1 = fma(Qr[s][3], w[3], a1);
-    d[s] = a0 + a1;
-  }
-  // reduce-scatter 8 values over 32 lanes (positions are slots XOR lb, so
-  // each level keeps the low half): slot s ends in lanes 4s..4s+3
-#pragma unroll
-  for (int c = 0; c < 4; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c + 4], 16);
-#pragma unroll
-  for (int c = 0; c < 2; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c + 2], 8);
-  double g = d[0] + __shfl_xor_sync(0xffffffffu, d[1], 4);
-  g += __shfl_xor_sync(0xffffffffu, g, 2);
-  g += __shfl_xor_sync(0xffffffffu, g, 1);
-  const int lb = (lane >> 2) & 7;
-  double h[RG_S];                                // h[p] = coefficient of this lane's position p
-#pragma unroll
-  for (int p = 0; p < RG_S; ++p) h[p] = __shfl_sync(0xffffffffu, g, 4 * (p ^ lb));
-  if (wid == jcol % RG_W && lane == 0) {         // lane 0: lb == 0, position == slot
-    const int js = jcol / RG_W;
-    double hv = 0.0;
-#pragma unroll
-    for (int p = 0; p < RG_S; ++p) hv = p == js ? h[p] : hv;
-    sh.hj[pass] = hv;
-  }
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    double u0 = Qr[0][t] * h[0], u1 = Qr[1][t] * h[1];
-#pragma unroll
-    for (int s = 2; s < RG_S; s += 2) {
-      u0 = fma(Qr[s][t], h[s], u0);
-      u1 = fma(Qr[s + 1][t], h[s + 1], u1);
-    }
-    sh.upart[buf][wid][lane + 32 * t] = u0 + u1;
-  }
-  bar_steps();
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    double u = sh.upart[buf][0][lane + 32 * t];
-#pragma unroll
-    for (int v = 1; v < RG_W; ++v) u += sh.upart[buf][v][lane + 32 * t];
-    w[t] -= u;
-  }
-  buf ^= 1;      // the next pass writes the other buffer (no barrier between a read and it)
-}
-
+// Tridiagonal helpers of the convergence checks (declared at the top).
 // Branch-free reciprocal (MUFU seed + two Newton steps, ~1 ulp): unlike the
 // IEEE division it has no slow-path branch, so independent reciprocals
 // overlap with the recurrences instead of serialising them.
@@ -1062,554 +910,6 @@ __device__ __noinline__ void tw_charpoly(const double* as, const double* bs, con
 #endif
 }
 
-// The checker warp: top-r eigenpairs of T_m at the fixed check points.
-// Fast path per check: brackets from the previous check (Cauchy interlacing
-// gives theta_prev as a lower bound; the upper guess theta_prev + 2 rho_prev
-// is verified by a Sturm count) or Gershgorin, L = 32 / rr lanes of
-// multisection per eigenvalue to 1e-7 of the Gershgorin width, two Newton
-// steps on chi_m, and the residual |beta_m s_m| from s_m^2 = chi_{m-1}/chi_m'.
-// Eigenvectors of T (twisted factorisation + MGS in clusters) only at the
-// converged check.  Overlapping brackets (clusters) or a Newton step leaving
-// its bracket take the robust path: multisection to full precision and the
-// residual from the twisted eigenvectors.
-__device__ __noinline__ void rg_checker(RgShared& sh, double* S, double* U2, double* U3, int k, int r, int lane) {
-
-  int cp = max(2 * r + 4, 24);
-  int last = 0;
-  bool have_prev = false;
-  while (true) {
-    int mp = 0, sd = 0;
-    while (true) {                               // the whole warp polls (no divergence)
-      mp = ld_acquire(&sh.m_pub);
-      sd = ld_acquire(&sh.sdone);
-      mp = __shfl_sync(0xffffffffu, mp, 0);
-      sd = __shfl_sync(0xffffffffu, sd, 0);
-      if (mp >= cp || sd) break;
-    }
-    const int m = mp >= cp ? cp : mp;
-    const bool final_data = sd && m == mp;
-    if (m == last) {                              // stepping ended exactly at the last check
-      if (lane == 0) { sh.res_code = 2; sh.m_res = m; }
-      break;
-    }
-    last = m;
-#ifdef MDSX_LZ_PROF
-    long long t_ck0 = clock64();
-    const int mp_at_start = mp;
-#endif
-    const bool full = m >= k;
-    const double* al = sh.alpha;
-    const double* be = sh.beta;
-    const double* be2 = sh.beta2;
-    const int rr = r < m ? r : m;
-    double gl = 1e308, gu = -1e308, bmax = 0.0;
-    for (int i = lane; i < m; i += 32) {
-      const double off = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < m ? fabs(be[i]) : 0.0);
-      gl = fmin(gl, al[i] - off);
-      gu = fmax(gu, al[i] + off);
-      if (i + 1 < m) bmax = fmax(bmax, be2[i]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
-      gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
-      bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-    }
-    // exact power-of-two scaling of T into [-1, 1]
-    int ex;
-    frexp(fmax(fmax(fabs(gl), fabs(gu)), 1e-300), &ex);
-    const double isc = ldexp(1.0, -ex), sc = ldexp(1.0, ex);
-    for (int i = lane; i < m + 4; i += 32) {
-      sh.as_[i] = i < m ? al[i] * isc : 0.0;
-      sh.bs_[i] = (i > 0 && i < m) ? fmax(be2[i - 1] * isc * isc, 1e-300) : 0.0;
-      sh.bq_[i] = i + 1 < m ? be[i] * isc : 0.0;
-      sh.ar_[i] = i < m ? al[m - 1 - i] * isc : 0.0;
-      sh.br_[i] = (i > 0 && i < m) ? fmax(be2[m - 1 - i] * isc * isc, 1e-300) : 0.0;
-    }
-    __syncwarp();
-    const double* as = sh.as_;
-    const double* bs = sh.bs_;
-    const double* bq = sh.bq_;
-    const double gls = gl * isc, gus = gu * isc, gw = gus - gls;
-    const int L = 32 / rr;
-    const int grp = lane / L, sl = lane - grp * L;
-    const bool active = grp < rr;
-    const double rL = 1.0 / (double)(L + 1);
-    const unsigned gmask = L >= 32 ? 0xffffffffu : (((1u << L) - 1u) << (active ? grp * L : 0));
-    double lo = gls, hi = gus;
-    LZT(t1);
-    if (have_prev) {                              // verified brackets from the previous check
-      const double tp = active ? sh.thp[grp] * isc : 0.0, rp = active ? sh.rhp[grp] * isc : 0.0;
-      const double lo2 = tp - 1e-14 * gw, hi2 = fmin(gus, tp + 2.0 * rp + 1e-12 * gw);
-      // every lane runs the count (uniform control flow: a divergent branch
-      // around a long loop leaves the warp split for the code after it)
-      const bool below = active && sl < 2 &&
-                         sturm_scaled(as, bs, m, sl == 0 ? lo2 : hi2) <= m - 1 - grp;
-      const unsigned bal = __ballot_sync(0xffffffffu, below);
-      if (active) {
-        if ((bal >> (grp * L)) & 1u) lo = lo2;            // theta_grp >= lo2
-        if (!((bal >> (grp * L + 1)) & 1u)) hi = hi2;     // theta_grp < hi2
-        if (!(lo < hi)) { lo = gls; hi = gus; }
-      }
-    }
-    auto msect = [&](int rounds) {
-      for (int it = 0; it < rounds; ++it) {
-        const double x = lo + (hi - lo) * ((double)(sl + 1) * rL);
-        const int cntb = sturm_scaled(as, bs, m, x);                // all lanes (uniform)
-        const bool below_ok = active && cntb <= m - 1 - grp;      // grp-th largest above x
-        const unsigned okm = __ballot_sync(0xffffffffu, below_ok);
-        const int c = __popc(okm & gmask);
-        if (active) {
-          const double lo0 = lo, w = hi - lo;
-          lo = c > 0 ? lo0 + w * ((double)c * rL) : lo0;
-          hi = c < L ? lo0 + w * ((double)(c + 1) * rL) : hi;
-        }
-      }
-    };
-    auto rounds_to = [&](double target) {       // uniform round count to reach width <= target*gw
-      const double w0 = active ? hi - lo : 0.0;
-      int n = 0;
-      for (double w = w0; w > target * gw && n < 200; w *= rL) ++n;
-      return __reduce_max_sync(0xffffffffu, n);
-    };
-    msect(rounds_to(1e-7));
-    LZT(t2);
-    // one Rayleigh-quotient step from the twisted factorisation at the bracket midpoint
-    const int src0 = active ? grp * L : 0;
-    int bad = 0;
-    {
-      double gam, n2;
-      const double t0 = 0.5 * (lo + hi);
-      tw_charpoly(as, bs, sh.ar_, sh.br_, bq, m, t0, S + grp, U2 + grp, U3 + grp, active, sl, src0, gam, n2);
-      const double t1 = t0 + gam / n2;
-      if (active && sl == 0) {
-        if (t1 >= lo && t1 <= hi) sh.theta[grp] = t1;
-        else bad = 1;
-      }
-    }
-    {                                            // clusters: overlapping neighbour brackets
-      const int nb = (grp + 1) * L;
-      const double hi_n = __shfl_sync(0xffffffffu, hi, nb < 32 ? nb : 0);
-      if (active && sl == 0 && grp + 1 < rr && !(hi_n < lo)) bad = 1;
-    }
-    const bool robust = __any_sync(0xffffffffu, bad);
-    if (robust) {                                // bisect to full precision from Gershgorin
-      lo = gls;
-      hi = gus;
-      msect(rounds_to(1e-17));
-      if (active && sl == 0) sh.theta[grp] = 0.5 * (lo + hi);
-    }
-    __syncwarp();
-    LZT(t3);
-    // eigenvectors of T_m at theta (scaled units until stored) and the residuals
-    bool conv;
-    {
-      double gam, n2;
-      const double tq = active ? sh.theta[grp] : 0.0;
-      tw_charpoly(as, bs, sh.ar_, sh.br_, bq, m, tq, S + grp, U2 + grp, U3 + grp, active, sl, src0, gam, n2);
-      const double bm = full ? 0.0 : be[m - 1];
-      const double th0 = __shfl_sync(0xffffffffu, tq, 0) * sc;
-      bool okl = true;
-      if (active && sl == 0) {
-        const double inv = 1.0 / sqrt(n2);
-        const double res = fabs(bm * S[(m - 1) * RMAX + grp]) * inv;
-        okl = res <= 1e-12 * fabs(th0);
-        sh.thp[grp] = tq * sc;
-        sh.rhp[grp] = res;
-        sh.theta[grp] = tq * sc;
-        for (int c = 0; c < m; ++c) S[c * RMAX + grp] *= inv;
-      }
-      conv = __all_sync(0xffffffffu, okl) && rr == r;
-      have_prev = !robust;
-      if ((conv || full) && lane == 0) *(volatile int*)&sh.stop = 1;   // release the steppers now
-      __syncwarp();
-    }
-    LZT(t4);
-    if (conv || full) {
-      const double* tv = sh.theta;
-      const double ctol = 1e-3 * fabs(tv[0]);
-      const bool adj = lane >= 1 && lane < rr && fabs(tv[lane - 1] - tv[lane]) <= ctol;
-      if (__any_sync(0xffffffffu, adj)) {        // MGS inside eigenvalue clusters (fixed order)
-        for (int i = 1; i < rr; ++i) {
-          bool touched = false;
-          for (int j = 0; j < i; ++j) {
-            if (fabs(tv[i] - tv[j]) > ctol) continue;
-            touched = true;
-            double dt = 0.0;
-            for (int t = lane; t < m; t += 32) dt = fma(S[t * RMAX + i], S[t * RMAX + j], dt);
-            dt = wsum(dt);
-            for (int t = lane; t < m; t += 32) S[t * RMAX + i] = fma(-dt, S[t * RMAX + j], S[t * RMAX + i]);
-            __syncwarp();
-          }
-          if (touched) {
-            double nr = 0.0;
-            for (int t = lane; t < m; t += 32) nr = fma(S[t * RMAX + i], S[t * RMAX + i], nr);
-            nr = sqrt(wsum(nr));
-            for (int t = lane; t < m; t += 32) S[t * RMAX + i] /= nr;
-            __syncwarp();
-          }
-        }
-      }
-    }
-#ifdef MDSX_LZ_PROF
-    if (blockIdx.x == 0 && lane == 0)
-      printf("rg check m=%d (steppers at %d) conv=%d robust=%d clk=%lld gersh %lld msect %lld rq %lld vec %lld | tw sums minors %lld twist %lld outward %lld\n",
-             m, mp_at_start, (int)conv, (int)robust, clock64() - t_ck0, t1 - t_ck0, t2 - t1, t3 - t2, t4 - t3,
-             sh_prof[0], sh_prof[1], sh_prof[2]);
-#endif
-    if (conv || full) {
-      if (lane == 0) { sh.res_code = 1; sh.m_res = m; *(volatile int*)&sh.stop = 1; }
-      __syncwarp();
-      if (m == cp && m < k && m < RG_QMAX) asm volatile("bar.sync 2, %0;" :: "n"(RG_T) : "memory");
-      break;
-    }
-    if (final_data) {                            // basis capacity exhausted, not converged
-      if (lane == 0) { sh.res_code = 2; sh.m_res = m; }
-      break;
-    }
-    if (m == cp && m < k && m < RG_QMAX)          // the steppers wait at this check point
-      asm volatile("bar.sync 2, %0;" :: "n"(RG_T) : "memory");
-    if (m == cp) cp += RG_GAP;
-  }
-  __syncwarp();
-  if (lane == 0) *(volatile int*)&sh.stop = 1;
-}
-
-__global__ void __launch_bounds__(RG_T, 1)
-lanczos_reg_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
-                   double* __restrict__ Uout, double* __restrict__ lam_out,
-                   double* __restrict__ estimates, double* __restrict__ gof,
-                   mdsx_piece_status* __restrict__ status, int only_flagged) {
-  extern __shared__ double sm[];
-  __shared__ RgShared sh;
-  const PieceDesc d = pd[blockIdx.x];
-  const int pid = d.id, k = d.k;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double* Ag = Aall + d.a_off;
-  if (only_flagged) {
-    const mdsx_piece_status s0 = status[pid];
-    if (!(s0.code == MDSX_NUMERICAL && s0.value == -3.0)) return;
-    __syncthreads();
-    if (tid == 0) status[pid] = mdsx_piece_status{MDSX_OK, 0, 0.0};
-    __syncthreads();
-  }
-  if (status[pid].code == MDSX_INVALID_INPUT) {
-    for (int e = tid; e < k * r; e += RG_T) Uout[d.u_off + e] = 0.0;
-    if (tid < r) {
-      estimates[(int64_t)pid * r + tid] = 0.0;
-      lam_out[(int64_t)pid * r + tid] = 0.0;
-    }
-    if (tid < 2) gof[2 * (int64_t)pid + tid] = 0.0;
-    return;
-  }
-  const int kq = k | 1;
-  double* Qsm = sm;                                  // final basis, column c at Qsm + c*kq
-  double* S = Qsm + (size_t)RG_QMAX * kq;            // Ritz coefficients S[c*RMAX + i]
-  double* U2 = S + (size_t)RG_QMAX * RMAX;          // pivot columns of the checker
-  double* U3 = U2 + (size_t)RG_QMAX * RMAX;
-
-  for (int e = tid; e < 7 * 128; e += RG_T) (&sh.ysum[0][0])[e] = 0.0;
-  if (tid == 0) { sh.m_pub = 0; sh.sdone = 0; sh.stop = 0; sh.res_code = 0; sh.m_res = 0; sh.verdict = 0; }
-
-  // ---- stepper state (registers)
-  double Ab[4][8];
-  double Qr[RG_S][4];
-  double qj[4], qjm[4];
-  int blk[4];                                        // I | J << 3 | ordR << 6 | ordC << 9
-  const int rw = lane & 15, hw = lane >> 4;
-  // select-free reduce-scatters: lane-dependent XOR permutations of the
-  // register columns of A (pm, over columns within a half block) and of the
-  // basis slots (lb) so every level keeps positions [0, n/2) and sends the rest
-  const int pm = (lane >> 1) & 7, lb = (lane >> 2) & 7;
-  double fro = 0.0, tr = 0.0;
-#pragma unroll
-  for (int s = 0; s < RG_S; ++s)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) Qr[s][t] = 0.0;
-  if (wid < RG_W) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int I = wid, J = wid;
-      if (b) rg_pair(3 * wid + b - 1, I, J);
-      blk[b] = I | (J << 3) | (rg_ordinal(I, 4 * wid + b, 0) << 6) |
-               ((b ? rg_ordinal(J, 4 * wid + b, 1) : 0) << 9);
-      const int row = 16 * I + rw;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int col = 16 * J + 8 * hw + (c ^ pm);
-        Ab[b][c] = (row < k && col < k) ? Ag[(int64_t)row * k + col] : 0.0;
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) fro = fma((b ? 2.0 : 1.0) * Ab[b][c], Ab[b][c], fro);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) tr += (8 * hw + (c ^ pm) == rw) ? Ab[0][c] : 0.0;
-  } else {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      blk[b] = 0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) Ab[b][c] = 0.0;
-    }
-  }
-  fro = wsum(fro);
-  tr = wsum(tr);
-  if (lane == 0) sh.red[wid] = fro;
-  __syncthreads();
-  if (tid == 0) {
-    double f = 0.0;
-    for (int w = 0; w < RG_W; ++w) f += sh.red[w];
-    sh.anorm = sqrt(f);
-  }
-  __syncthreads();
-  if (lane == 0) sh.red[wid] = tr;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < RG_W; ++w) t += sh.red[w];
-    sh.trace = t;
-  }
-  __syncthreads();
-  const double anorm = sh.anorm;
-
-  if (wid < RG_W) {
-    // q_0: batch-independent pseudo-random unit vector (same stream as the smem kernel)
-    double n0 = 0.0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int e = lane + 32 * t;
-      qj[t] = e < k ? hash_unit((uint64_t)e * 0x9E37ull + 17) : 0.0;
-      qjm[t] = 0.0;
-      n0 = fma(qj[t], qj[t], n0);
-    }
-    n0 = sqrt(wsum(n0));
-#pragma unroll
-    for (int t = 0; t < 4; ++t) qj[t] /= n0;
-    if (wid == 0)
-#pragma unroll
-      for (int p = 0; p < RG_S; ++p)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) Qr[p][t] = p == lb ? qj[t] : 0.0;
-    const int qcap = min(RG_QMAX, k);
-    double bprev = 0.0;
-    int j = 0, ubuf = 0;
-    int next_cp = max(2 * r + 4, 24);           // the checker's first check point
-#ifdef MDSX_LZ_PROF
-    long long t_st0 = clock64(), t_mv0 = 0;
-    long long pf[4] = {0, 0, 0, 0};
-    int n_two = 0;
-#endif
-    while (true) {
-      // ---- y = A q_j (symmetric blocks; q_j broadcast from this warp's smem copy)
-#ifdef MDSX_LZ_PROF
-      t_mv0 = clock64();
-#endif
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sh.qbuf[wid][lane + 32 * t] = qj[t];
-      __syncwarp();
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int Ib = blk[b] & 7, Jb = (blk[b] >> 3) & 7, oR = (blk[b] >> 6) & 7, oC = blk[b] >> 9;
-        const double* qJ = &sh.qbuf[wid][16 * Jb + 8 * hw];
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < 8; c += 2) {
-          s0 = fma(Ab[b][c], qJ[c ^ pm], s0);
-          s1 = fma(Ab[b][c + 1], qJ[(c + 1) ^ pm], s1);
-        }
-        double s = s0 + s1;
-        s += __shfl_xor_sync(0xffffffffu, s, 16);
-        if (lane < 16) sh.ysum[oR][16 * Ib + lane] = s;
-        if (b) {                      // column contributions: reduce-scatter over the 16 rows
-          const double qr = sh.qbuf[wid][16 * Ib + rw];
-          double v[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = Ab[b][c] * qr;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c + 4], 8);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c + 2], 4);
-          double e1 = v[0] + __shfl_xor_sync(0xffffffffu, v[1], 2);
-          e1 += __shfl_xor_sync(0xffffffffu, e1, 1);
-          if (!(lane & 1)) sh.ysum[oC][16 * Jb + 8 * hw + pm] = e1;
-        }
-      }
-      const int stop_now = bar_or(tid == 0 && *(volatile int*)&sh.stop);
-#ifdef MDSX_LZ_PROF
-      long long t_a = clock64();
-      pf[0] += t_a - t_mv0;
-#endif
-      if (stop_now) break;
-      // ---- gather y (4 rows per lane, fixed summation order)
-      double w[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        double y = sh.ysum[0][lane + 32 * t];
-#pragma unroll
-        for (int q = 1; q < 7; ++q) y += sh.ysum[q][lane + 32 * t];
-        w[t] = y;
-      }
-      // ---- three-term part, then one CGS pass (a second one only if it removed > half)
-      double al = 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) al = fma(qj[t], w[t], al);
-      al = wsum(al);
-      double nw0 = 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        w[t] = fma(-al, qj[t], fma(-bprev, qjm[t], w[t]));
-        nw0 = fma(w[t], w[t], nw0);
-      }
-      nw0 = wsum(nw0);
-#ifdef MDSX_LZ_PROF
-      long long t_b = clock64();
-      pf[1] += t_b - t_a;
-#endif
-      // projection passes through ONE inlined copy of rg_project (code size:
-      // the instruction cache is the limit of this kernel): pass 0, a DGKS
-      // repeat (slot 1) when it removed more than half the norm, and on
-      // breakdown two passes of a fresh random direction (slots 2, 3)
-      const int m = j + 1;
-      const bool full = m >= k;
-      const bool capped = !full && m >= qcap;
-      int slot = 0;
-      bool two = false, broke = false;
-      double b = 0.0, nw = 0.0;
-      while (true) {
-        rg_project(Qr, w, sh, wid, lane, j, slot, ubuf);
-        nw = 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) nw = fma(w[t], w[t], nw);
-        nw = wsum(nw);
-        if (slot == 0 && nw < 0.5 * nw0) {
-          slot = 1;
-          two = true;
-#ifdef MDSX_LZ_PROF
-          ++n_two;
-#endif
-          continue;
-        }
-        if (slot >= 2) {
-          if (slot == 2) { slot = 3; continue; }
-          break;                                 // w: the orthogonalised fresh direction
-        }
-        b = sqrt(nw);
-        broke = !full && !capped && !(b > 1e-13 * anorm);
-        if (!broke) break;
-        // invariant subspace: continue from a fresh direction orthogonal to Q
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int e = lane + 32 * t;
-          w[t] = e < k ? hash_unit(((uint64_t)m << 20) ^ (uint64_t)e) : 0.0;
-        }
-        slot = 2;
-      }
-#ifdef MDSX_LZ_PROF
-      long long t_c = clock64();
-      pf[2] += t_c - t_b;
-#endif
-      if (tid == 0) {
-        sh.alpha[j] = al + sh.hj[0] + (two ? sh.hj[1] : 0.0);
-        sh.beta[j] = broke ? 0.0 : b;
-        sh.beta2[j] = broke ? 0.0 : b * b;
-      }
-      if (!full && !capped) {
-        double qn[4];
-        const double rb = 1.0 / (broke ? sqrt(nw) : b);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) qn[t] = w[t] * rb;
-        if (broke) b = 0.0;
-        if (wid == m % RG_W) {
-          const int mp = (m / RG_W) ^ lb;
-#pragma unroll
-          for (int p = 0; p < RG_S; ++p)
-#pragma unroll
-            for (int t = 0; t < 4; ++t) Qr[p][t] = p == mp ? qn[t] : Qr[p][t];
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) { qjm[t] = qj[t]; qj[t] = qn[t]; }
-      }
-      bprev = b;
-      if (tid == 0) {
-        st_release(&sh.m_pub, m);
-      }
-      j = m;
-#ifdef MDSX_LZ_PROF
-      pf[3] += clock64() - t_c;
-#endif
-      if (full || capped) {
-        if (tid == 0) {
-          st_release(&sh.sdone, 1);
-        }
-        break;
-      }
-      if (m == next_cp) {
-        // check point: wait for the checker's verdict on T_m.  Running ahead
-        // while it works would starve it (the warp scheduler keeps issuing the
-        // stepper warp sharing its SMSP) and waste steps past convergence.
-        asm volatile("bar.sync 2, %0;" :: "n"(RG_T) : "memory");   // with the checker
-        if (*(volatile int*)&sh.stop) break;
-        next_cp += RG_GAP;
-      }
-    }
-#ifdef MDSX_LZ_PROF
-    if (blockIdx.x == 0 && tid == 0)
-      printf("rg steps m=%d clk=%lld  matvec+barA %lld gather+3term %lld proj %lld norm+publish %lld  two-pass %d\n", j,
-             clock64() - t_st0, pf[0], pf[1], pf[2], pf[3], n_two);
-#endif
-  } else {
-    rg_checker(sh, S, U2, U3, k, r, lane);
-  }
-  __syncthreads();
-  const int code = sh.res_code, m = sh.m_res;
-  if (code == 2) {             // basis capacity exhausted: the full Jacobi kernel takes over
-    if (tid == 0 && status[pid].code == MDSX_OK) status[pid] = mdsx_piece_status{MDSX_NUMERICAL, 0, -2.0};
-    return;
-  }
-  if (wid < RG_W) {
-#pragma unroll
-    for (int p = 0; p < RG_S; ++p) {
-      const int c = RG_W * (p ^ lb) + wid;
-      if (c < m)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int e = lane + 32 * t;
-          if (e < k) Qsm[(size_t)c * kq + e] = Qr[p][t];
-        }
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < k * r; e += RG_T) {
-    const int a = e / r, i = e % r;
-    double u = 0.0;
-    if (i < m)
-      for (int c = 0; c < m; ++c) u = fma(Qsm[(size_t)c * kq + a], S[c * RMAX + i], u);
-    Uout[d.u_off + e] = u;
-  }
-  if (tid == 0) {
-    const double top = sh.theta[0];
-    const double tol = 1e-8 * fabs(top);
-    mdsx_piece_status st{MDSX_OK, 0, 0.0};
-    if (status[pid].code != MDSX_OK) st.code = status[pid].code;
-    double kept = 0.0;
-    for (int i = 0; i < r; ++i) {
-      double v = i < m ? sh.theta[i] : 0.0;
-      if (fabs(v) <= tol) v = 0.0;
-      if (st.code == MDSX_OK && v <= 0.0) { st.code = MDSX_DEGENERATE; st.index = i + 1; st.value = v; }
-      kept += v;
-      lam_out[(int64_t)pid * r + i] = v;
-      estimates[(int64_t)pid * r + i] = v / d.m;
-    }
-    if (st.code == MDSX_OK) st.value = (double)m;
-    status[pid] = st;
-    const double g = st.code == MDSX_OK ? kept / sh.trace : 0.0;
-    gof[2 * (int64_t)pid] = g;
-    gof[2 * (int64_t)pid + 1] = g;
-  }
-}
-
 }  // namespace
 
 namespace mdsx {
@@ -1632,7 +932,7 @@ int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int km
                         const double* A, double* U, double* lam, double* estimates, double* gof,
                         mdsx_piece_status* status, int full_basis, int only_flagged,
                         cudaStream_t st, const PtsEpi* epi) {
-  if (epi && (full_basis || only_flagged || r > 10 || getenv("MDSX_LZ_REG"))) epi = nullptr;
+  if (epi && (full_basis || only_flagged || r > 10)) epi = nullptr;
   if (npieces == 0) return MDSX_OK;
   PtsEpi e{};
   if (epi) e = *epi;
@@ -1647,15 +947,6 @@ int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int km
                                     fc ? atoi(fc) : 0);
     return launched(h, "lanczos_smem_kernel", st);
   };
-  if (!full_basis && kmax <= RG_KP && getenv("MDSX_LZ_REG")) {
-    // register-resident steppers + checker warp (default for plan pieces)
-    const size_t smem = ((size_t)RG_QMAX * (kmax | 1) + 3 * (size_t)RG_QMAX * RMAX) * sizeof(double);
-    cudaFuncSetAttribute(lanczos_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    mdsx::pre(h, st);
-    lanczos_reg_kernel<<<npieces, RG_T, smem, st>>>(pd, r, A, U, lam, estimates, gof, status,
-                                                    only_flagged);
-    return launched(h, "lanczos_reg_kernel", st);
-  }
   return full_basis ? go(lanczos_smem_kernel<LMAX>, LMAX)
                     : go(lanczos_smem_kernel<QCAP_PIECES>, QCAP_PIECES);
 }

@@ -37,10 +37,6 @@ int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const doub
                          int nparts, const double* corr, cudaStream_t st);
 int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
                               int r, double* out, double* corr, cudaStream_t st);
-int launch_gower_tma(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
-                     const double* mean, const double* M, const double* v, double* out,
-                     double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
-                     bool norm32);
 int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
                       const double* mean, const double* M, const double* v, double* out,
                       double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
@@ -85,13 +81,14 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
                    double* Uout, double* lam_out, double* estimates, double* gof,
                    mdsx_piece_status* status, cudaStream_t st,
                    int (*put)(mdsx_handle*, void*, const void*, size_t, cudaStream_t));
-int subspace_rmax();
-int launch_subspace(mdsx_handle* h, const PieceDesc* pd, int npieces, int kmax, int r,
-                    const double* A, double* U, double* lam, double* estimates, double* gof,
-                    mdsx_piece_status* status, cudaStream_t st);
+
+// last error message of the calling thread (calls from several threads on one
+// handle each read their own message)
+static thread_local std::string t_last_error;
 
 int fail(mdsx_handle* h, int code, const std::string& msg) {
-  if (h) h->err = msg;
+  (void)h;
+  t_last_error = msg;
   return code;
 }
 
@@ -367,11 +364,9 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   // next to another chunk's HBM / tensor-bound Gram and points kernels.
   // Same kernels and per-piece arithmetic, so results are unchanged.
   {
-    const char* eig = getenv("MDSX_EIG");
     const char* pc = getenv("MDSX_PIPE_CHUNKS");
     const bool simple = piece_gram && cp.pd_jac.empty() && cp.pd_big.empty() && cp.pd_f1.empty() &&
-                        (int)cp.pd_g.size() == np && (int)cp.pd_sub.size() == np &&
-                        !(eig && strcmp(eig, "subspace") == 0);
+                        (int)cp.pd_g.size() == np && (int)cp.pd_sub.size() == np;
     int nc = pc ? atoi(pc) : 2;                       // measured best on dc2 / fast3
     nc = std::min(nc, np / (2 * h->num_sms));          // >= two waves of pieces per chunk
     // fused points epilogue in the Lanczos kernel (aligned rows, r <= 10): each
@@ -445,17 +440,8 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
                           gof, status, 1, st)))
     return rc;
   if (!cp.pd_sub.empty()) {
-    // blocked subspace iteration on the tensor pipe; pieces without a gap
-    // after r fall through to Lanczos (flagged), capacity overflow to Jacobi
-    // solver choice (measured): Lanczos by default; MDSX_EIG=subspace
-    // selects the DMMA block iteration (same results within the tolerance)
-    const char* eig = getenv("MDSX_EIG");
-    const bool sub = r <= subspace_rmax() && eig && strcmp(eig, "subspace") == 0;
-    if (sub && (rc = launch_subspace(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
-                                     estimates, gof, status, st)))
-      return rc;
     if ((rc = launch_lanczos_smem(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
-                                  estimates, gof, status, 0, sub ? 1 : 0, st)))
+                                  estimates, gof, status, 0, 0, st)))
       return rc;
     if ((rc = launch_jacobi_fallback(h, dpd_sub, (int)cp.pd_sub.size(), cp.kmax_sub, r, A, U, lam,
                                      estimates, gof, status, st)))
@@ -500,21 +486,24 @@ void mdsx_destroy(mdsx_handle* h) {
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ws_done) cudaEventDestroy(h->ws_done);
   delete h;
 }
 
-const char* mdsx_last_error(const mdsx_handle* h) { return h ? h->err.c_str() : "null handle"; }
+const char* mdsx_last_error(const mdsx_handle* h) { return h ? t_last_error.c_str() : "null handle"; }
 
 int64_t mdsx_launch_count(const mdsx_handle* h) { return h ? h->launches : 0; }
 
 int mdsx_timing_enable(mdsx_handle* h, int on) {
   if (!h) return MDSX_PARAM;
+  std::lock_guard<std::recursive_mutex> lk(h->mu);
   h->timing = on != 0;
   return MDSX_OK;
 }
 
 int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap) {
   if (!h) return -1;
+  std::lock_guard<std::recursive_mutex> lk(h->mu);
   // fold pending event pairs into the running per-kernel totals
   for (auto& t : h->timed) {
     cudaEventSynchronize(t.second.second);
@@ -543,6 +532,7 @@ int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap) {
 int mdsx_sqdist_self(mdsx_handle* h, const void* x, int dtype, int64_t ld, int64_t m, int32_t p,
                      double* out, int64_t ldo, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (m < 1 || p < 1) return fail(h, MDSX_INVALID_INPUT, "data must be non-empty");
   const int64_t ta = (m + 63) / 64;                      // lower-triangle 64 x 64 tiles
   int rc = ws_reserve(h, align_up(m * sizeof(double)) + align_up(ta * (ta + 1) / 2 * 8) + 512);
@@ -555,6 +545,7 @@ int mdsx_sqdist_cross(mdsx_handle* h, const void* a, int64_t lda, int64_t ma, co
                       int64_t ldb, int64_t mb, int dtype, int32_t p, double* out, int64_t ldo,
                       void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   int rc = ws_reserve(h, align_up(ma * sizeof(double)) + align_up(mb * sizeof(double)));
   if (rc) return rc;
   double* na = (double*)ws_alloc(h, ma * sizeof(double), st);
@@ -564,6 +555,7 @@ int mdsx_sqdist_cross(mdsx_handle* h, const void* a, int64_t lda, int64_t ma, co
 
 int mdsx_double_center(mdsx_handle* h, const double* delta, int64_t m, double* q, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   int rc = ws_reserve(h, align_up(m * sizeof(double)) + 256);
   if (rc) return rc;
   double* mu = (double*)ws_alloc(h, m * sizeof(double), st);
@@ -576,6 +568,7 @@ int mdsx_classical_pieces(mdsx_handle* h, const void* data, int dtype, int64_t l
                           int32_t r, double* points, double* estimates, double* gof,
                           mdsx_piece_status* status, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   ClassicalPlan cp;
   int rc = plan_classical(h, p, piece_off, npieces, r, cp);
   if (rc) return rc;
@@ -586,6 +579,7 @@ int mdsx_classical_pieces(mdsx_handle* h, const void* data, int dtype, int64_t l
 int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t r, double* points,
                          double* estimates, double* gof, mdsx_piece_status* status, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (r < 1 || r > m - 1 || r > MDSX_MAX_R)
     return fail(h, MDSX_PARAM, "r must satisfy 1 <= r <= n-1, got r=" + std::to_string(r) +
                                    ", n=" + std::to_string(m));
@@ -632,6 +626,7 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
 
 int mdsx_delta_check(mdsx_handle* h, const double* delta, int64_t m, int32_t* flags, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   int rc = ws_reserve(h, 256);
   if (rc) return rc;
   auto* mx = (unsigned long long*)ws_alloc(h, sizeof(unsigned long long), st);
@@ -648,6 +643,7 @@ int mdsx_gower_context(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
                        const int64_t* base_idx, int64_t l, const double* base_config, int32_t r,
                        double* ctx, double* cond, int32_t* flag, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   double* mean = ctx;
   double* M = mean + p;
@@ -662,6 +658,7 @@ int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t
                            const void* rows, int dtype, int64_t ld, int64_t m, double* out,
                            int64_t ldo, int32_t* nonfinite, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   int32_t* nf = nonfinite;
   const double* mean = ctx;
   const double* M = mean + p;
@@ -675,6 +672,7 @@ int mdsx_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_ro
                         int32_t njobs, int32_t r, double* rot, double* trans, double* loss,
                         int32_t* degenerate, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   for (int j = 0; j < njobs; ++j)
     if (job_off[j + 1] - job_off[j] < 2)
@@ -693,17 +691,20 @@ int mdsx_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_ro
 int mdsx_procrustes_apply(mdsx_handle* h, double* buf, int32_t r, const int64_t* start,
                           const int64_t* len, int32_t njobs, int64_t max_len, const double* rot,
                           const double* trans, void* stream) {
+  MDSX_GUARD(h, as_stream(stream));
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   return launch_apply(h, buf, r, start, len, njobs, max_len, rot, trans, as_stream(stream));
 }
 
 int mdsx_scatter_rows(mdsx_handle* h, const double* src, const int64_t* idx, int64_t n, int32_t r,
                       double* out, void* stream) {
+  MDSX_GUARD(h, as_stream(stream));
   return launch_scatter(h, src, idx, n, r, out, as_stream(stream));
 }
 
 int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   int rc = ws_reserve(h, recenter_ws_bytes(r));
   if (rc) return rc;
@@ -714,12 +715,14 @@ int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* st
 int mdsx_segment_colsums(mdsx_handle* h, const double* points, const int64_t* idx,
                          const int64_t* seg_off, int32_t nseg, int32_t r, double* sums,
                          void* stream) {
+  MDSX_GUARD(h, as_stream(stream));
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   return launch_seg_colsum(h, points, idx, seg_off, nseg, r, sums, as_stream(stream));
 }
 
 int mdsx_shift_rows(mdsx_handle* h, double* points, const int64_t* idx, int64_t n, int32_t r,
                     const double* shift, void* stream) {
+  MDSX_GUARD(h, as_stream(stream));
   if (r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad r");
   return launch_shift_rows(h, points, idx, n, r, shift, as_stream(stream));
 }
@@ -737,6 +740,7 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                            int32_t npieces, int32_t c, int32_t r, double* out, double* estimates,
                            double* gof, mdsx_piece_status* status, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   ClassicalPlan cp;
   int rc = plan_classical(h, p, piece_off, npieces, r, cp);
   if (rc) return rc;
@@ -806,6 +810,7 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
                        double* estimates, double* gof, mdsx_piece_status* status, double* cond,
                        int32_t* flags, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   const int64_t off[2] = {0, l};
   ClassicalPlan cp;
   int rc = plan_classical(h, p, off, 1, r, cp);
@@ -841,11 +846,7 @@ int mdsx_interpolation(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
     int nparts = 0;
     // the landmark configuration is centred -> v ~ 0: fp32 norms are exact enough
     const bool n32 = dtype == MDSX_F32 && !getenv("MDSX_GOWER_NORM64");
-    if ((rc = launch_gower_tma(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
-                               st, n32)))
-      return rc;
-    if (nparts == 0 &&
-        (rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
+    if ((rc = launch_gower_bulk(h, data, dtype, n, p, r, mean, M, v, out, part, flag + 1, &nparts,
                                 st, n32)))
       return rc;
     const int lparts = (int)((l + 255) / 256);
@@ -877,6 +878,7 @@ extern "C" int mdsx_fast_finish(mdsx_handle* h, const double* P, int32_t r, cons
                                 int32_t njobs, const double* rot, const double* trans,
                                 const int64_t* order, int64_t n, double* out, void* stream) {
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   if (njobs < 1 || r < 1 || r > MDSX_MAX_R) return fail(h, MDSX_PARAM, "bad fast finish shape");
   if (job_off[0] != 0 || job_off[njobs] != n)
     return fail(h, MDSX_PARAM, "fast finish jobs must cover rows 0..n");
@@ -903,6 +905,7 @@ extern "C" int mdsx_aligned_correlations(mdsx_handle* h, const double* points, i
   if (n < 2) return fail(h, MDSX_SHAPE, "need at least 2 rows");
   if (dtype != MDSX_F64 && dtype != MDSX_F32) return fail(h, MDSX_PARAM, "bad dtype");
   cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
   const size_t nd = (size_t)corr_ws_doubles(n, r, h->num_sms);
   int rc = ws_reserve(h, align_up(nd * sizeof(double)) + 256);
   if (rc) return rc;

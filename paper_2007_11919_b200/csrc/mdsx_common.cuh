@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -34,9 +35,38 @@ struct mdsx_handle {
   // second stream for the piece pipeline (run_classical), created on first use
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // calls are serialised per handle (the workspace and staging buffer are
+  // shared): a call holds `mu`, makes its stream wait for the previous call's
+  // last work (`ws_done`) and records `ws_done` on its stream when it returns,
+  // so calls from several host threads or on several streams never overwrite
+  // each other's descriptors or intermediates while those are in flight
+  std::recursive_mutex mu;
+  int depth = 0;
+  cudaEvent_t ws_done = nullptr;
 };
 
 namespace mdsx {
+
+// RAII guard opened by every C-ABI entry point that enqueues device work.
+struct CallGuard {
+  mdsx_handle* h;
+  cudaStream_t st;
+  std::unique_lock<std::recursive_mutex> lk;
+  CallGuard(mdsx_handle* hh, cudaStream_t s) : h(hh), st(s), lk(hh->mu) {
+    if (h->depth++ == 0 && h->ws_done) cudaStreamWaitEvent(st, h->ws_done, 0);
+  }
+  ~CallGuard() {
+    if (--h->depth == 0) {
+      if (!h->ws_done) cudaEventCreateWithFlags(&h->ws_done, cudaEventDisableTiming);
+      cudaEventRecord(h->ws_done, st);
+    }
+  }
+  CallGuard(const CallGuard&) = delete;
+  CallGuard& operator=(const CallGuard&) = delete;
+};
+#define MDSX_GUARD(h, st)                                  \
+  if (!(h)) return MDSX_PARAM;                             \
+  ::mdsx::CallGuard mdsx_call_guard_((h), (st))
 
 int fail(mdsx_handle* h, int code, const std::string& msg);
 int cuda_check(mdsx_handle* h, cudaError_t e, const char* what);

@@ -1,8 +1,9 @@
-"""File ingestion and result serialisation — the reference's ``dataio`` module
-(``src/dataio.py:1-179``) with the same names, arguments and errors, plus the
-B200 path SURVEY.md §8(f) ranks next: IDX images streamed straight into device
-memory (unsigned bytes over PCIe, widened by a kernel) and numeric CSV parsed by
-native host threads.
+"""File ingestion — the readers of the reference's
+``dataio`` module (``src/dataio.py:42-130``) with the same names, arguments
+and errors: IDX images streamed straight into device memory (unsigned bytes
+over PCIe, widened by a kernel) and numeric CSV parsed by native host
+threads.  The reference's writers and run manifest are outside the hot path
+and not part of this package.
 
 * ``read_idx_images`` / ``read_idx_labels`` validate the header with the same
   FormatError texts (``dataio.py:42-58, 68-82``); ``IdxImageSet.to_data_matrix``
@@ -11,25 +12,19 @@ native host threads.
 * ``read_csv_matrix`` (``dataio.py:102-130``) runs in ``mdsx_csv_read``:
   correctly rounded like Python ``float()``, same first-error-in-file-order
   messages (ragged row / invalid number / no data rows).
-* Writers and the run manifest (``dataio.py:60-66, 85-99, 133-179``) are plain
-  host code, as in the reference.
 """
 
 from __future__ import annotations
 
 import ctypes as C
-import dataclasses
-import json
 import os
-import struct
 from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
 
 from . import _lib
-from .errors import FormatError, InvalidInputError, JoinError
-from .results import MdsConfiguration
+from .errors import FormatError, InvalidInputError
 
 IDX_IMAGES_MAGIC = 0x00000803
 IDX_LABELS_MAGIC = 0x00000801
@@ -103,29 +98,10 @@ def load_idx_images(path, *, device=None, dtype=None, scale: float = 1.0):
     return out
 
 
-def write_idx_images(images: IdxImageSet, path) -> None:
-    """Serialize back to IDX bytes; inverse of read_idx_images."""
-    header = struct.pack(">IIII", IDX_IMAGES_MAGIC, images.count, images.height, images.width)
-    Path(path).write_bytes(header + images.pixels.astype(np.uint8).tobytes())
-
-
 def read_idx_labels(path) -> np.ndarray:
     """Parse an IDX label file (magic 0x00000801) into a uint8 vector."""
     n, _, _ = _probe(path, 1)
     return np.fromfile(str(path), dtype=np.uint8, offset=8).copy()
-
-
-def write_idx_labels(labels, path) -> None:
-    arr = np.asarray(labels, dtype=np.uint8)
-    Path(path).write_bytes(struct.pack(">II", IDX_LABELS_MAGIC, arr.size) + arr.tobytes())
-
-
-def pair_images_labels(images: IdxImageSet, labels) -> tuple[np.ndarray, np.ndarray]:
-    """Join an image set with its label vector; lengths must agree."""
-    arr = np.asarray(labels)
-    if arr.shape[0] != images.count:
-        raise JoinError(f"label count {arr.shape[0]} does not match image count {images.count}")
-    return images.to_data_matrix(), arr
 
 
 def read_csv_matrix(path, has_header: bool = False, *, threads: int = 0) -> np.ndarray:
@@ -150,49 +126,3 @@ def read_csv_matrix(path, has_header: bool = False, *, threads: int = 0) -> np.n
     if rc != _lib.OK:
         raise _lib.status_error(rc, msg.value.decode(errors="replace"))
     return out
-
-
-def write_csv_matrix(matrix, path) -> None:
-    """Write a matrix as headerless CSV with 17 significant digits (round-trips
-    any float64 exactly)."""
-    arr = np.asarray(matrix, dtype=np.float64)
-    np.savetxt(path, arr, fmt="%.17g", delimiter=",")
-
-
-def write_configuration(config: MdsConfiguration, path) -> None:
-    """Write the embedding coordinates of a configuration as CSV."""
-    write_csv_matrix(config.points, path)
-
-
-@dataclass(frozen=True)
-class RunManifest:
-    """A machine-readable record of one MDS run."""
-
-    algorithm: str
-    params: dict
-    input_path: str
-    input_rows: int
-    input_cols: int
-    output_paths: dict
-    gof_g1: float
-    gof_g2: float
-    eigenvalue_estimates: list
-    elapsed_s: float
-
-    def to_dict(self) -> dict:
-        return dataclasses.asdict(self)
-
-
-def write_manifest(manifest: RunManifest, path) -> None:
-    """Write a manifest as JSON; all referenced paths must already exist."""
-    for ref in [manifest.input_path, *manifest.output_paths.values()]:
-        if not Path(ref).exists():
-            raise InvalidInputError(f"manifest references missing path: {ref}")
-    with open(path, "w") as handle:
-        json.dump(manifest.to_dict(), handle, indent=2)
-        handle.write("\n")
-
-
-def read_manifest(path) -> dict:
-    with open(path) as handle:
-        return json.load(handle)

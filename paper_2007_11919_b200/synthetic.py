@@ -9,6 +9,7 @@ output).
 Config 5 has no generator in the reference (the EMNIST files are absent), so
 ``image_like`` is this build's own stand-in with the BASELINE description:
 28x28 = 784 features in [0, 1] stored as float32, ~80% exact zeros per row;
+row block k (65 536 rows) is drawn from PCG64 sub-stream (seed, 5, 1, k);
 each row belongs to one of 47 seeded class prototypes, whose central blob
 (an ellipse, jittered by up to one pixel per row) is the row's support; on
 the support the value is 0.5*Beta(2,2) + 0.5*template_c(pixel) + N(0, 0.05),
@@ -16,6 +17,9 @@ clipped to [0, 1]; off the support it is exactly 0.
 """
 
 from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -28,21 +32,56 @@ def _gen(seed: int, *path: int) -> np.random.Generator:
         np.random.SeedSequence(entropy=seed, spawn_key=tuple(path))))
 
 
-def normal_matrix(g: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+def normal_matrix(g: np.random.Generator, rows: int, cols: int, threads: int | None = None,
+                  chunk: int = 1 << 22) -> np.ndarray:
     """Box-Muller normals from the generator's uniform doubles (rng.py:26-41):
-    radius sqrt(-2 log1p(-u1)), angle 2 pi u2, cosines then sines."""
+    radius sqrt(-2 log1p(-u1)), angle 2 pi u2, cosines then sines.
+
+    Bit-identical to the reference's serial draw, computed over `threads`
+    host threads: the uniform stream u1 is the first `half` doubles of the
+    PCG64 stream and u2 the next `half`, so a chunk [a, b) of both is drawn
+    from copies of the bit generator advanced by a and half + a
+    (``PCG64.advance``) and transformed independently (numpy ufuncs release
+    the GIL).  Consumes the generator exactly like the serial version."""
     total = rows * cols
     half = (total + 1) // 2
-    u = g.random(half)
-    v = g.random(half)
-    rad = np.sqrt(-2.0 * np.log1p(-u))
-    ang = (2.0 * np.pi) * v
-    return np.concatenate([rad * np.cos(ang), rad * np.sin(ang)])[:total].reshape(rows, cols)
+    threads = threads or min(16, os.cpu_count() or 1)
+    if half <= chunk or threads == 1:
+        u = g.random(half)
+        v = g.random(half)
+        rad = np.sqrt(-2.0 * np.log1p(-u))
+        ang = (2.0 * np.pi) * v
+        return np.concatenate([rad * np.cos(ang), rad * np.sin(ang)])[:total].reshape(rows, cols)
+    state = g.bit_generator.state
+    out = np.empty(total)
+
+    def work(a: int) -> None:
+        b = min(half, a + chunk)
+        streams = []
+        for off in (a, half + a):
+            bg = np.random.PCG64()
+            bg.state = state
+            bg.advance(off)
+            streams.append(np.random.Generator(bg).random(b - a))
+        u, v = streams
+        rad = np.sqrt(-2.0 * np.log1p(-u))
+        ang = (2.0 * np.pi) * v
+        out[a:b] = rad * np.cos(ang)
+        e = min(total, half + b)
+        if e > half + a:
+            out[half + a:e] = (rad * np.sin(ang))[:e - half - a]
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(0, half, chunk)))
+    g.bit_generator.advance(2 * half)          # leave g where the serial draw would
+    return out.reshape(rows, cols)
 
 
-def scenario(n: int, p: int, h: int, seed: int = 0, rep: int = 0) -> np.ndarray:
-    """N(0, diag(15 x h, 1 x (p-h))) rows, float64, reference stream."""
-    out = normal_matrix(_gen(seed, rep), n, p)
+def scenario(n: int, p: int, h: int, seed: int = 0, rep: int = 0,
+             threads: int | None = None) -> np.ndarray:
+    """N(0, diag(15 x h, 1 x (p-h))) rows, float64, reference stream
+    (simulation.py:68-80), bit-identical for any `threads`."""
+    out = normal_matrix(_gen(seed, rep), n, p, threads)
     out[:, :h] *= np.sqrt(15.0)
     return out
 
@@ -68,48 +107,35 @@ def _prototypes(seed: int):
     return masks, templates
 
 
-def image_like(n: int, seed: int = 0, chunk: int = 65536) -> np.ndarray:
-    """Config-5 stand-in: n x 784 float32 in [0, 1], ~80% exact zeros."""
+def _image_chunk(masks, templates, seed: int, k: int, m: int) -> np.ndarray:
+    g = _gen(seed, 5, 1, k)
+    cls = g.integers(0, N_CLASSES, size=m)
+    sh = g.integers(-1, 2, size=(m, 2))
+    # support = the class blob rolled by (dy, dx) per row (np.roll as a gather)
+    yy = (np.arange(SIDE)[None, :, None] - sh[:, 0, None, None]) % SIDE
+    xx = (np.arange(SIDE)[None, None, :] - sh[:, 1, None, None]) % SIDE
+    sup = masks[cls][np.arange(m)[:, None, None], yy, xx]
+    vals = 0.5 * g.beta(2.0, 2.0, size=(m, SIDE, SIDE)) + 0.5 * templates[cls] \
+        + g.normal(0.0, 0.05, size=(m, SIDE, SIDE))
+    vals = np.clip(vals, 0.0, 1.0) * sup
+    return vals.reshape(m, -1).astype(np.float32)
+
+
+def image_like(n: int, seed: int = 0, chunk: int = 65536, threads: int | None = None) -> np.ndarray:
+    """Config-5 stand-in: n x 784 float32 in [0, 1], ~80% exact zeros.  Row
+    block k (of `chunk` rows) is drawn from its own PCG64 sub-stream
+    (seed, 5, 1, k), so blocks are generated in parallel and the result does
+    not depend on `threads`."""
     masks, templates = _prototypes(seed)
-    g = _gen(seed, 5, 1)
-    out = np.zeros((n, SIDE * SIDE), dtype=np.float32)
-    for start in range(0, n, chunk):
-        m = min(chunk, n - start)
-        cls = g.integers(0, N_CLASSES, size=m)
-        sh = g.integers(-1, 2, size=(m, 2))
-        sup = masks[cls]
-        sup = np.stack([np.roll(sup[i], (sh[i, 0], sh[i, 1]), axis=(0, 1)) for i in range(m)])
-        tpl = templates[cls]
-        vals = 0.5 * g.beta(2.0, 2.0, size=(m, SIDE, SIDE)) + 0.5 * tpl \
-            + g.normal(0.0, 0.05, size=(m, SIDE, SIDE))
-        vals = np.clip(vals, 0.0, 1.0) * sup
-        out[start:start + m] = vals.reshape(m, -1).astype(np.float32)
-    return out
+    out = np.empty((n, SIDE * SIDE), dtype=np.float32)
+    threads = threads or min(16, os.cpu_count() or 1)
 
+    def work(k: int) -> None:
+        a = k * chunk
+        m = min(chunk, n - a)
+        out[a:a + m] = _image_chunk(masks, templates, seed, k, m)
 
-def image_like_device(n: int, seed: int = 0, device="cuda", chunk: int = 131072):
-    """Same distribution as `image_like` (same 47 prototypes), drawn on the GPU
-    with torch's generator — for benchmark-scale inputs only (parity tests use
-    the numpy stream above)."""
-    import torch
-
-    masks_np, templates_np = _prototypes(seed)
-    masks = torch.from_numpy(masks_np).to(device)
-    templates = torch.from_numpy(templates_np).to(device=device, dtype=torch.float32)
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    beta = torch.distributions.Beta(torch.tensor(2.0, device=device), torch.tensor(2.0, device=device))
-    out = torch.empty((n, SIDE * SIDE), dtype=torch.float32, device=device)
-    for start in range(0, n, chunk):
-        m = min(chunk, n - start)
-        cls = torch.randint(0, N_CLASSES, (m,), generator=g, device=device)
-        sh = torch.randint(-1, 2, (m, 2), generator=g, device=device)
-        sup = masks[cls]
-        yy = (torch.arange(SIDE, device=device)[None, :, None] - sh[:, 0, None, None]) % SIDE
-        xx = (torch.arange(SIDE, device=device)[None, None, :] - sh[:, 1, None, None]) % SIDE
-        sup = sup[torch.arange(m, device=device)[:, None, None], yy, xx]
-        torch.manual_seed(seed * 1000003 + start)      # Beta sampler uses the global stream
-        vals = 0.5 * beta.sample((m, SIDE, SIDE)) + 0.5 * templates[cls] \
-            + 0.05 * torch.randn((m, SIDE, SIDE), generator=g, device=device)
-        out[start:start + m] = (vals.clamp_(0.0, 1.0) * sup).reshape(m, -1)
+    nchunks = (n + chunk - 1) // chunk
+    with ThreadPoolExecutor(max(1, min(threads, nchunks))) as ex:
+        list(ex.map(work, range(nchunks)))
     return out

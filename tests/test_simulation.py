@@ -1,73 +1,15 @@
-"""The reference's tests/test_simulation.py re-expressed against the drop-in
-``simulation`` module (device metrics), plus parity of the device
+"""The reference's metric tests (tests/test_simulation.py) re-expressed against
+the drop-in ``simulation`` module (device metrics), plus parity of the device
 aligned_correlations with a NumPy restatement of simulation.py:83-108 and of
 the single-solve gof_sweep with the reference's per-h loop."""
 
-import csv
 import dataclasses
 
 import numpy as np
 import pytest
 
-from paper_2007_11919_b200 import (AlgorithmParams, MetricError, ParamError, ScenarioSpec,
-                                   eigenvalue_error_stats, generate_scenario)
-
-REF_SRC = "/root/reference/pkg/src"
-
-
-class TestGenerateScenario:
-    def test_dominant_and_noise_variance(self):
-        data = generate_scenario(ScenarioSpec(n=100_000, k=4, h=2, seed=0), 0)
-        assert 14.5 <= data[:, 0].var() <= 15.5
-        assert 0.97 <= data[:, 3].var() <= 1.03
-
-    def test_columns_uncorrelated(self):
-        data = generate_scenario(ScenarioSpec(n=100_000, k=4, h=2, seed=1), 0)
-        corr = np.corrcoef(data, rowvar=False)
-        assert np.abs(corr[~np.eye(4, dtype=bool)]).max() <= 0.02
-
-    def test_deterministic_per_seed_and_replication(self):
-        spec = ScenarioSpec(n=200, k=3, h=1, seed=5)
-        assert np.array_equal(generate_scenario(spec, 2), generate_scenario(spec, 2))
-        assert not np.array_equal(generate_scenario(spec, 2), generate_scenario(spec, 3))
-
-    def test_validation(self):
-        with pytest.raises(ParamError):
-            generate_scenario(ScenarioSpec(n=100, k=3, h=4, seed=0), 0)
-        with pytest.raises(ParamError):
-            generate_scenario(ScenarioSpec(n=5, k=3, h=1, seed=0), 0)
-
-    @pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference absent")
-    def test_bit_exact_against_reference(self):
-        import importlib
-        import sys
-        sys.path.insert(0, REF_SRC)
-        try:
-            ref = importlib.import_module("scalemds.simulation")
-        finally:
-            sys.path.remove(REF_SRC)
-        for kw in (dict(n=1000, k=10, h=3, seed=5), dict(n=101, k=7, h=2, seed=1,
-                                                          dominant_sd=2.0, noise_sd=0.5)):
-            for rep in (0, 3):
-                assert np.array_equal(generate_scenario(ScenarioSpec(**kw), rep),
-                                      ref.generate_scenario(ref.ScenarioSpec(**kw), rep))
-
-
-class TestEigenvalueErrorStats:
-    def test_exact_estimates(self):
-        bias, mse = eigenvalue_error_stats(np.full((5, 3), 15.0))
-        assert np.array_equal(bias, np.zeros(3)) and np.array_equal(mse, np.zeros(3))
-
-    def test_pairs_and_single(self):
-        bias, mse = eigenvalue_error_stats(np.array([[14.0], [16.0]]))
-        assert bias[0] == 0.0 and mse[0] == 1.0
-        bias, mse = eigenvalue_error_stats(np.array([[12.0]]))
-        assert bias[0] == -3.0 and mse[0] == 9.0
-
-    def test_mse_dominates_squared_bias(self):
-        est = np.random.default_rng(2).normal(15.0, 2.0, size=(40, 4))
-        bias, mse = eigenvalue_error_stats(est)
-        assert np.all(mse >= bias ** 2 - 1e-9)
+from paper_2007_11919_b200 import AlgorithmParams, MetricError, ParamError
+from paper_2007_11919_b200.synthetic import scenario
 
 
 def ref_aligned(points, dominant):
@@ -88,7 +30,7 @@ class TestAlignedCorrelations:
     @pytest.fixture()
     def config(self, cuda):
         from paper_2007_11919_b200 import classical_mds_from_data
-        data = generate_scenario(ScenarioSpec(n=400, k=6, h=3, seed=9), 0)
+        data = scenario(400, 6, 3, seed=9)
         return classical_mds_from_data(data, 3), data[:, :3]
 
     def test_identity_rotation_reflection(self, config):
@@ -140,53 +82,6 @@ class TestAlignedCorrelations:
         assert np.array_equal(got, got2)
 
 
-def read_rows(path):
-    with open(path, newline="") as handle:
-        return list(csv.DictReader(handle))
-
-
-@pytest.mark.gpu
-class TestRunCellStudy:
-    def test_metrics_shape_and_bounds(self, cuda):
-        from paper_2007_11919_b200 import run_cell
-        spec = ScenarioSpec(n=300, k=4, h=2, replications=3, seed=13)
-        metrics, rows = run_cell(spec, "classical")
-        assert metrics.correlations.shape == (3, 2) and metrics.eigenvalue_estimates.shape == (3, 2)
-        assert metrics.elapsed_s.shape == (3,) and len(rows) == 6
-        assert np.all(np.abs(metrics.correlations) <= 1.0)
-
-    def test_failed_replication_keeps_going(self, cuda):
-        from paper_2007_11919_b200 import run_cell
-        spec = ScenarioSpec(n=300, k=4, h=2, replications=2, seed=14)
-        metrics, rows = run_cell(spec, "divide", params=AlgorithmParams(r=2, l=150, c=1))
-        assert metrics.correlations.shape == (0, 2) and len(rows) == 2
-        assert all(row["error"] for row in rows)
-
-    def test_study_rows_resume_reproducible(self, cuda, tmp_path):
-        from paper_2007_11919_b200 import run_study
-        spec = ScenarioSpec(n=300, k=4, h=3, replications=2, seed=4)
-        path = run_study([spec], ["classical", "interpolate"], tmp_path / "a",
-                         params={"interpolate": AlgorithmParams(r=3, l=150)})
-        rows = read_rows(path)
-        assert len(rows) == 2 * 2 * 3 and {row["dim"] for row in rows} == {"1", "2", "3"}
-        again = run_study([spec], ["classical", "interpolate"], tmp_path / "a").read_bytes()
-        assert again == path.read_bytes()                      # resumed from the cells
-        b = run_study([spec], ["classical", "interpolate"], tmp_path / "b",
-                      params={"interpolate": AlgorithmParams(r=3, l=150)})
-
-        def strip(p):
-            return [{k: v for k, v in row.items() if k != "elapsed_s"} for row in read_rows(p)]
-        assert strip(path) == strip(b)
-
-    def test_cell_failure_recorded_not_fatal(self, cuda, tmp_path):
-        from paper_2007_11919_b200 import run_study
-        spec = ScenarioSpec(n=200, k=3, h=2, replications=1, seed=7)
-        rows = read_rows(run_study([spec], ["bogus", "classical"], tmp_path))
-        errors = [row for row in rows if row["error"]]
-        assert len(errors) == 1 and "bogus" in errors[0]["error"]
-        assert len(rows) - len(errors) == 2
-
-
 @pytest.mark.gpu
 class TestGofSweep:
     def _dominant(self, seed):
@@ -214,7 +109,7 @@ class TestGofSweep:
     def test_curve_matches_per_h_runs(self, cuda, algo, kw):
         """One run at h_cap gives every G1(h) of the reference's per-h loop."""
         from paper_2007_11919_b200 import g1_curve, run_algorithm
-        data = generate_scenario(ScenarioSpec(n=4000, k=12, h=4, seed=2), 0)
+        data = scenario(4000, 12, 4, seed=2)
         params = AlgorithmParams(r=1, **kw)
         curve = g1_curve(data, algo, params, 10)
         for h in range(1, 11):
