@@ -1,7 +1,7 @@
 """Benchmark: MDS points embedded / second on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
-                    [--impl ours|reference]
+                    [--impl ours|reference] [--scaling auto|weak|strong]
 
 Workloads (BASELINE.json configs; default = config 2, the metric's config):
   dc2      divide-and-conquer  n=1e6   p=100 fp64  l=1000 c=20 r=10
@@ -10,26 +10,30 @@ Workloads (BASELINE.json configs; default = config 2, the metric's config):
   interp1  interpolation       n=1e4   p=10  fp64  l=500       r=2
   img5dc / img5fast / img5interp   config 5 (n=814,255, p=784 fp32, r=10)
 
-A step = one full algorithm call over the whole (device-resident) input with
-the plan passed explicitly (planning is host work done before timing); it
-ends with the n x r configuration on the device in input row order.
-Inputs are larger than L2 (126 MB) for every full-size workload, so no
-separate flush is needed.  `e2e` repeats the measurement through the public
-API from pinned HOST memory: H2D of the input, the plan's index upload, the
-kernels, and the D2H of the n x r result and the fit figures, every step.
+Input: the reference's own scenario stream (simulation.py:68-80, bit-exact,
+generated on the host by parallel PCG64 sub-streams; config 4 cast to
+float32) or the config-5 image-like stand-in, so the result can be checked
+against the fixtures produced by running the reference itself
+(tests/golden/full_*.npz): the line's ``parity`` block.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling.  Every algorithm
-runs ONE global problem of N x the config's rows through
-paper_2007_11919_b200.distributed (input replicated on every GPU outside the
-timed region; each rank solves its contiguous share of subsets / rows /
-level-1 subtrees; only per-segment sums and fit figures are exchanged —
-all-gathers over NCCL).  The timed region is
-bracketed by barriers and the max over ranks is reported; the n x r result
-stays sharded on the devices (gathering it is not part of the metric).
+A step = one full algorithm call over the device-resident input with the plan
+passed explicitly (planning is host work, reported as ``planner_ms``); it
+ends with the n x r configuration on the device in input row order.  Every
+full-size input is larger than L2 (126 MB), so no flush is needed.  ``e2e``
+repeats the call through the public API with the input as a PAGEABLE numpy
+array (what a scalemds user passes): H2D of the input (staged by mdsx_h2d)
+and of the plan indices, the kernels, and the D2H of the n x r result.
 
---impl reference: the CPU oracle port of the reference algorithm (this repo's
-oracle/, a restatement of /root/reference's numpy path) on the host cores,
-rank 0 only, each step a bounded sample of the workload.
+Multi-GPU: ``--gpus N`` without torchrun starts N ranks itself (torch's
+launcher on 127.0.0.1); under torchrun one process per GPU.  Scaling: weak
+for D&C / fast (N x the config's rows, one global plan), strong for config 4
+("rows sharded across 1/2/4/8 GPUs", fixed n = 1e7).  Each rank holds only
+the rows its share needs (distributed.local_rows); the step exchanges only
+small record tensors over NCCL; max over ranks.
+
+--impl reference: the reference algorithm's CPU restatement (oracle/, the
+reference's own numpy code path) on the host cores, rank 0 only, each step a
+bounded sample of the workload.
 """
 
 from __future__ import annotations
@@ -37,6 +41,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -48,6 +53,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 
 METRIC = "MDS points embedded/sec"
 UNIT = "points/s"
@@ -58,7 +64,7 @@ WORKLOADS = {
     "fast3": dict(algo="fast", n=1_000_000, p=100, h=10, l=1000, c=None, s=20, r=10,
                   dtype="f64", data="gaussian"),
     "interp4": dict(algo="interpolate", n=10_000_000, p=100, h=10, l=2000, c=None, s=None, r=10,
-                    dtype="f32", data="gaussian"),
+                    dtype="f32", data="gaussian", strong=True),
     "interp1": dict(algo="interpolate", n=10_000, p=10, h=2, l=500, c=None, s=None, r=2,
                     dtype="f64", data="gaussian"),
     "img5dc": dict(algo="divide", n=814_255, p=784, h=0, l=1000, c=20, s=None, r=10,
@@ -68,7 +74,6 @@ WORKLOADS = {
     "img5interp": dict(algo="interpolate", n=814_255, p=784, h=0, l=1000, c=None, s=None, r=10,
                        dtype="f32", data="image"),
 }
-
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
@@ -92,6 +97,16 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -180,57 +195,24 @@ def measured_peaks(dev) -> dict:
     return peaks
 
 
-# ------------------------------------------------------------------ data
-def make_data(w: dict, dev, seed: int):
-    import torch
-    n, p = w["n"], w["p"]
+# ------------------------------------------------------------------ data / plans
+def host_input(w: dict, n: int) -> np.ndarray:
+    """The workload's input on the host: the reference scenario stream
+    (bit-exact, parallel) or the config-5 stand-in."""
+    from paper_2007_11919_b200.synthetic import image_like, scenario
     if w["data"] == "image":
-        from paper_2007_11919_b200.synthetic import image_like_device
-        return image_like_device(n, seed=seed, device=dev)
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    dt = torch.float32 if w["dtype"] == "f32" else torch.float64
-    x = torch.randn(n, p, generator=g, dtype=dt, device=dev)
-    x[:, :w["h"]] *= 15.0 ** 0.5
-    return x
+        return image_like(n, seed=0)
+    x = scenario(n, w["p"], w["h"], seed=0)
+    return x.astype(np.float32) if w["dtype"] == "f32" else x
 
 
-def make_plan(w: dict, seed: int):
+def make_plan(w: dict, n: int, seed: int = 0):
     from paper_2007_11919_b200 import plans
     if w["algo"] == "divide":
-        return plans.plan_divide_conquer(w["n"], w["l"], w["c"], seed)
+        return plans.plan_divide_conquer(n, w["l"], w["c"], seed)
     if w["algo"] == "fast":
-        return plans.plan_fast(w["n"], w["l"], w["s"], seed)
-    return plans.interpolation_sample(w["n"], w["l"], seed)
-
-
-class ShardedRun:
-    """bench adapter for distributed.sharded_* (N>1, weak scaling)."""
-
-    def __init__(self, w, x, plan, dev):
-        from paper_2007_11919_b200 import AlgorithmParams
-        from paper_2007_11919_b200 import distributed as dd
-        self.dd, self.w = dd, w
-        self.be = dd.GpuBackend(x, reuse=True)     # per-plan setup once, like the 1-GPU runners
-        self.comm = dd.Comm(device=dev)
-        self.plan = plan
-        self.prm = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=0)
-        self.res = None
-
-    def launch(self):
-        if self.w["algo"] == "divide":
-            self.res = self.dd.sharded_divide_and_conquer(self.be, self.w["n"], self.prm, self.comm,
-                                                          plan=self.plan)
-        elif self.w["algo"] == "fast":
-            self.res = self.dd.sharded_fast(self.be, self.w["n"], self.prm, self.comm, plan=self.plan)
-        else:
-            self.res = self.dd.sharded_interpolation(self.be, self.w["n"], self.prm, self.comm,
-                                                     sample=self.plan)
-
-    def finish(self, return_device=True):
-        from paper_2007_11919_b200 import MdsConfiguration
-        r = self.res
-        return MdsConfiguration(r.out, r.estimates, r.gof_g1, r.gof_g2)
+        return plans.plan_fast(n, w["l"], w["s"], seed)
+    return plans.interpolation_sample(n, w["l"], seed)
 
 
 def make_run(w: dict, x, plan):
@@ -240,6 +222,29 @@ def make_run(w: dict, x, plan):
     if w["algo"] == "fast":
         return FastRun(x, plan, w["r"])
     return InterpolationRun(x, plan, w["r"])
+
+
+class ShardedRun:
+    """bench adapter for the distributed classes (N > 1)."""
+
+    def __init__(self, w, x_local, n, plan, comm, x_landmarks=None):
+        from paper_2007_11919_b200 import distributed as dd
+        be = dd.GpuBackend(x_local.device)
+        if w["algo"] == "divide":
+            self.impl = dd.ShardedDivide(be, x_local, plan, w["r"], comm)
+        elif w["algo"] == "fast":
+            self.impl = dd.ShardedFast(be, x_local, plan, w["r"], comm)
+        else:
+            self.impl = dd.ShardedInterpolation(be, x_local, n, plan, w["r"], comm, x_landmarks)
+        self.res = None
+
+    def launch(self):
+        self.res = self.impl.launch()
+
+    def finish(self, return_device=True):
+        from paper_2007_11919_b200 import MdsConfiguration
+        r = self.res.finish()
+        return MdsConfiguration(r.out, r.estimates, r.gof_g1, r.gof_g2)
 
 
 # ------------------------------------------------------------------ work models
@@ -254,24 +259,30 @@ def piece_sizes(w: dict, plan) -> list:
 
 def fused_points(w: dict) -> bool:
     """The piece pipeline computes points inside the Lanczos kernel (mdsx_api.cu
-    run_classical): form-0 pieces with k <= 104, r <= 10, aligned rows."""
+    run_classical): D&C / fast, every piece form 0 with k <= 104, r <= 10,
+    aligned rows."""
     return (w["algo"] in ("divide", "fast") and w["p"] <= 104 and w["r"] <= 10
             and not os.environ.get("MDSX_NO_FUSE"))
 
 
-def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
-    """Work of ONE launch of `kernel` in one step (DESIGN.md §3 work models):
-    flops for compute-bound kernels (fp64), bytes for streaming ones."""
+def kernel_work(w: dict, n: int, plan, kernel: str, krylov_dims=None, executed=0.0) -> dict | None:
+    """Algorithmic work of ONE step's launches of `kernel` (DESIGN.md §3 work
+    models): flops for compute-bound kernels (fp64), bytes for streaming ones."""
     p, r = w["p"], w["r"]
     esize = 4 if w["dtype"] == "f32" else 8
     sizes = piece_sizes(w, plan)
-    if kernel in ("gram_dmma_kernel", "gram_piece_kernel", "gram_kernel"):
-        fl = 0.0
-        for m in sizes:
-            if (p < m) == (kernel != "gram_kernel"):
-                k, K = (p, m) if p < m else (m, p)
-                fl += K * k * (k + 1)          # symmetric rank-K update of a k x k Gram
-        return {"bound": "tensor", "flops": fl, "model": "SYRK m*p*(p+1) per piece"}
+    form0 = [m for m in sizes if p < m]
+    form1 = [m for m in sizes if p >= m]
+    if kernel in ("gram_piece_kernel", "gram_tile_async_kernel", "gram_dmma_kernel"):
+        return {"bound": "tensor", "flops": float(sum(m * p * (p + 1) for m in form0)),
+                "model": "SYRK m*p*(p+1) per form-0 piece (p x p Gram of the centred rows)"}
+    if kernel in ("gram_rows_async_kernel", "gram_kernel"):
+        return {"bound": "tensor", "flops": float(sum(m * (m + 1) * p for m in form1)),
+                "model": "SYRK m*(m+1)*p per form-1 piece (m x m Gram of the centred rows)"}
+    if kernel == "bgemm_dmma_kernel" and executed > 0:
+        return {"bound": "tensor", "flops": float(executed),
+                "model": "executed block-Krylov products, 2*M*N*K per task of a piece not yet "
+                         "converged (counted by the launcher)"}
     if kernel == "lanczos_smem_kernel" and krylov_dims is not None:
         fl = 0.0
         for m, steps in zip(sizes, krylov_dims):
@@ -282,95 +293,123 @@ def kernel_work(w: dict, plan, kernel: str, krylov_dims=None) -> dict | None:
         krylov_model = ("sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
                         "+ 6k (three-term part)")
         if fused_points(w):
-            # the piece pipeline's Lanczos kernel also streams every piece's rows
-            # for its points (points_stream.cuh): its algorithmic traffic
             tot = sum(sizes)
             by = tot * p * esize + tot * r * 8 + sum(min(m, p) ** 2 * 8 for m in sizes)
-            return {"bound": "hbm", "bytes": by, "flops": fl,
-                    "model": "rows*p*sizeof(in) (points stream) + rows*r*8 (points) + k^2*8 "
-                             "per piece (Gram read); Krylov phase: " + krylov_model}
+            return {"bound": "hbm", "bytes": float(by), "flops": fl,
+                    "limiter": "latency (dependent Krylov steps, per-step barriers)",
+                    "model": "rows*p*sizeof(in) (points epilogue streams every piece's rows) + "
+                             "rows*r*8 (points) + k^2*8 per piece (Gram read); Krylov phase: "
+                             + krylov_model}
         return {"bound": "tensor", "flops": fl, "model": krylov_model}
-    if kernel in ("gower_affine_kernel", "gower_stream_kernel", "gower_bulk_kernel"):
-        n = w["n"]
-        return {"bound": "hbm", "bytes": n * p * esize + n * r * 8,
-                "model": "n*p*sizeof(in) + n*r*8"}
+    if kernel in ("gower_affine_kernel", "gower_bulk_kernel"):
+        return {"bound": "hbm", "bytes": float(n * p * esize + n * r * 8),
+                "model": "n*p*sizeof(in) + n*r*8 (one read of every row, one write)"}
     if kernel == "subtract_mean_kernel":
-        n = w["n"]
-        return {"bound": "hbm", "bytes": 2 * n * r * 8, "model": "read + write of the n x r output"}
-    if kernel in ("points_kernel", "points_rows_kernel", "points_piece_kernel"):
+        return {"bound": "hbm", "bytes": float(2 * n * r * 8),
+                "model": "read + write of the n x r output"}
+    if kernel in ("points_kernel", "points_piece_kernel"):
+        if fused_points(w):
+            return None          # only the pieces the Lanczos epilogue left pending
         tot = sum(sizes)
-        return {"bound": "hbm", "bytes": tot * p * esize + tot * r * 8,
+        return {"bound": "hbm", "bytes": float(tot * p * esize + tot * r * 8),
                 "model": "rows*p*sizeof(in) + rows*r*8"}
+    if kernel == "dc_stitch_kernel":
+        tot = sum(sizes)
+        return {"bound": "hbm", "bytes": float(tot * r * 8 + n * r * 8 + n * 8),
+                "model": "read piece points + write n x r + read row indices"}
     return None
 
 
+def step_bytes(w: dict, n: int) -> float:
+    """One-pass algorithmic traffic of a whole step: every input row read once,
+    the n x r configuration written once, one int64 plan index per row."""
+    esize = 4 if w["dtype"] == "f32" else 8
+    idx = 0 if w["algo"] == "interpolate" else 8
+    return float(n * (w["p"] * esize + w["r"] * 8 + idx))
+
+
 # ------------------------------------------------------------------ CPU oracle sample
-def oracle_sample(w: dict, x_host: np.ndarray, budget_s: float, cores: int):
-    """Time the oracle (oracle/mds_oracle.py, the reference's numpy path) on a
-    bounded prefix of the workload's rows with the same p, l, c/s, r, using a
-    pool of `cores` threads and single-threaded BLAS (the reference's tuned
-    setting).  Returns (points/s, sample description)."""
-    from threadpoolctl import threadpool_limits
-
-    from oracle import mds_oracle as orc
-
-    algo = w["algo"]
-    kw = dict(l=w["l"])
-    if algo == "divide":
-        kw["c"] = w["c"]
-    if algo == "fast":
-        kw["s"] = w["s"]
-    if algo == "fast":
-        n_s = min(w["n"], (w["l"] // w["s"]) * 400)   # one level-1 subtree: 50 leaves + alignment
-    elif algo == "divide":
-        n_s = min(w["n"], max(4 * w["l"], 8 * cores * (w["l"] - w["c"])))
-    else:
-        n_s = min(w["n"], max(4 * w["l"], 100_000))
-    with threadpool_limits(1):
-        t0 = time.perf_counter()
-        orc.run(algo, x_host[:n_s], w["r"], seed=0, threads=cores, **kw)
-        dt = time.perf_counter() - t0
-        if dt < budget_s * 0.5 and n_s < w["n"] and algo != "fast":
-            n_s = int(min(w["n"], n_s * max(1.0, budget_s / max(dt, 1e-3))))
-            t0 = time.perf_counter()
-            orc.run(algo, x_host[:n_s], w["r"], seed=0, threads=cores, **kw)
-            dt = time.perf_counter() - t0
-    desc = (f"oracle {algo} on the first {n_s} rows (same p,l,c/s,r; seed 0), "
-            f"{cores}-thread pool, BLAS 1 thread")
-    return n_s / dt, desc, n_s
-
-
-def host_copy(x) -> np.ndarray:
-    return x.cpu().numpy()
-
-
-# ------------------------------------------------------------------ arms
-def run_reference(args, w):
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return 0
-    import torch
-    cores = os.cpu_count() or 1
-    if w["data"] == "image":
-        from paper_2007_11919_b200.synthetic import image_like
-        xh = image_like(min(w["n"], 200_000), seed=0)
-    else:
-        from paper_2007_11919_b200.synthetic import scenario
-        nh = min(w["n"], 300_000)
-        xh = scenario(nh, w["p"], w["h"], seed=0)
-        if w["dtype"] == "f32":
-            xh = xh.astype(np.float32)
-    w2 = dict(w, n=xh.shape[0])
-    # size the per-step sample on one calibration run (~6 s per step)
-    rate, desc, n_s = oracle_sample(w2, xh, 6.0, cores)
-    from threadpoolctl import threadpool_limits
-
-    from oracle import mds_oracle as orc
+def oracle_kwargs(w):
     kw = dict(l=w["l"])
     if w["algo"] == "divide":
         kw["c"] = w["c"]
     if w["algo"] == "fast":
         kw["s"] = w["s"]
+    return kw
+
+
+def oracle_sample(w: dict, x_host: np.ndarray, budget_s: float, cores: int, tuned: bool = True):
+    """Time the oracle (oracle/mds_oracle.py, the reference's numpy path) on a
+    bounded prefix of the workload's rows with the same p, l, c/s, r.
+    tuned: a pool of `cores` threads, BLAS 1 thread (the reference's tuned
+    setting); otherwise the reference defaults (threads=None, BLAS default).
+    Returns (points/s, sample description, rows)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import mds_oracle as orc
+
+    algo = w["algo"]
+    kw = oracle_kwargs(w)
+    n = x_host.shape[0]
+    if algo == "fast":
+        n_s = min(n, (w["l"] // w["s"]) * 400)   # one level-1 subtree: 50 leaves + alignment
+    elif algo == "divide":
+        n_s = min(n, max(4 * w["l"], 4 * cores * (w["l"] - w["c"])))
+    else:
+        n_s = min(n, max(4 * w["l"], 100_000))
+    threads = cores if tuned else None
+
+    def once(m):
+        t0 = time.perf_counter()
+        if tuned:
+            with threadpool_limits(1):
+                orc.run(algo, x_host[:m], w["r"], seed=0, threads=threads, **kw)
+        else:
+            orc.run(algo, x_host[:m], w["r"], seed=0, threads=threads, **kw)
+        return time.perf_counter() - t0
+
+    dt = once(n_s)
+    if dt < budget_s * 0.5 and n_s < n and algo != "fast":
+        n_s = int(min(n, n_s * max(1.0, budget_s / max(dt, 1e-3))))
+        dt = once(n_s)
+    setting = (f"{cores}-thread pool, BLAS 1 thread (tuned)" if tuned else
+               "reference defaults: threads=None (pool of min(pieces, cores)), BLAS default threads")
+    desc = f"oracle {algo} on the first {n_s} rows (same p,l,c/s,r; seed 0), {setting}"
+    return n_s / dt, desc, n_s
+
+
+# ------------------------------------------------------------------ arms
+def workload_config(name, w, gpus, n, scaling):
+    cfg = {"workload": f"{name}: {w['algo']} n={n} p={w['p']} {w['dtype']} l={w['l']}"
+                       + (f" c={w['c']}" if w['c'] else "") + (f" s={w['s']}" if w['s'] else "")
+                       + f" r={w['r']}",
+           "algorithm": w["algo"], "n": n, "n_per_gpu": n // gpus if scaling == "strong" else w["n"],
+           "p": w["p"], "l": w["l"], "r": w["r"], "input_dtype": w["dtype"],
+           "parallelism": f"dp{gpus} ({'rows' if w['algo'] == 'interpolate' else 'partitions'} "
+                          f"sharded, {scaling} scaling)",
+           "l2_flush": "inputs larger than L2 (126 MB): no flush",
+           "compute_precision": "fp64 throughout (fp32 inputs widened in-kernel)",
+           "input": ("reference scenario stream (simulation.py:68-80), seed 0"
+                     if w["data"] == "gaussian" else "config-5 image-like stand-in, seed 0")}
+    if w["c"]:
+        cfg["c"] = w["c"]
+    if w["s"]:
+        cfg["s"] = w["s"]
+    return cfg
+
+
+def run_reference(args, w):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    nh = min(w["n"], 200_000 if w["data"] == "image" else 300_000)
+    xh = host_input(w, nh)
+    rate, desc, n_s = oracle_sample(dict(w, n=nh), xh, 6.0, cores)
+    from threadpoolctl import threadpool_limits
+
+    from oracle import mds_oracle as orc
+    kw = oracle_kwargs(w)
     times = []
     with threadpool_limits(1):
         for i in range(args.warmup + args.steps):
@@ -380,33 +419,80 @@ def run_reference(args, w):
                 times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = n_s / t
+    scaling = scaling_mode(args, w)
+    n = w["n"] if scaling == "strong" else w["n"] * args.gpus
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, w, args.gpus),
+        "config": workload_config(args.workload, w, args.gpus, n, scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": desc},
+                         "cpu_model": cpu_model(), "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(name, w, gpus):
-    cfg = {"workload": f"{name}: {w['algo']} n={w['n']} p={w['p']} {w['dtype']} l={w['l']}"
-                       + (f" c={w['c']}" if w['c'] else "") + (f" s={w['s']}" if w['s'] else "")
-                       + f" r={w['r']}",
-           "algorithm": w["algo"], "n_per_gpu": w["n"], "p": w["p"], "l": w["l"], "r": w["r"],
-           "input_dtype": w["dtype"], "parallelism": f"dp{gpus} (rows/partitions sharded)",
-           "l2_flush": "inputs larger than L2 (126 MB)",
-           "compute_precision": "fp64 throughout (fp32 inputs widened in-kernel)"}
-    if w["c"]:
-        cfg["c"] = w["c"]
-    if w["s"]:
-        cfg["s"] = w["s"]
-    return cfg
+def scaling_mode(args, w) -> str:
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong" if w.get("strong") else "weak"
+
+
+def parity_block(name: str, w: dict, points, est, g1, g2) -> dict | None:
+    """Compare this run's result with the fixture made by the reference itself."""
+    import full_configs as fc
+    if name == "interp1":
+        from conftest import golden
+        g = golden("cfg1_interp")
+        P = np.asarray(points, dtype=np.float64)
+        s = np.sign(np.sum(P * g["points"], axis=0))
+        s[s == 0] = 1
+        return {"fixture": "tests/golden/cfg1_interp.npz (reference, full size)",
+                "points_rel_err": float(np.linalg.norm(P * s - g["points"]) /
+                                        np.linalg.norm(g["points"])),
+                "estimates_rel_err": float(np.linalg.norm(np.asarray(est) - g["estimates"]) /
+                                           np.linalg.norm(g["estimates"])),
+                "g1_abs_err": abs(float(g1) - float(g["g1"]))}
+    if name not in fc.FULL:
+        return None
+    rep = fc.compare(name, points, est, g1, g2)
+    rep["tolerance"] = "north star: 1e-6 relative Frobenius after sign fix, eigenvalues 1e-6"
+    return rep
+
+
+def distribute_rows(w, x_host, plan, n, comm, dev):
+    """Rank 0 holds the global host input; every rank receives the rows of its
+    share (distributed.local_rows order) over NCCL.  Returns (x_local device,
+    x_local host copy, landmark rows on rank 0 for interpolation)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_11919_b200 import _device as D
+    from paper_2007_11919_b200 import distributed as dd
+    dt = torch.float32 if w["dtype"] == "f32" else torch.float64
+    p = w["p"]
+    rows_k = [dd.local_rows(w["algo"], plan, n, comm.world, k) for k in range(comm.world)]
+    mine = None
+    if comm.rank == 0:
+        xg = D.from_host(np.ascontiguousarray(x_host), dev)
+        for k in range(comm.world):
+            part = xg.index_select(0, torch.from_numpy(rows_k[k]).to(dev))
+            if k == 0:
+                mine = part
+            else:
+                dist.send(part, dst=k)
+        land = xg.index_select(0, torch.from_numpy(np.asarray(plan)).to(dev)) \
+            if w["algo"] == "interpolate" else None
+        del xg
+    else:
+        mine = torch.empty((len(rows_k[comm.rank]), p), dtype=dt, device=dev)
+        dist.recv(mine, src=0)
+        land = None
+    torch.cuda.synchronize(dev)
+    return mine, mine.cpu().numpy(), land
 
 
 def run_ours(args, w):
@@ -415,205 +501,262 @@ def run_ours(args, w):
 
     ws, rank, local = dist_env()
     force = os.environ.get("MDSX_BENCH_SHARDED") == "1"   # exercise the N>1 path on one GPU
-    if ws > 1 or force:
+    sharded = ws > 1 or force
+    if sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    from paper_2007_11919_b200 import _lib, divide_and_conquer_mds, fast_mds, interpolation_mds
-    from paper_2007_11919_b200 import AlgorithmParams, InterpPlan
+    from paper_2007_11919_b200 import (AlgorithmParams, InterpPlan, divide_and_conquer_mds,
+                                       fast_mds, interpolation_mds)
     from paper_2007_11919_b200 import _device as D
+    from paper_2007_11919_b200 import distributed as dd
 
     peaks = measured_peaks(dev)
-    sharded = ws > 1 or force
+    scaling = scaling_mode(args, w)
+    n = w["n"] if scaling == "strong" else w["n"] * ws
+    t0 = time.perf_counter()
+    plan = make_plan(w, n)
+    planner_ms = (time.perf_counter() - t0) * 1e3
+    x_host = host_input(w, n) if rank == 0 else None
+    comm = dd.Comm(device=dev) if sharded else None
     if sharded:
-        # one global problem of ws x n rows, replicated input, same seed everywhere
-        w = dict(w, n=w["n"] * ws)
-        seed = 0
+        x, x_local_host, land = distribute_rows(w, x_host, plan, n, comm, dev)
+        run = ShardedRun(w, x, n, plan, comm, land)
     else:
-        seed = 0
-    x = make_data(w, dev, seed)
-    plan = make_plan(w, seed)
-    if sharded:
-        run = ShardedRun(w, x, plan, dev)
-    else:
+        x = D.from_host(np.ascontiguousarray(x_host), dev)
         run = make_run(w, x, plan)
     h = D.handle(dev)
-    log(f"[rank {rank}] data {tuple(x.shape)} {x.dtype}; warmup {args.warmup}")
+    log(f"[rank {rank}] n={n} local rows {x.shape[0]} {x.dtype}; planner {planner_ms:.1f} ms; "
+        f"warmup {args.warmup}")
     for _ in range(args.warmup):
         run.launch()
     torch.cuda.synchronize()
     run.finish(return_device=True)          # statuses OK (raises otherwise)
 
     stream = torch.cuda.current_stream(dev)
-    h.timing_report()
-    h.timing(True)
     l0 = h.launches()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     smi_idx = int(vis.split(",")[local]) if vis and vis.split(",")[local].isdigit() else local
     with ClockSampler(smi_idx) as clk:
-        if ws > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
         for _ in range(args.steps):
             run.launch()
-        t1.record(stream)
+        ev1.record(stream)
         torch.cuda.synchronize()
-        if ws > 1:
+        if sharded:
             dist.barrier()
-    h.timing(False)
     launches = h.launches() - l0
-    ms = t0.elapsed_time(t1) / args.steps
-    kernels = h.timing_report()
-    if ws > 1:
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if sharded:
         tm = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         ms = float(tm.item())
     cfg_out = run.finish(return_device=True)
-    value = (w["n"] if sharded else w["n"] * ws) / (ms / 1e3)
+    value = n / (ms / 1e3)
+
+    # per-kernel timing pass (not the measurement): the same steps with every
+    # kernel on ONE stream (MDSX_PIPE_SERIAL), so a launch's event time is its
+    # own duration, not time shared with the other pipeline stream
+    os.environ["MDSX_PIPE_SERIAL"] = "1"
+    h.timing_report()
+    h.timing(True)
+    tsteps = max(1, min(args.steps, 5))
+    for _ in range(tsteps):
+        run.launch()
+    torch.cuda.synchronize()
+    h.timing(False)
+    kernels = h.timing_report(with_work=True)
+    del os.environ["MDSX_PIPE_SERIAL"]
     try:       # Krylov dimension per piece (solver diagnostics in the status records)
         st = D.decode_status(run.status)
         krylov = [float(v) for v in st["value"]]
     except AttributeError:
         krylov = None
 
-    # roofline of the dominant kernel (average launch duration over the timed region)
-    total_k = sum(v[0] for v in kernels.values())
+    roof, per_kernel = None, {}
+    total_k = sum(v[0] for v in kernels.values()) or 1.0
     dom = max(kernels, key=lambda k: kernels[k][0]) if kernels else None
-    roof = None
-    if dom:
-        ms_k, cnt = kernels[dom]
-        per_launch_ms = ms_k / cnt
-        work = kernel_work(w, plan, dom, krylov)
-        launches_per_step = cnt / args.steps
-        if work and work["bound"] == "hbm":
-            ach = work["bytes"] / launches_per_step / (per_launch_ms / 1e3) / 1e9
-            peak = peaks["hbm_gbs"]
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": None, "peak_src": peaks["hbm_src"],
-                    "work_model": work["model"]}
-        elif work:
-            ach = work["flops"] / launches_per_step / (per_launch_ms / 1e3) / 1e12
-            peak = peaks["fp64_tflops"]
-            roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak,
-                    "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-                    "precision": "fp64", "peak_src": peaks["fp64_src"],
-                    "work_model": work["model"]}
-        if roof is not None:
-            roof["share_of_kernel_time"] = ms_k / total_k
-            if w["algo"] in ("divide", "fast"):
-                roof["note"] = ("two-stream piece pipeline: launch durations include time "
-                                "shared with the other stream's kernels")
-            roof["avg_launch_ms"] = per_launch_ms
-            traffic = TRAFFIC.get((args.workload, dom))
-            if traffic:
-                roof["traffic"] = traffic["bytes"]
-                roof["traffic_src"] = traffic["src"]
-    per_kernel = {}
-    for kname, (ms_k, cnt) in kernels.items():
-        wk = kernel_work(w, plan, kname, krylov)
+    ranked = sorted(kernels, key=lambda k: -kernels[k][0])
+    for kname in ranked:
+        ms_k, cnt, executed = kernels[kname]
+        wk = kernel_work(w, n if not sharded else x.shape[0], plan, kname, krylov,
+                         executed / tsteps) if not sharded else None
         if not wk:
             continue
-        t = ms_k / cnt / 1e3
-        lps = cnt / args.steps
+        t = ms_k / tsteps / 1e3                     # seconds per step of this kernel
+        ent = {"ms_per_step": ms_k / tsteps, "launches_per_step": cnt / tsteps,
+               "share_of_kernel_time": ms_k / total_k}
         if wk["bound"] == "hbm":
-            per_kernel[kname] = {"GB/s": wk["bytes"] / lps / t / 1e9,
-                                 "frac_hbm": wk["bytes"] / lps / t / 1e9 / peaks["hbm_gbs"]}
-            if "flops" in wk:
-                per_kernel[kname]["TFLOP/s"] = wk["flops"] / lps / t / 1e12
-                per_kernel[kname]["frac_fp64"] = wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]
-        else:
-            per_kernel[kname] = {"TFLOP/s": wk["flops"] / lps / t / 1e12,
-                                 "frac_fp64": wk["flops"] / lps / t / 1e12 / peaks["fp64_tflops"]}
+            ent["GB/s"] = wk["bytes"] / t / 1e9
+            ent["frac_hbm"] = ent["GB/s"] / peaks["hbm_gbs"]
+        if "flops" in wk:
+            ent["TFLOP/s"] = wk["flops"] / t / 1e12
+            ent["frac_fp64"] = ent["TFLOP/s"] / peaks["fp64_tflops"]
+        per_kernel[kname] = ent
+        if roof is None:
+            if wk["bound"] == "hbm":
+                roof = {"kernel": kname, "bound": "hbm", "achieved": ent["GB/s"],
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ent["frac_hbm"],
+                        "peak_src": peaks["hbm_src"]}
+            else:
+                roof = {"kernel": kname, "bound": "tensor", "achieved": ent["TFLOP/s"],
+                        "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": ent["frac_fp64"],
+                        "precision": "fp64 (DMMA / DFMA share one pipe)",
+                        "peak_src": peaks["fp64_src"]}
+            roof.update(traffic=None, work_model=wk["model"],
+                        avg_launch_ms=ms_k / cnt, launches_per_step=cnt / tsteps,
+                        share_of_kernel_time=ms_k / total_k,
+                        timing="serialised pass (MDSX_PIPE_SERIAL: all chunks on one stream), "
+                               "CUDA events on the launching stream")
+            if "limiter" in wk:
+                roof["limiter"] = wk["limiter"]
+            if kname != dom:
+                roof["note"] = f"dominant kernel {dom} has no work model; largest modelled kernel"
+            traffic = TRAFFIC.get((args.workload, kname))
+            if traffic:
+                roof["traffic"] = traffic["bytes"] / (cnt / tsteps)
+                roof["traffic_src"] = traffic["src"]
+    for ent in per_kernel.values():
+        for key in ("frac_hbm", "frac_fp64"):
+            if ent.get(key, 0) > 1.2:
+                ent["suspect"] = f"{key} above 1.2: work model overstates this kernel"
+    step_roof = {"bytes_per_step": step_bytes(w, n if not sharded else x.shape[0]),
+                 "model": "one read of every input row + one write of n x r + one int64 plan "
+                          "index per row (D&C / fast)"}
+    step_roof["achieved_GBs"] = step_roof["bytes_per_step"] / (ms / 1e3) / 1e9
+    step_roof["frac_hbm"] = step_roof["achieved_GBs"] / peaks["hbm_gbs"]
 
-    # e2e through the public API from pinned host memory
-    if sharded:                 # per-rank kernel times cover 1/ws of the plan: no roofline
-        roof, per_kernel = None, {}
+    # ---- e2e through the public API (pageable numpy input, what users pass)
     e2e = None
-    if not args.no_e2e and sharded:
-        # public distributed API from pinned host memory: H2D of the (replicated)
-        # input on every rank, the sharded run, and the gather of n x r to rank 0
-        host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-        host.copy_(x)
+    params = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=0)
+    parity = None
+    if not args.no_e2e and not sharded:
+        del run
+        torch.cuda.empty_cache()
+        fn = {"divide": divide_and_conquer_mds, "fast": fast_mds,
+              "interpolate": interpolation_mds}[w["algo"]]
+        kw = dict(plan=plan if w["algo"] != "interpolate" else InterpPlan([plan], n, w["l"], 0),
+                  device=dev)
+        k_e2e = max(1, min(args.steps, 5))
+        res = None
+        for _ in range(2):        # steady state: one result alive while the next call runs
+            res = fn(x_host, params, **kw)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(k_e2e):
+            res = fn(x_host, params, **kw)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t) / k_e2e
+        n_idx = len(plan) if w["algo"] == "interpolate" else (
+            sum(len(q) for q in plan.subsets) if w["algo"] == "divide" else 2 * n)
+        e2e = {"value": n / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": int(x_host.nbytes + 8 * n_idx),
+               "d2h_bytes_per_step": int(n * w["r"] * 8), "steps": k_e2e,
+               "path": f"paper_2007_11919_b200.{fn.__name__}(numpy array (pageable), plan=...)"}
+        parity = parity_block(args.workload, w, res.points, res.eigenvalue_estimates,
+                              res.gof_g1, res.gof_g2)
+    elif not args.no_e2e and sharded:
+        # per rank: its own rows from pageable host memory -> device, the
+        # sharded step, the gather of n x r to rank 0 and its D2H
+        from paper_2007_11919_b200.distributed import gather_points
         k_e2e = max(1, min(args.steps, 3))
-        from paper_2007_11919_b200 import distributed as dd
         dist.barrier()
         torch.cuda.synchronize()
         t = time.perf_counter()
         for _ in range(k_e2e):
-            x.copy_(host, non_blocking=True)
-            run.launch()
-            dd.gather_points(run.res, w["n"], w["r"], run.comm)
+            xd = D.from_host(x_local_host, dev)
+            if w["algo"] == "interpolate":
+                land = D.from_host(np.ascontiguousarray(x_host[plan]), dev) if rank == 0 else None
+                run2 = ShardedRun(w, xd, n, plan, comm, land)
+            else:
+                run2 = ShardedRun(w, xd, n, plan, comm)
+            run2.launch()
+            pts = gather_points(run2.res, n, comm)
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t) / k_e2e
         tm = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         e2e_s = float(tm.item())
-        e2e = {"value": w["n"] / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
-               "h2d_bytes_per_step": int(x.numel() * x.element_size() * ws),
-               "d2h_bytes_per_step": int(w["n"] * w["r"] * 8), "steps": k_e2e,
-               "path": "paper_2007_11919_b200.distributed (pinned host input on every rank, "
-                       "gather to rank 0)"}
-    if not args.no_e2e and not sharded:
-        host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-        host.copy_(x)
-        del run
-        torch.cuda.empty_cache()
-        prm = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=seed)
-        fn = {"divide": divide_and_conquer_mds, "fast": fast_mds,
-              "interpolate": interpolation_mds}[w["algo"]]
-        kw = dict(plan=plan if w["algo"] != "interpolate" else InterpPlan([plan], w["n"], w["l"], seed),
-                  device=dev)
-        k_e2e = max(1, min(args.steps, 5))
-        res = None
-        for _ in range(2):        # steady state: one result alive while the next call runs
-            res = fn(host, prm, **kw)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        t = time.perf_counter()
-        for _ in range(k_e2e):
-            res = fn(host, prm, **kw)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t) / k_e2e
-        if ws > 1:
-            tm = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            e2e_s = float(tm.item())
-        n_idx = len(plan) if w["algo"] == "interpolate" else (
-            sum(len(q) for q in plan.subsets) if w["algo"] == "divide" else 2 * w["n"])
-        e2e = {"value": w["n"] * ws / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
-               "h2d_bytes_per_step": int(x.numel() * x.element_size() + 8 * n_idx),
-               "d2h_bytes_per_step": int(w["n"] * w["r"] * 8), "steps": k_e2e,
-               "path": f"paper_2007_11919_b200.{fn.__name__}(pinned host tensor, plan=...)"}
-        del host
+        hb = torch.tensor([x_local_host.nbytes], device=dev, dtype=torch.float64)
+        dist.all_reduce(hb)
+        e2e = {"value": n / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": int(hb.item()), "d2h_bytes_per_step": int(n * w["r"] * 8),
+               "steps": k_e2e,
+               "path": "paper_2007_11919_b200.distributed (each rank H2Ds its own rows from "
+                       "pageable host memory; NCCL gather of n x r to rank 0, D2H there)"}
+        if rank == 0 and ws == 1:
+            parity = parity_block(args.workload, w, pts, run2.res.estimates,
+                                  run2.res.gof_g1, run2.res.gof_g2)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        xh = host_copy(x[:min(w["n"], 300_000)])
-        rate, desc, _ = oracle_sample(dict(w, n=xh.shape[0]), xh, 8.0, os.cpu_count() or 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": desc}
+        cores = os.cpu_count() or 1
+        nh = min(n, 300_000)
+        xs = x_host[:nh]
+        rate, desc, _ = oracle_sample(dict(w, n=nh), xs, 8.0, cores, tuned=True)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+               "cpu_model": cpu_model()}
+        if not args.no_cpu_default:
+            rate_d, desc_d, _ = oracle_sample(dict(w, n=nh), xs, 8.0, cores, tuned=False)
+            cpu["reference_defaults"] = {"value": rate_d, "unit": UNIT, "sample": desc_d}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.workload, w, ws),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "gpu_launches": launches,
-            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(kernels.items())},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.workload, w, ws, n, scaling),
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "parity": parity, "clocks": clk.summary(), "gpu_launches": launches,
+            "planner_ms": planner_ms,
+            "host": {"cpu_model": cpu_model(), "cores": os.cpu_count()},
             "kernel_rooflines": per_kernel,
+            "kernels_ms_per_step_serialised": {k: v[0] / tsteps for k, v in sorted(kernels.items())},
             "peaks": peaks,
-            "fit": {"g1": cfg_out.gof_g1, "estimates": [float(v) for v in cfg_out.eigenvalue_estimates]},
+            "fit": {"g1": cfg_out.gof_g1,
+                    "estimates": [float(v) for v in cfg_out.eigenvalue_estimates]},
         }
         print(json.dumps(line), flush=True)
-    if ws > 1 or force:
+    if sharded:
         dist.destroy_process_group()
     return 0
+
+
+def check_launch(args):
+    """--check-launch: the self-launch plumbing only (rendezvous + one
+    collective); gloo on CPU, NCCL when every rank has a GPU."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= ws
+    dist.init_process_group("nccl" if use_nccl else "gloo")
+    dev = torch.device("cuda", local) if use_nccl else torch.device("cpu")
+    t = torch.tensor([rank], dtype=torch.int64, device=dev)
+    out = [torch.empty_like(t) for _ in range(ws)]
+    dist.all_gather(out, t)
+    if rank == 0:
+        print(json.dumps({"check": "launch", "n_gpus": ws, "ranks_seen": [int(v) for v in out],
+                          "backend": dist.get_backend()}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without torchrun: start N ranks with torch's launcher."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    log(f"self-launch: {' '.join(cmd)}")
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -623,13 +766,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="dc2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-default", action="store_true",
+                    help="skip the reference-defaults CPU sample (oversubscribed BLAS)")
+    ap.add_argument("--check-launch", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
     w = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not (
+            args.impl == "reference"):
+        return self_launch(args)
+    if args.check_launch:
+        return check_launch(args)
     if args.impl == "reference":
         return run_reference(args, w)
     return run_ours(args, w)

@@ -17,6 +17,8 @@
  *   mdsx_sqdist_self        <- euclidean_distance_matrix (linalg.py:61-82)
  *   mdsx_sqdist_cross       <- cross_squared_distances (linalg.py:85-104)
  *   mdsx_double_center      <- double_center (linalg.py:107-121)
+ *   mdsx_sym_eigvals        <- the full spectrum of symmetric_eigen / eigvalsh
+ *                              (linalg.py:149-169) used by classical_mds
  *   mdsx_gower_context      <- gower_context (algorithms.py:193-217)
  *   mdsx_gower_interpolate  <- gower_interpolate (algorithms.py:220-242)
  *   mdsx_procrustes_fit     <- fit_procrustes (procrustes.py:53-78), batched
@@ -113,6 +115,13 @@ int mdsx_classical_pieces(mdsx_handle* h, const void* data, int dtype, int64_t l
                           int32_t npieces, int32_t r, double* points, double* estimates,
                           double* gof, mdsx_piece_status* status, void* stream);
 
+/* Every eigenvalue (ascending, n doubles into w) of the symmetric n x n
+ * device matrix a (row-major, full storage; a is not modified): Householder
+ * tridiagonalisation + bisection.  Replaces the full-spectrum eigvalsh /
+ * dsyevd that classical_mds needs for G1/G2 and the DegenerateRank rule
+ * (classical.py:88-150, linalg.py:149-169) beyond the in-kernel Jacobi size. */
+int mdsx_sym_eigvals(mdsx_handle* h, const double* a, int64_t n, double* w, void* stream);
+
 /* Validity flags of a squared-distance matrix (linalg.py:41-58), OR-ed into
  * *flags (device int32, caller-zeroed): 1 non-finite, 2 asymmetric,
  * 4 nonzero diagonal, 8 negative entries (tolerance 1e-9 max(|d|max, 1)). */
@@ -135,9 +144,14 @@ int mdsx_gower_context(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
                        int32_t r, double* ctx, double* cond, int32_t* flag, void* stream);
 /* out (m x r, ldo) = Gower coordinates of rows data[0..m) in the base frame;
  * *nonfinite (device int32, caller-zeroed) is set if an input is not finite. */
+/* flags: MDSX_GOWER_CENTRED = the context's base configuration has zero
+ * column means (true for interpolation_mds's landmark MDS): v ~ 0, so the
+ * squared norms of fp32 rows may be formed on the fp32 pipe. */
+#define MDSX_GOWER_CENTRED 1
 int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
                            const void* rows, int dtype, int64_t ld, int64_t m,
-                           double* out, int64_t ldo, int32_t* nonfinite, void* stream);
+                           double* out, int64_t ldo, int32_t* nonfinite, int32_t flags,
+                           void* stream);
 
 /* ---- Procrustes ----------------------------------------------------------- */
 /* Job j aligns src rows src_rows[job_off[j]..job_off[j+1]) of src (ld = r)

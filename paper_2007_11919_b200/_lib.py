@@ -40,6 +40,7 @@ SIGNATURES = {
     "mdsx_sqdist_self": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _vp]),
     "mdsx_sqdist_cross": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _int, _i32, _vp, _i64, _vp]),
     "mdsx_double_center": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "mdsx_sym_eigvals": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "mdsx_delta_check": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "mdsx_classical_pieces": (_int, [_vp, _vp, _int, _i64, _i32, _vp, _vp, _i32, _i32,
                                      _vp, _vp, _vp, _vp, _vp]),
@@ -48,7 +49,7 @@ SIGNATURES = {
     "mdsx_gower_context": (_int, [_vp, _vp, _int, _i64, _i32, _vp, _i64, _vp, _i32, _vp, _vp,
                                   _vp, _vp]),
     "mdsx_gower_interpolate": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _int, _i64, _i64, _vp,
-                                      _i64, _vp, _vp]),
+                                      _i64, _vp, _i32, _vp]),
     "mdsx_procrustes_fit": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
                                    _vp, _vp]),
     "mdsx_procrustes_apply": (_int, [_vp, _vp, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
@@ -125,15 +126,16 @@ class Handle:
     def timing(self, on: bool) -> None:
         self.lib.mdsx_timing_enable(self.ptr, 1 if on else 0)
 
-    def timing_report(self) -> dict:
-        """{kernel: (total_ms, launches)} since the last report."""
+    def timing_report(self, with_work: bool = False) -> dict:
+        """{kernel: (total_ms, launches)} since the last report; with_work:
+        (total_ms, launches, executed flops credited by the launcher or 0)."""
         n = int(self.lib.mdsx_timing_report(self.ptr, None, 0))
         buf = C.create_string_buffer(n + 1)
         self.lib.mdsx_timing_report(self.ptr, buf, n + 1)
         out = {}
         for line in buf.value.decode().splitlines():
-            name, ms, cnt = line.split()
-            out[name] = (float(ms), int(cnt))
+            name, ms, cnt, work = line.split()
+            out[name] = (float(ms), int(cnt), float(work)) if with_work else (float(ms), int(cnt))
         return out
 
     def call(self, name: str, *args) -> None:

@@ -184,6 +184,8 @@ namespace mdsx {
 GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
                        const std::vector<GemmTask>& batch) {
   GemmBatch b{(int64_t)items.size(), 0, 0};
+  b.task_off = (int64_t)tasks.size();
+  b.ntasks = (int64_t)batch.size();
   if (batch.empty()) return b;
   b.narrow = batch[0].N <= 16 ? 1 : 0;
   if (b.narrow) {

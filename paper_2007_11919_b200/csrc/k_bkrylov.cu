@@ -429,6 +429,25 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
   bk_init_kernel<<<n, KT, 0, st>>>(dbd);
   if ((rc = launched(h, "bk_init_kernel", st))) return rc;
   std::vector<int> hdone(n, 0);
+  // executed block-product flops (pieces converged in an earlier cycle skip
+  // their tasks; re-projection tasks keyed on the device-only flags are not
+  // credited) -> the kernel's work column of mdsx_timing_report
+  double* work = nullptr;
+  for (auto& w : h->work)
+    if (w.first == "bgemm_dmma_kernel") work = &w.second;
+  if (!work) {
+    h->work.push_back({"bgemm_dmma_kernel", 0.0});
+    work = &h->work.back().second;
+  }
+  auto launch_bgemm = [&](mdsx_handle* hh, const GemmTask* dt, const int4* di, const GemmBatch& g,
+                          cudaStream_t s2) {
+    for (int64_t i = g.task_off; i < g.task_off + g.ntasks; ++i) {
+      const GemmTask& t = tasks[i];
+      const int64_t q = t.skip - done;
+      if (q >= 0 && q < n && !hdone[q]) *work += 2.0 * t.M * t.N * t.K;
+    }
+    return mdsx::launch_bgemm(hh, dt, di, g, s2);
+  };
   for (int cyc = 0; cyc < MAX_CYCLES; ++cyc) {
     mdsx::pre(h, st);
     bk_orth_kernel<<<n, KT, 0, st>>>(dbd, done, 0, noamp, 0);

@@ -85,6 +85,9 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
 // last error message of the calling thread (calls from several threads on one
 // handle each read their own message)
 static thread_local std::string t_last_error;
+size_t eigvals_ws_doubles(int64_t n);
+int launch_sym_eigvals(mdsx_handle* h, const double* A, int64_t n, double* w, double* ws,
+                       cudaStream_t st);
 
 int fail(mdsx_handle* h, int code, const std::string& msg) {
   (void)h;
@@ -368,6 +371,7 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     const bool simple = piece_gram && cp.pd_jac.empty() && cp.pd_big.empty() && cp.pd_f1.empty() &&
                         (int)cp.pd_g.size() == np && (int)cp.pd_sub.size() == np;
     int nc = pc ? atoi(pc) : 2;                       // measured best on dc2 / fast3
+    const bool serial = getenv("MDSX_PIPE_SERIAL") != nullptr;
     nc = std::min(nc, np / (2 * h->num_sms));          // >= two waves of pieces per chunk
     // fused points epilogue in the Lanczos kernel (aligned rows, r <= 10): each
     // CTA streams its piece's rows right after its eigenvectors, next to the
@@ -392,7 +396,9 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
       for (int c = 0; c < nc; ++c) {
         const int j0 = (int)((int64_t)np * c / nc), j1 = (int)((int64_t)np * (c + 1) / nc);
         const int n = j1 - j0;
-        cudaStream_t s = (c & 1) ? h->aux : st;
+        // MDSX_PIPE_SERIAL: every chunk on the caller's stream (same kernels and
+        // chunks, no overlap) -- bench.py's per-kernel timing pass
+        cudaStream_t s = (c & 1) && !serial ? h->aux : st;
         if ((rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd + j0, n, A, mu, status, s)))
           return rc;
         if ((rc = launch_lanczos_smem(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
@@ -518,13 +524,21 @@ int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap) {
   }
   h->timed.clear();
   std::string out;
-  for (auto& a : h->report)
-    out += a.first + " " + std::to_string(a.second.first) + " " + std::to_string(a.second.second) + "\n";
+  for (auto& a : h->report) {
+    double w = 0.0;
+    for (auto& x : h->work)
+      if (x.first == a.first) w = x.second;
+    char wb[64];
+    snprintf(wb, sizeof wb, "%.17g", w);
+    out += a.first + " " + std::to_string(a.second.first) + " " + std::to_string(a.second.second) +
+           " " + wb + "\n";
+  }
   if (buf && cap > 0) {  // a call with a buffer consumes the totals
     const size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
     std::memcpy(buf, out.data(), n);
     buf[n] = 0;
     h->report.clear();
+    h->work.clear();
   }
   return (int64_t)out.size();
 }
@@ -624,6 +638,19 @@ int mdsx_classical_delta(mdsx_handle* h, const double* delta, int64_t m, int32_t
                        cand, st);
 }
 
+int mdsx_sym_eigvals(mdsx_handle* h, const double* a, int64_t n, double* w, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if (n < 1) return fail(h, MDSX_SHAPE, "matrix must be non-empty");
+  if (n > 20000) return fail(h, MDSX_PARAM, "n exceeds the exact-size guard (20000)");
+  const size_t nd = eigvals_ws_doubles(n);
+  int rc = ws_reserve(h, align_up(nd * sizeof(double)) + 256);
+  if (rc) return rc;
+  double* ws = (double*)ws_alloc(h, nd * sizeof(double), st);
+  if (!ws) return MDSX_CUDA;
+  return launch_sym_eigvals(h, a, n, w, ws, st);
+}
+
 int mdsx_delta_check(mdsx_handle* h, const double* delta, int64_t m, int32_t* flags, void* stream) {
   cudaStream_t st = as_stream(stream);
   MDSX_GUARD(h, st);
@@ -656,7 +683,7 @@ int mdsx_gower_context(mdsx_handle* h, const void* data, int dtype, int64_t ld, 
 
 int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
                            const void* rows, int dtype, int64_t ld, int64_t m, double* out,
-                           int64_t ldo, int32_t* nonfinite, void* stream) {
+                           int64_t ldo, int32_t* nonfinite, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
   MDSX_GUARD(h, st);
   int32_t* nf = nonfinite;
@@ -664,6 +691,23 @@ int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t
   const double* M = mean + p;
   const double* v = M + (int64_t)p * r;
   (void)l;
+  if (m < 1) return MDSX_OK;
+  // dense aligned rows, packed output: the bulk-copy streaming kernel (its
+  // per-CTA column sums go to scratch); otherwise the per-row kernel
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  if (ld == p && ldo == r && r <= 16 && ((size_t)p * es) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(rows) & 15) == 0 &&
+      h->num_sms * r * sizeof(double) <= recenter_ws_bytes(r)) {
+    int rc = ws_reserve(h, recenter_ws_bytes(r) + 256);
+    if (rc) return rc;
+    double* part = (double*)ws_alloc(h, recenter_ws_bytes(r), st);
+    int nparts = 0;
+    const bool n32 = dtype == MDSX_F32 && (flags & MDSX_GOWER_CENTRED) && !getenv("MDSX_GOWER_NORM64");
+    if ((rc = launch_gower_bulk(h, rows, dtype, m, p, r, mean, M, v, out, part, nf, &nparts, st,
+                                n32)))
+      return rc;
+    if (nparts > 0) return MDSX_OK;
+  }
   return launch_gower_affine(h, rows, dtype, ld, m, p, r, mean, M, v, out, ldo, nf, st);
 }
 

@@ -32,6 +32,10 @@ struct mdsx_handle {
   std::vector<cudaEvent_t> event_pool;
   std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> timed;
   std::vector<std::pair<std::string, std::pair<double, int64_t>>> report;
+  // executed work credited to a kernel by its launcher (flops), reported
+  // as the 4th column of mdsx_timing_report; only kernels whose work depends
+  // on run-time iteration counts (block-Krylov products) record it
+  std::vector<std::pair<std::string, double>> work;
   // second stream for the piece pipeline (run_classical), created on first use
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -165,6 +169,7 @@ struct GemmTask {
 struct GemmBatch {
   int64_t item_off, nitems;
   int narrow;
+  int64_t task_off = 0, ntasks = 0;   // host bookkeeping (work accounting)
 };
 
 // Host launchers implemented in the kernel translation units.

@@ -1,46 +1,56 @@
 """Multi-GPU sharding of the partition algorithms.
 
-One process per GPU (``torchrun``), ``torch.distributed`` for the plumbing
-(NCCL on GPUs; gloo in the CPU tests).  Every rank holds the input (replicated
-once, outside any timed region) and the plan (drawn bit-exactly on every rank
-from the same seed), so the only exchanges are small:
+One process per GPU (``torchrun`` / ``bench.py --gpus N``), ``torch.distributed``
+for the plumbing: NCCL on GPUs (gloo with CPU tensors in the tests).  Every
+rank draws the plan bit-exactly from the seed; each rank holds ONLY the input
+rows its share needs (``*_shard(...).local_rows``, in that order), so the
+host->device traffic of N ranks adds up to about one copy of the input.
 
-* divide-and-conquer: every rank solves the anchor piece (subset 1) itself and
-  its contiguous share of subsets 2..p, aligns them locally (the anchor is
-  known everywhere — no broadcast needed), and writes their rows of the n x r
-  output.  Per-subset column sums of the owned rows and per-subset fit figures
-  are all-gathered and combined in plan order, so the re-centring shift and
-  G1/G2/estimates are identical on every rank and independent of the number
-  of ranks.
-* fast: the root's level-1 subtrees are dealt to ranks (contiguous blocks);
-  every rank solves its subtrees completely (leaves, alignment sets, internal
-  alignments) and the root's alignment set (samples of ALL children, raw
-  rows — computed redundantly, no broadcast needed), aligns its children onto
-  their slices of it, and writes their rows.  Per-child column sums and fit
-  figures are all-gathered and combined in child order (the reference's
-  recursion, algorithms.py:314-320).
-* interpolation: rank 0 computes the landmark MDS and Gower context and
-  broadcasts it (the north star's "computed once and broadcast"); each rank
-  streams a contiguous block of rows; per-block column sums are all-gathered
-  (fixed 65 536-row blocks, plan order) for the re-centring.
+The step stays on the device: per-rank kernels, then one all-gather of small
+fixed-size record tensors (per-piece fit figures, statuses and per-segment
+column sums), a plan-order sort and fold of those records for the final
+re-centring, and one shift pass.  Nothing is read on the host until
+``finish()``, which decodes the gathered records identically on every rank
+(so every rank raises the same exception for a failing piece — no rank can
+be left waiting in a collective), and ``gather_points`` assembles the n x r
+configuration on rank 0 with one NCCL gather.
 
-The per-rank compute is behind a small backend interface: ``GpuBackend``
-(libmdsx kernels, the product) and, for the CPU tests only, an oracle-backed
-backend in ``tests/``.  ``gather_points`` assembles the full n x r result on
-rank 0 (outside the timed region in bench.py).
+* divide-and-conquer (algorithms.py:128-172): every rank solves the anchor
+  (subset 1) and its contiguous share of subsets 2..p and aligns them locally
+  (the anchor is known everywhere, so nothing is broadcast).
+* fast (algorithms.py:285-348): the root's level-1 subtrees are dealt to ranks
+  in contiguous blocks; every rank also solves the root's alignment set (raw
+  rows of every child's samples — computed redundantly) and aligns its
+  children onto their slices of it.
+* interpolation (algorithms.py:245-274): rank 0 solves the landmark set and
+  the Gower context and broadcasts them as one device vector; every rank
+  streams a contiguous block of rows (fixed 65 536-row blocks).
+
+The re-centring mean is a fold of per-segment sums in plan order (subsets,
+level-1 children, row blocks), and every segment is summed by one rank, so
+results are bitwise identical for every world size.  The per-rank compute is
+behind a small backend interface: ``GpuBackend`` (libmdsx kernels, the
+product); the CPU tests drive the same code with an oracle-backed backend in
+``tests/``.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
+from .errors import InvalidInputError, NumericalError
 from .params import AlgorithmParams
 from .plans import (DcPlan, FastPlan, flatten_fast_shard, flatten_subsets, interpolation_sample,
                     plan_divide_conquer, plan_fast)
+from .results import MdsConfiguration
 
 SUM_BLOCK = 65536      # canonical row block of the interpolation re-centring sums
+_SENTINEL = 2.0 ** 62  # record id of padding rows (sorts after every real id)
+_STATUS = np.dtype([("code", np.int32), ("index", np.int32), ("value", np.float64)])
 
 
 def shard(count: int, world: int, rank: int) -> tuple[int, int]:
@@ -50,552 +60,608 @@ def shard(count: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-class ShardResult:
-    """One rank's share of a sharded run.  `rows` (global row indices, input
-    order) and `local` (their positions in `out`) may be given as arrays or
-    as (lo, hi) ranges, materialised only when asked for (gather time)."""
-
-    def __init__(self, rows, out, local, estimates, gof_g1, gof_g2, backend=None):
-        self._rows, self._local = rows, local
-        self.out = out
-        self.estimates = estimates
-        self.gof_g1, self.gof_g2 = gof_g1, gof_g2
-        self.backend = backend
-
-    @staticmethod
-    def _arr(v):
-        if isinstance(v, tuple):
-            return np.arange(v[0], v[1], dtype=np.int64)
-        return v() if callable(v) else v
-
-    @property
-    def rows(self) -> np.ndarray:
-        return self._arr(self._rows)
-
-    @property
-    def local(self) -> np.ndarray:
-        return self._arr(self._local)
-
-    def points(self) -> np.ndarray:
-        """(len(rows), r) float64 on the host."""
-        if isinstance(self._local, tuple) and self._local[0] == 0 and \
-                self._local[1] == self.out.shape[0]:
-            return self.backend.take_all(self.out)
-        return self.backend.take(self.out, self.local)
+def decode_status(t) -> np.ndarray:
+    """(k, 2) float64 status records (16-byte mdsx_piece_status) -> structured."""
+    raw = np.ascontiguousarray(t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else t,
+                               dtype=np.float64)
+    return raw.view(np.uint8).reshape(-1, 16).copy().view(_STATUS).reshape(-1)
 
 
+# ------------------------------------------------------------------ collectives
 class Comm:
-    """Collectives used by the sharded algorithms (a torch.distributed group)."""
+    """Tensor collectives over a torch.distributed group (device tensors with
+    NCCL, CPU tensors with gloo)."""
 
     def __init__(self, group=None, device=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = device if device is not None else torch.device("cpu")
+        self.nccl = dist.get_backend(group) == "nccl"
 
-    def allgather(self, arr: np.ndarray) -> list:
-        """All-gather equally shaped float64 arrays -> list in rank order."""
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
-        return [o.cpu().numpy() for o in out]
-
-    def allgather_ragged(self, arr: np.ndarray) -> list:
-        """All-gather float64 arrays of different leading sizes (padded)."""
-        arr = np.ascontiguousarray(arr, dtype=np.float64)
-        n = np.array([arr.shape[0]], dtype=np.float64)
-        sizes = [int(s[0]) for s in self.allgather(n)]
-        width = int(np.prod(arr.shape[1:])) if arr.ndim > 1 else 1
-        pad = np.zeros((max(sizes), width))
-        pad[:arr.shape[0]] = arr.reshape(arr.shape[0], width)
-        parts = self.allgather(pad)
-        return [p[:s].reshape((s,) + arr.shape[1:]) for p, s in zip(parts, sizes)]
-
-    def broadcast(self, arr: np.ndarray, src: int = 0) -> np.ndarray:
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.device)
-        dist.broadcast(t, src=src, group=self.group)
-        return t.cpu().numpy()
-
-
-# ------------------------------------------------------------------ GPU backend
-class GpuBackend:
-    """Per-rank compute on the rank's GPU through the C-ABI."""
-
-    def __init__(self, x: torch.Tensor, reuse: bool = False):
-        """reuse=True: keep the per-plan setup (flattened sub-plans, uploaded
-        index arrays, result buffers) across calls with the same plan, as the
-        single-GPU runners do (results of a call are overwritten by the next)."""
-        from . import _device as D
-        self.D = D
-        self.x = x
-        self.dev = x.device
-        self.reuse = reuse
-        self._cache = {}
-
-    def dc_subplan(self, subsets: list, c: int, r: int, key=None):
-        """D&C of a sub-plan (anchor first) without re-centring -> (out_dev, est, gof, status)."""
-        D, x = self.D, self.x
-        ck = ("dc", key, c, r)
-        if self.reuse and key is not None and ck in self._cache:
-            ridx, off, out, est, gof, st, own = self._cache[ck]
-            self._own = own                 # every owned row is rewritten: no clearing pass
-            return self._run_dc(ridx, off, c, r, out, est, gof, st)
-        rows, off = flatten_subsets(subsets)
-        ridx = D.index_tensor(rows, self.dev)
-        npc = len(subsets)
-        out = torch.zeros((x.shape[0], r), dtype=torch.float64, device=self.dev)
-        est = D.empty((npc, r), self.dev)
-        gof = D.empty((npc, 2), self.dev)
-        st = D.status_tensor(npc, self.dev)
-        # rows each subset contributes (anchor: all; others: own rows) as device
-        # index segments carved from the uploaded plan indices (no second upload)
-        keep = np.ones(int(off[-1]), dtype=bool)
-        for j in range(1, npc):
-            keep[off[j]:off[j] + c] = False
-        own = ridx[torch.from_numpy(keep).to(self.dev)]
-        sizes = np.diff(off) - np.r_[0, np.full(npc - 1, c)]
-        own_off = np.zeros(npc + 1, dtype=np.int64)
-        np.cumsum(sizes, out=own_off[1:])
-        self._own = (own, own_off,
-                     torch.from_numpy(np.ascontiguousarray(own_off)).to(self.dev))
-        if self.reuse and key is not None:
-            self._cache[ck] = (ridx, off, out, est, gof, st, self._own)
-        return self._run_dc(ridx, off, c, r, out, est, gof, st)
-
-    def _run_dc(self, ridx, off, c, r, out, est, gof, st):
-        D, x = self.D, self.x
-        npc = len(off) - 1
-        D.handle(self.dev).call(
-            "mdsx_divide_conquer_ex", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
-            x.shape[1], ridx.data_ptr(), off.ctypes.data, npc, c, r, out.data_ptr(),
-            est.data_ptr(), gof.data_ptr(), st.data_ptr(), 1, D.stream_ptr(self.dev))
-        return out, est.cpu().numpy(), gof.cpu().numpy(), D.decode_status(st)
-
-    def own_segment_sums(self, out, r: int) -> np.ndarray:
-        """Column sums of each dc_subplan subset's own rows (fixed order)."""
-        own, own_off, own_off_dev = self._own
-        return self._segsums(out, own.data_ptr(), own_off, r, own_off_dev)
-
-    def shift_own(self, out, mean: np.ndarray) -> None:
-        own = self._own[0]
-        self._shift(out, own.data_ptr(), own.numel(), mean)
-
-    def range_sums(self, out, offsets: np.ndarray, r: int) -> np.ndarray:
-        """Column sums of the contiguous row ranges [offsets[j], offsets[j+1]) of out."""
-        return self._segsums(out, None, offsets, r)
-
-    def shift_all(self, out, mean: np.ndarray) -> None:
-        self._shift(out, None, out.shape[0], mean)
-
-    def _segsums(self, out, idx_ptr, offsets, r, doff=None):
-        D = self.D
-        nseg = len(offsets) - 1
-        sums = D.empty((max(nseg, 1), r), self.dev)
-        if nseg > 0:
-            if doff is None:
-                doff = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(self.dev)
-            D.handle(self.dev).call("mdsx_segment_colsums", out.data_ptr(), idx_ptr,
-                                    doff.data_ptr(), nseg, r, sums.data_ptr(),
-                                    D.stream_ptr(self.dev))
-        return sums.cpu().numpy()[:nseg]
-
-    def _shift(self, out, idx_ptr, n, mean):
-        D = self.D
-        m = torch.from_numpy(np.ascontiguousarray(mean, dtype=np.float64)).to(self.dev)
-        D.handle(self.dev).call("mdsx_shift_rows", out.data_ptr(), idx_ptr, n, out.shape[1],
-                                m.data_ptr(), D.stream_ptr(self.dev))
-
-    def fast_subtrees(self, plan: FastPlan, lo: int, hi: int, r: int, key=None):
-        """One rank's share of fast MDS (plans.flatten_fast_shard), aligned,
-        not re-centred -> (out_dev (rows in flat.order), flat, est, gof, status)."""
-        from .algorithms import FastRun
-        D = self.D
-        ck = ("fast", key, lo, hi, r)
-        run = self._cache.get(ck) if self.reuse and key is not None else None
-        if run is None:
-            flat = flatten_fast_shard(plan, lo, hi)
-            run = FastRun(self.x, plan, r, flat=flat, local=True)
-            if self.reuse and key is not None:
-                self._cache[ck] = run
-        flat = run.flat
-        run.launch()
-        out = run.pts[:len(flat.order)]
-        return out, flat, run.est.cpu().numpy(), run.gof.cpu().numpy(), D.decode_status(run.status)
-
-    def segment_sums(self, out, segments: list, r: int) -> np.ndarray:
-        D = self.D
-        rows, off = flatten_subsets(segments)
-        ridx = D.index_tensor(rows, self.dev)
-        doff = D.index_tensor(off, self.dev)
-        sums = D.empty((len(segments), r), self.dev)
-        D.handle(self.dev).call("mdsx_segment_colsums", out.data_ptr(), ridx.data_ptr(),
-                                doff.data_ptr(), len(segments), r, sums.data_ptr(),
-                                D.stream_ptr(self.dev))
-        return sums.cpu().numpy()
-
-    def shift(self, out, rows: np.ndarray, mean: np.ndarray) -> None:
-        D = self.D
-        ridx = D.index_tensor(rows, self.dev)
-        m = torch.from_numpy(np.ascontiguousarray(mean)).to(self.dev)
-        D.handle(self.dev).call("mdsx_shift_rows", out.data_ptr(), ridx.data_ptr(), len(rows),
-                                out.shape[1], m.data_ptr(), D.stream_ptr(self.dev))
-
-    def take(self, out, rows: np.ndarray) -> np.ndarray:
-        return out[self.D.index_tensor(rows, self.dev)].cpu().numpy()
-
-    def take_all(self, out) -> np.ndarray:
-        return self.D.to_host(out)
-
-    def place(self, out, local: np.ndarray, values: np.ndarray) -> None:
-        """out[local[i]] = values[i] (mdsx_scatter_rows)."""
-        if len(local) == 0:
-            return
-        D = self.D
-        src = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(self.dev)
-        D.handle(self.dev).call("mdsx_scatter_rows", src.data_ptr(),
-                                D.index_tensor(local, self.dev).data_ptr(), len(local),
-                                out.shape[1], out.data_ptr(), D.stream_ptr(self.dev))
-
-    # interpolation pieces -------------------------------------------------
-    def landmark_context(self, sample: np.ndarray, r: int):
-        """Classical MDS of the sample + Gower context, flattened for broadcast."""
-        from .primitives import classical_pieces, raise_piece_status
-        D, x = self.D, self.x
-        idx = D.index_tensor(sample, self.dev)
-        pts, est, gof, st = classical_pieces(x, idx, np.array([0, len(sample)], np.int64), r)
-        raise_piece_status(D.decode_status(st)[0], r, "sample subset")
-        h = D.handle(self.dev)
-        l, p = len(sample), x.shape[1]
-        size = int(h.lib.mdsx_gower_context_size(l, p, r))
-        ctx = D.empty((size,), self.dev)
-        cond = D.empty((1,), self.dev)
-        flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        h.call("mdsx_gower_context", x.data_ptr(), D.dtype_code(x), p, p, idx.data_ptr(), l,
-               pts.data_ptr(), r, ctx.data_ptr(), cond.data_ptr(), flag.data_ptr(),
-               D.stream_ptr(self.dev))
-        if int(flag.item()):
-            from .errors import NumericalError
-            raise NumericalError("base covariance is ill-conditioned or not positive definite")
-        g = gof.cpu().numpy()[0]
-        return (np.concatenate([ctx.cpu().numpy(), pts.cpu().numpy().ravel()]),
-                est.cpu().numpy()[0], float(g[0]), float(g[1]))
-
-    def _cached_index(self, key, arr: np.ndarray):
-        ck = ("idx", key)
-        if ck not in self._cache:
-            self._cache[ck] = self.D.index_tensor(arr, self.dev)
-        return self._cache[ck]
-
-    def landmark_context_dev(self, sample: np.ndarray, r: int):
-        """landmark_context kept on the device: (head, check) with head =
-        [g1, g2, est(r), context, landmark configuration] as one device vector
-        (broadcast as is) and check() raising the deferred failures."""
-        from .primitives import classical_pieces, raise_piece_status
-        D, x = self.D, self.x
-        idx = self._cached_index(("sample", id(sample)), sample)
-        pts, est, gof, st = classical_pieces(x, idx, np.array([0, len(sample)], np.int64), r)
-        h = D.handle(self.dev)
-        l, p = len(sample), x.shape[1]
-        size = int(h.lib.mdsx_gower_context_size(l, p, r))
-        head = D.empty((2 + r + size + l * r,), self.dev)
-        cond = D.empty((1,), self.dev)
-        flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        h.call("mdsx_gower_context", x.data_ptr(), D.dtype_code(x), p, p, idx.data_ptr(), l,
-               pts.data_ptr(), r, head[2 + r:].data_ptr(), cond.data_ptr(), flag.data_ptr(),
-               D.stream_ptr(self.dev))
-        head[0:2] = gof[0]
-        head[2:2 + r] = est[0]
-        head[2 + r + size:] = pts.reshape(-1)
-
-        def check():
-            raise_piece_status(D.decode_status(st)[0], r, "sample subset")
-            if int(flag.item()):
-                from .errors import NumericalError
-                raise NumericalError("base covariance is ill-conditioned or not positive definite")
-        return head, check
-
-    def gower_rows_dev(self, head, l: int, r: int, lo: int, hi: int):
-        D, x = self.D, self.x
-        p = x.shape[1]
-        h = D.handle(self.dev)
-        rows = x[lo:hi]
-        out = D.empty((hi - lo, r), self.dev)
-        nf = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        h.call("mdsx_gower_interpolate", head[2 + r:].data_ptr(), l, p, r, rows.data_ptr(),
-               D.dtype_code(x), p, hi - lo, out.data_ptr(), r, nf.data_ptr(),
-               D.stream_ptr(self.dev))
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        """[world * t.shape[0], ...]: every rank's equally shaped tensor, rank order."""
+        if self.world == 1:
+            return t
+        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
+                          device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
         return out
 
-    def place_dev(self, out, key, local: np.ndarray, values_dev) -> None:
-        """out[local[i]] = values_dev[i] with the index upload cached under key."""
-        if len(local) == 0:
-            return
-        D = self.D
-        li = self._cached_index(key, local)
-        D.handle(self.dev).call("mdsx_scatter_rows", values_dev.data_ptr(), li.data_ptr(),
-                                len(local), out.shape[1], out.data_ptr(), D.stream_ptr(self.dev))
+    def broadcast_(self, t: torch.Tensor, src: int = 0) -> torch.Tensor:
+        if self.world > 1:
+            dist.broadcast(t, src=src, group=self.group)
+        return t
 
-    def gower_rows(self, packed: np.ndarray, l: int, r: int, lo: int, hi: int):
-        D, x = self.D, self.x
-        p = x.shape[1]
-        h = D.handle(self.dev)
-        size = int(h.lib.mdsx_gower_context_size(l, p, r))
-        ctx = torch.from_numpy(np.ascontiguousarray(packed[:size])).to(self.dev)
-        rows = x[lo:hi]
-        out = D.empty((hi - lo, r), self.dev)
-        nf = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        h.call("mdsx_gower_interpolate", ctx.data_ptr(), l, p, r, rows.data_ptr(),
-               D.dtype_code(x), p, hi - lo, out.data_ptr(), r, nf.data_ptr(),
-               D.stream_ptr(self.dev))
-        return out
+    def gather(self, t: torch.Tensor, dst: int = 0):
+        """Equally shaped tensors of every rank -> [world, ...] on `dst`, None elsewhere."""
+        if self.world == 1:
+            return t[None]
+        if self.rank == dst:
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            dist.gather(t.contiguous(), gather_list=parts, dst=dst, group=self.group)
+            return torch.stack(parts)
+        dist.gather(t.contiguous(), dst=dst, group=self.group)
+        return None
 
-
-# ------------------------------------------------------------------ algorithms
-def fold_rows(rows: np.ndarray, r: int) -> np.ndarray:
-    """Left fold (((0 + s_0) + s_1) + ...) of the rows in the given order: a
-    sequential running sum, identical on every rank and for every world size
-    (np.add.reduce would pair them up instead)."""
-    if len(rows) == 0:
-        return np.zeros(r)
-    return np.cumsum(np.asarray(rows, dtype=np.float64), axis=0)[-1]
+    def max_int(self, v: int) -> int:
+        if self.world == 1:
+            return int(v)
+        t = torch.tensor([v], dtype=torch.int64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
 
 
-def sharded_divide_and_conquer(backend, n: int, params: AlgorithmParams, comm: Comm,
-                               plan: DcPlan | None = None) -> ShardResult:
-    """divide_and_conquer_mds (algorithms.py:128-172) over comm.world ranks."""
-    prm = params.resolved("divide")
-    plan = plan if plan is not None else plan_divide_conquer(n, prm.l, prm.c, prm.seed)
-    P, c, r = plan.p, prm.c, prm.r
-    lo, hi = shard(P - 1, comm.world, comm.rank)
-    mine = list(range(1 + lo, 1 + hi))                    # owned subsets besides the anchor
-    out, est, gof, st = backend.dc_subplan([plan.subsets[0]] + [plan.subsets[j] for j in mine], c, r,
-                                           key=(id(plan), lo, hi))
-    from .primitives import raise_piece_status
-    if np.any(st["code"] == 3):
-        from .errors import InvalidInputError
-        raise InvalidInputError("data contains non-finite values")
-    labels = [0] + mine
-    bad = np.flatnonzero(st["code"] != 0)
-    if bad.size:                                          # first failing subset in plan order
-        raise_piece_status(st[bad[0]], r, f"subset {labels[bad[0]] + 1}")
-    # rows each subset contributes (anchor: all its rows; others: own rows)
-    own = [plan.subsets[0]] + [plan.subsets[j][c:] for j in mine]
-    sums = backend.own_segment_sums(out, r)              # (1 + len(mine), r)
-    # plan-order all-gather of per-subset sums and fit figures
-    width = 3 + 2 * r                                    # [j, g1, g2, est(r), sums(r)]
-    recs = np.zeros((len(mine), width))
-    recs[:, 0] = mine
-    recs[:, 1:3] = gof[1:1 + len(mine)]
-    recs[:, 3:3 + r] = est[1:1 + len(mine)]
-    recs[:, 3 + r:3 + 2 * r] = sums[1:1 + len(mine)]
-    allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
-    allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
-    seg_sums = np.vstack([sums[0:1], allrecs[:, 3 + r:3 + 2 * r]])
-    total = fold_rows(seg_sums, r)                        # plan order
-    mean = total / n
-    backend.shift_own(out, mean)
-    sizes = np.fromiter((len(q) for q in plan.subsets), dtype=np.float64, count=P)
-    weights = sizes.copy()
-    weights[1:] -= c                                      # algorithms.py:158-166
-    g1s = np.concatenate([gof[0:1, 0], allrecs[:, 1]])
-    g2s = np.concatenate([gof[0:1, 1], allrecs[:, 2]])
-    ests = np.vstack([est[0:1], allrecs[:, 3:3 + r]])
-    g1 = float(np.dot(weights, g1s) / n)
-    g2 = float(np.dot(weights, g2s) / n)
-    per = ests * (sizes / weights)[:, None]
-    # the anchor's rows belong to rank 0; index lists built only when gathered
-    parts = own if comm.rank == 0 else own[1:]
-    rows = (lambda: np.concatenate(parts)) if parts else np.empty(0, np.int64)
-    return ShardResult(rows, out, rows, per.mean(axis=0), g1, g2, backend)
+def _pad_rows(t: torch.Tensor, rows: int, fill: float = 0.0) -> torch.Tensor:
+    if t.shape[0] == rows:
+        return t
+    pad = torch.full((rows - t.shape[0],) + tuple(t.shape[1:]), fill, dtype=t.dtype,
+                     device=t.device)
+    return torch.cat([t, pad])
 
 
-def sharded_fast(backend, n: int, params: AlgorithmParams, comm: Comm,
-                 plan: FastPlan | None = None) -> ShardResult:
-    """fast_mds (algorithms.py:285-348) over comm.world ranks."""
-    from .errors import InvalidInputError
-    from .primitives import raise_piece_status
-    prm = params.resolved("fast")
-    r = prm.r
-    plan = plan if plan is not None else plan_fast(n, prm.l, prm.s, prm.seed)
-    if plan.root.is_leaf:                                 # n <= l: classical MDS (algorithms.py:337-338)
-        out, est, gof, st = backend.dc_subplan([plan.root.indices], 1, r)
-        raise_piece_status(st[0], r, "leaf 1")
-        rows = plan.root.indices if comm.rank == 0 else np.empty(0, np.int64)
-        return ShardResult(rows, out, rows, est[0], float(gof[0, 0]), float(gof[0, 1]), backend)
-    kids = plan.root.children
-    lo, hi = shard(len(kids), comm.world, comm.rank)
-    out, flat, est, gof, st = backend.fast_subtrees(plan, lo, hi, r, key=id(plan))
-    # failures: a consistent decision on every rank (all raise, no rank hangs)
-    root_pid = len(flat.piece_off) - 2                    # the root alignment set, evaluated last
-    ev = np.asarray(flat.eval_order, dtype=np.int64)
-    bad = np.flatnonzero((ev != root_pid) & (st["code"][ev] != 0))
-    first = int(bad[0]) if bad.size else -1
-    flags = np.array([float(np.any(st["code"] == 3)), float(first >= 0)])
-    allflags = np.vstack(comm.allgather(flags)) if comm.world > 1 else flags[None]
-    if allflags[:, 0].any():
-        raise InvalidInputError("data contains non-finite values")
-    if allflags[:, 1].any():
-        culprit = int(np.flatnonzero(allflags[:, 1])[0])
-        if culprit == comm.rank:
-            pid = flat.eval_order[first]
-            raise_piece_status(st[pid], r, flat.labels[pid])
-        raise RuntimeError(f"fast MDS failed on rank {culprit}")
-    raise_piece_status(st[root_pid], r, flat.labels[root_pid])
-    # per-child aggregates of the owned subtrees (algorithms.py:289-320); a node
-    # whose children are all leaves is reduced with array ops over its leaf range
-    leaf = [0]
-
-    def agg(node):
-        if node.is_leaf:
-            j = leaf[0]
-            leaf[0] += 1
-            return gof[j, 0], gof[j, 1], est[j], node.size
-        kids_ = node.children
-        if all(ch.is_leaf for ch in kids_):
-            j0 = leaf[0]
-            leaf[0] += len(kids_)
-            sizes = np.array([ch.size for ch in kids_], dtype=np.float64)
-            tot = sizes.sum()
-            return (float(np.dot(sizes, gof[j0:leaf[0], 0]) / tot),
-                    float(np.dot(sizes, gof[j0:leaf[0], 1]) / tot),
-                    est[j0:leaf[0]].mean(axis=0), int(tot))
-        fits = [agg(ch) for ch in kids_]
-        sizes = np.array([f[3] for f in fits], dtype=np.float64)
-        tot = sizes.sum()
-        return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
-                float(np.dot(sizes, [f[1] for f in fits]) / tot),
-                np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
-
-    mine = kids[lo:hi]
-    shape = _fast_shape(plan, mine, backend)
-    if shape is not None:                                 # two-level subtrees: array ops only
-        owner, lsize = shape
-        starts_l = np.searchsorted(owner, np.arange(len(mine) + 1))
-        g1c, g2c = np.ascontiguousarray(gof[:, 0]), np.ascontiguousarray(gof[:, 1])
-        fits = [(float(np.dot(lsize[a:b], g1c[a:b]) / lsize[a:b].sum()),
-                 float(np.dot(lsize[a:b], g2c[a:b]) / lsize[a:b].sum()),
-                 est[a:b].mean(axis=0), int(lsize[a:b].sum()))
-                for a, b in zip(starts_l[:-1], starts_l[1:])]
-    else:
-        fits = [agg(ch) for ch in mine]
-    starts = np.cumsum([0] + [ch.size for ch in mine]).astype(np.int64)
-    sums = backend.range_sums(out, starts, r)
-    width = 4 + 2 * r                                     # [i, g1, g2, size, est(r), sums(r)]
-    recs = np.zeros((len(mine), width))
-    if fits:
-        recs[:, 0] = np.arange(lo, lo + len(mine))
-        recs[:, 1] = [f[0] for f in fits]
-        recs[:, 2] = [f[1] for f in fits]
-        recs[:, 3] = [f[3] for f in fits]
-        recs[:, 4:4 + r] = np.stack([f[2] for f in fits])
-        recs[:, 4 + r:] = sums[:len(mine)]
-    allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
-    allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
-    sizes = allrecs[:, 3]
-    tot = sizes.sum()
-    g1 = float(np.dot(sizes, allrecs[:, 1]) / tot)
-    g2 = float(np.dot(sizes, allrecs[:, 2]) / tot)
-    estimates = allrecs[:, 4:4 + r].mean(axis=0)
-    total = fold_rows(allrecs[:, 4 + r:], r)              # child order
-    backend.shift_all(out, total / n)
-    return ShardResult(flat.order, out, (0, len(flat.order)), estimates, g1, g2, backend)
+def _gather_records(comm: Comm, recs: torch.Tensor, kmax: int, count: int) -> torch.Tensor:
+    """All-gather per-rank record rows (column 0 = global id), drop padding
+    and return the `count` real records sorted by id (on the device)."""
+    allr = comm.all_gather(_pad_rows(recs, kmax, _SENTINEL))
+    order = torch.argsort(allr[:, 0], stable=True)
+    return allr.index_select(0, order[:count])
 
 
-def _fast_shape(plan, mine, backend):
-    """For subtrees whose children are all leaves (the BASELINE fast plans):
-    (child index of every leaf in DFS order, leaf sizes), cached per plan on
-    the backend; None for deeper trees."""
-    cache = getattr(backend, "_fast_shape_cache", None)
-    if cache is None:
-        cache = backend._fast_shape_cache = {}
-    key = (id(plan), id(mine[0]) if mine else 0, len(mine))
-    if key not in cache:
-        if not mine or not all(not ch.is_leaf and all(g.is_leaf for g in ch.children)
-                               for ch in mine):
-            cache[key] = None
-        else:
-            owner = np.concatenate([np.full(len(ch.children), t, np.int64)
-                                    for t, ch in enumerate(mine)])
-            lsize = np.array([g.size for ch in mine for g in ch.children], dtype=np.float64)
-            cache[key] = (owner, lsize)
-    return cache[key]
+def _fold_mean(sums: torch.Tensor, n: int) -> torch.Tensor:
+    """Column sums folded in record order (the same tensor shape on every
+    world size -> the same arithmetic), divided by n."""
+    return torch.cumsum(sums, dim=0)[-1] / n
 
 
-def sharded_interpolation(backend, n: int, params: AlgorithmParams, comm: Comm,
-                          sample: np.ndarray | None = None) -> ShardResult:
-    """interpolation_mds (algorithms.py:245-274) over comm.world ranks."""
-    prm = params.resolved("interpolate")
-    r, l = prm.r, prm.l
-    sample = sample if sample is not None else interpolation_sample(n, l, prm.seed)
-    l = len(sample)
-    blocks = (n + SUM_BLOCK - 1) // SUM_BLOCK
-    b_lo, b_hi = shard(blocks, comm.world, comm.rank)
-    lo, hi = b_lo * SUM_BLOCK, min(n, b_hi * SUM_BLOCK)
-    in_shard = (sample >= lo) & (sample < hi)
-    if hasattr(backend, "landmark_context_dev"):
-        # device-resident: the context is computed on rank 0 and broadcast as a
-        # device vector (no host round trip inside the step)
-        check = None
-        if comm.rank == 0:
-            head_dev, check = backend.landmark_context_dev(sample, r)
-        else:
-            size = backend_context_len(backend, l, r) + 2 + r
-            head_dev = torch.zeros(size, dtype=torch.float64, device=backend.dev)
-        if comm.world > 1:
-            dist.broadcast(head_dev, src=0, group=comm.group)
-        out = backend.gower_rows_dev(head_dev, l, r, lo, hi)
-        base_dev = head_dev[-l * r:].reshape(l, r)
-        if in_shard.all():
-            vals = base_dev
-        else:
-            sel = backend._cached_index(("insel", id(sample), lo, hi), np.flatnonzero(in_shard))
-            vals = base_dev.index_select(0, sel)
-        backend.place_dev(out, ("local", id(sample), lo, hi), (sample[in_shard] - lo).astype(np.int64),
-                          vals)
-        if check is not None:
-            check()
-        head_small = head_dev[:2 + r].cpu().numpy()
-        g1, g2, est = float(head_small[0]), float(head_small[1]), head_small[2:2 + r]
-    else:
-        if comm.rank == 0:
-            packed, est, g1, g2 = backend.landmark_context(sample, r)
-            head = np.concatenate([[g1, g2], est, packed])
-        else:
-            size = backend_context_len(backend, l, r) + 2 + r
-            head = np.zeros(size)
-        head = comm.broadcast(head, src=0) if comm.world > 1 else head
-        g1, g2, est, packed = float(head[0]), float(head[1]), head[2:2 + r], head[2 + r:]
-        base = packed[-l * r:].reshape(l, r)
-        out = backend.gower_rows(packed, l, r, lo, hi)        # (hi - lo) x r, shard-local rows
-        # landmark rows inside the shard take the classical configuration
-        backend.place(out, (sample[in_shard] - lo).astype(np.int64), base[in_shard])
-    bounds = np.minimum(hi, np.arange(b_lo, b_hi + 1, dtype=np.int64) * SUM_BLOCK) - lo
-    sums = backend.range_sums(out, bounds, r)
-    recs = np.hstack([np.arange(b_lo, b_hi, dtype=np.float64)[:, None], sums])
-    allrecs = np.concatenate(comm.allgather_ragged(recs)) if comm.world > 1 else recs
-    allrecs = allrecs[np.argsort(allrecs[:, 0], kind="stable")]
-    total = fold_rows(allrecs[:, 1:], r)                  # canonical block order
-    backend.shift_all(out, total / n)
-    return ShardResult((lo, hi), out, (0, hi - lo), est, g1, g2, backend)
+@dataclass
+class ShardResult:
+    """One rank's share: `out` rows [report_lo, report_hi) are this rank's
+    rows of the configuration; finish() fills the fit figures."""
+
+    out: torch.Tensor
+    report_lo: int
+    report_hi: int
+    finish_fn: object
+    estimates: np.ndarray | None = None
+    gof_g1: float | None = None
+    gof_g2: float | None = None
+    rows_fn: object = None          # rank k -> global row ids of its reported rows
+
+    def finish(self) -> "ShardResult":
+        if self.estimates is None:
+            self.estimates, self.gof_g1, self.gof_g2 = self.finish_fn()
+        return self
 
 
-def backend_context_len(backend, l: int, r: int) -> int:
-    return backend.context_len(l, r) if hasattr(backend, "context_len") else \
-        _gpu_context_len(backend, l, r)
-
-
-def _gpu_context_len(backend, l: int, r: int) -> int:
-    h = backend.D.handle(backend.dev)
-    return int(h.lib.mdsx_gower_context_size(l, backend.x.shape[1], r)) + l * r
-
-
-def gather_points(res: ShardResult, n: int, r: int, comm: Comm) -> np.ndarray | None:
-    """Assemble the full n x r configuration on rank 0 (None elsewhere)."""
-    block = np.hstack([res.rows[:, None].astype(np.float64), res.points()])
-    parts = comm.allgather_ragged(block) if comm.world > 1 else [block]
+def gather_points(res: ShardResult, n: int, comm: Comm, to_host: bool = True):
+    """Assemble the full n x r configuration on rank 0 (None elsewhere):
+    one gather of every rank's reported rows (padded to the largest share),
+    one device scatter into input row order."""
+    res.finish()
+    r = res.out.shape[1]
+    mine = res.out[res.report_lo:res.report_hi]
+    cap = comm.max_int(mine.shape[0])
+    parts = comm.gather(_pad_rows(mine, cap))
     if comm.rank != 0:
         return None
-    out = np.empty((n, r))
-    for part in parts:
-        out[part[:, 0].astype(np.int64)] = part[:, 1:]
-    return out
+    rows, vals = [], []
+    for k in range(comm.world):
+        idx = res.rows_fn(k)
+        rows.append(idx)
+        vals.append(parts[k, :len(idx)])
+    idx_t = torch.from_numpy(np.ascontiguousarray(np.concatenate(rows), dtype=np.int64)).to(
+        res.out.device)
+    out = torch.empty((n, r), dtype=res.out.dtype, device=res.out.device)
+    out.index_copy_(0, idx_t, torch.cat(vals))
+    if not to_host:
+        return out
+    from . import _device as D
+    return D.to_host(out) if out.is_cuda else out.numpy()
+
+
+# ================================================================= D&C
+@dataclass
+class DcShard:
+    """Rank `rank`'s share of a D&C plan.  Local matrix rows: the anchor subset
+    (connecting rows first), then the own rows of every owned subset."""
+
+    pieces: np.ndarray        # global subset ids, anchor (0) first
+    local_rows: np.ndarray    # global row id of each local matrix row
+    row_idx: np.ndarray       # flattened per-subset local row lists
+    piece_off: np.ndarray
+    own_off: np.ndarray       # own-row segments of the subsets in local order
+    report_lo: int            # first local row this rank reports (anchor: rank 0 only)
+
+
+def dc_shard(plan: DcPlan, world: int, rank: int) -> DcShard:
+    P, c = plan.p, plan.c
+    lo, hi = shard(P - 1, world, rank)
+    mine = np.arange(1 + lo, 1 + hi, dtype=np.int64)
+    anchor = np.asarray(plan.subsets[0], dtype=np.int64)
+    l0 = len(anchor)
+    own = [np.asarray(plan.subsets[j][c:], dtype=np.int64) for j in mine]
+    sizes = np.array([l0] + [len(o) for o in own], dtype=np.int64)
+    own_off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=own_off[1:])
+    local_rows = np.concatenate([anchor] + own) if own else anchor.copy()
+    conn = np.arange(c, dtype=np.int64)
+    lists = [np.arange(l0, dtype=np.int64)] + [
+        np.concatenate([conn, np.arange(own_off[i + 1], own_off[i + 2], dtype=np.int64)])
+        for i in range(len(own))]
+    row_idx, piece_off = flatten_subsets(lists)
+    return DcShard(np.concatenate([[0], mine]), local_rows, row_idx, piece_off, own_off,
+                   0 if rank == 0 else l0)
+
+
+class ShardedDivide:
+    """divide_and_conquer_mds over comm.world ranks.  `x_local` holds the rows
+    ``dc_shard(plan, world, rank).local_rows`` in that order."""
+
+    def __init__(self, backend, x_local, plan: DcPlan, r: int, comm: Comm):
+        self.be, self.x, self.plan, self.r, self.comm = backend, x_local, plan, r, comm
+        self.sh = sh = dc_shard(plan, comm.world, comm.rank)
+        if x_local.shape[0] != len(sh.local_rows):
+            raise ValueError(f"rank {comm.rank}: local matrix has {x_local.shape[0]} rows, "
+                             f"the shard needs {len(sh.local_rows)}")
+        dev = backend.device
+        self.dev = dev
+        self.row_idx = backend.index(sh.row_idx)
+        self.own_off = backend.index(sh.own_off)
+        npc = len(sh.pieces)
+        self.out = torch.empty((len(sh.local_rows), r), dtype=torch.float64, device=dev)
+        self.est = torch.empty((npc, r), dtype=torch.float64, device=dev)
+        self.gof = torch.empty((npc, 2), dtype=torch.float64, device=dev)
+        self.status = torch.zeros((npc, 2), dtype=torch.float64, device=dev)
+        self.sums = torch.empty((npc, r), dtype=torch.float64, device=dev)
+        self.ids = torch.tensor(sh.pieces, dtype=torch.float64, device=dev)[:, None]
+        self.first = 0 if comm.rank == 0 else 1          # the anchor's record: rank 0 only
+        self.kmax = 1 + shard(plan.p - 1, comm.world, 0)[1]
+        self._rows_cache: dict = {}
+        self.recs = None
+
+    def launch(self) -> ShardResult:
+        be, sh, r = self.be, self.sh, self.r
+        be.dc_run(self.x, self.row_idx, sh.piece_off, self.plan.c, r, self.out, self.est,
+                  self.gof, self.status)
+        be.range_sums(self.out, self.own_off, len(sh.pieces), self.sums)
+        # record: [subset id, g1, g2, est(r), sums(r), status(2)]
+        recs = torch.cat([self.ids, self.gof, self.est, self.sums, self.status], dim=1)[self.first:]
+        self.recs = _gather_records(self.comm, recs, self.kmax, self.plan.p)
+        mean = _fold_mean(self.recs[:, 3 + r:3 + 2 * r], self.plan.n)
+        be.shift_rows(self.out, mean)
+        return ShardResult(self.out, sh.report_lo, len(sh.local_rows), self.finish,
+                           rows_fn=self.rows_of)
+
+    def rows_of(self, k: int) -> np.ndarray:
+        if k not in self._rows_cache:
+            s = dc_shard(self.plan, self.comm.world, k)
+            self._rows_cache[k] = s.local_rows[s.report_lo:]
+        return self._rows_cache[k]
+
+    def finish(self):
+        """Host decode of the gathered records (identical on every rank)."""
+        from .primitives import raise_piece_status
+        r, plan = self.r, self.plan
+        recs = self.recs.cpu().numpy()
+        st = decode_status(recs[:, 3 + 2 * r:])
+        if np.any(st["code"] == 3):
+            raise InvalidInputError("data contains non-finite values")
+        bad = np.flatnonzero(st["code"] != 0)
+        if bad.size:                                      # first failing subset in plan order
+            raise_piece_status(st[bad[0]], r, f"subset {bad[0] + 1}")
+        sizes = np.fromiter((len(q) for q in plan.subsets), dtype=np.float64, count=plan.p)
+        weights = sizes.copy()
+        weights[1:] -= plan.c                             # algorithms.py:158-166
+        g1 = float(np.dot(weights, recs[:, 1]) / plan.n)
+        g2 = float(np.dot(weights, recs[:, 2]) / plan.n)
+        per = recs[:, 3:3 + r] * (sizes / weights)[:, None]
+        return per.mean(axis=0), g1, g2
+
+
+# ================================================================= interpolation
+@dataclass
+class InterpShard:
+    lo: int
+    hi: int                   # global rows [lo, hi) of this rank
+    b_lo: int
+    b_hi: int                 # canonical sum blocks [b_lo, b_hi)
+    land_pos: np.ndarray      # local positions of the landmarks inside [lo, hi)
+    land_sel: np.ndarray      # ... and their index in the sample
+
+    @property
+    def local_rows(self) -> np.ndarray:
+        return np.arange(self.lo, self.hi, dtype=np.int64)
+
+
+def interp_shard(n: int, sample: np.ndarray, world: int, rank: int) -> InterpShard:
+    blocks = (n + SUM_BLOCK - 1) // SUM_BLOCK
+    b_lo, b_hi = shard(blocks, world, rank)
+    lo, hi = b_lo * SUM_BLOCK, min(n, b_hi * SUM_BLOCK)
+    sel = np.flatnonzero((sample >= lo) & (sample < hi)).astype(np.int64)
+    return InterpShard(lo, hi, b_lo, b_hi, (sample[sel] - lo).astype(np.int64), sel)
+
+
+class ShardedInterpolation:
+    """interpolation_mds over comm.world ranks.  `x_local` holds rows
+    [lo, hi) of ``interp_shard``; rank 0 also gets the landmark rows
+    `x_landmarks` (sample order)."""
+
+    def __init__(self, backend, x_local, n: int, sample: np.ndarray, r: int, comm: Comm,
+                 x_landmarks=None):
+        self.be, self.x, self.n, self.r, self.comm = backend, x_local, n, r, comm
+        self.sample = np.asarray(sample, dtype=np.int64)
+        self.l = l = len(self.sample)
+        self.sh = sh = interp_shard(n, self.sample, comm.world, comm.rank)
+        if x_local.shape[0] != sh.hi - sh.lo:
+            raise ValueError(f"rank {comm.rank}: local matrix has {x_local.shape[0]} rows, "
+                             f"the shard needs {sh.hi - sh.lo}")
+        if comm.rank == 0 and x_landmarks is None:
+            raise ValueError("rank 0 needs the landmark rows")
+        self.xl = x_landmarks
+        dev = self.dev = backend.device
+        p = x_local.shape[1]
+        self.head_len = backend.head_len(l, p, r)
+        self.head = torch.zeros(self.head_len, dtype=torch.float64, device=dev)
+        self.out = torch.empty((sh.hi - sh.lo, r), dtype=torch.float64, device=dev)
+        self.land_pos = backend.index(sh.land_pos)
+        self.land_sel = backend.index(sh.land_sel)
+        nb = sh.b_hi - sh.b_lo
+        bounds = np.minimum(sh.hi, np.arange(sh.b_lo, sh.b_hi + 1, dtype=np.int64) * SUM_BLOCK) - sh.lo
+        self.bounds = backend.index(bounds)
+        self.nb = nb
+        self.sums = torch.empty((nb, r), dtype=torch.float64, device=dev)
+        self.ids = torch.arange(sh.b_lo, sh.b_hi, dtype=torch.float64, device=dev)[:, None]
+        self.nf = torch.zeros((nb, 1), dtype=torch.float64, device=dev)
+        self.blocks = (n + SUM_BLOCK - 1) // SUM_BLOCK
+        self.kmax = shard(self.blocks, comm.world, 0)[1]
+        self.recs = None
+
+    def launch(self) -> ShardResult:
+        be, sh, r, l = self.be, self.sh, self.r, self.l
+        if self.comm.rank == 0:
+            be.landmark_head(self.xl, r, self.head)
+        self.comm.broadcast_(self.head, 0)
+        flag = be.gower_rows(self.head, l, r, self.x, self.out)
+        base = self.head[-l * r:].view(l, r)
+        if len(sh.land_sel):
+            be.scatter_rows(base.index_select(0, self.land_sel), self.land_pos, self.out)
+        be.range_sums(self.out, self.bounds, self.nb, self.sums)
+        if self.nb:
+            self.nf[0, 0] = flag
+        recs = torch.cat([self.ids, self.sums, self.nf], dim=1)
+        self.recs = _gather_records(self.comm, recs, self.kmax, self.blocks)
+        be.shift_rows(self.out, _fold_mean(self.recs[:, 1:1 + r], self.n))
+        return ShardResult(self.out, 0, sh.hi - sh.lo, self.finish, rows_fn=self.rows_of)
+
+    def rows_of(self, k: int) -> np.ndarray:
+        s = interp_shard(self.n, self.sample, self.comm.world, k)
+        return np.arange(s.lo, s.hi, dtype=np.int64)
+
+    def finish(self):
+        from .primitives import raise_piece_status
+        r = self.r
+        head = self.head[:self.be.HEAD_FIXED + r].cpu().numpy()
+        g1, g2, est = float(head[0]), float(head[1]), head[2:2 + r]
+        st = decode_status(head[2 + r:4 + r])[0]
+        flag, cond = int(head[4 + r]), float(head[5 + r])
+        if int(st["code"]) == 3 or self.recs[:, 1 + r].abs().sum().item() > 0:
+            raise InvalidInputError("data contains non-finite values")
+        raise_piece_status(st, r, "sample subset")
+        if flag == 1:
+            raise NumericalError(f"base covariance is ill-conditioned (condition estimate "
+                                 f"{cond:.3e}); the requested dimension exceeds the usable rank")
+        if flag == 2:
+            raise NumericalError("base covariance is not positive definite")
+        return est.copy(), g1, g2
+
+
+# ================================================================= fast
+@dataclass
+class FastShard:
+    lo: int
+    hi: int                   # level-1 children [lo, hi) of the root
+    flat: object              # plans.FastFlat with piece rows remapped to local rows
+    flat_global: object       # ... as flattened (global row ids)
+    local_rows: np.ndarray    # owned subtree rows (DFS order), then extra alignment rows
+    n_own: int                # rows of the owned subtrees (reported)
+    leaf_base: int            # global DFS index of the first owned leaf
+    eval_base: int            # global evaluation position of the first owned piece
+    child_off: np.ndarray     # owned children's row ranges in local order
+
+
+def _subtree_counts(node) -> tuple[int, int]:
+    """(leaves, pieces) of a subtree: every leaf and every internal node's
+    alignment set is one classical-MDS piece."""
+    if node.is_leaf:
+        return 1, 1
+    lv, pc = 0, 1
+    for ch in node.children:
+        a, b = _subtree_counts(ch)
+        lv += a
+        pc += b
+    return lv, pc
+
+
+def fast_shard(plan: FastPlan, world: int, rank: int, counts=None) -> FastShard:
+    kids = plan.root.children
+    lo, hi = shard(len(kids), world, rank)
+    flat = flatten_fast_shard(plan, lo, hi)
+    order = flat.order
+    need = np.unique(flat.piece_rows)
+    pos = np.full(plan.n, -1, dtype=np.int64)
+    pos[order] = np.arange(len(order), dtype=np.int64)
+    extra = need[pos[need] < 0]
+    local_rows = np.concatenate([order, extra])
+    pos[extra] = len(order) + np.arange(len(extra), dtype=np.int64)
+    from dataclasses import replace
+    flat_l = replace(flat, piece_rows=pos[flat.piece_rows], order=np.arange(len(order), dtype=np.int64))
+    counts = counts if counts is not None else [_subtree_counts(ch) for ch in kids]
+    leaf_base = int(sum(c[0] for c in counts[:lo]))
+    eval_base = int(sum(c[1] for c in counts[:lo]))
+    child_off = np.concatenate([[0], np.cumsum([kids[i].size for i in range(lo, hi)])]).astype(np.int64)
+    return FastShard(lo, hi, flat_l, flat, local_rows, len(order), leaf_base, eval_base, child_off)
+
+
+class ShardedFast:
+    """fast_mds over comm.world ranks.  `x_local` holds the rows
+    ``fast_shard(plan, world, rank).local_rows`` in that order."""
+
+    def __init__(self, backend, x_local, plan: FastPlan, r: int, comm: Comm):
+        if plan.root.is_leaf:
+            raise ValueError("a single-leaf fast plan is classical MDS (no sharding)")
+        self.be, self.x, self.plan, self.r, self.comm = backend, x_local, plan, r, comm
+        self.counts = [_subtree_counts(ch) for ch in plan.root.children]
+        self.sh = sh = fast_shard(plan, comm.world, comm.rank, self.counts)
+        if x_local.shape[0] != len(sh.local_rows):
+            raise ValueError(f"rank {comm.rank}: local matrix has {x_local.shape[0]} rows, "
+                             f"the shard needs {len(sh.local_rows)}")
+        dev = self.dev = backend.device
+        self.run = backend.fast_prepare(x_local, plan, sh.flat, r)
+        nk = sh.hi - sh.lo
+        self.child_off = backend.index(sh.child_off)
+        self.sums = torch.empty((nk, r), dtype=torch.float64, device=dev)
+        self.child_ids = torch.arange(sh.lo, sh.hi, dtype=torch.float64, device=dev)[:, None]
+        flat = sh.flat
+        root_pid = len(flat.piece_off) - 2
+        ev = [pid for pid in flat.eval_order if pid != root_pid]
+        self.root_pid = root_pid
+        # piece records in global evaluation order (root alignment set: rank 0, last)
+        ev_ids = np.arange(sh.eval_base, sh.eval_base + len(ev), dtype=np.float64)
+        total_pieces = int(sum(c[1] for c in self.counts))
+        self.total_pieces = total_pieces + 1
+        leaf_of = np.full(len(flat.piece_off) - 1, -1.0)
+        leaf_of[:flat.n_leaves] = sh.leaf_base + np.arange(flat.n_leaves)
+        sel = list(ev)
+        ids = list(ev_ids)
+        if comm.rank == 0:
+            sel.append(root_pid)
+            ids.append(float(total_pieces))
+        self.piece_sel = backend.index(np.asarray(sel, dtype=np.int64))
+        self.piece_ids = torch.tensor(np.stack([ids, leaf_of[sel]], axis=1), dtype=torch.float64,
+                                      device=dev)
+        kmax_c = comm.max_int(nk)
+        self.kmax_c = kmax_c
+        self.kmax_p = comm.max_int(len(sel))
+        self.recs_c = self.recs_p = None
+
+    def launch(self) -> ShardResult:
+        be, sh, r = self.be, self.sh, self.r
+        pts, est, gof, status = be.fast_run(self.run)
+        out = pts[:sh.n_own]
+        be.range_sums(out, self.child_off, sh.hi - sh.lo, self.sums)
+        recs_c = torch.cat([self.child_ids, self.sums], dim=1)
+        self.recs_c = _gather_records(self.comm, recs_c, self.kmax_c, len(self.plan.root.children))
+        # piece records: [eval position, global leaf index (-1: alignment set), g1, g2, est, status]
+        s = self.piece_sel
+        recs_p = torch.cat([self.piece_ids, gof.index_select(0, s), est.index_select(0, s),
+                            status.index_select(0, s)], dim=1)
+        self.recs_p = _gather_records(self.comm, recs_p, self.kmax_p, self.total_pieces)
+        be.shift_rows(out, _fold_mean(self.recs_c[:, 1:1 + r], self.plan.n))
+        return ShardResult(out, 0, sh.n_own, self.finish, rows_fn=self.rows_of)
+
+    def rows_of(self, k: int) -> np.ndarray:
+        kids = self.plan.root.children
+        lo, hi = shard(len(kids), self.comm.world, k)
+        return (np.concatenate([ch.indices for ch in kids[lo:hi]]) if hi > lo
+                else np.empty(0, dtype=np.int64))
+
+    def _label(self, pos: int) -> str:
+        """Label of the piece at global evaluation position `pos` (error path)."""
+        if pos == self.total_pieces - 1:
+            return "root alignment set"
+        for k in range(self.comm.world):
+            sh = fast_shard(self.plan, self.comm.world, k, self.counts)
+            root_pid = len(sh.flat.piece_off) - 2
+            ev = [pid for pid in sh.flat.eval_order if pid != root_pid]
+            if sh.eval_base <= pos < sh.eval_base + len(ev):
+                return sh.flat.labels[ev[pos - sh.eval_base]]
+        return f"piece {pos + 1}"
+
+    def finish(self):
+        from .primitives import raise_piece_status
+        r = self.r
+        recs = self.recs_p.cpu().numpy()
+        st = decode_status(recs[:, 4 + r:])
+        if np.any(st["code"] == 3):
+            raise InvalidInputError("data contains non-finite values")
+        bad = np.flatnonzero(st["code"] != 0)
+        if bad.size:                                  # first failure in evaluation order
+            raise_piece_status(st[bad[0]], r, self._label(int(recs[bad[0], 0])))
+        leaves = recs[recs[:, 1] >= 0]
+        leaves = leaves[np.argsort(leaves[:, 1], kind="stable")]
+        gof, est = leaves[:, 2:4], leaves[:, 4:4 + r]
+        leaf = iter(range(len(leaves)))
+
+        def agg(node):                                 # algorithms.py:289-320
+            if node.is_leaf:
+                j = next(leaf)
+                return gof[j, 0], gof[j, 1], est[j], node.size
+            fits = [agg(ch) for ch in node.children]
+            sizes = np.array([f[3] for f in fits], dtype=np.float64)
+            tot = sizes.sum()
+            return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
+                    float(np.dot(sizes, [f[1] for f in fits]) / tot),
+                    np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
+
+        g1, g2, e, _ = agg(self.plan.root)
+        return e, float(g1), float(g2)
+
+
+# ================================================================= GPU backend
+class GpuBackend:
+    """Per-rank compute through the C-ABI on the rank's GPU."""
+
+    HEAD_FIXED = 6            # [g1, g2] + est(r) + [status(2), flag, cond] -> 2 + r + 4
+
+    def __init__(self, device):
+        from . import _device as D
+        self.D = D
+        self.device = torch.device(device)
+
+    def index(self, a: np.ndarray) -> torch.Tensor:
+        return self.D.index_tensor(np.asarray(a, dtype=np.int64), self.device)
+
+    def _h(self):
+        return self.D.handle(self.device), self.D.stream_ptr(self.device)
+
+    def dc_run(self, x, row_idx, piece_off, c, r, out, est, gof, status) -> None:
+        h, sp = self._h()
+        off = np.ascontiguousarray(piece_off, dtype=np.int64)
+        h.call("mdsx_divide_conquer_ex", x.data_ptr(), self.D.dtype_code(x), x.shape[1],
+               x.shape[0], x.shape[1], row_idx.data_ptr(), off.ctypes.data, len(off) - 1, c, r,
+               out.data_ptr(), est.data_ptr(), gof.data_ptr(), status.data_ptr(), 1, sp)
+
+    def range_sums(self, out, off_dev, nseg, sums) -> None:
+        if nseg == 0:
+            return
+        h, sp = self._h()
+        h.call("mdsx_segment_colsums", out.data_ptr(), None, off_dev.data_ptr(), nseg,
+               out.shape[1], sums.data_ptr(), sp)
+
+    def shift_rows(self, out, mean) -> None:
+        if out.shape[0] == 0:
+            return
+        h, sp = self._h()
+        mean = mean.contiguous()
+        h.call("mdsx_shift_rows", out.data_ptr(), None, out.shape[0], out.shape[1],
+               mean.data_ptr(), sp)
+
+    def scatter_rows(self, src, idx, out) -> None:
+        h, sp = self._h()
+        src = src.contiguous()
+        h.call("mdsx_scatter_rows", src.data_ptr(), idx.data_ptr(), idx.numel(), out.shape[1],
+               out.data_ptr(), sp)
+
+    # interpolation -------------------------------------------------------
+    def head_len(self, l: int, p: int, r: int) -> int:
+        h = self.D.handle(self.device)
+        return 2 + r + 4 + int(h.lib.mdsx_gower_context_size(l, p, r)) + l * r
+
+    def landmark_head(self, xl, r: int, head) -> None:
+        """head = [g1, g2, est(r), status(2), flag, cond, context, landmark
+        configuration] of the landmark rows `xl` (classical MDS + Gower context)."""
+        from .primitives import classical_pieces
+        D = self.D
+        l, p = xl.shape
+        idx = self._iota(l)
+        pts, est, gof, st = classical_pieces(xl, idx, np.array([0, l], np.int64), r)
+        h, sp = self._h()
+        size = int(h.lib.mdsx_gower_context_size(l, p, r))
+        c0 = 2 + r + 4
+        flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        h.call("mdsx_gower_context", xl.data_ptr(), D.dtype_code(xl), p, p, idx.data_ptr(), l,
+               pts.data_ptr(), r, head[c0:c0 + size].data_ptr(), head[5 + r:6 + r].data_ptr(),
+               flag.data_ptr(), sp)
+        head[0:2] = gof[0]
+        head[2:2 + r] = est[0]
+        head[2 + r:4 + r] = st[0]
+        head[4 + r] = flag[0].to(torch.float64)
+        head[c0 + size:] = pts.reshape(-1)
+
+    def _iota(self, l: int) -> torch.Tensor:
+        key = ("iota", l)
+        cache = self.__dict__.setdefault("_cache", {})
+        if key not in cache:
+            cache[key] = torch.arange(l, dtype=torch.int64, device=self.device)
+        return cache[key]
+
+    def gower_rows(self, head, l: int, r: int, x, out) -> torch.Tensor:
+        """Gower coordinates of every row of x into out; returns the
+        non-finite flag (device scalar, float64)."""
+        D = self.D
+        h, sp = self._h()
+        p = x.shape[1]
+        nf = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if x.shape[0]:
+            h.call("mdsx_gower_interpolate", head[2 + r + 4:].data_ptr(), l, p, r, x.data_ptr(),
+                   D.dtype_code(x), p, x.shape[0], out.data_ptr(), r, nf.data_ptr(), 1, sp)
+        return nf[0].to(torch.float64)
+
+    # fast ----------------------------------------------------------------
+    def fast_prepare(self, x, plan, flat, r):
+        from .algorithms import FastRun
+        return FastRun(x, plan, r, flat=flat, local=True)
+
+    def fast_run(self, run):
+        run.launch()
+        return run.pts, run.est, run.gof, run.status
+
+
+# ================================================================= entry points
+def sharded_divide_and_conquer(backend, x_local, n: int, params: AlgorithmParams, comm: Comm,
+                               plan: DcPlan | None = None) -> ShardResult:
+    """divide_and_conquer_mds (algorithms.py:128-172) over comm.world ranks;
+    returns this rank's finished share (fit figures filled)."""
+    prm = params.resolved("divide")
+    plan = plan if plan is not None else plan_divide_conquer(n, prm.l, prm.c, prm.seed)
+    return ShardedDivide(backend, x_local, plan, prm.r, comm).launch().finish()
+
+
+def sharded_interpolation(backend, x_local, n: int, params: AlgorithmParams, comm: Comm,
+                          sample: np.ndarray | None = None, x_landmarks=None) -> ShardResult:
+    prm = params.resolved("interpolate")
+    sample = sample if sample is not None else interpolation_sample(n, prm.l, prm.seed)
+    return ShardedInterpolation(backend, x_local, n, sample, prm.r, comm,
+                                x_landmarks).launch().finish()
+
+
+def sharded_fast(backend, x_local, n: int, params: AlgorithmParams, comm: Comm,
+                 plan: FastPlan | None = None) -> ShardResult:
+    prm = params.resolved("fast")
+    plan = plan if plan is not None else plan_fast(n, prm.l, prm.s, prm.seed)
+    return ShardedFast(backend, x_local, plan, prm.r, comm).launch().finish()
+
+
+def local_rows(algo: str, plan, n: int, world: int, rank: int) -> np.ndarray:
+    """Global row ids of the local matrix rank `rank` needs, in order."""
+    if algo == "divide":
+        return dc_shard(plan, world, rank).local_rows
+    if algo == "fast":
+        return fast_shard(plan, world, rank).local_rows
+    return interp_shard(n, np.asarray(plan, dtype=np.int64), world, rank).local_rows
+
+
+def to_configuration(res: ShardResult, points) -> MdsConfiguration:
+    res.finish()
+    return MdsConfiguration(points, res.estimates, res.gof_g1, res.gof_g2)

@@ -197,12 +197,15 @@ def classical_mds(delta, r: int, *, exact_guard: int = EXACT_SIZE_GUARD, device=
     if n > JACOBI_KMAX:
         # beyond the in-kernel full-spectrum solver: the top-r pairs come from
         # the block-Krylov kernels below; the full spectrum that G1/G2 and the
-        # DegenerateRank rule need (classical.py:88-150) from cuSOLVER's
-        # eigenvalue-only routine on the device (a library call, off the hot path)
+        # DegenerateRank rule need (classical.py:88-150) from the device
+        # tridiagonalisation + bisection (mdsx_sym_eigvals)
         q = D.empty((n, n), dev)
-        D.handle(dev).call("mdsx_double_center", d.data_ptr(), n, q.data_ptr(), D.stream_ptr(dev))
-        ev = torch.linalg.eigvalsh(q).cpu().numpy()[::-1].copy()
-        del q
+        w = D.empty((n,), dev)
+        h = D.handle(dev)
+        h.call("mdsx_double_center", d.data_ptr(), n, q.data_ptr(), D.stream_ptr(dev))
+        h.call("mdsx_sym_eigvals", q.data_ptr(), n, w.data_ptr(), D.stream_ptr(dev))
+        ev = w.cpu().numpy()[::-1].copy()
+        del q, w
         ev = np.delete(ev, int(np.argmin(np.abs(ev))))          # the structural zero (Q 1 = 0)
         ev[np.abs(ev) <= EIGENVALUE_ZERO_TOL * float(np.abs(ev).max(initial=0.0))] = 0.0
         bad = np.nonzero(ev[:r] <= 0.0)[0]
@@ -324,7 +327,7 @@ def gower_interpolate(ctx: GowerContext, new_rows, *, device=None) -> np.ndarray
     nf = torch.zeros(1, dtype=torch.int32, device=dev)
     D.handle(dev).call("mdsx_gower_interpolate", ctx.device_ctx.data_ptr(), ctx.l, p, r,
                        y.data_ptr(), D.dtype_code(y), p, m, out.data_ptr(), r, nf.data_ptr(),
-                       D.stream_ptr(dev))
+                       0, D.stream_ptr(dev))
     if int(nf.item()):
         raise InvalidInputError("new_rows contains non-finite values")
     return out.cpu().numpy()

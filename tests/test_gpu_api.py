@@ -457,3 +457,88 @@ def test_fast_finish_c_abi(cuda):
     got = out.cpu().numpy()
     assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
     assert np.abs(got.mean(axis=0)).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("nbytes,dtype", [(5 << 20, np.float64), ((100 << 20) + 24, np.float64),
+                                          ((37 << 20) + 4, np.float32)])
+def test_staged_h2d(cuda, nbytes, dtype):
+    """mdsx_h2d: pageable host -> device through the pinned chunk rings of the
+    host thread pool, exact, with odd sizes (last chunk partial) and the
+    source overwritten right after the call returns."""
+    from paper_2007_11919_b200 import _device as D
+    count = nbytes // np.dtype(dtype).itemsize
+    src = np.random.default_rng(count).standard_normal(count).astype(dtype)
+    want = src.copy()
+    got = D.from_host(src, cuda)
+    src[:] = -1.0                                     # the call has finished reading the source
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_two_threads_share_a_handle(cuda):
+    """Two host threads on two torch streams call the library through ONE
+    handle (shared workspace and staging): each result equals its
+    single-threaded run bitwise (calls are serialised and stream-ordered)."""
+    import threading
+
+    import torch
+    import paper_2007_11919_b200 as mds_
+    from paper_2007_11919_b200.synthetic import scenario
+    xs = [scenario(40_000, 30, 5, seed=s) for s in (1, 2)]
+    prm = [mds_.AlgorithmParams(r=5, l=700, c=12, seed=3), mds_.AlgorithmParams(r=5, l=900, seed=4)]
+    names = ["divide", "interpolate"]
+    want = [mds_.run_algorithm(nm, x, p) for nm, x, p in zip(names, xs, prm)]
+    got = [None, None]
+
+    def work(i):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(4):
+                got[i] = mds_.run_algorithm(names[i], xs[i], prm[i])
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for a, b in zip(got, want):
+        assert np.array_equal(a.points, b.points)
+        assert np.array_equal(a.eigenvalue_estimates, b.eigenvalue_estimates)
+
+
+@pytest.mark.parametrize("n,kind", [(1, "rand"), (2, "rand"), (3, "rand"), (113, "rand"),
+                                    (300, "centred_delta"), (257, "clustered"), (640, "low_rank"),
+                                    (1500, "rand")])
+def test_sym_eigvals_against_lapack(cuda, n, kind):
+    """mdsx_sym_eigvals (Householder tridiagonalisation + bisection, no library
+    call) against LAPACK dsyevd: every eigenvalue within 1e-12 ||A||, for
+    indefinite, clustered (repeated) and rank-deficient spectra."""
+    import torch
+    from paper_2007_11919_b200 import _device as D
+    rng = np.random.default_rng(n)
+    if kind == "rand":
+        a = rng.standard_normal((n, n))
+        a = a + a.T
+    elif kind == "centred_delta":                 # doubly centred non-Euclidean delta
+        x = rng.standard_normal((n, 5))
+        d = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1) + rng.uniform(0, 0.3, (n, n))
+        d = (d + d.T) / 2
+        np.fill_diagonal(d, 0)
+        j = np.eye(n) - 1.0 / n
+        a = -0.5 * j @ d @ j
+    elif kind == "clustered":
+        q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = np.repeat([5.0, -2.0, 1e-3, 0.0], (n + 3) // 4)[:n]
+        a = (q * lam) @ q.T
+        a = (a + a.T) / 2
+    else:
+        y = rng.standard_normal((n, 7))
+        a = y @ y.T
+    want = np.linalg.eigvalsh(a)
+    ad = torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+    w = D.empty((n,), cuda)
+    D.handle(cuda).call("mdsx_sym_eigvals", ad.data_ptr(), n, w.data_ptr(), D.stream_ptr(cuda))
+    got = w.cpu().numpy()
+    scale = max(np.abs(want).max(), 1e-300)
+    assert np.abs(got - want).max() <= 1e-12 * scale * max(1.0, n / 500), (
+        np.abs(got - want).max() / scale)
+    assert np.array_equal(ad.cpu().numpy(), a)      # input untouched
