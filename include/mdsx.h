@@ -30,7 +30,9 @@
  *   mdsx_fast_finish        <- the root's child alignment (algorithms.py:310-311) +
  *                              points[root.indices] = block (:341-342) + _recentered
  *                              (:122-125) in one pass
- * fast_mds (algorithms.py:323-348) is composed from mdsx_classical_pieces,
+ *   mdsx_fast_mds           <- fast_mds (algorithms.py:285-348) for plans with form-0
+ *                              leaves (the BASELINE shapes), one call
+ * Other fast_mds plans (algorithms.py:323-348) are composed from mdsx_classical_pieces,
  * mdsx_procrustes_fit/apply and mdsx_fast_finish (or mdsx_scatter_rows +
  * mdsx_recenter) by the host.
  */
@@ -173,6 +175,34 @@ int mdsx_scatter_rows(mdsx_handle* h, const double* src, const int64_t* idx, int
                       int32_t r, double* out, void* stream);
 /* points (n x r) -= column means (fixed-order, deterministic reduction). */
 int mdsx_recenter(mdsx_handle* h, double* points, int64_t n, int32_t r, void* stream);
+/* fast_mds (algorithms.py:285-348) in one call for plans whose leaves are
+ * all form 0 (more rows than features) with p <= 128, r <= 16 and 16-byte
+ * aligned rows: classical MDS of every leaf and alignment set (eigenpairs;
+ * points only for the alignment sets and the tracked rows), the Procrustes
+ * fits level by level (deepest first), and ONE pass over the leaf rows
+ * writing out[out_idx[i]] = (x - mu_leaf) U_leaf T_tot + t_tot (- the column
+ * mean when recenter != 0, algorithms.py:122-125).  The plan arrays come
+ * from the host flattener (paper_2007_11919_b200.plans.fast_route). */
+typedef struct mdsx_fast_plan {
+  int32_t npieces, n_leaves, nlevels;
+  const int64_t* piece_off;   /* host, npieces + 1: leaves (DFS order) then alignment sets */
+  const int64_t* row_idx;     /* device, piece_off[npieces] data rows */
+  const int64_t* out_idx;     /* device, piece_off[n_leaves]: output row of every leaf row */
+  int64_t ntracked;
+  const int64_t* trk_row;     /* device: data row of every tracked row */
+  const int32_t* trk_leaf;    /* device: its leaf */
+  const int32_t* level_njobs; /* host, nlevels (deepest first) */
+  const int64_t* job_off;     /* host, per level njobs + 1 entries, concatenated */
+  const int64_t* job_src;     /* device: tracked-row ids of each job's samples, concatenated */
+  const int64_t* job_tgt;     /* device: alignment-set point rows (targets), concatenated */
+  const int32_t* trk_job;     /* device, nlevels x ntracked: job at that level or -1 */
+  const int32_t* leaf_job;    /* device, nlevels x n_leaves: job at that level or -1 */
+} mdsx_fast_plan;
+int mdsx_fast_mds(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                  const mdsx_fast_plan* plan, int32_t r, int64_t n_out, int32_t recenter,
+                  double* out, double* estimates, double* gof, mdsx_piece_status* status,
+                  void* stream);
+
 /* out[order[i]] = P[i] @ rot_j + trans_j - mean for the rows i of job j
  * (HOST job_off: njobs+1 offsets covering 0..n), mean = the column mean of
  * the result (from per-job sums pushed through each fit; fixed order). */

@@ -23,6 +23,15 @@ class PieceStatus(C.Structure):
     _fields_ = [("code", C.c_int32), ("index", C.c_int32), ("value", C.c_double)]
 
 
+class FastPlanC(C.Structure):
+    """mdsx_fast_plan (include/mdsx.h)."""
+    _fields_ = [("npieces", C.c_int32), ("n_leaves", C.c_int32), ("nlevels", C.c_int32),
+                ("piece_off", C.c_void_p), ("row_idx", C.c_void_p), ("out_idx", C.c_void_p),
+                ("ntracked", C.c_int64), ("trk_row", C.c_void_p), ("trk_leaf", C.c_void_p),
+                ("level_njobs", C.c_void_p), ("job_off", C.c_void_p), ("job_src", C.c_void_p),
+                ("job_tgt", C.c_void_p), ("trk_job", C.c_void_p), ("leaf_job", C.c_void_p)]
+
+
 _vp = C.c_void_p
 _i32 = C.c_int32
 _i64 = C.c_int64
@@ -55,6 +64,8 @@ SIGNATURES = {
     "mdsx_procrustes_apply": (_int, [_vp, _vp, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
     "mdsx_scatter_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_recenter": (_int, [_vp, _vp, _i64, _i32, _vp]),
+    "mdsx_fast_mds": (_int, [_vp, _vp, _int, _i64, _i32, C.POINTER(FastPlanC), _i32, _i64, _i32,
+                              _vp, _vp, _vp, _vp, _vp]),
     "mdsx_fast_finish": (_int, [_vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp]),
     "mdsx_divide_conquer": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
                                    _vp, _vp, _vp, _vp, _vp]),

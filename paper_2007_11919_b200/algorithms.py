@@ -23,7 +23,7 @@ import torch
 from . import _device as D
 from .errors import InvalidInputError, NumericalError, ParamError
 from .params import ALGORITHM_NAMES, AlgorithmParams
-from .plans import (DcPlan, FastPlan, InterpPlan, flatten_fast, flatten_subsets,
+from .plans import (DcPlan, FastPlan, InterpPlan, fast_route, flatten_fast, flatten_subsets,
                     flatten_subsets_cached,
                     interpolation_sample, plan_divide_conquer, plan_fast)
 from .primitives import classical_mds_from_data, raise_piece_status
@@ -161,6 +161,14 @@ class FastRun:
         self.dev = dev = x.device
         flat = self.flat = flat if flat is not None else flatten_fast(plan)
         self.piece_rows = D.index_tensor(flat.piece_rows, dev)
+        npc = len(flat.piece_off) - 1
+        self.est = D.empty((npc, r), dev)
+        self.gof = D.empty((npc, 2), dev)
+        self.status = D.status_tensor(npc, dev)
+        self.route = None
+        if _fast_route_ok(x, flat, r):
+            self._setup_route(flat, plan, r, dev, local)
+            return
         self.order = D.index_tensor(flat.order, dev)
         self.levels = []
         for lv in flat.levels:
@@ -171,12 +179,8 @@ class FastRun:
                 length=D.index_tensor(lv.length, dev), max_len=int(lv.length.max()), nj=nj,
                 rot=D.empty((nj, r, r), dev), trans=D.empty((nj, r), dev),
                 loss=D.empty((nj,), dev), deg=torch.empty(nj, dtype=torch.int32, device=dev)))
-        npc = len(flat.piece_off) - 1
         total = int(flat.piece_off[-1])
         self.pts = D.empty((total, r), dev)
-        self.est = D.empty((npc, r), dev)
-        self.gof = D.empty((npc, 2), dev)
-        self.status = D.status_tensor(npc, dev)
         self.out = None if local else D.empty((plan.n, r), dev)
         # the shallowest level's jobs tile rows 0..n of the working buffer
         # contiguously: its apply, the scatter and the re-centring run as one
@@ -190,9 +194,51 @@ class FastRun:
                     and np.array_equal(off[1:-1], st_[:-1] + ln_[:-1])):
                 self.finish_off = np.ascontiguousarray(off)
 
+    def _setup_route(self, flat, plan, r, dev, local):
+        """mdsx_fast_mds (one call: no leaf point matrices, fused output
+        pass) for plans with form-0 leaves (k_dcout.cu)."""
+        import ctypes as C
+
+        from ._lib import FastPlanC
+        rt = fast_route(flat)
+        nl = flat.n_leaves
+        leaf_total = int(flat.piece_off[nl])
+        keep = self._keep = {
+            "piece_off": np.ascontiguousarray(flat.piece_off, dtype=np.int64),
+            "level_njobs": np.ascontiguousarray(rt.level_njobs, dtype=np.int32),
+            "job_off": np.ascontiguousarray(rt.job_off, dtype=np.int64),
+            "trk_row": D.index_tensor(rt.trk_row, dev),
+            "trk_leaf": torch.from_numpy(np.ascontiguousarray(rt.trk_leaf, np.int32)).to(dev),
+            "job_src": D.index_tensor(rt.job_src, dev),
+            "job_tgt": D.index_tensor(rt.job_tgt, dev),
+            "trk_job": torch.from_numpy(np.ascontiguousarray(rt.trk_job, np.int32)).to(dev),
+            "leaf_job": torch.from_numpy(np.ascontiguousarray(rt.leaf_job, np.int32)).to(dev),
+        }
+        if local:
+            keep["out_idx"] = torch.arange(leaf_total, dtype=torch.int64, device=dev)
+            self.out = D.empty((leaf_total, r), dev)
+            self.pts = self.out               # the rank's rows in DFS order (distributed.py)
+        else:
+            keep["out_idx"] = self.piece_rows[:leaf_total]
+            self.out = D.empty((plan.n, r), dev)
+        ptr = lambda a: a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()  # noqa: E731
+        self.route = FastPlanC(
+            len(flat.piece_off) - 1, nl, len(rt.level_njobs), ptr(keep["piece_off"]),
+            self.piece_rows.data_ptr(), keep["out_idx"].data_ptr(), len(rt.trk_row),
+            ptr(keep["trk_row"]), ptr(keep["trk_leaf"]), ptr(keep["level_njobs"]),
+            ptr(keep["job_off"]), ptr(keep["job_src"]), ptr(keep["job_tgt"]),
+            ptr(keep["trk_job"]), ptr(keep["leaf_job"]))
+        self._route_ref = C.byref(self.route)
+
     def launch(self) -> None:
         x, r, dev = self.x, self.r, self.dev
         h, sp = D.handle(dev), D.stream_ptr(dev)
+        if self.route is not None:
+            h.call("mdsx_fast_mds", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[1],
+                   self._route_ref, r, self.out.shape[0], 0 if self.local else 1,
+                   self.out.data_ptr(), self.est.data_ptr(), self.gof.data_ptr(),
+                   self.status.data_ptr(), sp)
+            return
         npc = len(self.flat.piece_off) - 1
         h.call("mdsx_classical_pieces", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[1],
                self.piece_rows.data_ptr(), self.flat.piece_off.ctypes.data, npc, r,
@@ -242,6 +288,20 @@ class FastRun:
 
         g1, g2, e, _ = agg(self.plan.root)
         return MdsConfiguration(_finish_points(self.out, return_device), e, float(g1), float(g2))
+
+
+def _fast_route_ok(x: torch.Tensor, flat, r: int) -> bool:
+    """mdsx_fast_mds handles plans whose leaves all have more rows than
+    features, with p <= 128, r <= 16 and 16-byte aligned rows."""
+    import os
+    p = x.shape[1]
+    if os.environ.get("MDSX_FAST_PIECES") or not flat.levels:
+        return False
+    if not (p <= 128 and r <= 16 and (p * x.element_size()) % 16 == 0 and x.data_ptr() % 16 == 0
+            and x.is_contiguous()):
+        return False
+    sizes = np.diff(np.asarray(flat.piece_off[:flat.n_leaves + 1]))
+    return bool(np.all(sizes > p))
 
 
 def fast_mds(data, params: AlgorithmParams, *, threads=None, device=None,

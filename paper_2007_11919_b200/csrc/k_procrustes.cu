@@ -754,6 +754,50 @@ __global__ void seg_colsum_kernel(const double* __restrict__ X, const int64_t* _
   if (lane == 0) sums[(int64_t)seg * r + c] = s;
 }
 
+// Contiguous segments (no row index): one CTA per segment streams the
+// segment's r * len doubles coalesced; the stride S = r * floor(T / r) keeps
+// thread t on column t % r, so each thread accumulates one column and the
+// per-column partials are folded in fixed thread order (deterministic).
+constexpr int SR_T = 500;
+__global__ void __launch_bounds__(SR_T)
+seg_colsum_rows_kernel(const double* __restrict__ X, const int64_t* __restrict__ off, int r,
+                       double* __restrict__ sums) {
+  __shared__ double red[SR_T];
+  const int t = threadIdx.x;
+  const int S = r * (SR_T / r);
+  const int64_t a = off[blockIdx.x] * r, b = off[blockIdx.x + 1] * r;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (t < S) {
+    int64_t e = a + t;
+    for (; e + 3 * S < b; e += 4 * S) {
+      s0 += X[e];
+      s1 += X[e + S];
+      s2 += X[e + 2 * S];
+      s3 += X[e + 3 * S];
+    }
+    for (; e < b; e += S) s0 += X[e];
+  }
+  red[t] = t < S ? (s0 + s1) + (s2 + s3) : 0.0;
+  __syncthreads();
+  if (t < r) {
+    double tot = 0.0;
+    for (int u = t; u < S; u += r) tot += red[u];
+    sums[(int64_t)blockIdx.x * r + t] = tot;
+  }
+}
+
+// X[0..n) rows -= shift: grid-stride over the n * r doubles with a stride that
+// is a multiple of r (each thread keeps one column's shift in a register)
+__global__ void __launch_bounds__(SR_T)
+shift_all_kernel(double* __restrict__ X, int64_t total, int r, const double* __restrict__ shift) {
+  const int t = threadIdx.x;
+  const int S = r * (SR_T / r);
+  if (t >= S) return;
+  const double sh = shift[t % r];
+  const int64_t step = (int64_t)gridDim.x * S;
+  for (int64_t e = (int64_t)blockIdx.x * S + t; e < total; e += step) X[e] -= sh;
+}
+
 __global__ void shift_rows_kernel(double* __restrict__ X, const int64_t* __restrict__ idx, int64_t n,
                                   int r, const double* __restrict__ shift) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -888,6 +932,11 @@ namespace mdsx {
 int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const int64_t* off,
                       int nseg, int r, double* sums, cudaStream_t st) {
   if (nseg == 0) return MDSX_OK;
+  if (!idx && r <= 32) {
+    mdsx::pre(h, st);
+    seg_colsum_rows_kernel<<<nseg, SR_T, 0, st>>>(X, off, r, sums);
+    return launched(h, "seg_colsum_kernel", st);
+  }
   const int64_t threads = (int64_t)nseg * r * 32;
   mdsx::pre(h, st);
   seg_colsum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(X, idx, off, nseg, r, sums);
@@ -897,6 +946,14 @@ int launch_seg_colsum(mdsx_handle* h, const double* X, const int64_t* idx, const
 int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, int r,
                       const double* shift, cudaStream_t st) {
   if (n == 0) return MDSX_OK;
+  if (!idx && r <= 32) {
+    const int64_t total = n * r;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 4 * SR_T - 1) / (4 * SR_T),
+                                                                  (int64_t)h->num_sms * 4));
+    mdsx::pre(h, st);
+    shift_all_kernel<<<blocks, SR_T, 0, st>>>(X, total, r, shift);
+    return launched(h, "shift_rows_kernel", st);
+  }
   mdsx::pre(h, st);
   shift_rows_kernel<<<(unsigned)((n * r + 255) / 256), 256, 0, st>>>(X, idx, n, r, shift);
   return launched(h, "shift_rows_kernel", st);

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -85,6 +86,37 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
 // last error message of the calling thread (calls from several threads on one
 // handle each read their own message)
 static thread_local std::string t_last_error;
+bool dc_out_route_ok(const void* data, int dtype, int64_t ld, int p, int r, int c);
+size_t dc_out_ws_doubles(int npieces, int p, int r, int c, int64_t m0);
+int launch_dc_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                     const int64_t* row_idx, const PieceDesc* pd, int npieces, int r, int c,
+                     int64_t m0, const double* mu, double* U, double* Pc, double* Pa,
+                     cudaStream_t st);
+int launch_dc_conn(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                   const int64_t* row_idx, const PieceDesc* pd, int pbase, int count, int r, int c,
+                   const double* mu, const double* U, double* Pc, cudaStream_t st);
+int launch_dc_compose(mdsx_handle* h, const PieceDesc* pd, int pbase, int count, int p, int r, int c,
+                      const double* U, const double* rot, const double* trans, const double* Pc,
+                      double* Uc, double* tvec, double* contrib, cudaStream_t st);
+int launch_piece_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                     const int64_t* row_idx, const int64_t* out_idx, const PieceDesc* pd,
+                     int npieces, int64_t max_m, int r, int c0, const double* mu, const double* Uc,
+                     const double* tvec, const double* mean, double* out, cudaStream_t st);
+int launch_dc_recentre(mdsx_handle* h, const double* contrib, int npieces, int r, int64_t n,
+                       double* mean, double* out, cudaStream_t st);
+int launch_trk_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                      const int64_t* trk_row, const int32_t* trk_leaf, int64_t ntrk,
+                      const PieceDesc* pd, int r, const double* mu, const double* U, double* P,
+                      cudaStream_t st);
+int launch_trk_apply(mdsx_handle* h, double* P, const int32_t* job, int64_t ntrk, int r,
+                     const double* rot, const double* trans, cudaStream_t st);
+int launch_fast_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                    const int64_t* row_idx, const int64_t* out_idx, const PieceDesc* pd, int nleaves,
+                    int64_t max_m, int nlev, const int32_t* leaf_job, const int64_t* lev_jbase,
+                    int r, const double* mu, const double* U, const double* rot, const double* trans,
+                    double* Uc, double* tvec, double* contrib, double* mean, int64_t n_recenter,
+                    double* out, cudaStream_t st);
+size_t points_ws_bytes(int npieces, int64_t max_m, int r);
 size_t eigvals_ws_doubles(int64_t n);
 int launch_sym_eigvals(mdsx_handle* h, const double* A, int64_t n, double* w, double* ws,
                        cudaStream_t st);
@@ -305,10 +337,25 @@ static size_t classical_ws_bytes(const ClassicalPlan& cp, int p, int r) {
 }
 
 // Runs K2 -> K1 -> K3 -> points for all pieces.  Workspace must be reserved.
+// Device buffers of a run_classical call that later stages of the same call
+// reuse (workspace of this call).
+struct ClassicalOut {
+  PieceDesc* dpd = nullptr;
+  double* mu = nullptr;
+  double* U = nullptr;
+  double* lam = nullptr;
+  // called once per piece chunk [j0, j1) right after its eigenpairs, on the
+  // stream that solved it (the piece pipeline's chunk streams, or the caller's
+  // stream for the whole batch): later stages of a chunk overlap the next
+  // chunk's eigensolver
+  std::function<int(int, int, cudaStream_t)> after_chunk;
+};
+
+// points == nullptr: eigenpairs only (no point matrices, no points epilogue).
 static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* data, int dtype,
                          int64_t ld, int p, const int64_t* row_idx, int r, double* points,
                          double* estimates, double* gof, mdsx_piece_status* status,
-                         cudaStream_t st) {
+                         cudaStream_t st, ClassicalOut* co = nullptr) {
   const int np = (int)cp.pd.size();
   PieceDesc* dpd = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
   PieceDesc* dpd_jac = (PieceDesc*)ws_alloc(h, np * sizeof(PieceDesc), st);
@@ -326,6 +373,7 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   double* lam = (double*)ws_alloc(h, (size_t)np * r * sizeof(double), st);
   double2* cand = (double2*)ws_alloc(h, points_ws_bytes(np, cp.max_m, r), st);
   if (!dpd || !dtiles || !mu || !A || !U || !lam || !cand) return MDSX_CUDA;
+  if (co) { co->dpd = dpd; co->mu = mu; co->U = U; co->lam = lam; }
   const int nsplit = (int)cp.pd_split.size();
   double* A_sp = nullptr;
   double* mu_sp = nullptr;
@@ -378,7 +426,7 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     // other CTA's Krylov phase; the points kernel then only takes the pieces
     // the epilogue left pending (Jacobi fallback / non-finite input)
     const size_t es = dtype == MDSX_F32 ? 4 : 8;
-    const bool fuse = simple && r <= 10 && data != nullptr && ((size_t)p * es) % 16 == 0 &&
+    const bool fuse = simple && r <= 10 && data != nullptr && points != nullptr && ((size_t)p * es) % 16 == 0 &&
                       ((size_t)ld * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(data) & 15) == 0 &&
                       !getenv("MDSX_POINTS_TILED") && !getenv("MDSX_NO_FUSE");
     int* pending = fuse ? (int*)ws_alloc(h, (size_t)np * sizeof(int), st) : nullptr;
@@ -407,9 +455,10 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
         if ((rc = launch_jacobi_fallback(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
                                          status, s)))
           return rc;
-        if ((rc = launch_points(h, data, dtype, ld, p, ridx, dpd + j0, n, cp.max_m, r, mu, U, lam,
-                                points, cand, s, true, pending)))
+        if (points && (rc = launch_points(h, data, dtype, ld, p, ridx, dpd + j0, n, cp.max_m, r, mu,
+                                          U, lam, points, cand, s, true, pending)))
           return rc;
+        if (co && co->after_chunk && (rc = co->after_chunk(j0, j1, s))) return rc;
       }
       cudaEventRecord(h->ev_join, h->aux);
       return cuda_check(h, cudaStreamWaitEvent(st, h->ev_join, 0), "pipeline join");
@@ -456,6 +505,8 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
   if (!cp.pd_big.empty() &&
       (rc = run_big_pieces(h, cp.pd_big, A, r, U, lam, estimates, gof, status, st, stage_put)))
     return rc;
+  if (co && co->after_chunk && (rc = co->after_chunk(0, np, st))) return rc;
+  if (!points) return MDSX_OK;
   return launch_points(h, data, dtype, ld, p, ridx, dpd, np, cp.max_m, r, mu, U, lam, points,
                        cand, st, cp.pd_f1.empty());
 }
@@ -493,6 +544,7 @@ void mdsx_destroy(mdsx_handle* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ws_done) cudaEventDestroy(h->ws_done);
+  if (h->ev_anchor) cudaEventDestroy(h->ev_anchor);
   delete h;
 }
 
@@ -796,6 +848,91 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
   }
   const int nj = std::max(npieces - 1, 0);
   const size_t fit_rows = (size_t)nj * c;
+  const bool rec = !(flags & MDSX_NO_RECENTER);
+  // form-0 pieces, aligned rows: no per-piece point matrices -- anchor signs
+  // and connecting-row points only, fits, then one fused output pass
+  // (k_dcout.cu); otherwise points of every piece, fits, stitch
+  if (npieces > 1 && cp.pd_f1.empty() && dc_out_route_ok(data, dtype, ld, p, r, c) &&
+      !getenv("MDSX_DC_POINTS")) {
+    const int64_t m0 = piece_off[1] - piece_off[0];
+    const size_t need = classical_ws_bytes(cp, p, r) + align_up(dc_out_ws_doubles(npieces, p, r, c, m0) * 8) + 4096 +
+                        align_up(fit_rows * sizeof(int64_t)) * 2 +
+                        align_up((size_t)(nj + 1) * sizeof(int64_t)) +
+                        align_up((size_t)nj * r * r * sizeof(double)) +
+                        align_up((size_t)nj * r * sizeof(double)) + align_up(nj * sizeof(double)) +
+                        align_up(nj * sizeof(int32_t)) + 8192;
+    if ((rc = ws_reserve(h, need))) return rc;
+    double* Pc = (double*)ws_alloc(h, (size_t)npieces * c * r * sizeof(double), st);
+    double* Uc = (double*)ws_alloc(h, (size_t)npieces * p * r * sizeof(double), st);
+    double* contrib = (double*)ws_alloc(h, (size_t)npieces * r * sizeof(double), st);
+    double* tvec = (double*)ws_alloc(h, (size_t)npieces * r * sizeof(double), st);
+    double* Pa = (double*)ws_alloc(h, (size_t)m0 * r * sizeof(double), st);
+    double* mean = (double*)ws_alloc(h, 64 * sizeof(double), st);
+    double* zero = (double*)ws_alloc(h, 64 * sizeof(double), st);
+    double* rot = (double*)ws_alloc(h, (size_t)nj * r * r * sizeof(double), st);
+    double* trans = (double*)ws_alloc(h, (size_t)nj * r * sizeof(double), st);
+    int64_t* trows = (int64_t*)ws_alloc(h, fit_rows * sizeof(int64_t), st);
+    int64_t* srows = (int64_t*)ws_alloc(h, fit_rows * sizeof(int64_t), st);
+    int64_t* joff = (int64_t*)ws_alloc(h, (size_t)(nj + 1) * sizeof(int64_t), st);
+    double* loss = (double*)ws_alloc(h, nj * sizeof(double), st);
+    int32_t* degen = (int32_t*)ws_alloc(h, nj * sizeof(int32_t), st);
+    if (!Pc || !Uc || !contrib || !tvec || !Pa || !mean || !zero || !rot || !trans || !trows ||
+        !srows || !joff || !loss || !degen)
+      return MDSX_CUDA;
+    std::vector<int64_t> ht(fit_rows), hs(fit_rows), hj(nj + 1);
+    for (int j = 0; j < nj; ++j) {
+      hj[j] = (int64_t)j * c;
+      for (int t = 0; t < c; ++t) {
+        ht[(size_t)j * c + t] = t;                              // anchor rows 0..c-1
+        hs[(size_t)j * c + t] = (int64_t)(j + 1) * c + t;       // piece j+1 connecting rows
+      }
+    }
+    hj[nj] = (int64_t)nj * c;
+    {
+      Stager sg(h, st);
+      if ((rc = sg.begin(fit_rows * 16 + (nj + 1) * 8 + 1024))) return rc;
+      if ((rc = sg.put(trows, ht.data(), fit_rows * sizeof(int64_t)))) return rc;
+      if ((rc = sg.put(srows, hs.data(), fit_rows * sizeof(int64_t)))) return rc;
+      if ((rc = sg.put(joff, hj.data(), (nj + 1) * sizeof(int64_t)))) return rc;
+      if ((rc = sg.end())) return rc;
+    }
+    if ((rc = cuda_check(h, cudaMemsetAsync(zero, 0, 64 * sizeof(double), st), "memset"))) return rc;
+    if (!h->ev_anchor) cudaEventCreateWithFlags(&h->ev_anchor, cudaEventDisableTiming);
+    // per chunk of pieces, on the stream that solved it: anchor signs (chunk 0),
+    // connecting points, fits, U' = U T, output rows (not yet re-centred)
+    ClassicalOut co;
+    co.after_chunk = [&](int j0, int j1, cudaStream_t s) -> int {
+      int e;
+      if (j0 == 0) {
+        if ((e = launch_dc_points(h, data, dtype, ld, p, row_idx, co.dpd, 1, r, c, m0, co.mu, co.U,
+                                  Pc, Pa, s)))
+          return e;
+        cudaEventRecord(h->ev_anchor, s);
+      } else {
+        cudaStreamWaitEvent(s, h->ev_anchor, 0);
+      }
+      const int a0 = std::max(j0, 1);
+      if (j1 > a0) {
+        if ((e = launch_dc_conn(h, data, dtype, ld, p, row_idx, co.dpd, a0, j1 - a0, r, c, co.mu,
+                                co.U, Pc, s)))
+          return e;
+        if ((e = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff + (a0 - 1), j1 - a0, r,
+                                       rot + (size_t)(a0 - 1) * r * r, trans + (size_t)(a0 - 1) * r,
+                                       loss + (a0 - 1), degen + (a0 - 1), s)))
+          return e;
+      }
+      if ((e = launch_dc_compose(h, co.dpd, j0, j1 - j0, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
+                                 contrib, s)))
+        return e;
+      return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd + j0, j1 - j0, cp.max_m,
+                              r, c, co.mu, Uc + (size_t)j0 * p * r, tvec + (size_t)j0 * r, zero, out, s);
+    };
+    if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, nullptr, estimates, gof, status,
+                            st, &co)))
+      return rc;
+    if (!rec) return MDSX_OK;
+    return launch_dc_recentre(h, contrib, npieces, r, n, mean, out, st);
+  }
   const size_t need = classical_ws_bytes(cp, p, r) + align_up(cp.total * r * sizeof(double)) +
                       align_up(fit_rows * sizeof(int64_t)) * 2 +
                       align_up((size_t)(nj + 1) * sizeof(int64_t)) +
@@ -842,7 +979,6 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
   }
   // stitch + final re-centring in one pass over P: the column mean comes from
   // per-piece sums of P pushed through each fit (no second pass over out)
-  const bool rec = !(flags & MDSX_NO_RECENTER);
   double* sws = rec ? (double*)ws_alloc(h, dc_stitch_ws_bytes(npieces, r, cp.max_m), st) : nullptr;
   if (rec && !sws) return MDSX_CUDA;
   return launch_dc_stitch(h, P, row_idx, toff, npieces, cp.max_m, c, r, rot, trans, out, st,
@@ -957,4 +1093,106 @@ extern "C" int mdsx_aligned_correlations(mdsx_handle* h, const double* points, i
   if (!part) return MDSX_CUDA;
   return launch_aligned_corr(h, points, n, r, dominant, dtype, ld, part, corr, rotation, zero_var,
                              st);
+}
+
+// fast_mds in one call (include/mdsx.h): see k_dcout.cu for the tail.
+extern "C" int mdsx_fast_mds(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                             const mdsx_fast_plan* fp, int32_t r, int64_t n_out, int32_t recenter,
+                             double* out, double* estimates, double* gof, mdsx_piece_status* status,
+                             void* stream) {
+  using namespace mdsx;
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if (!fp || fp->npieces < 2 || fp->n_leaves < 1 || fp->n_leaves >= fp->npieces || fp->nlevels < 1)
+    return fail(h, MDSX_PARAM, "bad fast plan");
+  const int np = fp->npieces, nl = fp->n_leaves, nal = np - nl, nlev = fp->nlevels;
+  if (!dc_out_route_ok(data, dtype, ld, p, r, 1))
+    return fail(h, MDSX_UNSUPPORTED, "fast route needs p <= 128, r <= 16 and 16-byte aligned rows");
+  ClassicalPlan cp;
+  int rc = plan_classical(h, p, fp->piece_off, np, r, cp);
+  if (rc) return rc;
+  for (int j = 0; j < nl; ++j)
+    if (cp.pd[j].form != 0) return fail(h, MDSX_UNSUPPORTED, "fast route needs form-0 leaves");
+  const int64_t leaf_total = fp->piece_off[nl] - fp->piece_off[0];
+  const int64_t al_total = fp->piece_off[np] - fp->piece_off[nl];
+  int64_t max_leaf = 0, max_al = 0;
+  for (int j = 0; j < np; ++j)
+    (j < nl ? max_leaf : max_al) = std::max<int64_t>(j < nl ? max_leaf : max_al, cp.pd[j].m);
+  int64_t njobs = 0;
+  for (int L = 0; L < nlev; ++L) njobs += fp->level_njobs[L];
+  const int64_t ntrk = fp->ntracked;
+  const size_t need = classical_ws_bytes(cp, p, r) + align_up(al_total * r * 8) +
+                      align_up(points_ws_bytes(nal, max_al, r)) + align_up(nal * sizeof(PieceDesc)) +
+                      align_up(ntrk * r * 8) + align_up(njobs * r * r * 8) + align_up(njobs * r * 8) * 2 +
+                      align_up(njobs * 4) + align_up((njobs + nlev) * 8) + align_up(nlev * 8) +
+                      align_up((size_t)nl * p * r * 8) + 2 * align_up((size_t)nl * r * 8) + 4096 * 4;
+  if ((rc = ws_reserve(h, need))) return rc;
+  ClassicalOut co;
+  if ((rc = run_classical(h, cp, data, dtype, ld, p, fp->row_idx, r, nullptr, estimates, gof, status,
+                          st, &co)))
+    return rc;
+  double* Pal = (double*)ws_alloc(h, al_total * r * 8, st);
+  double2* cand = (double2*)ws_alloc(h, points_ws_bytes(nal, max_al, r), st);
+  PieceDesc* dpd_al = (PieceDesc*)ws_alloc(h, nal * sizeof(PieceDesc), st);
+  double* Ptrk = (double*)ws_alloc(h, std::max<int64_t>(ntrk, 1) * r * 8, st);
+  double* rot = (double*)ws_alloc(h, njobs * r * r * 8, st);
+  double* trans = (double*)ws_alloc(h, njobs * r * 8, st);
+  double* loss = (double*)ws_alloc(h, njobs * 8, st);
+  int32_t* degen = (int32_t*)ws_alloc(h, njobs * 4, st);
+  int64_t* joff_d = (int64_t*)ws_alloc(h, (njobs + nlev) * 8, st);
+  int64_t* jbase_d = (int64_t*)ws_alloc(h, nlev * 8, st);
+  double* Uc = (double*)ws_alloc(h, (size_t)nl * p * r * 8, st);
+  double* tvec = (double*)ws_alloc(h, (size_t)nl * r * 8, st);
+  double* contrib = (double*)ws_alloc(h, (size_t)nl * r * 8, st);
+  double* mean = (double*)ws_alloc(h, 64 * 8, st);
+  if (!Pal || !cand || !dpd_al || !Ptrk || !rot || !trans || !loss || !degen || !joff_d || !jbase_d ||
+      !Uc || !tvec || !contrib || !mean)
+    return MDSX_CUDA;
+  // alignment sets: full points with the canonical column signs (targets)
+  std::vector<PieceDesc> al(cp.pd.begin() + nl, cp.pd.end());
+  for (auto& d : al) d.pt_off -= leaf_total;
+  std::vector<int64_t> jb(nlev), joff_all;
+  {
+    int64_t base = 0, ko = 0;
+    for (int L = 0; L < nlev; ++L) {
+      jb[L] = base;
+      const int nj = fp->level_njobs[L];
+      for (int t = 0; t <= nj; ++t) joff_all.push_back(fp->job_off[ko + t]);
+      ko += nj + 1;
+      base += nj;
+    }
+  }
+  Stager sg(h, st);
+  if ((rc = sg.begin(nal * sizeof(PieceDesc) + joff_all.size() * 8 + nlev * 8 + 1024))) return rc;
+  if ((rc = sg.put(dpd_al, al.data(), nal * sizeof(PieceDesc)))) return rc;
+  if ((rc = sg.put(joff_d, joff_all.data(), joff_all.size() * 8))) return rc;
+  if ((rc = sg.put(jbase_d, jb.data(), nlev * 8))) return rc;
+  if ((rc = sg.end())) return rc;
+  if ((rc = launch_points(h, data, dtype, ld, p, fp->row_idx, dpd_al, nal, max_al, r, co.mu, co.U,
+                          co.lam, Pal, cand, st, true)))
+    return rc;
+  // tracked rows in their leaves' frames, then level by level: fit, carry up
+  if ((rc = launch_trk_points(h, data, dtype, ld, p, fp->trk_row, fp->trk_leaf, ntrk, co.dpd, r,
+                              co.mu, co.U, Ptrk, st)))
+    return rc;
+  int64_t soff = 0, ko = 0;
+  for (int L = 0; L < nlev; ++L) {
+    const int nj = fp->level_njobs[L];
+    const int64_t nsrc = fp->job_off[ko + nj] - fp->job_off[ko];
+    if (nj > 0) {
+      if ((rc = launch_procrustes_fit(h, Pal, fp->job_tgt + soff, Ptrk, fp->job_src + soff,
+                                      joff_d + ko, nj, r, rot + jb[L] * r * r, trans + jb[L] * r,
+                                      loss + jb[L], degen + jb[L], st)))
+        return rc;
+      if (L + 1 < nlev &&
+          (rc = launch_trk_apply(h, Ptrk, fp->trk_job + (int64_t)L * ntrk, ntrk, r,
+                                 rot + jb[L] * r * r, trans + jb[L] * r, st)))
+        return rc;
+    }
+    soff += nsrc;
+    ko += nj + 1;
+  }
+  return launch_fast_out(h, data, dtype, ld, p, fp->row_idx, fp->out_idx, co.dpd, nl, max_leaf, nlev,
+                         fp->leaf_job, jbase_d, r, co.mu, co.U, rot, trans, Uc, tvec, contrib, mean,
+                         recenter ? n_out : 0, out, st);
 }

@@ -39,6 +39,7 @@ struct mdsx_handle {
   // second stream for the piece pipeline (run_classical), created on first use
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_anchor = nullptr;   // D&C: anchor signs/targets ready (chunked tail)
   // calls are serialised per handle (the workspace and staging buffer are
   // shared): a call holds `mu`, makes its stream wait for the previous call's
   // last work (`ws_done`) and records `ws_done` on its stream when it returns,

@@ -415,3 +415,54 @@ def _flatten_fast(root: FastNode, span) -> FastFlat:
     eval_order = [i if kind == "leaf" else n_leaves + i for kind, i in post]
     return FastFlat(np.asarray(order).astype(np.int64, copy=False), piece_rows, piece_off,
                     n_leaves, levels, labels_leaf + labels_align, eval_order)
+
+
+@dataclass
+class FastRoute:
+    """Host arrays of ``mdsx_fast_mds`` (include/mdsx.h) for a flattened plan:
+    the TRACKED rows (working-buffer rows some alignment job samples) with
+    their data rows and leaves, and per level (deepest first) the jobs'
+    sources (tracked ids) and targets (rows of the alignment-set points, in
+    piece order), the job owning each tracked row and each leaf at that
+    level (-1: none)."""
+
+    trk_pos: np.ndarray
+    trk_row: np.ndarray
+    trk_leaf: np.ndarray
+    level_njobs: np.ndarray
+    job_off: np.ndarray
+    job_src: np.ndarray
+    job_tgt: np.ndarray
+    trk_job: np.ndarray
+    leaf_job: np.ndarray
+
+
+def fast_route(flat: FastFlat) -> FastRoute:
+    nl = flat.n_leaves
+    off = np.asarray(flat.piece_off, dtype=np.int64)
+    leaf_total = int(off[nl])
+    leaf_of = np.repeat(np.arange(nl, dtype=np.int32), np.diff(off[:nl + 1]))
+    levels = flat.levels
+    src_all = (np.concatenate([lv.src_rows for lv in levels]) if levels
+               else np.empty(0, np.int64))
+    trk_pos = np.unique(src_all).astype(np.int64)
+    leaf_start = off[:nl]
+    njobs, joffs, srcs, tgts, tj, lj = [], [], [], [], [], []
+    for lv in levels:
+        st = np.asarray(lv.start, np.int64)
+        ln = np.asarray(lv.length, np.int64)
+        njobs.append(len(st))
+        joffs.append(np.asarray(lv.job_off, np.int64))
+        srcs.append(np.searchsorted(trk_pos, lv.src_rows).astype(np.int64))
+        tgts.append(np.asarray(lv.tgt_rows, np.int64) - leaf_total)
+
+        def owner(pos):
+            k = np.searchsorted(st, pos, side="right") - 1
+            ok = (k >= 0) & (pos < st[np.maximum(k, 0)] + ln[np.maximum(k, 0)])
+            return np.where(ok, k, -1).astype(np.int32)
+        tj.append(owner(trk_pos))
+        lj.append(owner(leaf_start))
+    cat = (lambda parts, dt: np.concatenate(parts).astype(dt) if parts else np.empty(0, dt))  # noqa: E731
+    return FastRoute(trk_pos, np.asarray(flat.piece_rows, np.int64)[trk_pos], leaf_of[trk_pos],
+                     np.asarray(njobs, np.int32), cat(joffs, np.int64), cat(srcs, np.int64),
+                     cat(tgts, np.int64), cat(tj, np.int32), cat(lj, np.int32))
