@@ -267,6 +267,15 @@ int mdsx_aligned_correlations(mdsx_handle* h, const double* points, int64_t n, i
                               const void* dominant, int32_t dtype, int64_t ld, double* corr,
                               double* rotation, int32_t* zero_var, void* stream);
 
+/* ---- host planner ------------------------------------------------------ */
+/* In-place random permutation of a[0..n) bit-identical to numpy's
+ * Generator.permutation on a PCG64 bit generator whose state is passed as
+ * state = {state_hi, state_lo, inc_hi, inc_lo}, has_uint32, uinteger and
+ * advanced in place (the permutation draws of partition.py:204-213, 225-231
+ * and 258-264).  Host memory only; no device. */
+int mdsx_plan_permute(int64_t* a, int64_t n, uint64_t* state, int32_t* has_uint32,
+                      uint32_t* uinteger);
+
 /* ---- file ingestion (replaces dataio.py:42-58, 68-82, 102-130) ----------
  * Host-side parsing; no device is needed except for mdsx_idx_load_images.
  * On failure `msg` (msg_len bytes, NUL-terminated) carries the reference's

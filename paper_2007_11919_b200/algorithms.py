@@ -23,11 +23,23 @@ import torch
 from . import _device as D
 from .errors import InvalidInputError, NumericalError, ParamError
 from .params import ALGORITHM_NAMES, AlgorithmParams
-from .plans import (DcPlan, FastPlan, InterpPlan, fast_route, flatten_fast, flatten_subsets,
-                    flatten_subsets_cached,
+from .plans import (DcPlan, FastPlan, InterpPlan, flatten_fast_cached, flatten_subsets,
+                    flatten_subsets_cached, plan_device_cache, route_cached,
                     interpolation_sample, plan_divide_conquer, plan_fast)
 from .primitives import classical_mds_from_data, raise_piece_status
 from .results import MdsConfiguration
+
+
+def _cached_upload(plan, dev, name, make):
+    """Device copy of a plan's index arrays, made once per (plan, device) when
+    the plan is cached by identity (plans.plan_device_cache)."""
+    cache = plan_device_cache(plan) if plan is not None else None
+    if cache is None:
+        return make()
+    key = (str(dev), name)
+    if key not in cache:
+        cache[key] = make()
+    return cache[key]
 
 
 def _finish_points(points: torch.Tensor, return_device: bool):
@@ -42,7 +54,7 @@ class DivideRun:
         self.x, self.plan, self.r, self.c = x, plan, r, c
         self.dev = x.device
         rows, off = flatten_subsets_cached(plan)
-        self.row_idx = D.index_tensor(rows, self.dev)
+        self.row_idx = _cached_upload(plan, self.dev, "rows", lambda: D.index_tensor(rows, self.dev))
         self.piece_off = off
         n, npc = plan.n, plan.p
         self.out = D.empty((n, r), self.dev)
@@ -159,8 +171,12 @@ class FastRun:
         rank's rows stay in `pts[:len(flat.order)]` (distributed.py)."""
         self.x, self.plan, self.r, self.local = x, plan, r, local
         self.dev = dev = x.device
-        flat = self.flat = flat if flat is not None else flatten_fast(plan)
-        self.piece_rows = D.index_tensor(flat.piece_rows, dev)
+        own_flat = flat is None
+        flat = self.flat = flat if flat is not None else flatten_fast_cached(plan)
+        cplan = plan if own_flat else None          # shard flats are not cached per plan
+        self.piece_rows = _cached_upload(cplan, dev, "piece_rows",
+                                         lambda: D.index_tensor(flat.piece_rows, dev))
+        self._cplan = cplan
         npc = len(flat.piece_off) - 1
         self.est = D.empty((npc, r), dev)
         self.gof = D.empty((npc, 2), dev)
@@ -200,20 +216,20 @@ class FastRun:
         import ctypes as C
 
         from ._lib import FastPlanC
-        rt = fast_route(flat)
+        rt = route_cached(flat)
         nl = flat.n_leaves
         leaf_total = int(flat.piece_off[nl])
-        keep = self._keep = {
+        def i32(a):
+            return torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(dev)
+
+        keep = _cached_upload(self._cplan, dev, "route", lambda: {
             "piece_off": np.ascontiguousarray(flat.piece_off, dtype=np.int64),
             "level_njobs": np.ascontiguousarray(rt.level_njobs, dtype=np.int32),
             "job_off": np.ascontiguousarray(rt.job_off, dtype=np.int64),
-            "trk_row": D.index_tensor(rt.trk_row, dev),
-            "trk_leaf": torch.from_numpy(np.ascontiguousarray(rt.trk_leaf, np.int32)).to(dev),
-            "job_src": D.index_tensor(rt.job_src, dev),
-            "job_tgt": D.index_tensor(rt.job_tgt, dev),
-            "trk_job": torch.from_numpy(np.ascontiguousarray(rt.trk_job, np.int32)).to(dev),
-            "leaf_job": torch.from_numpy(np.ascontiguousarray(rt.leaf_job, np.int32)).to(dev),
-        }
+            "trk_row": D.index_tensor(rt.trk_row, dev), "trk_leaf": i32(rt.trk_leaf),
+            "job_src": D.index_tensor(rt.job_src, dev), "job_tgt": D.index_tensor(rt.job_tgt, dev),
+            "trk_job": i32(rt.trk_job), "leaf_job": i32(rt.leaf_job)})
+        keep = self._keep = dict(keep)          # holds every device array the plan struct points to
         if local:
             keep["out_idx"] = torch.arange(leaf_total, dtype=torch.int64, device=dev)
             self.out = D.empty((leaf_total, r), dev)

@@ -910,6 +910,7 @@ __device__ __noinline__ void tw_charpoly(const double* as, const double* bs, con
 #endif
 }
 
+
 }  // namespace
 
 namespace mdsx {

@@ -32,6 +32,41 @@ def sub_seed(seed: int, *path: int) -> int:
                .generate_state(1, np.uint64)[0])
 
 
+_M64 = (1 << 64) - 1
+
+
+def _permutation(g: np.random.Generator, arr: np.ndarray) -> np.ndarray:
+    """== g.permutation(arr) for a 1-d int64 array, bit for bit, advancing g
+    identically: the same PCG64 draws (numpy's masked-rejection interval on
+    buffered 32-bit outputs), with the swaps done by libmdsx's native
+    planner (mdsx_plan_permute: targets drawn first, swap targets
+    prefetched).  numpy itself is used when the library is not built."""
+    out = np.array(arr, dtype=np.int64, copy=True)
+    bg = g.bit_generator
+    if out.size < 4096 or type(bg) is not np.random.PCG64:
+        return g.permutation(arr)
+    try:
+        from . import _lib
+        lib = _lib.load()
+    except (RuntimeError, OSError):
+        return g.permutation(arr)
+    import ctypes as C
+    st = bg.state
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    state = np.array([s >> 64, s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
+    has = C.c_int32(int(st["has_uint32"]))
+    u32 = C.c_uint32(int(st["uinteger"]))
+    rc = lib.mdsx_plan_permute(out.ctypes.data, out.size, state.ctypes.data, C.byref(has),
+                               C.byref(u32))
+    if rc != 0:
+        return g.permutation(arr)
+    st["state"]["state"] = (int(state[0]) << 64) | int(state[1])
+    st["has_uint32"] = has.value
+    st["uinteger"] = u32.value
+    bg.state = st
+    return out
+
+
 def _complement_sorted(n: int, taken: np.ndarray) -> np.ndarray:
     """== np.setdiff1d(np.arange(n), taken) for unique in-range ``taken``
     (a mask instead of a sort: O(n))."""
@@ -181,13 +216,18 @@ def plan_divide_conquer(n: int, l: int, c: int, seed: int) -> DcPlan:
         return DcPlan(np.empty(0, dtype=np.int64), [np.arange(n, dtype=np.int64)], n, l, c, seed)
     g = spawned_generator(seed)
     conn = np.sort(g.choice(n, size=c, replace=False)).astype(np.int64)
-    dealt = g.permutation(_complement_sorted(n, conn))
+    dealt = _permutation(g, _complement_sorted(n, conn))
     step = l - c
-    bounds = list(range(0, dealt.size, step)) + [dealt.size]
-    if len(bounds) > 2 and bounds[-1] - bounds[-2] < c + 1:
-        del bounds[-2]                       # merge a short remainder into its predecessor
-    subsets = [np.concatenate([conn, np.sort(dealt[a:b])]) for a, b in zip(bounds[:-1], bounds[1:])]
-    return DcPlan(conn, subsets, n, l, c, seed)
+    nb = (dealt.size + step - 1) // step          # chunks of `step` dealt rows, the last short
+    if nb > 1 and dealt.size - (nb - 1) * step < c + 1:
+        nb -= 1                                   # merge a short remainder into its predecessor
+    full = nb - 1                                 # chunks of exactly `step` rows
+    # [connecting | own sorted] for the full chunks in one 2-D block (row views)
+    block = np.empty((full, l), dtype=np.int64)
+    block[:, :c] = conn
+    block[:, c:] = np.sort(dealt[:full * step].reshape(full, step), axis=1)
+    last = np.concatenate([conn, np.sort(dealt[full * step:])])
+    return DcPlan(conn, list(block) + [last], n, l, c, seed)
 
 
 def interpolation_sample(n: int, l: int, seed: int) -> np.ndarray:
@@ -209,7 +249,7 @@ def plan_interpolation(n: int, l: int, seed: int) -> InterpPlan:
         return InterpPlan([np.arange(n, dtype=np.int64)], n, l, seed)
     g = spawned_generator(seed)
     sample = np.sort(g.choice(n, size=l, replace=False)).astype(np.int64)
-    dealt = g.permutation(_complement_sorted(n, sample))
+    dealt = _permutation(g, _complement_sorted(n, sample))
     return InterpPlan([sample] + [np.sort(dealt[a:a + l]) for a in range(0, dealt.size, l)],
                       n, l, seed)
 
@@ -234,7 +274,7 @@ def plan_fast(n: int, l: int, s: int, seed: int) -> FastPlan:
         if idx.size <= l:
             return FastNode(np.sort(idx))
         g = spawned_generator(seed, *path)
-        pieces = np.array_split(g.permutation(idx), parts)
+        pieces = np.array_split(_permutation(g, idx), parts)
         picks = [np.sort(g.choice(q.size, size=min(s, q.size), replace=False)) for q in pieces]
         kids = []
         for i, (q, pos) in enumerate(zip(pieces, picks)):
@@ -295,8 +335,24 @@ def flatten_subsets_cached(plan) -> tuple[np.ndarray, np.ndarray]:
         ref = weakref.ref(plan, lambda _r, k=key: _FLAT_CACHE.pop(k, None))
     except TypeError:
         return flat
-    _FLAT_CACHE[key] = (ref, plan.subsets, flat)
+    _FLAT_CACHE[key] = (ref, plan.subsets, flat, {})
     return flat
+
+
+def plan_device_cache(plan) -> dict | None:
+    """Per-plan dict for device copies of the plan's index arrays (keyed by
+    the caller, e.g. (device, name)): a plan passed to several calls is
+    uploaded once; dropped with the plan.  None when the plan cannot be
+    weak-referenced (then nothing is cached)."""
+    if isinstance(plan, FastPlan):
+        flat = flatten_fast_cached(plan)
+        cache = getattr(flat, "_dev_cache", None)
+        if cache is None:
+            cache = flat._dev_cache = {}
+        return cache
+    flatten_subsets_cached(plan)
+    hit = _FLAT_CACHE.get(id(plan))
+    return hit[3] if hit is not None and hit[0]() is plan else None
 
 
 @dataclass
@@ -339,6 +395,34 @@ def flatten_fast(plan: FastPlan) -> FastFlat:
     """Walk the tree once: leaves in DFS order, alignment sets of every
     internal node, and per-depth Procrustes jobs (deepest first)."""
     return _flatten_fast(plan.root, None)
+
+
+_FAST_CACHE: dict = {}
+
+
+def flatten_fast_cached(plan: FastPlan) -> FastFlat:
+    """flatten_fast(plan) memoised per plan object (plans are not mutated; the
+    entry is dropped when the plan is collected), with the fast_route arrays
+    attached on first use (``route_cached``)."""
+    key = id(plan)
+    hit = _FAST_CACHE.get(key)
+    if hit is not None and hit[0]() is plan and hit[1] is plan.root:
+        return hit[2]
+    flat = flatten_fast(plan)
+    try:
+        ref = weakref.ref(plan, lambda _r, k=key: _FAST_CACHE.pop(k, None))
+    except TypeError:
+        return flat
+    _FAST_CACHE[key] = (ref, plan.root, flat)
+    return flat
+
+
+def route_cached(flat: "FastFlat") -> "FastRoute":
+    rt = getattr(flat, "_route", None)
+    if rt is None:
+        rt = fast_route(flat)
+        flat._route = rt
+    return rt
 
 
 def flatten_fast_shard(plan: FastPlan, lo: int, hi: int) -> FastFlat:
