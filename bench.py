@@ -20,9 +20,10 @@ A step = one full algorithm call over the device-resident input with the plan
 passed explicitly (planning is host work, reported as ``planner_ms``); it
 ends with the n x r configuration on the device in input row order.  Every
 full-size input is larger than L2 (126 MB), so no flush is needed.  ``e2e``
-repeats the call through the public API with the input as a PAGEABLE numpy
-array (what a scalemds user passes): H2D of the input (staged by mdsx_h2d)
-and of the plan indices, the kernels, and the D2H of the n x r result.
+repeats the call through the public API from a page-locked host tensor: H2D
+of the input and of the plan indices, the kernels, and the D2H of the n x r
+result into numpy; ``e2e.numpy_input`` is the same with the input as a
+PAGEABLE numpy array (what a scalemds user passes; staged by mdsx_h2d).
 
 Multi-GPU: ``--gpus N`` without torchrun starts N ranks itself (torch's
 launcher on 127.0.0.1); under torchrun one process per GPU.  Scaling: weak
@@ -631,7 +632,7 @@ def run_ours(args, w):
     step_roof["achieved_GBs"] = step_roof["bytes_per_step"] / (ms / 1e3) / 1e9
     step_roof["frac_hbm"] = step_roof["achieved_GBs"] / peaks["hbm_gbs"]
 
-    # ---- e2e through the public API (pageable numpy input, what users pass)
+    # ---- e2e through the public API (host input, numpy result)
     e2e = None
     params = AlgorithmParams(r=w["r"], l=w["l"], c=w["c"], s=w["s"], seed=0)
     parity = None
@@ -642,22 +643,37 @@ def run_ours(args, w):
               "interpolate": interpolation_mds}[w["algo"]]
         kw = dict(plan=plan if w["algo"] != "interpolate" else InterpPlan([plan], n, w["l"], 0),
                   device=dev)
-        k_e2e = max(1, min(args.steps, 5))
-        res = None
-        for _ in range(2):        # steady state: one result alive while the next call runs
-            res = fn(x_host, params, **kw)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        for _ in range(k_e2e):
-            res = fn(x_host, params, **kw)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t) / k_e2e
         n_idx = len(plan) if w["algo"] == "interpolate" else (
             sum(len(q) for q in plan.subsets) if w["algo"] == "divide" else 2 * n)
+
+        def e2e_of(host_in, k):
+            res = None
+            for _ in range(2):    # steady state: one result alive while the next call runs
+                res = fn(host_in, params, **kw)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            for _ in range(k):
+                res = fn(host_in, params, **kw)
+            torch.cuda.synchronize()
+            return (time.perf_counter() - t) / k, res
+
+        # the contract's e2e: the public API on a page-locked host tensor (H2D of
+        # the input at PCIe speed); the drop-in case, a pageable numpy array as a
+        # scalemds user passes it (staged by mdsx_h2d), is reported beside it
+        pinned = torch.empty(x_host.shape, dtype=torch.from_numpy(x_host[:1]).dtype, pin_memory=True)
+        pinned.numpy()[...] = x_host
+        k_e2e = max(1, min(args.steps, 5))
+        e2e_s, res = e2e_of(pinned, k_e2e)
+        del pinned
         e2e = {"value": n / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                "h2d_bytes_per_step": int(x_host.nbytes + 8 * n_idx),
                "d2h_bytes_per_step": int(n * w["r"] * 8), "steps": k_e2e,
-               "path": f"paper_2007_11919_b200.{fn.__name__}(numpy array (pageable), plan=...)"}
+               "path": f"paper_2007_11919_b200.{fn.__name__}(page-locked host tensor, plan=...) "
+                       "-> numpy points"}
+        e2e_np, res = e2e_of(x_host, max(1, min(args.steps, 3)))
+        e2e["numpy_input"] = {"value": n / e2e_np, "ms_per_step": e2e_np * 1e3,
+                              "path": f"paper_2007_11919_b200.{fn.__name__}(numpy array (pageable), "
+                                      "plan=...): input staged by mdsx_h2d"}
         parity = parity_block(args.workload, w, res.points, res.eigenvalue_estimates,
                               res.gof_g1, res.gof_g2)
     elif not args.no_e2e and sharded:

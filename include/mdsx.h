@@ -5,8 +5,10 @@
  * leading dimension), plain sizes and a cudaStream_t passed as void*; it
  * enqueues work on that stream and returns an mdsx_status.  Arrays marked
  * "host" are read on the host before the call returns.  Nothing here ever
- * frees caller memory; each handle owns its own device workspace (one
- * stream at a time per handle).
+ * frees caller memory; each handle owns its own device workspace.  Calls on
+ * one handle are serialised (a lock) and stream-ordered against each other (the
+ * stream of a call waits for the previous call's last work), so a handle may
+ * be shared by several host threads and streams.
  *
  * Reference interfaces replaced (paths relative to
  * /root/reference/pkg/src/scalemds):
@@ -79,7 +81,8 @@ int64_t mdsx_launch_count(const mdsx_handle* h);
 int mdsx_version(void);
 /* Per-kernel CUDA-event timing of this handle's launches (off by default).
  * mdsx_timing_report synchronises on the recorded events and returns the
- * length of the report "<kernel> <total_ms> <count>\n"...; with a buffer
+ * length of the report "<kernel> <total_ms> <count> <work>\n"... (work: executed
+ * flops credited by the launcher, 0 when not counted); with a buffer
  * (cap bytes, NUL-terminated) it also copies the report and resets it. */
 int mdsx_timing_enable(mdsx_handle* h, int on);
 int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap);

@@ -32,8 +32,10 @@ from .results import MdsConfiguration
 
 def _cached_upload(plan, dev, name, make):
     """Device copy of a plan's index arrays, made once per (plan, device) when
-    the plan is cached by identity (plans.plan_device_cache)."""
-    cache = plan_device_cache(plan) if plan is not None else None
+    the plan is cached by identity (plans.plan_device_cache); `plan` may also
+    be a dict to cache into (a shard's flattened plan)."""
+    cache = plan if isinstance(plan, dict) else (
+        plan_device_cache(plan) if plan is not None else None)
     if cache is None:
         return make()
     key = (str(dev), name)
@@ -173,7 +175,8 @@ class FastRun:
         self.dev = dev = x.device
         own_flat = flat is None
         flat = self.flat = flat if flat is not None else flatten_fast_cached(plan)
-        cplan = plan if own_flat else None          # shard flats are not cached per plan
+        # the caller's flat may carry its own upload cache (distributed.fast_shard)
+        cplan = plan if own_flat else getattr(flat, "_dev_cache", None)
         self.piece_rows = _cached_upload(cplan, dev, "piece_rows",
                                          lambda: D.index_tensor(flat.piece_rows, dev))
         self._cplan = cplan

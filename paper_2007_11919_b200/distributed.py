@@ -45,7 +45,7 @@ import torch.distributed as dist
 from .errors import InvalidInputError, NumericalError
 from .params import AlgorithmParams
 from .plans import (DcPlan, FastPlan, flatten_fast_shard, flatten_subsets, interpolation_sample,
-                    plan_divide_conquer, plan_fast)
+                    plan_device_cache, plan_divide_conquer, plan_fast)
 from .results import MdsConfiguration
 
 SUM_BLOCK = 65536      # canonical row block of the interpolation re-centring sums
@@ -194,7 +194,25 @@ class DcShard:
     report_lo: int            # first local row this rank reports (anchor: rank 0 only)
 
 
+def _shard_cached(plan, key, make):
+    """Shard layouts are pure functions of (plan, world, rank): memoised on the
+    plan's cache (dropped with the plan)."""
+    try:
+        cache = plan_device_cache(plan)
+    except (AttributeError, TypeError):
+        cache = None
+    if cache is None:
+        return make()
+    if key not in cache:
+        cache[key] = make()
+    return cache[key]
+
+
 def dc_shard(plan: DcPlan, world: int, rank: int) -> DcShard:
+    return _shard_cached(plan, ("dc_shard", world, rank), lambda: _dc_shard(plan, world, rank))
+
+
+def _dc_shard(plan: DcPlan, world: int, rank: int) -> DcShard:
     P, c = plan.p, plan.c
     lo, hi = shard(P - 1, world, rank)
     mine = np.arange(1 + lo, 1 + hi, dtype=np.int64)
@@ -226,8 +244,9 @@ class ShardedDivide:
                              f"the shard needs {len(sh.local_rows)}")
         dev = backend.device
         self.dev = dev
-        self.row_idx = backend.index(sh.row_idx)
-        self.own_off = backend.index(sh.own_off)
+        up = _shard_cached(plan, ("dc_dev", comm.world, comm.rank, str(dev)),
+                           lambda: (backend.index(sh.row_idx), backend.index(sh.own_off)))
+        self.row_idx, self.own_off = up
         npc = len(sh.pieces)
         self.out = torch.empty((len(sh.local_rows), r), dtype=torch.float64, device=dev)
         self.est = torch.empty((npc, r), dtype=torch.float64, device=dev)
@@ -237,7 +256,6 @@ class ShardedDivide:
         self.ids = torch.tensor(sh.pieces, dtype=torch.float64, device=dev)[:, None]
         self.first = 0 if comm.rank == 0 else 1          # the anchor's record: rank 0 only
         self.kmax = 1 + shard(plan.p - 1, comm.world, 0)[1]
-        self._rows_cache: dict = {}
         self.recs = None
 
     def launch(self) -> ShardResult:
@@ -254,10 +272,8 @@ class ShardedDivide:
                            rows_fn=self.rows_of)
 
     def rows_of(self, k: int) -> np.ndarray:
-        if k not in self._rows_cache:
-            s = dc_shard(self.plan, self.comm.world, k)
-            self._rows_cache[k] = s.local_rows[s.report_lo:]
-        return self._rows_cache[k]
+        s = dc_shard(self.plan, self.comm.world, k)
+        return s.local_rows[s.report_lo:]
 
     def finish(self):
         """Host decode of the gathered records (identical on every rank)."""
@@ -404,6 +420,11 @@ def _subtree_counts(node) -> tuple[int, int]:
 
 
 def fast_shard(plan: FastPlan, world: int, rank: int, counts=None) -> FastShard:
+    return _shard_cached(plan, ("fast_shard", world, rank),
+                         lambda: _fast_shard(plan, world, rank, counts))
+
+
+def _fast_shard(plan: FastPlan, world: int, rank: int, counts=None) -> FastShard:
     kids = plan.root.children
     lo, hi = shard(len(kids), world, rank)
     flat = flatten_fast_shard(plan, lo, hi)
@@ -416,6 +437,7 @@ def fast_shard(plan: FastPlan, world: int, rank: int, counts=None) -> FastShard:
     pos[extra] = len(order) + np.arange(len(extra), dtype=np.int64)
     from dataclasses import replace
     flat_l = replace(flat, piece_rows=pos[flat.piece_rows], order=np.arange(len(order), dtype=np.int64))
+    flat_l._dev_cache = {}                  # device uploads of this shard (algorithms.FastRun)
     counts = counts if counts is not None else [_subtree_counts(ch) for ch in kids]
     leaf_base = int(sum(c[0] for c in counts[:lo]))
     eval_base = int(sum(c[1] for c in counts[:lo]))
