@@ -421,6 +421,7 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     int nc = pc ? atoi(pc) : 2;                       // measured best on dc2 / fast3
     const bool serial = getenv("MDSX_PIPE_SERIAL") != nullptr;
     nc = std::min(nc, np / (2 * h->num_sms));          // >= two waves of pieces per chunk
+    if (pc == nullptr && nc > 2) nc = 2;
     // fused points epilogue in the Lanczos kernel (aligned rows, r <= 10): each
     // CTA streams its piece's rows right after its eigenvectors, next to the
     // other CTA's Krylov phase; the points kernel then only takes the pieces
@@ -433,20 +434,24 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
     if (fuse && !pending) return MDSX_CUDA;
     PtsEpi epi{data, dtype == MDSX_F32 ? 1 : 0, ld, p, ridx, mu, points, pending};
     if (simple && nc > 1) {
-      if (!h->aux) {
-        if ((rc = cuda_check(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking), "stream")))
-          return rc;
+      nc = std::min(nc, 4);
+      if (!h->pipe[0]) {
+        for (int c = 0; c < 4; ++c) {
+          if ((rc = cuda_check(h, cudaStreamCreateWithFlags(&h->pipe[c], cudaStreamNonBlocking),
+                               "stream")))
+            return rc;
+          cudaEventCreateWithFlags(&h->ev_pj[c], cudaEventDisableTiming);
+        }
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
       }
       cudaEventRecord(h->ev_fork, st);
-      cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
+      for (int c = 0; c < nc && !serial; ++c) cudaStreamWaitEvent(h->pipe[c], h->ev_fork, 0);
       for (int c = 0; c < nc; ++c) {
         const int j0 = (int)((int64_t)np * c / nc), j1 = (int)((int64_t)np * (c + 1) / nc);
         const int n = j1 - j0;
         // MDSX_PIPE_SERIAL: every chunk on the caller's stream (same kernels and
         // chunks, no overlap) -- bench.py's per-kernel timing pass
-        cudaStream_t s = (c & 1) && !serial ? h->aux : st;
+        cudaStream_t s = serial ? st : h->pipe[c];
         if ((rc = launch_gram_piece(h, data, dtype, ld, p, ridx, dpd + j0, n, A, mu, status, s)))
           return rc;
         if ((rc = launch_lanczos_smem(h, dpd + j0, n, cp.kmax_sub, r, A, U, lam, estimates, gof,
@@ -460,8 +465,11 @@ static int run_classical(mdsx_handle* h, const ClassicalPlan& cp, const void* da
           return rc;
         if (co && co->after_chunk && (rc = co->after_chunk(j0, j1, s))) return rc;
       }
-      cudaEventRecord(h->ev_join, h->aux);
-      return cuda_check(h, cudaStreamWaitEvent(st, h->ev_join, 0), "pipeline join");
+      for (int c = 0; c < nc && !serial; ++c) {
+        cudaEventRecord(h->ev_pj[c], h->pipe[c]);
+        if ((rc = cuda_check(h, cudaStreamWaitEvent(st, h->ev_pj[c], 0), "pipeline join"))) return rc;
+      }
+      return MDSX_OK;
     }
   }
   // form 0: DMMA Gram with fused shifted means;  form 1: means pass + row Gram
@@ -541,6 +549,10 @@ void mdsx_destroy(mdsx_handle* h) {
   for (auto& t : h->timed) { cudaEventDestroy(t.second.first); cudaEventDestroy(t.second.second); }
   for (auto e : h->event_pool) cudaEventDestroy(e);
   if (h->aux) cudaStreamDestroy(h->aux);
+  for (int c = 0; c < 4; ++c) {
+    if (h->pipe[c]) cudaStreamDestroy(h->pipe[c]);
+    if (h->ev_pj[c]) cudaEventDestroy(h->ev_pj[c]);
+  }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ws_done) cudaEventDestroy(h->ws_done);
