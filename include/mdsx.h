@@ -278,6 +278,13 @@ int mdsx_aligned_correlations(mdsx_handle* h, const double* points, int64_t n, i
  * and 258-264).  Host memory only; no device. */
 int mdsx_plan_permute(int64_t* a, int64_t n, uint64_t* state, int32_t* has_uint32,
                       uint32_t* uinteger);
+/* Generator.choice(pops[i], min(s, pops[i]), replace=False) for i = 0..npop-1
+ * in sequence on the same PCG64 state (the sampling positions of
+ * partition.py:258-264), bit-identical to numpy; out[i * s ..] receives the
+ * picks (unsorted).  MDSX_UNSUPPORTED when a population needs a path numpy
+ * takes only for k == pop. */
+int mdsx_plan_choices(const int64_t* pops, int32_t npop, int32_t s, int64_t* out,
+                      uint64_t* state, int32_t* has_uint32, uint32_t* uinteger);
 
 /* ---- file ingestion (replaces dataio.py:42-58, 68-82, 102-130) ----------
  * Host-side parsing; no device is needed except for mdsx_idx_load_images.

@@ -12,6 +12,7 @@
 // one at a time, which is where numpy's loop spends its time.
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "../../include/mdsx.h"
@@ -39,6 +40,21 @@ struct Pcg64 {
     has32 = 1;
     u32 = (uint32_t)(v >> 32);
     return (uint32_t)v;
+  }
+  // numpy's buffered_bounded_lemire_uint32 on the generator's 32-bit buffer:
+  // a uniform integer in [0, rng] (rng < 2^32 - 1)
+  uint32_t lemire32(uint32_t rng) {
+    const uint32_t rx = rng + 1u;
+    uint64_t m = (uint64_t)next32() * rx;
+    uint32_t left = (uint32_t)m;
+    if (left < rx) {
+      const uint32_t thr = (uint32_t)(0u - rx) % rx;
+      while (left < thr) {
+        m = (uint64_t)next32() * rx;
+        left = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
   }
   uint64_t interval(uint64_t mx) {
     if (mx == 0) return 0;
@@ -88,6 +104,64 @@ int mdsx_plan_permute(int64_t* a, int64_t n, uint64_t* state, int32_t* has_uint3
       const int64_t v = a[i];
       a[i] = a[j];
       a[j] = v;
+    }
+  }
+  state[0] = (uint64_t)(g.s >> 64);
+  state[1] = (uint64_t)g.s;
+  *has_uint32 = g.has32;
+  *uinteger = g.u32;
+  return MDSX_OK;
+}
+
+// Generator.choice(pop, k, replace=False) for each of npop populations in
+// sequence on one PCG64 stream (the sampling positions of partition.py:258-264):
+// k = min(s, pop_i); Floyd's algorithm (j = pop-k .. pop-1: draw v in [0, j],
+// take j instead when v was taken) then a Fisher-Yates shuffle of the k picks,
+// both with the 32-bit Lemire draws, when pop <= 10000 or k <= pop / 50; a
+// partial Fisher-Yates of 0..pop-1 from the tail otherwise -- numpy's two
+// methods.  out[i * s ..] receives the k picks of population i (unsorted).
+// Returns MDSX_UNSUPPORTED (state untouched) when a population needs another
+// path (k == pop, pop >= 2^32).
+int mdsx_plan_choices(const int64_t* pops, int32_t npop, int32_t s, int64_t* out, uint64_t* state,
+                      int32_t* has_uint32, uint32_t* uinteger) {
+  if (npop < 0 || s < 1 || !pops || !out || !state || !has_uint32 || !uinteger) return MDSX_PARAM;
+  for (int i = 0; i < npop; ++i) {
+    const int64_t pop = pops[i], k = pop < s ? pop : s;
+    if (pop < 1 || k >= pop || pop >= ((int64_t)1 << 31)) return MDSX_UNSUPPORTED;
+  }
+  Pcg64 g;
+  g.s = ((unsigned __int128)state[0] << 64) | state[1];
+  g.inc = ((unsigned __int128)state[2] << 64) | state[3];
+  g.has32 = *has_uint32;
+  g.u32 = *uinteger;
+  std::vector<int64_t> tail;
+  for (int i = 0; i < npop; ++i) {
+    const int64_t pop = pops[i], k = pop < s ? pop : s;
+    int64_t* o = out + (int64_t)i * s;
+    if (pop <= 10000 || k <= pop / 50) {
+      // Floyd (numpy's hash set is only a membership test; k is small here)
+      for (int64_t j = pop - k, t = 0; j < pop; ++j, ++t) {
+        const int64_t v = g.lemire32((uint32_t)j);
+        bool dup = false;
+        for (int64_t q = 0; q < t; ++q) dup |= (o[q] == v);
+        o[t] = dup ? j : v;
+      }
+      for (int64_t q = k - 1; q >= 1; --q) {
+        const int64_t jj = g.lemire32((uint32_t)q);
+        const int64_t tmp = o[q];
+        o[q] = o[jj];
+        o[jj] = tmp;
+      }
+    } else {
+      tail.resize((size_t)pop);
+      for (int64_t q = 0; q < pop; ++q) tail[(size_t)q] = q;
+      for (int64_t q = pop - 1; q >= std::max<int64_t>(pop - k, 1); --q) {
+        const int64_t jj = g.lemire32((uint32_t)q);
+        const int64_t tmp = tail[(size_t)q];
+        tail[(size_t)q] = tail[(size_t)jj];
+        tail[(size_t)jj] = tmp;
+      }
+      for (int64_t q = 0; q < k; ++q) o[q] = tail[(size_t)(pop - k + q)];
     }
   }
   state[0] = (uint64_t)(g.s >> 64);

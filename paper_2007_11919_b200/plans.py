@@ -67,6 +67,40 @@ def _permutation(g: np.random.Generator, arr: np.ndarray) -> np.ndarray:
     return out
 
 
+def _choices_sorted(g: np.random.Generator, pops, s: int) -> list:
+    """[np.sort(g.choice(pop, size=min(s, pop), replace=False)) for pop in pops],
+    bit for bit and advancing g identically, in ONE native call
+    (mdsx_plan_choices: numpy's Floyd / tail-shuffle methods on the same
+    32-bit Lemire draws); numpy itself when the library is not built or a
+    population needs another of numpy's paths."""
+    pops = np.ascontiguousarray(pops, dtype=np.int64)
+    bg = g.bit_generator
+    lib = None
+    if type(bg) is np.random.PCG64 and pops.size:
+        try:
+            from . import _lib
+            lib = _lib.load()
+        except (RuntimeError, OSError):
+            lib = None
+    if lib is not None:
+        import ctypes as C
+        st = bg.state
+        st_s, inc = st["state"]["state"], st["state"]["inc"]
+        state = np.array([st_s >> 64, st_s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
+        has = C.c_int32(int(st["has_uint32"]))
+        u32 = C.c_uint32(int(st["uinteger"]))
+        out = np.empty(pops.size * s, dtype=np.int64)
+        rc = lib.mdsx_plan_choices(pops.ctypes.data, pops.size, s, out.ctypes.data, state.ctypes.data,
+                                   C.byref(has), C.byref(u32))
+        if rc == 0:
+            st["state"]["state"] = (int(state[0]) << 64) | int(state[1])
+            st["has_uint32"] = has.value
+            st["uinteger"] = u32.value
+            bg.state = st
+            return [np.sort(out[i * s:i * s + min(s, int(q))]) for i, q in enumerate(pops)]
+    return [np.sort(g.choice(int(q), size=min(s, int(q)), replace=False)) for q in pops]
+
+
 def _complement_sorted(n: int, taken: np.ndarray) -> np.ndarray:
     """== np.setdiff1d(np.arange(n), taken) for unique in-range ``taken``
     (a mask instead of a sort: O(n))."""
@@ -275,7 +309,7 @@ def plan_fast(n: int, l: int, s: int, seed: int) -> FastPlan:
             return FastNode(np.sort(idx))
         g = spawned_generator(seed, *path)
         pieces = np.array_split(_permutation(g, idx), parts)
-        picks = [np.sort(g.choice(q.size, size=min(s, q.size), replace=False)) for q in pieces]
+        picks = _choices_sorted(g, [q.size for q in pieces], s)
         kids = []
         for i, (q, pos) in enumerate(zip(pieces, picks)):
             kid = grow(q, path + (i,))

@@ -136,3 +136,30 @@ class TestFlatteners:
                 tgt = lv.tgt_rows[lv.job_off[t]:lv.job_off[t + 1]]
                 assert tgt.min() >= 5000
         assert sorted(flat.eval_order) == list(range(len(flat.piece_off) - 1))
+
+
+def test_native_permutation_and_choices_match_numpy():
+    """mdsx_plan_permute / mdsx_plan_choices (the native planner) against
+    numpy's Generator on PCG64: identical outputs AND identical generator
+    state afterwards (including the buffered 32-bit half), for populations
+    that take numpy's Floyd and tail-shuffle paths."""
+    from paper_2007_11919_b200 import plans
+    rng = np.random.default_rng(5)
+    for trial in range(400):
+        seed = int(rng.integers(0, 1 << 30))
+        g1 = np.random.Generator(np.random.PCG64(seed))
+        g2 = np.random.Generator(np.random.PCG64(seed))
+        if trial % 2:                                  # leave a buffered 32-bit half
+            g1.integers(0, 7)
+            g2.integers(0, 7)
+        n = int(rng.choice([5000, 4096, 20000, 123457]))
+        a = np.arange(n, dtype=np.int64) * 3
+        assert np.array_equal(plans._permutation(g1, a), g2.permutation(a))
+        s = int(rng.integers(1, 60))
+        pops = [max(int(q), s + 1) for q in rng.choice(
+            [rng.integers(1, 100), rng.integers(100, 12000), rng.integers(10000, 200000),
+             50 * s, 50 * s + 1], size=int(rng.integers(1, 5)))]
+        got = plans._choices_sorted(g1, pops, s)
+        want = [np.sort(g2.choice(q, size=min(s, q), replace=False)) for q in pops]
+        assert all(np.array_equal(x, y) for x, y in zip(got, want))
+        assert g1.bit_generator.state == g2.bit_generator.state
