@@ -288,25 +288,79 @@ class FastRun:
         st = D.decode_status(self.status)
         if np.any(st["code"] == 3):
             raise InvalidInputError("data contains non-finite values")
-        for pid in self.flat.eval_order:
+        ev = np.asarray(self.flat.eval_order, dtype=np.int64)
+        bad = np.flatnonzero(st["code"][ev] != 0)
+        if bad.size:                                   # first failure in evaluation order
+            pid = int(ev[bad[0]])
             raise_piece_status(st[pid], self.r, self.flat.labels[pid])
         gof = self.gof.cpu().numpy()
         est = self.est.cpu().numpy()
-        leaf = iter(range(self.flat.n_leaves))
-
-        def agg(node):                                 # algorithms.py:289-320
-            if node.is_leaf:
-                j = next(leaf)
-                return gof[j, 0], gof[j, 1], est[j], node.size
-            fits = [agg(ch) for ch in node.children]
-            sizes = np.array([f[3] for f in fits], dtype=np.float64)
-            tot = sizes.sum()
-            return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
-                    float(np.dot(sizes, [f[1] for f in fits]) / tot),
-                    np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
-
-        g1, g2, e, _ = agg(self.plan.root)
+        g1, g2, e = fast_aggregate(self.plan, self.flat, gof, est)
         return MdsConfiguration(_finish_points(self.out, return_device), e, float(g1), float(g2))
+
+
+def fast_aggregate(plan: FastPlan, flat, gof: np.ndarray, est: np.ndarray):
+    """The recursive fit aggregation of algorithms.py:289-320 (G1/G2
+    size-weighted over children, estimates the plain mean of the children's),
+    evaluated level by level with array operations over a program cached on
+    the flattened plan: internal nodes grouped by height, children
+    contiguous per parent."""
+    prog = getattr(flat, "_agg", None)
+    if prog is None:
+        prog = flat._agg = _fast_agg_program(plan, flat.n_leaves)
+    nl = flat.n_leaves
+    sizes, groups = prog
+    n_nodes = len(sizes)
+    g1 = np.zeros(n_nodes)
+    g2 = np.zeros(n_nodes)
+    es = np.zeros((n_nodes, est.shape[1]))
+    g1[:nl], g2[:nl], es[:nl] = gof[:nl, 0], gof[:nl, 1], est[:nl]
+    for parents, children, starts in groups:
+        w = sizes[children]
+        g1[parents] = np.add.reduceat(w * g1[children], starts) / sizes[parents]
+        g2[parents] = np.add.reduceat(w * g2[children], starts) / sizes[parents]
+        cnt = np.diff(np.append(starts, len(children)))
+        es[parents] = np.add.reduceat(es[children], starts, axis=0) / cnt[:, None]
+    root = n_nodes - 1
+    return g1[root], g2[root], es[root]
+
+
+def _fast_agg_program(plan: FastPlan, nl: int):
+    """(node sizes, [(parents, children, segment starts) per height]) with
+    leaves 0..nl-1 in DFS order and internal nodes numbered in post-order
+    (the root last)."""
+    sizes, kids_of, height = [], {}, {}
+    leaf = [0]
+    internal = []
+
+    def walk(node):
+        if node.is_leaf:
+            i = leaf[0]
+            leaf[0] += 1
+            return i, 0
+        res = [walk(ch) for ch in node.children]
+        internal.append((node.size, [c for c, _ in res], 1 + max(h for _, h in res)))
+        return -len(internal), internal[-1][2]        # provisional id (negative)
+
+    walk(plan.root)
+    leaf_sizes = [lv.size for lv in plan.leaves()] if hasattr(plan, "leaves") else []
+    n_int = len(internal)
+    sizes = np.zeros(nl + n_int)
+    sizes[:nl] = leaf_sizes[:nl] if leaf_sizes else 0.0
+
+    def gid(c):
+        return c if c >= 0 else nl + (-c - 1)
+    by_h: dict = {}
+    for k, (sz, ch, h) in enumerate(internal):
+        sizes[nl + k] = sz
+        by_h.setdefault(h, []).append((nl + k, [gid(c) for c in ch]))
+    groups = []
+    for h in sorted(by_h):
+        parents = np.array([p for p, _ in by_h[h]], dtype=np.int64)
+        children = np.concatenate([np.asarray(c, np.int64) for _, c in by_h[h]])
+        starts = np.cumsum([0] + [len(c) for _, c in by_h[h]])[:-1].astype(np.int64)
+        groups.append((parents, children, starts))
+    return sizes, groups
 
 
 def _fast_route_ok(x: torch.Tensor, flat, r: int) -> bool:

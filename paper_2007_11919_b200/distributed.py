@@ -532,21 +532,10 @@ class ShardedFast:
             raise_piece_status(st[bad[0]], r, self._label(int(recs[bad[0], 0])))
         leaves = recs[recs[:, 1] >= 0]
         leaves = leaves[np.argsort(leaves[:, 1], kind="stable")]
-        gof, est = leaves[:, 2:4], leaves[:, 4:4 + r]
-        leaf = iter(range(len(leaves)))
-
-        def agg(node):                                 # algorithms.py:289-320
-            if node.is_leaf:
-                j = next(leaf)
-                return gof[j, 0], gof[j, 1], est[j], node.size
-            fits = [agg(ch) for ch in node.children]
-            sizes = np.array([f[3] for f in fits], dtype=np.float64)
-            tot = sizes.sum()
-            return (float(np.dot(sizes, [f[0] for f in fits]) / tot),
-                    float(np.dot(sizes, [f[1] for f in fits]) / tot),
-                    np.stack([f[2] for f in fits]).mean(axis=0), int(tot))
-
-        g1, g2, e, _ = agg(self.plan.root)
+        from .algorithms import fast_aggregate
+        from .plans import flatten_fast_cached
+        g1, g2, e = fast_aggregate(self.plan, flatten_fast_cached(self.plan), leaves[:, 2:4],
+                                   leaves[:, 4:4 + r])                 # algorithms.py:289-320
         return e, float(g1), float(g2)
 
 
