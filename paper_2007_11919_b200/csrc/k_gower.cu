@@ -14,6 +14,7 @@
 // The literal tile form (distance tile -> subtract from q -> project) is
 // kept as gower_tile_kernel for the function-level seam and verification.
 #include "mdsx_common.cuh"
+#include "bulk.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -451,33 +452,6 @@ gower_stream_kernel(const T* __restrict__ X, int64_t m, int p, int r,
 // full sums of output columns [j*KF, (j+1)*KF); it writes them and adds them to
 // its per-column running sums (fixed order -> per-CTA column partials for the
 // final re-centring).
-namespace bulk {
-__device__ __forceinline__ unsigned saddr(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
-}
-__device__ __forceinline__ void bar_fence() {
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void load(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)),
-               "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-      ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void wait(uint64_t* b, unsigned phase) {
-  asm volatile(
-      "{\n.reg .pred P;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      "@!P bra WAIT_%=;\n}\n" ::"r"(saddr(b)), "r"(phase) : "memory");
-}
-}  // namespace bulk
 
 constexpr int GB_THREADS = 256;                  // compute threads (8 warps)
 constexpr int GB_CTA = GB_THREADS + 32;          // + one producer warp

@@ -10,7 +10,9 @@
 // kernel) and flag non-finite input.  Output: lower triangle computed,
 // mirrored to the upper -> exactly symmetric; fixed reduction order.
 #include "mdsx_common.cuh"
+#include "bulk.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -317,14 +319,27 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
 
 // ---- one CTA per piece for k <= 104 (the config 2/3 shape).  The lower
 // triangle of the k x k Gram in 8x8 blocks (NB*(NB+1)/2 block pairs) is split
-// over the 4 warps; each warp runs all rows, so no cross-warp reduction.  Rows
-// are gathered 64 at a time with cp.async into a double-buffered stage whose
-// pitch P makes the m8n8k4 fragment loads bank-conflict free; one fragment
-// per 8-feature block and k4-step serves both the A (rows) and B (columns)
-// operand of every block pair that touches it.  Shift x0 = first row; column
-// sums (for C = sum y y^T - s s^T / m) by warp 0; mu = x0 + s/m published.
-constexpr int GP_THREADS = 128;
-constexpr int GP_KC = 64;
+// over 4 compute warps; each warp runs all rows, so no cross-warp reduction.
+//
+// Rows reach shared memory through a warp-specialised ring: a producer warp
+// gathers GP_KC rows per stage, one cp.async.bulk (TMA engine) per row issued
+// by its own lane (row index loaded a stage ahead), completing on the stage's
+// `full` mbarrier; the compute warps release a stage on its `empty` mbarrier,
+// so no CTA-wide barrier sits in the main loop.  Padding columns [p, P) of the
+// stage are zero (written once), the producer fills the rows that round the
+// last stage up to a multiple of 4 with the shift row, and only the last
+// 8-feature block masks features >= p, so (x - x0) is exactly 0 on every
+// padded position.  The pitch P is congruent so that the 32 lanes of an
+// m8n8k4 fragment load hit distinct banks.
+// One fragment per 8-feature block and k4-step serves both the A (rows) and B
+// (columns) operand of every block pair that touches it.  Shift x0 = first
+// row; the producer also accumulates the column sums s = sum (x - x0) of each
+// stage after the compute warps were handed it (C = sum y y^T - s s^T / m);
+// mu = x0 + s/m is published with the Gram.
+constexpr int GP_THREADS = 128;                 // compute warps
+constexpr int GP_CTA = GP_THREADS + 32;         // + producer warp
+constexpr int GP_KC = 32;                       // rows per stage (one per producer lane)
+constexpr int GP_HDR = 2048;                    // mbarriers, x0, column sums, flag
 
 __host__ __device__ constexpr int pair_i(int t) {
   int i = 0;
@@ -342,31 +357,22 @@ struct GpQuarter {
 };
 
 template <typename T, int NB, int Q>
-__device__ __forceinline__ void gp_chunk(const T* __restrict__ stg, int P, int nk4, int rows_left,
-                                         const double* x0r, unsigned fmask, int gid, int tig,
-                                         double (*acc)[2], double* colsum) {
+__device__ __forceinline__ void gp_chunk(const T* __restrict__ stg, int P, int nk4, const double* x0r,
+                                         bool lastmask, int gid, int tig, double (*acc)[2]) {
   using QQ = GpQuarter<NB, Q>;
+  const T* src = stg + (size_t)tig * P + gid;
 #pragma unroll 2
   for (int k4 = 0; k4 < nk4; ++k4) {
-    const int row = 4 * k4 + tig;
-    const bool rok = row < rows_left;
-    const T* src = stg + (size_t)row * P + gid;
     double f[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const bool fok = (fmask >> b) & 1u;           // feature < k (inside the staged row)
-      const double v = fok ? (double)src[8 * b] : 0.0;
-      f[b] = (rok && fok) ? v - x0r[b] : 0.0;
-    }
-    if constexpr (Q == 0) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) colsum[b] += f[b];
-    }
+    for (int b = 0; b < NB; ++b) f[b] = (double)src[8 * b] - x0r[b];
+    if (lastmask) f[NB - 1] = 0.0;             // features >= P of the last block
 #pragma unroll
     for (int u = 0; u < QQ::CNT; ++u) {
       const int t = QQ::LO + u;
       dmma(acc[u][0], acc[u][1], f[pair_i(t)], f[pair_j(t)]);
     }
+    src += 4 * P;
   }
 }
 
@@ -390,106 +396,124 @@ __device__ __forceinline__ void gp_store(double (*acc)[2], const double* s, doub
   }
 }
 
-template <typename T, int NB>
-__global__ void __launch_bounds__(GP_THREADS, 2)
+template <typename T, int NB, int NS>
+__global__ void __launch_bounds__(GP_CTA, 2)
 gram_piece_kernel(const T* __restrict__ X, int64_t ld, int p, int P,
                   const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
                   double* __restrict__ A, double* __restrict__ mu_all,
                   mdsx_piece_status* __restrict__ status) {
-  extern __shared__ __align__(16) unsigned char gp_smem[];
-  T* stage = reinterpret_cast<T*>(gp_smem);               // 2 x GP_KC x P
-  __shared__ double x0s[8 * NB], ssum[8 * NB];
-  __shared__ int bad;
+  extern __shared__ __align__(128) unsigned char gp_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(gp_smem);
+  uint64_t* empty = full + NS;
+  double* x0s = reinterpret_cast<double*>(gp_smem + 128);          // 8 NB <= 104
+  double* ssum = x0s + 104;
+  int* bad = reinterpret_cast<int*>(ssum + 104);
+  T* stage = reinterpret_cast<T*>(gp_smem + GP_HDR);                // NS x GP_KC x P
   const PieceDesc d = pd[blockIdx.x];
   const int k = d.k, m = d.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int64_t* ridx = row_idx + d.row_off;
-  const int pieces16 = (int)((size_t)p * sizeof(T) / 16);
   const size_t stage_elems = (size_t)GP_KC * P;
-  auto issue = [&](int c, int buf) {
-    const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
-    T* dst0 = stage + (size_t)buf * stage_elems;
-    // warp w copies rows w, w+4, ...: their indices are loaded in parallel
-    // (lane i holds row w + 4i) and broadcast, not chased one by one
-    constexpr int RPW = GP_KC / (GP_THREADS / 32);
-    const int myr = warp + (GP_THREADS / 32) * lane;
-    const int64_t myidx = (lane < RPW && myr < nr) ? ridx[r0 + myr] : 0;
-#pragma unroll 4
-    for (int i = 0; i < RPW; ++i) {
-      const int rr = warp + (GP_THREADS / 32) * i;
-      const int64_t gi = __shfl_sync(0xffffffffu, myidx, i);
-      if (rr < nr) {
-        const char* src = reinterpret_cast<const char*>(X + gi * ld);
-        char* dst = reinterpret_cast<char*>(dst0 + (size_t)rr * P);
-        for (int q = lane; q < pieces16; q += 32) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 16 * q);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * q));
-        }
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
   const int nchunks = (m + GP_KC - 1) / GP_KC;
-  issue(0, 0);
-  if (tid < 8 * NB) x0s[tid] = tid < k ? (double)X[ridx[0] * ld + tid] : 0.0;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  double x0r[NB];
-  unsigned fmask = 0;
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    x0r[b] = x0s[8 * b + gid];
-    fmask |= (8 * b + gid < k ? 1u : 0u) << b;
-  }
-  constexpr int QS = GpQuarter<NB, 0>::QS;
-  double acc[QS][2];
-#pragma unroll
-  for (int u = 0; u < QS; ++u) acc[u][0] = acc[u][1] = 0.0;
-  double colsum[NB];
-#pragma unroll
-  for (int b = 0; b < NB; ++b) colsum[b] = 0.0;
 
-  for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
-      issue(c + 1, (c + 1) & 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
-    __syncthreads();
-    const T* stg = stage + (size_t)(c & 1) * stage_elems;
-    const int rows_left = m - c * GP_KC;
-    const int nk4 = (min(GP_KC, rows_left) + 3) / 4;
-    switch (warp) {
-      case 0: gp_chunk<T, NB, 0>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
-      case 1: gp_chunk<T, NB, 1>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
-      case 2: gp_chunk<T, NB, 2>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
-      default: gp_chunk<T, NB, 3>(stg, P, nk4, rows_left, x0r, fmask, gid, tig, acc, colsum); break;
-    }
-    __syncthreads();                               // the buffer is refilled next iteration
+  // zero padding columns [p, P) of every stage row (never written by the copies)
+  for (int e = tid; P > p && e < NS * GP_KC * (P - p); e += GP_CTA) {
+    const int row = e / (P - p), c = p + e % (P - p);
+    stage[(size_t)row * P + c] = T(0);
   }
-  if (warp == 0) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      double sv = colsum[b];
-      sv += __shfl_xor_sync(0xffffffffu, sv, 1);
-      sv += __shfl_xor_sync(0xffffffffu, sv, 2);
-      if (tig == 0) ssum[8 * b + gid] = sv;
-      if (tig == 0 && 8 * b + gid < k && !isfinite(sv)) bad = 1;
+  if (tid < 8 * NB) x0s[tid] = tid < k ? (double)X[ridx[0] * ld + tid] : 0.0;
+  if (tid == 0) {
+    *bad = 0;
+    for (int s = 0; s < NS; ++s) {
+      bulk::bar_init(&full[s], 1);
+      bulk::bar_init(&empty[s], GP_THREADS / 32);
     }
+    bulk::bar_fence();
   }
   __syncthreads();
-  const double inv_m = 1.0 / (double)m;
-  double* out = A + d.a_off;
-  switch (warp) {
-    case 0: gp_store<T, NB, 0>(acc, ssum, inv_m, k, gid, tig, out); break;
-    case 1: gp_store<T, NB, 1>(acc, ssum, inv_m, k, gid, tig, out); break;
-    case 2: gp_store<T, NB, 2>(acc, ssum, inv_m, k, gid, tig, out); break;
-    default: gp_store<T, NB, 3>(acc, ssum, inv_m, k, gid, tig, out); break;
+
+  if (warp == GP_THREADS / 32) {
+    // ---- producer: gather rows, then column sums of the stages handed over
+    const unsigned row_bytes = (unsigned)((size_t)p * sizeof(T));
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};       // features lane + 32 q
+    double x0l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x0l[q] = lane + 32 * q < 8 * NB ? x0s[lane + 32 * q] : 0.0;
+    auto colsums = [&](int c) {
+      const int s = c % NS;
+      bulk::wait(&full[s], (unsigned)((c / NS) & 1));
+      const T* stg = stage + (size_t)s * stage_elems;
+      const int nr = min(GP_KC, m - c * GP_KC);
+      for (int i = 0; i < nr; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (lane + 32 * q < p) cs[q] += (double)stg[(size_t)i * P + lane + 32 * q] - x0l[q];
+    };
+    int64_t nidx = lane < m ? ridx[lane] : 0;
+    int64_t nidx2 = GP_KC + lane < m ? ridx[GP_KC + lane] : 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % NS;
+      const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
+      const int64_t idx = nidx;
+      nidx = nidx2;
+      if (r0 + 2 * GP_KC + lane < m) nidx2 = ridx[r0 + 2 * GP_KC + lane];
+      if (c >= NS) bulk::wait(&empty[s], (unsigned)((c / NS - 1) & 1));
+      T* dst = stage + (size_t)s * stage_elems;
+      const int npad = ((nr + 3) & ~3) - nr;     // rows that complete the last k4 group
+      for (int e = lane; e < npad * p; e += 32)
+        dst[(size_t)(nr + e / p) * P + e % p] = (T)x0s[e % p];
+      __syncwarp();
+      if (lane == 0) bulk::arrive_expect(&full[s], (unsigned)nr * row_bytes);
+      __syncwarp();
+      if (lane < nr) bulk::copy(dst + (size_t)lane * P, X + idx * ld, row_bytes, &full[s]);
+      if (c >= NS - 1) colsums(c - (NS - 1));
+    }
+    for (int c = max(0, nchunks - (NS - 1)); c < nchunks; ++c) colsums(c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = lane + 32 * q;
+      if (a < 8 * NB) ssum[a] = a < p ? cs[q] : 0.0;
+      if (a < k && !isfinite(cs[q])) *bad = 1;
+    }
+  } else {
+    // ---- compute warps
+    double x0r[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) x0r[b] = x0s[8 * b + gid];
+    const bool lastmask = 8 * (NB - 1) + gid >= P;    // the stage pitch may be < 8 NB
+    constexpr int QS = GpQuarter<NB, 0>::QS;
+    double acc[QS][2];
+#pragma unroll
+    for (int u = 0; u < QS; ++u) acc[u][0] = acc[u][1] = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % NS;
+      bulk::wait(&full[s], (unsigned)((c / NS) & 1));
+      const T* stg = stage + (size_t)s * stage_elems;
+      const int nk4 = (min(GP_KC, m - c * GP_KC) + 3) / 4;
+      switch (warp) {
+        case 0: gp_chunk<T, NB, 0>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
+        case 1: gp_chunk<T, NB, 1>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
+        case 2: gp_chunk<T, NB, 2>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
+        default: gp_chunk<T, NB, 3>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
+      }
+      __syncwarp();
+      if (lane == 0) bulk::arrive(&empty[s]);
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(GP_CTA));          // column sums ready
+    const double inv_m = 1.0 / (double)m;
+    double* out = A + d.a_off;
+    switch (warp) {
+      case 0: gp_store<T, NB, 0>(acc, ssum, inv_m, k, gid, tig, out); break;
+      case 1: gp_store<T, NB, 1>(acc, ssum, inv_m, k, gid, tig, out); break;
+      case 2: gp_store<T, NB, 2>(acc, ssum, inv_m, k, gid, tig, out); break;
+      default: gp_store<T, NB, 3>(acc, ssum, inv_m, k, gid, tig, out); break;
+    }
+    if (tid < k) mu_all[(int64_t)d.id * p + tid] = x0s[tid] + ssum[tid] * inv_m;
+    if (tid == 0 && *bad) status[d.id].code = MDSX_INVALID_INPUT;
+    return;
   }
-  if (tid < k) mu_all[(int64_t)d.id * p + tid] = x0s[tid] + ssum[tid] * inv_m;
-  if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
+  asm volatile("bar.sync 1, %0;\n" ::"r"(GP_CTA));
 }
 
 // Combine the centred Grams of a piece's row ranges (parallel-variance
@@ -569,8 +593,8 @@ int launch_gram_combine(mdsx_handle* h, const PieceDesc* pd, const int4* rng, in
 }
 
 
-// Pitch (elements) of a staged row: >= p, 16-byte multiple, and congruent so
-// that the 32 lanes of an m8n8k4 fragment load hit distinct banks.
+// Pitch (elements) of a staged row: >= p, 16-byte multiple, and congruent so that the 32 lanes of an m8n8k4 fragment load hit
+// distinct banks.
 static int gp_pitch(int p, size_t es) {
   int P = p;
   if (es == 8) { while (P % 16 != 4) ++P; }
@@ -589,15 +613,16 @@ int launch_gram_piece(mdsx_handle* h, const void* data, int dtype, int64_t ld, i
                       double* mu, mdsx_piece_status* status, cudaStream_t st) {
   if (npieces == 0) return MDSX_OK;
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
-  const int P = gp_pitch(p, es);
-  const size_t smem = 2 * (size_t)GP_KC * P * es;
   auto go = [&](auto tag, auto nb) {
     using T = decltype(tag);
     constexpr int NB = decltype(nb)::value;
-    auto kern = gram_piece_kernel<T, NB>;
+    constexpr int NS = 4;
+    const int P = gp_pitch(std::max(p, 8 * (NB - 1)), es);   // only the last block can pass P
+    const size_t smem = GP_HDR + (size_t)NS * GP_KC * P * es + 64;   // + overrun of the last fragment
+    auto kern = gram_piece_kernel<T, NB, NS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
-    kern<<<npieces, GP_THREADS, smem, st>>>((const T*)data, ld, p, P, row_idx, pd, A, mu, status);
+    kern<<<npieces, GP_CTA, smem, st>>>((const T*)data, ld, p, P, row_idx, pd, A, mu, status);
     return launched(h, "gram_piece_kernel", st);
   };
   using N4 = std::integral_constant<int, 4>;
