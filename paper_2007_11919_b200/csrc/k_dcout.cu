@@ -15,6 +15,7 @@
 // (x - mu_j) U'_j + t_j - mean with U'_j = U_j T_j, on the fp64 tensor pipe
 // (DMMA m8n8k4: 8 rows x 8 columns per fragment, U' held in registers).
 #include "mdsx_common.cuh"
+#include "bulk.cuh"
 
 #include <algorithm>
 #include <type_traits>
@@ -172,38 +173,80 @@ dc_mean2_kernel(const double* __restrict__ contrib, int npieces, int r, double i
 
 // The output pass: out[oidx[row]] = (x - mu_j) Uc_j + tvec_j - mean for the
 // rows [first_j, m_j) of piece j (first_j = 0 for piece 0 or when c0 == 0,
-// else c0).  Grid (row ranges of OR rows, pieces), 4 warps; rows gathered
-// CR = 64 at a time by cp.async into a double-buffered stage (pitch P:
-// conflict-free m8n8k4 fragments); each warp computes two 8-row tiles per
-// chunk on the fp64 tensor pipe with the K range split over two accumulator
-// sets (eight independent DMMA chains per warp).  U' fragments live in
-// registers for the whole CTA, the piece mean in shared memory.
-constexpr int OT = 128;
-constexpr int CR = 64;            // rows per chunk (4 warps x 2 tiles x 8)
-constexpr int OR = 256;           // rows per CTA
+// else c0).  Grid (row ranges of up to PO_ROWS rows, pieces).  Rows reach
+// shared memory through the same warp-specialised ring as the Gram: a
+// producer warp gathers PO_KC rows per stage, one cp.async.bulk per row (row
+// index loaded two stages ahead), on the stage's `full` mbarrier; each of the
+// 4 compute warps takes one 8-row tile of a stage on the fp64 tensor pipe
+// (m8n8k4, the K range split over two accumulator sets) and releases the
+// stage on its `empty` mbarrier.  U' fragments live in registers for the whole
+// CTA, the piece mean in shared memory; the stage pitch P (== 4 mod 16
+// doubles) makes the fragment loads conflict-free and the padding columns
+// [p, P) are zero.
+constexpr int PO_THREADS = 128;   // compute warps
+constexpr int PO_CTA = PO_THREADS + 32;
+constexpr int PO_KC = 32;         // rows per stage (one per producer lane, 4 tiles of 8)
+constexpr int PO_NS = 4;          // stages
+constexpr int PO_ROWS = 256;      // rows per CTA
+constexpr int PO_HDR = 2048;      // mbarriers + piece mean
 
 template <typename T, int K4, int NT>
-__global__ void __launch_bounds__(OT)
+__global__ void __launch_bounds__(PO_CTA, 2)
 piece_out_kernel(const T* __restrict__ X, int64_t ld, int p, int P, const int64_t* __restrict__ row_idx,
                  const int64_t* __restrict__ out_idx, const PieceDesc* __restrict__ pd, int r, int c0,
                  const double* __restrict__ mu_all, const double* __restrict__ Uc,
                  const double* __restrict__ tvec, const double* __restrict__ mean,
                  double* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char do_smem[];
-  T* stage = reinterpret_cast<T*>(do_smem);
-  double* smu = reinterpret_cast<double*>(do_smem + 2 * (size_t)CR * P * sizeof(T));
+  extern __shared__ __align__(128) unsigned char do_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(do_smem);
+  uint64_t* empty = full + PO_NS;
+  double* smu = reinterpret_cast<double*>(do_smem + 128);           // 4 K4 <= 128
+  T* stage = reinterpret_cast<T*>(do_smem + PO_HDR);
   const int j = blockIdx.y;                       // local piece (Uc, tvec are offset)
   const PieceDesc d = pd[j];
   const int first = d.id == 0 ? 0 : c0;
-  const int r0 = first + blockIdx.x * OR;
+  const int r0 = first + blockIdx.x * PO_ROWS;
   if (r0 >= d.m) return;
-  const int nrows = min(OR, d.m - r0);
+  const int nrows = min(PO_ROWS, d.m - r0);
+  const int nch = (nrows + PO_KC - 1) / PO_KC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int64_t* ridx = row_idx + d.row_off + r0;
   const int64_t* oidx = (out_idx ? out_idx : row_idx) + d.row_off + r0;
+  const size_t stage_elems = (size_t)PO_KC * P;
+  for (int e = tid; e < 4 * K4; e += PO_CTA) smu[e] = e < p ? mu_all[(int64_t)d.id * p + e] : 0.0;
+  for (int e = tid; P > p && e < PO_NS * PO_KC * (P - p); e += PO_CTA)
+    stage[(size_t)(e / (P - p)) * P + p + e % (P - p)] = T(0);
+  if (tid == 0) {
+    for (int s = 0; s < PO_NS; ++s) {
+      bulk::bar_init(&full[s], 1);
+      bulk::bar_init(&empty[s], PO_THREADS / 32);
+    }
+    bulk::bar_fence();
+  }
+  __syncthreads();
+
+  if (warp == PO_THREADS / 32) {                  // ---- producer
+    const unsigned row_bytes = (unsigned)((size_t)p * sizeof(T));
+    int64_t nidx = lane < nrows ? ridx[lane] : 0;
+    int64_t nidx2 = PO_KC + lane < nrows ? ridx[PO_KC + lane] : 0;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % PO_NS;
+      const int b0 = c * PO_KC, nr = min(PO_KC, nrows - b0);
+      const int64_t idx = nidx;
+      nidx = nidx2;
+      if (b0 + 2 * PO_KC + lane < nrows) nidx2 = ridx[b0 + 2 * PO_KC + lane];
+      if (c >= PO_NS) bulk::wait(&empty[s], (unsigned)((c / PO_NS - 1) & 1));
+      if (lane == 0) bulk::arrive_expect(&full[s], (unsigned)nr * row_bytes);
+      __syncwarp();
+      if (lane < nr)
+        bulk::copy(stage + (size_t)s * stage_elems + (size_t)lane * P, X + idx * ld, row_bytes, &full[s]);
+    }
+    return;
+  }
+
+  // ---- compute warps
   const double* U = Uc + (int64_t)j * p * r;
-  for (int e = tid; e < 4 * K4; e += OT) smu[e] = e < p ? mu_all[(int64_t)d.id * p + e] : 0.0;
   double bf[K4][NT];
 #pragma unroll
   for (int k4 = 0; k4 < K4; ++k4) {
@@ -222,89 +265,46 @@ piece_out_kernel(const T* __restrict__ X, int64_t ld, int p, int P, const int64_
       const int q = 8 * n + 2 * tig + v;
       add[n][v] = q < r ? tvec[(int64_t)j * r + q] - mean[q] : 0.0;
     }
-  const int pieces16 = (int)((size_t)p * sizeof(T) / 16);
-  const size_t stage_elems = (size_t)CR * P;
-  const int nch = (nrows + CR - 1) / CR;
-  auto issue = [&](int ch, int buf) {
-    const int b0 = ch * CR, nr = min(CR, nrows - b0);
-    T* dst0 = stage + (size_t)buf * stage_elems;
-    constexpr int RPW = CR / (OT / 32);                 // 16 rows per warp
-    const int myr = warp + (OT / 32) * lane;
-    const int64_t myidx = (lane < RPW && myr < nr) ? ridx[b0 + myr] : 0;
+  for (int c = 0; c < nch; ++c) {
+    const int s = c % PO_NS;
+    const int b0 = c * PO_KC, nr = min(PO_KC, nrows - b0);
+    bulk::wait(&full[s], (unsigned)((c / PO_NS) & 1));
+    const int tr = 8 * warp;                       // this warp's tile: stage rows tr .. tr+7
+    double acc[NT][2][2];
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const int rr = warp + (OT / 32) * i;
-      const int64_t gi = __shfl_sync(0xffffffffu, myidx, i);
-      if (rr < nr) {
-        const char* src = reinterpret_cast<const char*>(X + gi * ld);
-        char* dst = reinterpret_cast<char*>(dst0 + (size_t)rr * P);
-        for (int q = lane; q < pieces16; q += 32) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 16 * q);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * q));
-        }
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-  issue(0, 0);
-  for (int ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) {
-      issue(ch + 1, (ch + 1) & 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
-    __syncthreads();
-    const T* stg = stage + (size_t)(ch & 1) * stage_elems;
-    const int tr0 = ch * CR + 16 * warp;               // this warp's tiles: rows tr0 .. tr0+15
-    if (tr0 < nrows) {
-      double acc[2][NT][2][2];                         // [tile][n][k half][v]
+    for (int n = 0; n < NT; ++n)
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int n = 0; n < NT; ++n)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) acc[t][n][h][0] = acc[t][n][h][1] = 0.0;
-      const T* x0 = stg + (size_t)(16 * warp + gid) * P + tig;
-      const T* x1 = x0 + (size_t)8 * P;
-      const bool ok0 = tr0 + gid < nrows, ok1 = tr0 + 8 + gid < nrows;
+      for (int hh = 0; hh < 2; ++hh) acc[n][hh][0] = acc[n][hh][1] = 0.0;
+    if (tr < nr) {
+      const T* x0 = stage + (size_t)s * stage_elems + (size_t)(tr + gid) * P + tig;
 #pragma unroll
       for (int k4 = 0; k4 < K4; ++k4) {
-        const int a = 4 * k4 + tig;
-        const bool aok = a < p;
-        const double m4 = smu[a];
-        const double xa = (ok0 && aok) ? (double)x0[4 * k4] - m4 : 0.0;
-        const double xb = (ok1 && aok) ? (double)x1[4 * k4] - m4 : 0.0;
+        const double xa = (double)x0[4 * k4] - smu[4 * k4 + tig];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          dmma(acc[0][n][k4 & 1][0], acc[0][n][k4 & 1][1], xa, bf[k4][n]);
-          dmma(acc[1][n][k4 & 1][0], acc[1][n][k4 & 1][1], xb, bf[k4][n]);
-        }
+        for (int n = 0; n < NT; ++n) dmma(acc[n][k4 & 1][0], acc[n][k4 & 1][1], xa, bf[k4][n]);
       }
-      // lane (gid, tig) holds out[row gid of each tile][8n + 2tig + v]
+    }
+    __syncwarp();
+    if (lane == 0) bulk::arrive(&empty[s]);
+    // lane (gid, tig) holds out[row gid of the tile][8n + 2tig + v]
+    const int row = b0 + tr + gid;
+    if (tr + gid < nr) {
+      double* o = out + oidx[row] * r;
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int row = tr0 + 8 * t + gid;
-        if (row < nrows) {
-          double* o = out + oidx[row] * r;
-#pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            const int q = 8 * n + 2 * tig;
-            const double v0 = acc[t][n][0][0] + acc[t][n][1][0] + add[n][0];
-            const double v1 = acc[t][n][0][1] + acc[t][n][1][1] + add[n][1];
-            if (q + 1 < r && !(r & 1)) {       // 16-byte aligned pair (row stride r doubles, r even)
-              *reinterpret_cast<double2*>(o + q) = make_double2(v0, v1);
-            } else if (q + 1 < r) {
-              o[q] = v0;
-              o[q + 1] = v1;
-            } else if (q < r) {
-              o[q] = v0;
-            }
-          }
+      for (int n = 0; n < NT; ++n) {
+        const int q = 8 * n + 2 * tig;
+        const double v0 = acc[n][0][0] + acc[n][1][0] + add[n][0];
+        const double v1 = acc[n][0][1] + acc[n][1][1] + add[n][1];
+        if (q + 1 < r && !(r & 1)) {             // 16-byte aligned pair (row stride r doubles, r even)
+          *reinterpret_cast<double2*>(o + q) = make_double2(v0, v1);
+        } else if (q + 1 < r) {
+          o[q] = v0;
+          o[q + 1] = v1;
+        } else if (q < r) {
+          o[q] = v0;
         }
       }
     }
-    __syncthreads();
   }
 }
 
@@ -384,18 +384,18 @@ int launch_piece_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, in
                      int npieces, int64_t max_m, int r, int c0, const double* mu, const double* Uc,
                      const double* tvec, const double* mean, double* out, cudaStream_t st) {
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
-  const int P = dco_pitch(p, es);
-  const dim3 grid((unsigned)((max_m + OR - 1) / OR), (unsigned)npieces);
+  const dim3 grid((unsigned)((max_m + PO_ROWS - 1) / PO_ROWS), (unsigned)npieces);
   auto go = [&](auto tag, auto k4, auto nt) {
     using Tt = decltype(tag);
     constexpr int K4 = decltype(k4)::value;
     constexpr int NT = decltype(nt)::value;
-    const size_t smem = 2 * (size_t)CR * P * es + 4 * K4 * sizeof(double);
+    const int P = dco_pitch(std::max(p, 4 * K4), es);      // fragment loads stay inside the row
+    const size_t smem = PO_HDR + (size_t)PO_NS * PO_KC * P * es;
     auto kern = piece_out_kernel<Tt, K4, NT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     mdsx::pre(h, st);
-    kern<<<grid, OT, smem, st>>>((const Tt*)data, ld, p, P, row_idx, out_idx, pd, r, c0, mu, Uc,
-                                 tvec, mean, out);
+    kern<<<grid, PO_CTA, smem, st>>>((const Tt*)data, ld, p, P, row_idx, out_idx, pd, r, c0, mu, Uc,
+                                     tvec, mean, out);
     return launched(h, "piece_out_kernel", st);
   };
   auto by_k = [&](auto tag, auto nt) {
