@@ -1,6 +1,6 @@
 """Per-kernel times (serialised pass, CUDA events per launch) of one workload,
 without result checks -- for A/B experiments with run-time switches:
-    MDSX_X=1 python tools/ktime.py dc2 [steps]"""
+    MDSX_X=1 python tools/ktime.py dc2 [steps] [n]"""
 import os
 import sys
 from pathlib import Path
@@ -13,6 +13,8 @@ from paper_2007_11919_b200 import _device as D
 name = sys.argv[1] if len(sys.argv) > 1 else "dc2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 w = dict(bench.WORKLOADS[name])
+if len(sys.argv) > 3:
+    w["n"] = int(sys.argv[3])
 dev = torch.device("cuda", 0)
 x = D.from_host(np.ascontiguousarray(bench.host_input(w, w["n"])), dev)
 plan = bench.make_plan(w, w["n"])
