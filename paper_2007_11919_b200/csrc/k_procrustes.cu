@@ -198,6 +198,206 @@ procrustes_fit_kernel(const double* __restrict__ tgt, const int64_t* __restrict_
 // ends the fit (further sweeps are no-ops, so groups of one warp simply run
 // until the slowest converges).  T = V L^T, t, loss and the degenerate flag
 // as procrustes_fit_kernel (the same rule for rank-deficient left bases).
+// ---- fast path for well-conditioned fits (r <= 16, K <= NS_KMAX rows):
+// one warp per fit, the K target/source rows staged in shared memory, the
+// cross-product B (r x r) formed by the 32 lanes, and its orthogonal polar
+// factor Q = L V^T (B = L S V^T) by the Newton-Schulz iteration
+//     X_0 = B / |B|_F,   X_{k+1} = X_k (3 I - X_k^T X_k) / 2,
+// quadratically convergent once the singular values of X_k are near 1 and
+// multiplying small ones by ~1.5 per step before that: a warp-parallel
+// sequence of r x r products instead of the serial plane rotations of the
+// Jacobi SVD.  T = V L^T = Q^T (the rotation procrustes.py:46-78 forms as
+// right @ left.T; the polar factor is unique for nonsingular B, so T is the
+// same).  Converged within NS_ITMAX steps  =>  s_min / s_max >~ 1e-7, so the
+// fit is not degenerate (procrustes.py:48, ratio 1e-12).  Fits that do not
+// converge (near-singular or rank-deficient B, whose rotation depends on the
+// completion of the left basis) or have more than NS_KMAX rows are marked
+// degenerate = -1 and recomputed by the Jacobi kernel launched right after.
+constexpr int NS_WARPS = 4;
+constexpr int NS_KMAX = 64;
+constexpr int NS_ITMAX = 40;
+
+template <int R>
+__global__ void __launch_bounds__(NS_WARPS * 32)
+procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
+                         const double* __restrict__ src, const int64_t* __restrict__ src_rows,
+                         const int64_t* __restrict__ job_off, int njobs,
+                         double* __restrict__ rot, double* __restrict__ trans,
+                         double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+  constexpr int RR = R * R;
+  constexpr int Q = (RR + 31) / 32;                 // matrix entries per lane
+  constexpr int WS = 2 * NS_KMAX * R + 2 * RR + 3 * R;
+  extern __shared__ double nsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * NS_WARPS + warp;
+  if (job >= njobs) return;
+  double* xs = nsm + (size_t)warp * WS;
+  double* ys = xs + NS_KMAX * R;
+  double* Xs = ys + NS_KMAX * R;
+  double* Gs = Xs + RR;
+  double* mx = Gs + RR;
+  double* my = mx + R;
+  double* tv = my + R;
+  const int64_t o = job_off[job];
+  const int K = (int)(job_off[job + 1] - o);
+  if (K > NS_KMAX || K < 1) {
+    if (lane == 0) degenerate[job] = -1;
+    return;
+  }
+  // lane entries e = lane + 32 q of an R x R matrix: row ea[q], column eb[q]
+  int ea[Q], eb[Q];
+  bool ev[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int e = lane + 32 * q;
+    ev[q] = e < RR;
+    ea[q] = ev[q] ? e / R : 0;
+    eb[q] = ev[q] ? e - ea[q] * R : 0;
+  }
+  for (int e = lane; e < K * R; e += 32) {
+    const int t = e / R, a = e - t * R;
+    xs[e] = tgt[tgt_rows[o + t] * R + a];
+    ys[e] = src[src_rows[o + t] * R + a];
+  }
+  __syncwarp();
+  if (lane < R || (lane >= 16 && lane - 16 < R)) {
+    const int a = lane & 15;
+    const double* v = lane < 16 ? xs : ys;
+    double m0 = 0.0, m1 = 0.0;
+    int t = 0;
+    for (; t + 1 < K; t += 2) {
+      m0 += v[t * R + a];
+      m1 += v[(t + 1) * R + a];
+    }
+    if (t < K) m0 += v[t * R + a];
+    (lane < 16 ? mx : my)[a] = (m0 + m1) / K;
+  }
+  __syncwarp();
+  for (int e = lane; e < K * R; e += 32) {          // centre in place
+    const int a = e % R;
+    xs[e] -= mx[a];
+    ys[e] -= my[a];
+  }
+  __syncwarp();
+  // B[a][b] = sum_t x_t[a] y_t[b] (centred)
+  double fro = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ev[q]) {
+      double c0 = 0.0, c1 = 0.0;
+      int t = 0;
+      for (; t + 1 < K; t += 2) {
+        c0 = fma(xs[t * R + ea[q]], ys[t * R + eb[q]], c0);
+        c1 = fma(xs[(t + 1) * R + ea[q]], ys[(t + 1) * R + eb[q]], c1);
+      }
+      if (t < K) c0 = fma(xs[t * R + ea[q]], ys[t * R + eb[q]], c0);
+      const double bv = c0 + c1;
+      Gs[lane + 32 * q] = bv;
+      fro = fma(bv, bv, fro);
+    }
+  }
+  fro = mdsx::warp_sum(fro);
+  __syncwarp();
+  // scale by a guaranteed upper bound of s_max, min(|B|_F, sqrt(|B|_1 |B|_inf)):
+  // every singular value of X_0 then lies in (0, 1] and the iteration stays
+  // monotone (a value above sqrt(3) would converge to -1, a wrong rotation)
+  double smax = sqrt(fro);
+  {
+    double rs = 0.0, cs = 0.0;
+    if (lane < R) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        rs += fabs(Gs[lane * R + c]);
+        cs += fabs(Gs[c * R + lane]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      rs = fmax(rs, __shfl_xor_sync(0xffffffffu, rs, off));
+      cs = fmax(cs, __shfl_xor_sync(0xffffffffu, cs, off));
+    }
+    smax = fmin(smax, sqrt(rs * cs));
+  }
+  const double inv = fro > 0.0 ? 1.0 / smax : 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q)
+    if (ev[q]) Xs[lane + 32 * q] = Gs[lane + 32 * q] * inv;
+  __syncwarp();
+  bool conv = false, last = false;
+  for (int it = 0; it < NS_ITMAX && fro > 0.0; ++it) {
+    double dev = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (ev[q]) {
+        double g = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) g = fma(Xs[i * R + ea[q]], Xs[i * R + eb[q]], g);
+        Gs[lane + 32 * q] = g;
+        dev = fmax(dev, fabs(g - (ea[q] == eb[q] ? 1.0 : 0.0)));
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, off));
+    if (dev < 1e-10) last = true;                   // one more step: error ~ dev^2, rounding-limited
+    __syncwarp();
+    double nx[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (ev[q]) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) s2 = fma(Xs[ea[q] * R + a], Gs[a * R + eb[q]], s2);
+        nx[q] = fma(1.5, Xs[lane + 32 * q], -0.5 * s2);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (ev[q]) Xs[lane + 32 * q] = nx[q];
+    __syncwarp();
+    if (last) { conv = true; break; }
+  }
+  if (!conv) {
+    if (lane == 0) degenerate[job] = -1;            // the Jacobi kernel takes this fit
+    return;
+  }
+  // T = Q^T (row-major), t = mx - my T, loss
+  double* T = rot + (size_t)job * RR;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ev[q]) {
+      const double v = Xs[eb[q] * R + ea[q]];
+      T[lane + 32 * q] = v;
+      Gs[lane + 32 * q] = v;
+    }
+  }
+  __syncwarp();
+  if (lane < R) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) s2 = fma(my[a], Gs[a * R + lane], s2);
+    const double t = mx[lane] - s2;
+    tv[lane] = t;
+    trans[(size_t)job * R + lane] = t;
+  }
+  __syncwarp();
+  // residuals of the centred rows: x_c - y_c T (the translation absorbs the means)
+  double ls = 0.0;
+  for (int e = lane; e < K * R; e += 32) {
+    const int t = e / R, b = e - t * R;
+    double s2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; ++a) s2 = fma(ys[t * R + a], Gs[a * R + b], s2);
+    const double d = xs[e] - s2;
+    ls = fma(d, d, ls);
+  }
+  ls = mdsx::warp_sum(ls);
+  if (lane == 0) {
+    loss[job] = ls;
+    degenerate[job] = 0;
+  }
+}
+
 constexpr int FR_WARPS = 2;
 
 template <int RM>
@@ -206,7 +406,7 @@ procrustes_fit_reg_kernel(const double* __restrict__ tgt, const int64_t* __restr
                           const double* __restrict__ src, const int64_t* __restrict__ src_rows,
                           const int64_t* __restrict__ job_off, int njobs, int r,
                           double* __restrict__ rot, double* __restrict__ trans,
-                          double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+                          double* __restrict__ loss, int32_t* __restrict__ degenerate, int redo) {
   extern __shared__ double sm[];
   const int P = (r + 1) >> 1;                  // lanes per fit
   const int FPW = 32 / P;                      // fits per warp
@@ -214,7 +414,9 @@ procrustes_fit_reg_kernel(const double* __restrict__ tgt, const int64_t* __restr
   const int g = lane / P, l = lane - g * P;
   const int gbase = g * P;
   const int job = (blockIdx.x * FR_WARPS + warp) * FPW + g;
-  const bool act = g < FPW && job < njobs;
+  // redo: only the fits the Newton-Schulz kernel handed over (degenerate == -1)
+  const bool act = g < FPW && job < njobs && (!redo || degenerate[job] == -1);
+  if (__ballot_sync(0xffffffffu, act) == 0u) return;
   // per-fit shared area: L, V (r x r, column-major), T (r x r, row-major), ms (r)
   double* Ls = sm + ((size_t)warp * FPW + (g < FPW ? g : 0)) * (3 * r * r + r);
   double* Vs = Ls + r * r;
@@ -966,6 +1168,38 @@ int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_
                           int32_t* degenerate, cudaStream_t st) {
   if (njobs == 0) return MDSX_OK;
   if (r <= 16 && !getenv("MDSX_FIT_WARP")) {
+    {                                            // Newton-Schulz fast path first
+      auto ns = [&](auto rc_) -> int {
+        constexpr int R = decltype(rc_)::value;
+        auto kern = procrustes_fit_ns_kernel<R>;
+        const size_t sm1 = (size_t)NS_WARPS * (2 * NS_KMAX * R + 2 * R * R + 3 * R) * sizeof(double);
+        if (sm1 > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        mdsx::pre(h, st);
+        kern<<<(njobs + NS_WARPS - 1) / NS_WARPS, NS_WARPS * 32, sm1, st>>>(
+            tgt, tgt_rows, src, src_rows, job_off_dev, njobs, rot, trans, loss, degenerate);
+        return launched(h, "procrustes_ns_kernel", st);
+      };
+      int rc = MDSX_OK;
+      switch (r) {
+        case 1: rc = ns(std::integral_constant<int, 1>{}); break;
+        case 2: rc = ns(std::integral_constant<int, 2>{}); break;
+        case 3: rc = ns(std::integral_constant<int, 3>{}); break;
+        case 4: rc = ns(std::integral_constant<int, 4>{}); break;
+        case 5: rc = ns(std::integral_constant<int, 5>{}); break;
+        case 6: rc = ns(std::integral_constant<int, 6>{}); break;
+        case 7: rc = ns(std::integral_constant<int, 7>{}); break;
+        case 8: rc = ns(std::integral_constant<int, 8>{}); break;
+        case 9: rc = ns(std::integral_constant<int, 9>{}); break;
+        case 10: rc = ns(std::integral_constant<int, 10>{}); break;
+        case 11: rc = ns(std::integral_constant<int, 11>{}); break;
+        case 12: rc = ns(std::integral_constant<int, 12>{}); break;
+        case 13: rc = ns(std::integral_constant<int, 13>{}); break;
+        case 14: rc = ns(std::integral_constant<int, 14>{}); break;
+        case 15: rc = ns(std::integral_constant<int, 15>{}); break;
+        default: rc = ns(std::integral_constant<int, 16>{}); break;
+      }
+      if (rc) return rc;
+    }
     const int P = (r + 1) / 2, fpw = 32 / P;
     const size_t sm2 = (size_t)FR_WARPS * fpw * (3 * r * r + r) * sizeof(double);
     const int blocks = (int)((njobs + (int64_t)FR_WARPS * fpw - 1) / ((int64_t)FR_WARPS * fpw));
@@ -976,7 +1210,7 @@ int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
       mdsx::pre(h, st);
       kern<<<blocks, FR_WARPS * 32, sm2, st>>>(tgt, tgt_rows, src, src_rows, job_off_dev, njobs, r,
-                                                rot, trans, loss, degenerate);
+                                                rot, trans, loss, degenerate, 1);
       return launched(h, "procrustes_fit_kernel", st);
     };
     if (r <= 4) return go(std::integral_constant<int, 4>{});

@@ -367,10 +367,12 @@ class TestAlgorithms:
 
 
 class TestProcrustesBatched:
-    """The batched fit kernels (lane-group register kernel for r <= 16, the
-    warp kernel above) against the oracle restatement of procrustes.py:46-78
-    on many jobs at once: every r up to 16, uneven job sizes, rank-deficient
-    cross products (collinear / constant sources)."""
+    """The batched fit kernels (Newton-Schulz polar factor with the
+    lane-group Jacobi kernel taking the fits it does not converge on, for
+    r <= 16; the warp kernel above) against the oracle restatement of
+    procrustes.py:46-78 on many jobs at once: every r up to 16, uneven job
+    sizes, rank-deficient cross products (collinear / constant sources),
+    near-singular and strongly anisotropic ones."""
 
     @staticmethod
     def _batch(mds, tgts, srcs, r):
@@ -403,6 +405,10 @@ class TestProcrustesBatched:
                 s[:, -1] = s[:, 0]
             elif j % 11 == 7:              # constant source: zero cross product
                 s = np.ones((k, r))
+            elif j % 11 in (5, 9):         # spread singular values: near-singular (Jacobi
+                q, _ = np.linalg.qr(rng.standard_normal((r, r)))     # redo) / anisotropic
+                sv = np.logspace(0, -9 if j % 11 == 5 else -2, r)
+                s = (t - t.mean(axis=0)) @ q * sv + rng.standard_normal(r)
             else:
                 q, _ = np.linalg.qr(rng.standard_normal((r, r)))
                 s = t @ q + rng.standard_normal((k, r)) * 0.1 + rng.standard_normal(r)
