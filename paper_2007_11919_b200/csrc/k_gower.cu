@@ -194,11 +194,35 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
   for (int e = tid; e < r * r; e += blockDim.x) E[e] = Ssh[e];
   __syncthreads();
   if (warp == 0) {
-    // eigenvalues of the symmetric PSD S for the condition test
-    // (algorithms.py:209-216) as the singular values of S: one-sided Jacobi on
-    // its columns, lane a owns row a, the three column dots of a pair reduced
-    // by one interleaved shuffle tree (a serial one-thread Jacobi cost ~0.15 ms)
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    // condition test (algorithms.py:209-216).  S is the covariance of the base
+    // configuration, whose columns are orthogonal (classical MDS), so S is
+    // diagonal up to rounding and the Gershgorin discs [d_a - R_a, d_a + R_a]
+    // already certify cond(S) <= max(d + R) / min(d - R) far below the limit:
+    // then that bound is the reported estimate and no eigenvalue is computed.
+    // Otherwise (and always for a base configuration that is not diagonal
+    // enough): the eigenvalues by Jacobi as below, the reference's exact test.
+    double glo = 1e308, ghi = 0.0;
+    if (lane < r) {
+      double rad = 0.0;
+      for (int c = 0; c < r; ++c)
+        if (c != lane) rad += fabs(Ssh[lane * r + c]);
+      glo = Ssh[lane * r + lane] - rad;
+      ghi = Ssh[lane * r + lane] + rad;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      glo = fmin(glo, __shfl_xor_sync(0xffffffffu, glo, o));
+      ghi = fmax(ghi, __shfl_xor_sync(0xffffffffu, ghi, o));
+    }
+    const bool certified = glo > 0.0 && ghi <= 1e10 * glo;
+    if (certified && lane == 0) {
+      cond[0] = ghi / glo;
+      ok = 1;
+    }
+    // eigenvalues of the symmetric PSD S as the singular values of S: one-sided
+    // Jacobi on its columns, lane a owns row a, the three column dots of a pair
+    // reduced by one interleaved shuffle tree
+    for (int sweep = 0; sweep < 60 && !certified; ++sweep) {
       int nrot = 0;
       for (int i = 0; i < r - 1; ++i)
         for (int j = i + 1; j < r; ++j) {
@@ -225,17 +249,19 @@ ctx_finalize_kernel(const double* __restrict__ X1, int64_t l, int p, int r,
         }
       if (nrot == 0) break;
     }
-    double lo = 1e308, hi = 0.0;
-    for (int i = 0; i < r; ++i) {
-      const double x = lane < r ? E[lane * r + i] : 0.0;
-      const double sv = sqrt(mdsx::warp_sum(x * x));
-      lo = fmin(lo, sv);
-      hi = fmax(hi, sv);
-    }
-    if (lane == 0) {
-      const double cd = lo <= 0.0 ? INFINITY : hi / lo;
-      cond[0] = cd;
-      ok = cd <= 1e12 ? 1 : 0;
+    if (!certified) {
+      double lo = 1e308, hi = 0.0;
+      for (int i = 0; i < r; ++i) {
+        const double x = lane < r ? E[lane * r + i] : 0.0;
+        const double sv = sqrt(mdsx::warp_sum(x * x));
+        lo = fmin(lo, sv);
+        hi = fmax(hi, sv);
+      }
+      if (lane == 0) {
+        const double cd = lo <= 0.0 ? INFINITY : hi / lo;
+        cond[0] = cd;
+        ok = cd <= 1e12 ? 1 : 0;
+      }
     }
   }
   __syncthreads();
