@@ -258,28 +258,26 @@ def piece_sizes(w: dict, plan) -> list:
     return [w["l"]]
 
 
-def fused_points(w: dict) -> bool:
-    """The piece pipeline computes points inside the Lanczos kernel (mdsx_api.cu
-    run_classical): D&C / fast, every piece form 0 with k <= 104, r <= 10,
-    aligned rows."""
-    return (w["algo"] in ("divide", "fast") and w["p"] <= 104 and w["r"] <= 10
-            and not os.environ.get("MDSX_NO_FUSE"))
-
-
-def kernel_work(w: dict, n: int, plan, kernel: str, krylov_dims=None, executed=0.0) -> dict | None:
+def kernel_work(w: dict, n: int, plan, kernel: str, krylov_dims=None, executed=0.0,
+                p_eff=None) -> dict | None:
     """Algorithmic work of ONE step's launches of `kernel` (DESIGN.md §3 work
-    models): flops for compute-bound kernels (fp64), bytes for streaming ones."""
+    models): flops for compute-bound kernels (fp64), bytes for streaming ones.
+    p_eff: the width the kernels actually ran at (column compaction of wide
+    inputs drops the all-zero columns, k_compact.cu); the bytes of the passes
+    over the input keep the stored width p."""
     p, r = w["p"], w["r"]
+    pe = int(p_eff or p)
     esize = 4 if w["dtype"] == "f32" else 8
     sizes = piece_sizes(w, plan)
-    form0 = [m for m in sizes if p < m]
-    form1 = [m for m in sizes if p >= m]
+    form0 = [m for m in sizes if pe < m]
+    form1 = [m for m in sizes if pe >= m]
     if kernel in ("gram_piece_kernel", "gram_tile_async_kernel", "gram_dmma_kernel"):
-        return {"bound": "tensor", "flops": float(sum(m * p * (p + 1) for m in form0)),
-                "model": "SYRK m*p*(p+1) per form-0 piece (p x p Gram of the centred rows)"}
+        return {"bound": "tensor", "flops": float(sum(m * pe * (pe + 1) for m in form0)),
+                "model": "SYRK m*p*(p+1) per form-0 piece (p x p Gram of the centred rows; "
+                         f"p = {pe} active columns)"}
     if kernel in ("gram_rows_async_kernel", "gram_kernel"):
-        return {"bound": "tensor", "flops": float(sum(m * (m + 1) * p for m in form1)),
-                "model": "SYRK m*(m+1)*p per form-1 piece (m x m Gram of the centred rows)"}
+        return {"bound": "tensor", "flops": float(sum(m * (m + 1) * pe for m in form1)),
+                "model": f"SYRK m*(m+1)*p per form-1 piece (m x m Gram; p = {pe} active columns)"}
     if kernel == "bgemm_dmma_kernel" and executed > 0:
         return {"bound": "tensor", "flops": float(executed),
                 "model": "executed block-Krylov products, 2*M*N*K per task of a piece not yet "
@@ -287,37 +285,40 @@ def kernel_work(w: dict, n: int, plan, kernel: str, krylov_dims=None, executed=0
     if kernel == "lanczos_smem_kernel" and krylov_dims is not None:
         fl = 0.0
         for m, steps in zip(sizes, krylov_dims):
-            k = min(m, p)
+            k = min(m, pe)
             if steps > 0:
                 j = np.arange(int(steps))
                 fl += float(np.sum(2.0 * k * k + 4.0 * k * (j + 1) + 6.0 * k))
-        krylov_model = ("sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
-                        "+ 6k (three-term part)")
-        if fused_points(w):
-            tot = sum(sizes)
-            by = tot * p * esize + tot * r * 8 + sum(min(m, p) ** 2 * 8 for m in sizes)
-            return {"bound": "hbm", "bytes": float(by), "flops": fl,
-                    "limiter": "latency (dependent Krylov steps, per-step barriers)",
-                    "model": "rows*p*sizeof(in) (points epilogue streams every piece's rows) + "
-                             "rows*r*8 (points) + k^2*8 per piece (Gram read); Krylov phase: "
-                             + krylov_model}
-        return {"bound": "tensor", "flops": fl, "model": krylov_model}
+        return {"bound": "tensor", "flops": fl,
+                "limiter": "latency (dependent Krylov steps, per-step barriers; fp64 FMA work "
+                           "is a few % of the pipe)",
+                "model": "sum over Krylov steps of 2k^2 (matvec) + 4k(j+1) (one CGS pass) "
+                         "+ 6k (three-term part)"}
     if kernel in ("gower_affine_kernel", "gower_bulk_kernel"):
-        return {"bound": "hbm", "bytes": float(n * p * esize + n * r * 8),
-                "model": "n*p*sizeof(in) + n*r*8 (one read of every row, one write)"}
+        return {"bound": "hbm", "bytes": float(n * pe * esize + n * r * 8),
+                "model": f"n*p*sizeof(in) + n*r*8 (one read of every row, one write; p = {pe})"}
     if kernel == "subtract_mean_kernel":
         return {"bound": "hbm", "bytes": float(2 * n * r * 8),
                 "model": "read + write of the n x r output"}
+    if kernel == "piece_out_kernel":
+        c = w.get("c") or 0
+        own = sum(sizes) - (c * (len(sizes) - 1) if w["algo"] == "divide" else 0)
+        return {"bound": "hbm", "bytes": float(own * (pe * esize + 2 * 8) + n * r * 8),
+                "model": "every output row's input row gathered once (p*sizeof(in)) + its "
+                         "two int64 indices + the n x r write"}
     if kernel in ("points_kernel", "points_piece_kernel"):
-        if fused_points(w):
-            return None          # only the pieces the Lanczos epilogue left pending
         tot = sum(sizes)
-        return {"bound": "hbm", "bytes": float(tot * p * esize + tot * r * 8),
+        if w["algo"] in ("divide", "fast") and pe <= 104:
+            return None          # alignment sets / anchor only: not the per-row pass
+        return {"bound": "hbm", "bytes": float(tot * pe * esize + tot * r * 8),
                 "model": "rows*p*sizeof(in) + rows*r*8"}
     if kernel == "dc_stitch_kernel":
         tot = sum(sizes)
         return {"bound": "hbm", "bytes": float(tot * r * 8 + n * r * 8 + n * 8),
                 "model": "read piece points + write n x r + read row indices"}
+    if kernel == "nonzero_cols_kernel":
+        return {"bound": "hbm", "bytes": float(n * p * esize),
+                "model": "one read of the input (active-column flags)"}
     return None
 
 
@@ -579,6 +580,8 @@ def run_ours(args, w):
     except AttributeError:
         krylov = None
 
+    # column compaction of wide inputs (k_compact.cu): the width the kernels ran at
+    p_eff = getattr(getattr(run, "compact", None), "active", None)
     roof, per_kernel = None, {}
     total_k = sum(v[0] for v in kernels.values()) or 1.0
     dom = max(kernels, key=lambda k: kernels[k][0]) if kernels else None
@@ -586,7 +589,7 @@ def run_ours(args, w):
     for kname in ranked:
         ms_k, cnt, executed = kernels[kname]
         wk = kernel_work(w, n if not sharded else x.shape[0], plan, kname, krylov,
-                         executed / tsteps) if not sharded else None
+                         executed / tsteps, p_eff=p_eff) if not sharded else None
         if not wk:
             continue
         t = ms_k / tsteps / 1e3                     # seconds per step of this kernel
@@ -722,11 +725,17 @@ def run_ours(args, w):
             cpu["reference_defaults"] = {"value": rate_d, "unit": UNIT, "sample": desc_d}
 
     if rank == 0:
+        config = workload_config(args.workload, w, ws, n, scaling)
+        if p_eff is not None:
+            config["active_columns"] = int(p_eff)
+            config["column_compaction"] = ("all-zero columns dropped inside every step "
+                                           "(k_compact.cu: one detection pass + one gather)"
+                                           if p_eff < 0.9 * w["p"] else "none (too few zero columns)")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.workload, w, ws, n, scaling),
+            "config": config,
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "parity": parity, "clocks": clk.summary(), "gpu_launches": launches,
             "planner_ms": planner_ms,

@@ -95,6 +95,20 @@ int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap);
 int mdsx_h2d(mdsx_handle* h, void* dst, const void* src, int64_t bytes, int32_t threads,
              void* stream);
 
+/* ---- column compaction of wide inputs ---------------------------------------
+ * Columns that are zero in every row contribute exactly zero to every Gram,
+ * eigenvector, mean, point and Gower term, so the algorithms may run on the
+ * matrix of the active columns (same configuration).  mdsx_active_columns:
+ * one pass over the n x p matrix (device), the indices of the columns with a
+ * nonzero (or non-finite) entry in ascending order written to the HOST array
+ * cols (p entries), their number to *count; synchronous.
+ * mdsx_gather_columns: out (n x ldo, device, same dtype) = the columns
+ * cols[0..pa) (device array) of data, zero columns pa..ldo-1. */
+int mdsx_active_columns(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                        int32_t p, int32_t* cols, int32_t* count, void* stream);
+int mdsx_gather_columns(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                        const int32_t* cols, int32_t pa, int64_t ldo, void* out, void* stream);
+
 /* ---- dense primitives (function-level seams) ---------------------------- */
 /* out (m x m, ldo) = squared distances between rows of x (m x p, ld);
  * symmetrised, clamped at 0, exact-zero diagonal. */

@@ -79,6 +79,49 @@ def from_host(arr: np.ndarray, dev: torch.device) -> torch.Tensor:
     return out
 
 
+COMPACT_MIN_P = 105          # the block-Krylov shapes (k > 104); narrower inputs skip the pass
+COMPACT_MAX_ACTIVE = 0.9     # compact when at most this fraction of the columns is active
+
+
+class ColumnCompactor:
+    """Column compaction of a wide device matrix (k_compact.cu): at every call
+    one pass finds the columns with a nonzero entry (the data may change
+    between launches), and when at most 90% are active they are gathered into
+    a persistent dense buffer whose rows stay 16-byte multiples; the
+    algorithms then run on it and return the same configuration (zero columns
+    contribute exactly zero to every Gram, eigenvector, mean, point and Gower
+    term).  Narrow inputs are returned as they are."""
+
+    def __init__(self, x: torch.Tensor):
+        self.x = x
+        self.buf = None
+        self.active = None           # number of active columns of the last call
+
+    def __call__(self) -> torch.Tensor:
+        import ctypes as C
+        x = self.x
+        n, p = x.shape
+        if p < COMPACT_MIN_P:
+            return x
+        dev = x.device
+        h = handle(dev)
+        cols = np.empty(p, dtype=np.int32)
+        cnt = C.c_int32(0)
+        h.call("mdsx_active_columns", x.data_ptr(), dtype_code(x), x.stride(0), n, p,
+               cols.ctypes.data, C.byref(cnt), stream_ptr(dev))
+        pa = self.active = int(cnt.value)
+        if pa == 0 or pa > COMPACT_MAX_ACTIVE * p:
+            return x
+        vw = 16 // x.element_size()
+        ldo = -(-pa // vw) * vw
+        if self.buf is None or tuple(self.buf.shape) != (n, ldo):
+            self.buf = torch.empty((n, ldo), dtype=x.dtype, device=dev)
+        cols_dev = torch.from_numpy(cols[:pa].copy()).to(dev)
+        h.call("mdsx_gather_columns", x.data_ptr(), dtype_code(x), x.stride(0), n,
+               cols_dev.data_ptr(), pa, ldo, self.buf.data_ptr(), stream_ptr(dev))
+        return self.buf
+
+
 def index_tensor(idx: np.ndarray, dev: torch.device) -> torch.Tensor:
     """Upload an int64 index array.  Large arrays go through page-locked
     staging and an async copy (stream-ordered; torch's caching host allocator

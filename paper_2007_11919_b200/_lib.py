@@ -78,6 +78,8 @@ SIGNATURES = {
     "mdsx_aligned_correlations": (_int, [_vp, _vp, _i64, _i32, _vp, _i32, _i64, _vp, _vp, _vp,
                                          _vp]),
     "mdsx_h2d": (_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "mdsx_active_columns": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, C.POINTER(_i32), _vp]),
+    "mdsx_gather_columns": (_int, [_vp, _vp, _int, _i64, _i64, _vp, _i32, _i64, _vp, _vp]),
     "mdsx_plan_choices": (_int, [_vp, _i32, _i32, _vp, _vp, C.POINTER(_i32), C.POINTER(C.c_uint32)]),
     "mdsx_plan_permute": (_int, [_vp, _i64, _vp, C.POINTER(_i32), C.POINTER(C.c_uint32)]),
     "mdsx_idx_probe": (_int, [C.c_char_p, _i32, C.POINTER(_i64), C.POINTER(_i32),

@@ -55,6 +55,7 @@ class DivideRun:
     def __init__(self, x: torch.Tensor, plan: DcPlan, r: int, c: int):
         self.x, self.plan, self.r, self.c = x, plan, r, c
         self.dev = x.device
+        self.compact = D.ColumnCompactor(x)
         rows, off = flatten_subsets_cached(plan)
         self.row_idx = _cached_upload(plan, self.dev, "rows", lambda: D.index_tensor(rows, self.dev))
         self.piece_off = off
@@ -65,7 +66,7 @@ class DivideRun:
         self.status = D.status_tensor(npc, self.dev)
 
     def launch(self) -> None:
-        x = self.x
+        x = self.compact()
         D.handle(self.dev).call(
             "mdsx_divide_conquer", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
             x.shape[1], self.row_idx.data_ptr(), self.piece_off.ctypes.data, self.plan.p, self.c,
@@ -112,6 +113,7 @@ class InterpolationRun:
     def __init__(self, x: torch.Tensor, sample: np.ndarray, r: int):
         self.x, self.r = x, r
         self.dev = x.device
+        self.compact = D.ColumnCompactor(x)
         self.sample = D.index_tensor(sample, self.dev)
         self.l = len(sample)
         self.out = D.empty((x.shape[0], r), self.dev)
@@ -122,7 +124,7 @@ class InterpolationRun:
         self.flags = torch.zeros(2, dtype=torch.int32, device=self.dev)
 
     def launch(self) -> None:
-        x = self.x
+        x = self.compact()
         D.handle(self.dev).call(
             "mdsx_interpolation", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[0],
             x.shape[1], self.sample.data_ptr(), self.l, self.r, self.out.data_ptr(),
@@ -173,6 +175,7 @@ class FastRun:
         rank's rows stay in `pts[:len(flat.order)]` (distributed.py)."""
         self.x, self.plan, self.r, self.local = x, plan, r, local
         self.dev = dev = x.device
+        self.compact = D.ColumnCompactor(x)
         own_flat = flat is None
         flat = self.flat = flat if flat is not None else flatten_fast_cached(plan)
         # the caller's flat may carry its own upload cache (distributed.fast_shard)
@@ -250,7 +253,7 @@ class FastRun:
         self._route_ref = C.byref(self.route)
 
     def launch(self) -> None:
-        x, r, dev = self.x, self.r, self.dev
+        x, r, dev = self.compact(), self.r, self.dev
         h, sp = D.handle(dev), D.stream_ptr(dev)
         if self.route is not None:
             h.call("mdsx_fast_mds", x.data_ptr(), D.dtype_code(x), x.shape[1], x.shape[1],

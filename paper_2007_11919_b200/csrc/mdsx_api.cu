@@ -148,7 +148,7 @@ cudaEvent_t pooled_event(mdsx_handle* h) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Grow the workspace to hold `bytes` for this call (device sync on growth).
-static int ws_reserve(mdsx_handle* h, size_t bytes) {
+int ws_reserve(mdsx_handle* h, size_t bytes) {
   h->ws_top = 0;
   if (bytes <= h->ws_size) return MDSX_OK;
   cudaError_t e = cudaDeviceSynchronize();

@@ -85,6 +85,8 @@ void ws_reset(mdsx_handle* h);
 // Reserve `bytes` (256-aligned) of device workspace; grows (after a device
 // sync) when needed.  Returns nullptr and sets h->err on failure.
 void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t st);
+// (re)sizes the per-handle workspace for the current call (bump pointer reset)
+int ws_reserve(mdsx_handle* h, size_t bytes);
 // Upload a small host array via the pinned staging buffer (async on st).
 int upload(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
