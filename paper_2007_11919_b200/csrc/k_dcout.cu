@@ -187,7 +187,7 @@ constexpr int PO_THREADS = 128;   // compute warps
 constexpr int PO_CTA = PO_THREADS + 32;
 constexpr int PO_KC = 32;         // rows per stage (one per producer lane, 4 tiles of 8)
 constexpr int PO_NS = 4;          // stages
-constexpr int PO_ROWS = 256;      // rows per CTA
+constexpr int PO_ROWS = 1024;     // rows per CTA
 constexpr int PO_HDR = 2048;      // mbarriers + piece mean
 
 template <typename T, int K4, int NT>
@@ -268,33 +268,35 @@ piece_out_kernel(const T* __restrict__ X, int64_t ld, int p, int P, const int64_
   for (int c = 0; c < nch; ++c) {
     const int s = c % PO_NS;
     const int b0 = c * PO_KC, nr = min(PO_KC, nrows - b0);
-    bulk::wait(&full[s], (unsigned)((c / PO_NS) & 1));
     const int tr = 8 * warp;                       // this warp's tile: stage rows tr .. tr+7
-    double acc[NT][2][2];
+    const int row = b0 + tr + gid;
+    // output row index loaded before the wait: its latency hides under the DMMAs
+    const int64_t orow = tr + gid < nr ? oidx[row] : 0;
+    bulk::wait(&full[s], (unsigned)((c / PO_NS) & 1));
+    double acc[NT][4][2];                          // K range split over four accumulator sets
 #pragma unroll
     for (int n = 0; n < NT; ++n)
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) acc[n][hh][0] = acc[n][hh][1] = 0.0;
+      for (int hh = 0; hh < 4; ++hh) acc[n][hh][0] = acc[n][hh][1] = 0.0;
     if (tr < nr) {
       const T* x0 = stage + (size_t)s * stage_elems + (size_t)(tr + gid) * P + tig;
 #pragma unroll
       for (int k4 = 0; k4 < K4; ++k4) {
         const double xa = (double)x0[4 * k4] - smu[4 * k4 + tig];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) dmma(acc[n][k4 & 1][0], acc[n][k4 & 1][1], xa, bf[k4][n]);
+        for (int n = 0; n < NT; ++n) dmma(acc[n][k4 & 3][0], acc[n][k4 & 3][1], xa, bf[k4][n]);
       }
     }
     __syncwarp();
     if (lane == 0) bulk::arrive(&empty[s]);
     // lane (gid, tig) holds out[row gid of the tile][8n + 2tig + v]
-    const int row = b0 + tr + gid;
     if (tr + gid < nr) {
-      double* o = out + oidx[row] * r;
+      double* o = out + orow * r;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int q = 8 * n + 2 * tig;
-        const double v0 = acc[n][0][0] + acc[n][1][0] + add[n][0];
-        const double v1 = acc[n][0][1] + acc[n][1][1] + add[n][1];
+        const double v0 = (acc[n][0][0] + acc[n][1][0]) + (acc[n][2][0] + acc[n][3][0]) + add[n][0];
+        const double v1 = (acc[n][0][1] + acc[n][1][1]) + (acc[n][2][1] + acc[n][3][1]) + add[n][1];
         if (q + 1 < r && !(r & 1)) {             // 16-byte aligned pair (row stride r doubles, r even)
           *reinterpret_cast<double2*>(o + q) = make_double2(v0, v1);
         } else if (q + 1 < r) {
