@@ -86,6 +86,10 @@ int mdsx_version(void);
  * (cap bytes, NUL-terminated) it also copies the report and resets it. */
 int mdsx_timing_enable(mdsx_handle* h, int on);
 int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap);
+/* The launches timed since the last report, one line each: "kernel start_ms
+ * end_ms" relative to the first launch's start event (a timeline of the piece
+ * pipeline's two streams); does not consume them.  Returns the text length. */
+int64_t mdsx_timing_trace(mdsx_handle* h, char* buf, int64_t cap);
 
 /* Copy `bytes` from a PAGEABLE host array (e.g. the numpy array the reference
  * API receives, linalg.py:28-38) to device memory, staged through page-locked

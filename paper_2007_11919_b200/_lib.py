@@ -46,6 +46,7 @@ SIGNATURES = {
     "mdsx_launch_count": (_i64, [_vp]),
     "mdsx_timing_enable": (_int, [_vp, _int]),
     "mdsx_timing_report": (_i64, [_vp, C.c_char_p, _i64]),
+    "mdsx_timing_trace": (_i64, [_vp, C.c_char_p, _i64]),
     "mdsx_sqdist_self": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _vp]),
     "mdsx_sqdist_cross": (_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _int, _i32, _vp, _i64, _vp]),
     "mdsx_double_center": (_int, [_vp, _vp, _i64, _vp, _vp]),
@@ -151,6 +152,18 @@ class Handle:
         for line in buf.value.decode().splitlines():
             name, ms, cnt, work = line.split()
             out[name] = (float(ms), int(cnt), float(work)) if with_work else (float(ms), int(cnt))
+        return out
+
+    def timing_trace(self) -> list:
+        """[(kernel, start_ms, end_ms)] of the launches timed since the last
+        report, relative to the first (mdsx_timing_trace)."""
+        n = int(self.lib.mdsx_timing_trace(self.ptr, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        self.lib.mdsx_timing_trace(self.ptr, buf, n + 1)
+        out = []
+        for line in buf.value.decode().splitlines():
+            name, a, b = line.split()
+            out.append((name, float(a), float(b)))
         return out
 
     def call(self, name: str, *args) -> None:

@@ -417,6 +417,14 @@ int launch_piece_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, in
 int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, int r,
                       const double* shift, cudaStream_t st);
 
+// Column mean of the D&C output from the per-piece contributions (fixed order).
+int launch_dc_mean(mdsx_handle* h, const double* contrib, int npieces, int r, int64_t n,
+                   double* mean, cudaStream_t st) {
+  mdsx::pre(h, st);
+  dc_mean2_kernel<<<1, 256, 0, st>>>(contrib, npieces, r, 1.0 / (double)n, mean);
+  return launched(h, "dc_mean_kernel", st);
+}
+
 // Final re-centring of the D&C output: mean from the per-piece contributions
 // (fixed order), one shift pass over the n x r output.
 int launch_dc_recentre(mdsx_handle* h, const double* contrib, int npieces, int r, int64_t n,

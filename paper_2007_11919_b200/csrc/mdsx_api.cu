@@ -102,6 +102,8 @@ int launch_piece_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, in
                      const int64_t* row_idx, const int64_t* out_idx, const PieceDesc* pd,
                      int npieces, int64_t max_m, int r, int c0, const double* mu, const double* Uc,
                      const double* tvec, const double* mean, double* out, cudaStream_t st);
+int launch_dc_mean(mdsx_handle* h, const double* contrib, int npieces, int r, int64_t n,
+                   double* mean, cudaStream_t st);
 int launch_dc_recentre(mdsx_handle* h, const double* contrib, int npieces, int r, int64_t n,
                        double* mean, double* out, cudaStream_t st);
 int launch_trk_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
@@ -571,6 +573,30 @@ int mdsx_timing_enable(mdsx_handle* h, int on) {
   return MDSX_OK;
 }
 
+int64_t mdsx_timing_trace(mdsx_handle* h, char* buf, int64_t cap) {
+  if (!h) return -1;
+  std::lock_guard<std::recursive_mutex> lk(h->mu);
+  std::string out;
+  if (!h->timed.empty()) {
+    cudaEvent_t base = h->timed.front().second.first;
+    for (auto& t : h->timed) {
+      cudaEventSynchronize(t.second.second);
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, base, t.second.first);
+      cudaEventElapsedTime(&b, base, t.second.second);
+      char line[160];
+      snprintf(line, sizeof line, "%s %.4f %.4f\n", t.first, a, b);
+      out += line;
+    }
+  }
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(out.size(), (size_t)cap - 1);
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
+}
+
 int64_t mdsx_timing_report(mdsx_handle* h, char* buf, int64_t cap) {
   if (!h) return -1;
   std::lock_guard<std::recursive_mutex> lk(h->mu);
@@ -913,37 +939,32 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
     // per chunk of pieces, on the stream that solved it: anchor signs (chunk 0),
     // connecting points, fits, U' = U T, output rows (not yet re-centred)
     ClassicalOut co;
+    // the anchor's signs and Procrustes targets right after its chunk's
+    // eigenpairs (next to the other chunks' eigensolvers); the rest of the tail
+    // once for every piece after the join: connecting points, fits, U' = U T,
+    // then the column mean from the per-piece contributions, so the single
+    // output pass writes the re-centred rows (no shift pass)
     co.after_chunk = [&](int j0, int j1, cudaStream_t s) -> int {
-      int e;
-      if (j0 == 0) {
-        if ((e = launch_dc_points(h, data, dtype, ld, p, row_idx, co.dpd, 1, r, c, m0, co.mu, co.U,
-                                  Pc, Pa, s)))
-          return e;
-        cudaEventRecord(h->ev_anchor, s);
-      } else {
-        cudaStreamWaitEvent(s, h->ev_anchor, 0);
-      }
-      const int a0 = std::max(j0, 1);
-      if (j1 > a0) {
-        if ((e = launch_dc_conn(h, data, dtype, ld, p, row_idx, co.dpd, a0, j1 - a0, r, c, co.mu,
-                                co.U, Pc, s)))
-          return e;
-        if ((e = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff + (a0 - 1), j1 - a0, r,
-                                       rot + (size_t)(a0 - 1) * r * r, trans + (size_t)(a0 - 1) * r,
-                                       loss + (a0 - 1), degen + (a0 - 1), s)))
-          return e;
-      }
-      if ((e = launch_dc_compose(h, co.dpd, j0, j1 - j0, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
-                                 contrib, s)))
-        return e;
-      return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd + j0, j1 - j0, cp.max_m,
-                              r, c, co.mu, Uc + (size_t)j0 * p * r, tvec + (size_t)j0 * r, zero, out, s);
+      (void)j1;
+      if (j0 != 0) return MDSX_OK;
+      return launch_dc_points(h, data, dtype, ld, p, row_idx, co.dpd, 1, r, c, m0, co.mu, co.U, Pc,
+                              Pa, s);
     };
     if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, nullptr, estimates, gof, status,
                             st, &co)))
       return rc;
-    if (!rec) return MDSX_OK;
-    return launch_dc_recentre(h, contrib, npieces, r, n, mean, out, st);
+    if ((rc = launch_dc_conn(h, data, dtype, ld, p, row_idx, co.dpd, 1, npieces - 1, r, c, co.mu,
+                             co.U, Pc, st)))
+      return rc;
+    if ((rc = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff, npieces - 1, r, rot, trans, loss,
+                                    degen, st)))
+      return rc;
+    if ((rc = launch_dc_compose(h, co.dpd, 0, npieces, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
+                                contrib, st)))
+      return rc;
+    if (rec && (rc = launch_dc_mean(h, contrib, npieces, r, n, mean, st))) return rc;
+    return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd, npieces, cp.max_m, r, c,
+                            co.mu, Uc, tvec, rec ? mean : zero, out, st);
   }
   const size_t need = classical_ws_bytes(cp, p, r) + align_up(cp.total * r * sizeof(double)) +
                       align_up(fit_rows * sizeof(int64_t)) * 2 +
