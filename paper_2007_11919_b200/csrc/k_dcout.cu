@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(128)
 dc_compose_kernel(const PieceDesc* __restrict__ pd, int pbase, int p, int r, int c,
                   const double* __restrict__ Uall, const double* __restrict__ rot,
                   const double* __restrict__ trans, const double* __restrict__ src,
-                  double* __restrict__ Uc, double* __restrict__ tvec, double* __restrict__ contrib) {
+                  double* __restrict__ Uc, double* __restrict__ tvec, double* __restrict__ contrib,
+                  const int32_t* __restrict__ pending) {
   const int j = pbase + blockIdx.x;
+  if (pending != nullptr && j > 0 && pending[j] == 0) return;   // composed by dc_fit_kernel
   const PieceDesc d = pd[j];
   const double* U = Uall + d.u_off;
   double* O = Uc + (int64_t)j * p * r;
@@ -374,10 +376,12 @@ int launch_dc_conn(mdsx_handle* h, const void* data, int dtype, int64_t ld, int 
 
 int launch_dc_compose(mdsx_handle* h, const PieceDesc* pd, int pbase, int count, int p, int r, int c,
                       const double* U, const double* rot, const double* trans, const double* Pc,
-                      double* Uc, double* tvec, double* contrib, cudaStream_t st) {
+                      double* Uc, double* tvec, double* contrib, cudaStream_t st,
+                      const int32_t* pending) {
   if (count <= 0) return MDSX_OK;
   mdsx::pre(h, st);
-  dc_compose_kernel<<<count, 128, 0, st>>>(pd, pbase, p, r, c, U, rot, trans, Pc, Uc, tvec, contrib);
+  dc_compose_kernel<<<count, 128, 0, st>>>(pd, pbase, p, r, c, U, rot, trans, Pc, Uc, tvec, contrib,
+                                           pending);
   return launched(h, "dc_compose_kernel", st);
 }
 

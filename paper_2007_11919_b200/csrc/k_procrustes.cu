@@ -217,33 +217,17 @@ constexpr int NS_WARPS = 4;
 constexpr int NS_KMAX = 64;
 constexpr int NS_ITMAX = 40;
 
+// The Newton-Schulz fit of one warp: xs / ys hold the K target / source rows
+// (R values each, overwritten by the centred rows); on success T (row-major,
+// global), t and the loss are written and true returned; false when the
+// iteration did not converge (the Jacobi kernel takes the fit).  On return Gs
+// holds T, mx / my the column means.
 template <int R>
-__global__ void __launch_bounds__(NS_WARPS * 32)
-procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
-                         const double* __restrict__ src, const int64_t* __restrict__ src_rows,
-                         const int64_t* __restrict__ job_off, int njobs,
-                         double* __restrict__ rot, double* __restrict__ trans,
-                         double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+__device__ bool ns_fit_warp(double* xs, double* ys, double* Xs, double* Gs, double* mx, double* my,
+                            double* tv, int K, int lane, double* __restrict__ T,
+                            double* __restrict__ trans_j, double* __restrict__ loss_j) {
   constexpr int RR = R * R;
   constexpr int Q = (RR + 31) / 32;                 // matrix entries per lane
-  constexpr int WS = 2 * NS_KMAX * R + 2 * RR + 3 * R;
-  extern __shared__ double nsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int job = blockIdx.x * NS_WARPS + warp;
-  if (job >= njobs) return;
-  double* xs = nsm + (size_t)warp * WS;
-  double* ys = xs + NS_KMAX * R;
-  double* Xs = ys + NS_KMAX * R;
-  double* Gs = Xs + RR;
-  double* mx = Gs + RR;
-  double* my = mx + R;
-  double* tv = my + R;
-  const int64_t o = job_off[job];
-  const int K = (int)(job_off[job + 1] - o);
-  if (K > NS_KMAX || K < 1) {
-    if (lane == 0) degenerate[job] = -1;
-    return;
-  }
   // lane entries e = lane + 32 q of an R x R matrix: row ea[q], column eb[q]
   int ea[Q], eb[Q];
   bool ev[Q];
@@ -253,11 +237,6 @@ procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restri
     ev[q] = e < RR;
     ea[q] = ev[q] ? e / R : 0;
     eb[q] = ev[q] ? e - ea[q] * R : 0;
-  }
-  for (int e = lane; e < K * R; e += 32) {
-    const int t = e / R, a = e - t * R;
-    xs[e] = tgt[tgt_rows[o + t] * R + a];
-    ys[e] = src[src_rows[o + t] * R + a];
   }
   __syncwarp();
   if (lane < R || (lane >= 16 && lane - 16 < R)) {
@@ -357,12 +336,8 @@ procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restri
     __syncwarp();
     if (last) { conv = true; break; }
   }
-  if (!conv) {
-    if (lane == 0) degenerate[job] = -1;            // the Jacobi kernel takes this fit
-    return;
-  }
+  if (!conv) return false;
   // T = Q^T (row-major), t = mx - my T, loss
-  double* T = rot + (size_t)job * RR;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     if (ev[q]) {
@@ -378,7 +353,7 @@ procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restri
     for (int a = 0; a < R; ++a) s2 = fma(my[a], Gs[a * R + lane], s2);
     const double t = mx[lane] - s2;
     tv[lane] = t;
-    trans[(size_t)job * R + lane] = t;
+    trans_j[lane] = t;
   }
   __syncwarp();
   // residuals of the centred rows: x_c - y_c T (the translation absorbs the means)
@@ -392,9 +367,146 @@ procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restri
     ls = fma(d, d, ls);
   }
   ls = mdsx::warp_sum(ls);
+  if (lane == 0) *loss_j = ls;
+  return true;
+}
+
+
+template <int R>
+__global__ void __launch_bounds__(NS_WARPS * 32)
+procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restrict__ tgt_rows,
+                         const double* __restrict__ src, const int64_t* __restrict__ src_rows,
+                         const int64_t* __restrict__ job_off, int njobs,
+                         double* __restrict__ rot, double* __restrict__ trans,
+                         double* __restrict__ loss, int32_t* __restrict__ degenerate) {
+  constexpr int RR = R * R;
+  constexpr int WS = 2 * NS_KMAX * R + 2 * RR + 3 * R;
+  extern __shared__ double nsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int job = blockIdx.x * NS_WARPS + warp;
+  if (job >= njobs) return;
+  double* xs = nsm + (size_t)warp * WS;
+  double* ys = xs + NS_KMAX * R;
+  double* Xs = ys + NS_KMAX * R;
+  double* Gs = Xs + RR;
+  double* mx = Gs + RR;
+  double* my = mx + R;
+  double* tv = my + R;
+  const int64_t o = job_off[job];
+  const int K = (int)(job_off[job + 1] - o);
+  if (K > NS_KMAX || K < 1) {
+    if (lane == 0) degenerate[job] = -1;
+    return;
+  }
+  for (int e = lane; e < K * R; e += 32) {
+    const int t = e / R, a = e - t * R;
+    xs[e] = tgt[tgt_rows[o + t] * R + a];
+    ys[e] = src[src_rows[o + t] * R + a];
+  }
+  const bool ok = ns_fit_warp<R>(xs, ys, Xs, Gs, mx, my, tv, K, lane, rot + (size_t)job * RR,
+                                 trans + (size_t)job * R, loss + job);
+  if (lane == 0) degenerate[job] = ok ? 0 : -1;   // -1: the Jacobi kernel takes this fit
+}
+
+// ---- D&C tail of one subset j >= 1 in one warp (k_dcout.cu route): the
+// points of its c connecting rows P = (x - mu_j) U_j (written to Pc for a
+// Jacobi redo), the Newton-Schulz fit onto the anchor's signed targets, and
+// when it converged the composition U'_j = U_j T_j, t_j and the subset's
+// contribution to the column sum, -(sum_i P_i) T_j + (m_j - c) t_j
+// (dc_compose_kernel's arithmetic); otherwise pending[j] = 1 and the Jacobi
+// fit + dc_compose_kernel (pending mode) finish it.
+template <int R, typename T>
+__global__ void __launch_bounds__(NS_WARPS * 32)
+dc_fit_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ row_idx,
+              const PieceDesc* __restrict__ pd, int npieces, int c,
+              const double* __restrict__ mu_all, const double* __restrict__ Uall,
+              double* __restrict__ Pc, double* __restrict__ rot, double* __restrict__ trans,
+              double* __restrict__ loss, int32_t* __restrict__ degenerate,
+              double* __restrict__ Uc, double* __restrict__ tvec, double* __restrict__ contrib,
+              int32_t* __restrict__ pending) {
+  constexpr int RR = R * R;
+  constexpr int WS = 2 * NS_KMAX * R + 2 * RR + 3 * R + R;
+  extern __shared__ double nsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = 1 + blockIdx.x * NS_WARPS + warp;
+  // layout: per-warp NS areas, then the c connecting rows (shared: the same rows
+  // for every subset), then per warp U_j (p x R) and mu_j (p)
+  double* xs = nsm + (size_t)warp * WS;
+  double* ys = xs + NS_KMAX * R;
+  double* Xs = ys + NS_KMAX * R;
+  double* Gs = Xs + RR;
+  double* mx = Gs + RR;
+  double* my = mx + R;
+  double* tv = my + R;
+  double* cs = tv + R;
+  double* rows = nsm + (size_t)NS_WARPS * WS;
+  double* Us = rows + (size_t)c * p + (size_t)warp * (p * R + p);
+  double* mus = Us + (size_t)p * R;
+  const bool act = j < npieces;
+  const PieceDesc d = pd[act ? j : 1];
+  {
+    // connecting rows: subset 1's first c row indices (every subset starts with them)
+    const PieceDesc d1 = pd[1];
+    for (int e = threadIdx.x; e < c * p; e += blockDim.x) {
+      const int t = e / p, a = e - t * p;
+      rows[e] = (double)X[row_idx[d1.row_off + t] * ld + a];
+    }
+  }
+  if (act) {
+    const double* U = Uall + d.u_off;
+    const double* mu = mu_all + (int64_t)d.id * p;
+    for (int e = lane; e < p * R; e += 32) Us[e] = U[e];
+    for (int e = lane; e < p; e += 32) mus[e] = mu[e];
+  }
+  __syncthreads();
+  if (!act) return;
+  const int K = c;
+  for (int e = lane; e < K * R; e += 32) xs[e] = Pc[e];   // the anchor's signed targets
+  // sources: points of the c connecting rows, lanes over (row, column) outputs
+  double* Pj = Pc + (int64_t)j * c * R;
+  for (int e = lane; e < K * R; e += 32) {
+    const int t = e / R, q = e - t * R;
+    const double* row = rows + (size_t)t * p;
+    double s0 = 0.0, s1 = 0.0;
+    int a = 0;
+    for (; a + 1 < p; a += 2) {
+      s0 = fma(row[a] - mus[a], Us[a * R + q], s0);
+      s1 = fma(row[a + 1] - mus[a + 1], Us[(a + 1) * R + q], s1);
+    }
+    if (a < p) s0 = fma(row[a] - mus[a], Us[a * R + q], s0);
+    const double v = s0 + s1;
+    ys[e] = v;
+    Pj[e] = v;
+  }
+  __syncwarp();
+  if (lane < R) {                                    // column sums of the raw source points
+    double s2 = 0.0;
+    for (int t = 0; t < K; ++t) s2 += ys[t * R + lane];
+    cs[lane] = s2;
+  }
+  const bool ok = ns_fit_warp<R>(xs, ys, Xs, Gs, mx, my, tv, K, lane, rot + (size_t)(j - 1) * RR,
+                                 trans + (size_t)(j - 1) * R, loss + (j - 1));
   if (lane == 0) {
-    loss[job] = ls;
-    degenerate[job] = 0;
+    degenerate[j - 1] = ok ? 0 : -1;
+    pending[j] = ok ? 0 : 1;
+  }
+  if (!ok) return;
+  __syncwarp();
+  double* O = Uc + (int64_t)j * p * R;
+  for (int e = lane; e < p * R; e += 32) {
+    const int a = e / R, q = e - a * R;
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < R; ++b) v = fma(Us[a * R + b], Gs[b * R + q], v);
+    O[e] = v;
+  }
+  if (lane < R) {
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < R; ++b) v = fma(cs[b], Gs[b * R + lane], v);
+    const double t = tv[lane];
+    tvec[(int64_t)j * R + lane] = t;
+    contrib[(int64_t)j * R + lane] = (double)(d.m - c) * t - v;
   }
 }
 
@@ -1162,13 +1274,65 @@ int launch_shift_rows(mdsx_handle* h, double* X, const int64_t* idx, int64_t n, 
 }
 
 
+// D&C tail of subsets 1 .. npieces-1 (dc_fit_kernel); r <= 16, c <= NS_KMAX.
+bool dc_fit_ok(int r, int c, int p) {
+  const size_t sm = ((size_t)NS_WARPS * (2 * NS_KMAX * r + 2 * r * r + 4 * r) + (size_t)c * p +
+                     (size_t)NS_WARPS * ((size_t)p * r + p)) * sizeof(double);
+  return r >= 1 && r <= 16 && c >= 1 && c <= NS_KMAX && sm <= 200 * 1024;
+}
+
+int launch_dc_fit(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int r, int c,
+                  const double* mu, const double* U, double* Pc, double* rot, double* trans,
+                  double* loss, int32_t* degen, double* Uc, double* tvec, double* contrib,
+                  int32_t* pending, cudaStream_t st) {
+  if (npieces <= 1) return MDSX_OK;
+  auto go = [&](auto rc_) -> int {
+    constexpr int R = decltype(rc_)::value;
+    const size_t sm = ((size_t)NS_WARPS * (2 * NS_KMAX * R + 2 * R * R + 4 * R) + (size_t)c * p +
+                       (size_t)NS_WARPS * ((size_t)p * R + p)) * sizeof(double);
+    const int blocks = (npieces - 1 + NS_WARPS - 1) / NS_WARPS;
+    mdsx::pre(h, st);
+    if (dtype == MDSX_F32) {
+      auto kern = dc_fit_kernel<R, float>;
+      if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<blocks, NS_WARPS * 32, sm, st>>>((const float*)data, ld, p, row_idx, pd, npieces, c, mu, U,
+                                              Pc, rot, trans, loss, degen, Uc, tvec, contrib, pending);
+    } else {
+      auto kern = dc_fit_kernel<R, double>;
+      if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<blocks, NS_WARPS * 32, sm, st>>>((const double*)data, ld, p, row_idx, pd, npieces, c, mu,
+                                               U, Pc, rot, trans, loss, degen, Uc, tvec, contrib, pending);
+    }
+    return launched(h, "dc_fit_kernel", st);
+  };
+  switch (r) {
+    case 1: return go(std::integral_constant<int, 1>{});
+    case 2: return go(std::integral_constant<int, 2>{});
+    case 3: return go(std::integral_constant<int, 3>{});
+    case 4: return go(std::integral_constant<int, 4>{});
+    case 5: return go(std::integral_constant<int, 5>{});
+    case 6: return go(std::integral_constant<int, 6>{});
+    case 7: return go(std::integral_constant<int, 7>{});
+    case 8: return go(std::integral_constant<int, 8>{});
+    case 9: return go(std::integral_constant<int, 9>{});
+    case 10: return go(std::integral_constant<int, 10>{});
+    case 11: return go(std::integral_constant<int, 11>{});
+    case 12: return go(std::integral_constant<int, 12>{});
+    case 13: return go(std::integral_constant<int, 13>{});
+    case 14: return go(std::integral_constant<int, 14>{});
+    case 15: return go(std::integral_constant<int, 15>{});
+    default: return go(std::integral_constant<int, 16>{});
+  }
+}
+
 int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
                           const double* src, const int64_t* src_rows, const int64_t* job_off_dev,
                           int njobs, int r, double* rot, double* trans, double* loss,
-                          int32_t* degenerate, cudaStream_t st) {
+                          int32_t* degenerate, cudaStream_t st, bool redo_only) {
   if (njobs == 0) return MDSX_OK;
   if (r <= 16 && !getenv("MDSX_FIT_WARP")) {
-    {                                            // Newton-Schulz fast path first
+    if (!redo_only) {                            // Newton-Schulz fast path first
       auto ns = [&](auto rc_) -> int {
         constexpr int R = decltype(rc_)::value;
         auto kern = procrustes_fit_ns_kernel<R>;

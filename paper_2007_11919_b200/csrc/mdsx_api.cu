@@ -13,7 +13,13 @@ namespace mdsx {
 int launch_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,
                           const double* src, const int64_t* src_rows, const int64_t* job_off_dev,
                           int njobs, int r, double* rot, double* trans, double* loss,
-                          int32_t* degenerate, cudaStream_t st);
+                          int32_t* degenerate, cudaStream_t st, bool redo_only = false);
+bool dc_fit_ok(int r, int c, int p);
+int launch_dc_fit(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
+                  const int64_t* row_idx, const PieceDesc* pd, int npieces, int r, int c,
+                  const double* mu, const double* U, double* Pc, double* rot, double* trans,
+                  double* loss, int32_t* degen, double* Uc, double* tvec, double* contrib,
+                  int32_t* pending, cudaStream_t st);
 int launch_apply(mdsx_handle* h, double* buf, int r, const int64_t* start, const int64_t* len,
                  int njobs, int64_t max_len, const double* rot, const double* trans,
                  cudaStream_t st);
@@ -97,7 +103,8 @@ int launch_dc_conn(mdsx_handle* h, const void* data, int dtype, int64_t ld, int 
                    const double* mu, const double* U, double* Pc, cudaStream_t st);
 int launch_dc_compose(mdsx_handle* h, const PieceDesc* pd, int pbase, int count, int p, int r, int c,
                       const double* U, const double* rot, const double* trans, const double* Pc,
-                      double* Uc, double* tvec, double* contrib, cudaStream_t st);
+                      double* Uc, double* tvec, double* contrib, cudaStream_t st,
+                      const int32_t* pending = nullptr);
 int launch_piece_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, int p,
                      const int64_t* row_idx, const int64_t* out_idx, const PieceDesc* pd,
                      int npieces, int64_t max_m, int r, int c0, const double* mu, const double* Uc,
@@ -898,7 +905,7 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                         align_up((size_t)(nj + 1) * sizeof(int64_t)) +
                         align_up((size_t)nj * r * r * sizeof(double)) +
                         align_up((size_t)nj * r * sizeof(double)) + align_up(nj * sizeof(double)) +
-                        align_up(nj * sizeof(int32_t)) + 8192;
+                        align_up(nj * sizeof(int32_t)) + align_up(npieces * sizeof(int32_t)) + 8192;
     if ((rc = ws_reserve(h, need))) return rc;
     double* Pc = (double*)ws_alloc(h, (size_t)npieces * c * r * sizeof(double), st);
     double* Uc = (double*)ws_alloc(h, (size_t)npieces * p * r * sizeof(double), st);
@@ -914,8 +921,9 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
     int64_t* joff = (int64_t*)ws_alloc(h, (size_t)(nj + 1) * sizeof(int64_t), st);
     double* loss = (double*)ws_alloc(h, nj * sizeof(double), st);
     int32_t* degen = (int32_t*)ws_alloc(h, nj * sizeof(int32_t), st);
+    int32_t* pending = (int32_t*)ws_alloc(h, (size_t)npieces * sizeof(int32_t), st);
     if (!Pc || !Uc || !contrib || !tvec || !Pa || !mean || !zero || !rot || !trans || !trows ||
-        !srows || !joff || !loss || !degen)
+        !srows || !joff || !loss || !degen || !pending)
       return MDSX_CUDA;
     std::vector<int64_t> ht(fit_rows), hs(fit_rows), hj(nj + 1);
     for (int j = 0; j < nj; ++j) {
@@ -953,15 +961,29 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
     if ((rc = run_classical(h, cp, data, dtype, ld, p, row_idx, r, nullptr, estimates, gof, status,
                             st, &co)))
       return rc;
-    if ((rc = launch_dc_conn(h, data, dtype, ld, p, row_idx, co.dpd, 1, npieces - 1, r, c, co.mu,
-                             co.U, Pc, st)))
-      return rc;
-    if ((rc = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff, npieces - 1, r, rot, trans, loss,
-                                    degen, st)))
-      return rc;
-    if ((rc = launch_dc_compose(h, co.dpd, 0, npieces, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
-                                contrib, st)))
-      return rc;
+    if (dc_fit_ok(r, c, p)) {
+      // one warp per subset: connecting points, Newton-Schulz fit, composition;
+      // fits it does not converge on: Jacobi fit + composition (pending mode)
+      if ((rc = launch_dc_fit(h, data, dtype, ld, p, row_idx, co.dpd, npieces, r, c, co.mu, co.U, Pc,
+                              rot, trans, loss, degen, Uc, tvec, contrib, pending, st)))
+        return rc;
+      if ((rc = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff, npieces - 1, r, rot, trans,
+                                      loss, degen, st, true)))
+        return rc;
+      if ((rc = launch_dc_compose(h, co.dpd, 0, npieces, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
+                                  contrib, st, pending)))
+        return rc;
+    } else {
+      if ((rc = launch_dc_conn(h, data, dtype, ld, p, row_idx, co.dpd, 1, npieces - 1, r, c, co.mu,
+                               co.U, Pc, st)))
+        return rc;
+      if ((rc = launch_procrustes_fit(h, Pc, trows, Pc, srows, joff, npieces - 1, r, rot, trans,
+                                      loss, degen, st)))
+        return rc;
+      if ((rc = launch_dc_compose(h, co.dpd, 0, npieces, p, r, c, co.U, rot, trans, Pc, Uc, tvec,
+                                  contrib, st)))
+        return rc;
+    }
     if (rec && (rc = launch_dc_mean(h, contrib, npieces, r, n, mean, st))) return rc;
     return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd, npieces, cp.max_m, r, c,
                             co.mu, Uc, tvec, rec ? mean : zero, out, st);
