@@ -453,34 +453,92 @@ int launch_dc_recentre(mdsx_handle* h, const double* contrib, int npieces, int r
 // rows of a leaf sum to zero, so mean = sum_leaves m_leaf t_tot / n.
 namespace {
 
-// points of tracked rows: warp per row (leaf id per row)
+// points of tracked rows (leaf id per row, rows grouped by leaf): a CTA takes
+// 16 consecutive tracked rows, stages them centred in shared memory (coalesced
+// row reads) together with U of the first and the last row's leaf (the window
+// spans one or two leaves unless leaves track fewer than 16 rows; rows of a
+// leaf in between read U from L1/L2), and a thread per (row, column) output
+// runs the p-long dot product
+constexpr int TK_ROWS = 16;
+
 template <typename T>
 __global__ void __launch_bounds__(128)
 trk_points_kernel(const T* __restrict__ X, int64_t ld, int p, const int64_t* __restrict__ trk_row,
                   const int32_t* __restrict__ trk_leaf, int64_t ntrk, const PieceDesc* __restrict__ pd,
                   int r, const double* __restrict__ mu_all, const double* __restrict__ Uall,
                   double* __restrict__ P) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (i >= ntrk) return;
-  const PieceDesc d = pd[trk_leaf[i]];
-  const double* U = Uall + d.u_off;
-  const double* mu = mu_all + (int64_t)d.id * p;
-  const T* row = X + trk_row[i] * ld;
-  double acc[RMX];
-#pragma unroll
-  for (int q = 0; q < RMX; ++q) acc[q] = 0.0;
-  for (int a = lane; a < p; a += 32) {
-    const double y = (double)row[a] - mu[a];
-#pragma unroll
-    for (int q = 0; q < RMX; ++q)
-      if (q < r) acc[q] = fma(y, U[a * r + q], acc[q]);
+  extern __shared__ double tk_sm[];
+  double* xs = tk_sm;                                   // TK_ROWS x (p + 1)
+  double* us = tk_sm + TK_ROWS * (p + 1);               // 2 x p x r
+  const int pp = p + 1;
+  const int64_t i0 = (int64_t)blockIdx.x * TK_ROWS;
+  const int nr = (int)min((int64_t)TK_ROWS, ntrk - i0);
+  const int l0 = trk_leaf[i0], l1 = trk_leaf[i0 + nr - 1];
+  const double* U0 = Uall + pd[l0].u_off;
+  const double* U1 = Uall + pd[l1].u_off;
+  __shared__ int64_t srow[TK_ROWS], smu[TK_ROWS];
+  __shared__ int sleaf[TK_ROWS];
+  if (threadIdx.x < nr) {                              // per-row metadata, loaded once
+    const int lf = trk_leaf[i0 + threadIdx.x];
+    sleaf[threadIdx.x] = lf;
+    srow[threadIdx.x] = trk_row[i0 + threadIdx.x] * ld;
+    smu[threadIdx.x] = (int64_t)pd[lf].id * p;
   }
+  // loads batched 8 per thread before their stores (one latency per batch,
+  // not per element)
+  for (int e0 = threadIdx.x; e0 < p * r; e0 += 8 * blockDim.x) {
+    double v0[8], v1[8];
 #pragma unroll
-  for (int q = 0; q < RMX; ++q) {
-    if (q >= r) break;
-    const double v = mdsx::warp_sum(acc[q]);
-    if (lane == 0) P[i * r + q] = v;
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v0[u] = e < p * r ? U0[e] : 0.0;
+      v1[u] = e < p * r ? U1[e] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < p * r) {
+        us[e] = v0[u];
+        us[p * r + e] = v1[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e0 = threadIdx.x; e0 < nr * p; e0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < nr * p) {
+        const int t = e / p, a = e - t * p;
+        v[u] = (double)X[srow[t] + a] - mu_all[smu[t] + a];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < nr * p) {
+        const int t = e / p, a = e - t * p;
+        xs[t * pp + a] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < nr * r; o += blockDim.x) {
+    const int t = o / r, q = o - t * r;
+    const int lf = sleaf[t];
+    const double* U = lf == l0 ? us : lf == l1 ? us + p * r : Uall + pd[lf].u_off;
+    const double* xr = xs + t * pp;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int a = 0;
+    for (; a + 3 < p; a += 4) {
+      s0 = fma(xr[a], U[a * r + q], s0);
+      s1 = fma(xr[a + 1], U[(a + 1) * r + q], s1);
+      s2 = fma(xr[a + 2], U[(a + 2) * r + q], s2);
+      s3 = fma(xr[a + 3], U[(a + 3) * r + q], s3);
+    }
+    for (; a < p; ++a) s0 = fma(xr[a], U[a * r + q], s0);
+    P[(i0 + t) * r + q] = (s0 + s1) + (s2 + s3);
   }
 }
 
@@ -563,13 +621,15 @@ int launch_trk_points(mdsx_handle* h, const void* data, int dtype, int64_t ld, i
                       const PieceDesc* pd, int r, const double* mu, const double* U, double* P,
                       cudaStream_t st) {
   if (ntrk == 0) return MDSX_OK;
-  const unsigned blocks = (unsigned)((ntrk * 32 + 127) / 128);
+  if (p > 128) return fail(h, MDSX_UNSUPPORTED, "tracked points: p > 128");
+  const unsigned blocks = (unsigned)((ntrk + TK_ROWS - 1) / TK_ROWS);
+  const size_t sm = ((size_t)TK_ROWS * (p + 1) + 2 * (size_t)p * r) * sizeof(double);
   mdsx::pre(h, st);
   if (dtype == MDSX_F32)
-    trk_points_kernel<float><<<blocks, 128, 0, st>>>((const float*)data, ld, p, trk_row, trk_leaf, ntrk,
+    trk_points_kernel<float><<<blocks, 128, sm, st>>>((const float*)data, ld, p, trk_row, trk_leaf, ntrk,
                                                      pd, r, mu, U, P);
   else
-    trk_points_kernel<double><<<blocks, 128, 0, st>>>((const double*)data, ld, p, trk_row, trk_leaf, ntrk,
+    trk_points_kernel<double><<<blocks, 128, sm, st>>>((const double*)data, ld, p, trk_row, trk_leaf, ntrk,
                                                       pd, r, mu, U, P);
   return launched(h, "rows_points_kernel", st);
 }
