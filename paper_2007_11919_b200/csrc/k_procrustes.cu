@@ -398,10 +398,33 @@ procrustes_fit_ns_kernel(const double* __restrict__ tgt, const int64_t* __restri
     if (lane == 0) degenerate[job] = -1;
     return;
   }
-  for (int e = lane; e < K * R; e += 32) {
-    const int t = e / R, a = e - t * R;
-    xs[e] = tgt[tgt_rows[o + t] * R + a];
-    ys[e] = src[src_rows[o + t] * R + a];
+  {
+    // row indices then values, loads batched (K <= NS_KMAX = 64 rows: two passes
+    // of 32 lanes), so a fit waits for two dependent latencies, not 2 K R / 32
+    int64_t tr0 = 0, sr0 = 0, tr1 = 0, sr1 = 0;
+    if (lane < K) { tr0 = tgt_rows[o + lane]; sr0 = src_rows[o + lane]; }
+    if (lane + 32 < K) { tr1 = tgt_rows[o + lane + 32]; sr1 = src_rows[o + lane + 32]; }
+    constexpr int EPL = (NS_KMAX * R + 31) / 32;      // elements per lane (upper bound)
+    double xv[EPL], yv[EPL];
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+      const int e = lane + 32 * u;
+      const int t = min(e, K * R - 1) / R, a = min(e, K * R - 1) - t * R;
+      const int64_t ta = __shfl_sync(0xffffffffu, tr0, t & 31), tb = __shfl_sync(0xffffffffu, tr1, t & 31);
+      const int64_t sa = __shfl_sync(0xffffffffu, sr0, t & 31), sb = __shfl_sync(0xffffffffu, sr1, t & 31);
+      if (e < K * R) {
+        xv[u] = tgt[(t < 32 ? ta : tb) * R + a];
+        yv[u] = src[(t < 32 ? sa : sb) * R + a];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+      const int e = lane + 32 * u;
+      if (e < K * R) {
+        xs[e] = xv[u];
+        ys[e] = yv[u];
+      }
+    }
   }
   const bool ok = ns_fit_warp<R>(xs, ys, Xs, Gs, mx, my, tv, K, lane, rot + (size_t)job * RR,
                                  trans + (size_t)job * R, loss + job);
