@@ -11,6 +11,7 @@
 // mirrored to the upper -> exactly symmetric; fixed reduction order.
 #include "mdsx_common.cuh"
 #include "bulk.cuh"
+#include "gram_ring.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -336,65 +337,11 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
 // row; the producer also accumulates the column sums s = sum (x - x0) of each
 // stage after the compute warps were handed it (C = sum y y^T - s s^T / m);
 // mu = x0 + s/m is published with the Gram.
-constexpr int GP_THREADS = 128;                 // compute warps
-constexpr int GP_CTA = GP_THREADS + 32;         // + producer warp
-constexpr int GP_KC = 32;                       // rows per stage (one per producer lane)
-constexpr int GP_HDR = 2048;                    // mbarriers, x0, column sums, flag
-
-__host__ __device__ constexpr int pair_i(int t) {
-  int i = 0;
-  while ((i + 1) * (i + 2) / 2 <= t) ++i;
-  return i;
-}
-__host__ __device__ constexpr int pair_j(int t) { return t - pair_i(t) * (pair_i(t) + 1) / 2; }
-
-template <int NB, int Q>
-struct GpQuarter {
-  static constexpr int NP = NB * (NB + 1) / 2;
-  static constexpr int QS = (NP + 3) / 4;               // pairs per warp (max)
-  static constexpr int LO = Q * QS;
-  static constexpr int CNT = (NP - LO) < QS ? (NP - LO) : QS;
-};
-
-template <typename T, int NB, int Q>
-__device__ __forceinline__ void gp_chunk(const T* __restrict__ stg, int P, int nk4, const double* x0r,
-                                         bool lastmask, int gid, int tig, double (*acc)[2]) {
-  using QQ = GpQuarter<NB, Q>;
-  const T* src = stg + (size_t)tig * P + gid;
-#pragma unroll 2
-  for (int k4 = 0; k4 < nk4; ++k4) {
-    double f[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) f[b] = (double)src[8 * b] - x0r[b];
-    if (lastmask) f[NB - 1] = 0.0;             // features >= P of the last block
-#pragma unroll
-    for (int u = 0; u < QQ::CNT; ++u) {
-      const int t = QQ::LO + u;
-      dmma(acc[u][0], acc[u][1], f[pair_i(t)], f[pair_j(t)]);
-    }
-    src += 4 * P;
-  }
-}
-
-template <typename T, int NB, int Q>
-__device__ __forceinline__ void gp_store(double (*acc)[2], const double* s, double inv_m, int k,
-                                         int gid, int tig, double* out) {
-  using QQ = GpQuarter<NB, Q>;
-#pragma unroll
-  for (int u = 0; u < QQ::CNT; ++u) {
-    const int t = QQ::LO + u;
-    const int bi = pair_i(t), bj = pair_j(t);
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int gi = 8 * bi + gid, gj = 8 * bj + 2 * tig + v;
-      if (gi < k && gj < k && gi >= gj) {
-        const double c = fma(-s[gi] * inv_m, s[gj], acc[u][v]);
-        out[(int64_t)gi * k + gj] = c;
-        out[(int64_t)gj * k + gi] = c;
-      }
-    }
-  }
-}
+using gring::GP_THREADS;
+using gring::GP_CTA;
+using gring::GP_KC;
+using gring::GP_HDR;
+using gring::gram_piece_body;
 
 template <typename T, int NB, int NS>
 __global__ void __launch_bounds__(GP_CTA, 2)
@@ -403,117 +350,8 @@ gram_piece_kernel(const T* __restrict__ X, int64_t ld, int p, int P,
                   double* __restrict__ A, double* __restrict__ mu_all,
                   mdsx_piece_status* __restrict__ status) {
   extern __shared__ __align__(128) unsigned char gp_smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(gp_smem);
-  uint64_t* empty = full + NS;
-  double* x0s = reinterpret_cast<double*>(gp_smem + 128);          // 8 NB <= 104
-  double* ssum = x0s + 104;
-  int* bad = reinterpret_cast<int*>(ssum + 104);
-  T* stage = reinterpret_cast<T*>(gp_smem + GP_HDR);                // NS x GP_KC x P
-  const PieceDesc d = pd[blockIdx.x];
-  const int k = d.k, m = d.m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int64_t* ridx = row_idx + d.row_off;
-  const size_t stage_elems = (size_t)GP_KC * P;
-  const int nchunks = (m + GP_KC - 1) / GP_KC;
-
-  // zero padding columns [p, P) of every stage row (never written by the copies)
-  for (int e = tid; P > p && e < NS * GP_KC * (P - p); e += GP_CTA) {
-    const int row = e / (P - p), c = p + e % (P - p);
-    stage[(size_t)row * P + c] = T(0);
-  }
-  if (tid < 8 * NB) x0s[tid] = tid < k ? (double)X[ridx[0] * ld + tid] : 0.0;
-  if (tid == 0) {
-    *bad = 0;
-    for (int s = 0; s < NS; ++s) {
-      bulk::bar_init(&full[s], 1);
-      bulk::bar_init(&empty[s], GP_THREADS / 32);
-    }
-    bulk::bar_fence();
-  }
-  __syncthreads();
-
-  if (warp == GP_THREADS / 32) {
-    // ---- producer: gather rows, then column sums of the stages handed over
-    const unsigned row_bytes = (unsigned)((size_t)p * sizeof(T));
-    double cs[4] = {0.0, 0.0, 0.0, 0.0};       // features lane + 32 q
-    double x0l[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) x0l[q] = lane + 32 * q < 8 * NB ? x0s[lane + 32 * q] : 0.0;
-    auto colsums = [&](int c) {
-      const int s = c % NS;
-      bulk::wait(&full[s], (unsigned)((c / NS) & 1));
-      const T* stg = stage + (size_t)s * stage_elems;
-      const int nr = min(GP_KC, m - c * GP_KC);
-      for (int i = 0; i < nr; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (lane + 32 * q < p) cs[q] += (double)stg[(size_t)i * P + lane + 32 * q] - x0l[q];
-    };
-    int64_t nidx = lane < m ? ridx[lane] : 0;
-    int64_t nidx2 = GP_KC + lane < m ? ridx[GP_KC + lane] : 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c % NS;
-      const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
-      const int64_t idx = nidx;
-      nidx = nidx2;
-      if (r0 + 2 * GP_KC + lane < m) nidx2 = ridx[r0 + 2 * GP_KC + lane];
-      if (c >= NS) bulk::wait(&empty[s], (unsigned)((c / NS - 1) & 1));
-      T* dst = stage + (size_t)s * stage_elems;
-      const int npad = ((nr + 3) & ~3) - nr;     // rows that complete the last k4 group
-      for (int e = lane; e < npad * p; e += 32)
-        dst[(size_t)(nr + e / p) * P + e % p] = (T)x0s[e % p];
-      __syncwarp();
-      if (lane == 0) bulk::arrive_expect(&full[s], (unsigned)nr * row_bytes);
-      __syncwarp();
-      if (lane < nr) bulk::copy(dst + (size_t)lane * P, X + idx * ld, row_bytes, &full[s]);
-      if (c >= NS - 1) colsums(c - (NS - 1));
-    }
-    for (int c = max(0, nchunks - (NS - 1)); c < nchunks; ++c) colsums(c);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int a = lane + 32 * q;
-      if (a < 8 * NB) ssum[a] = a < p ? cs[q] : 0.0;
-      if (a < k && !isfinite(cs[q])) *bad = 1;
-    }
-  } else {
-    // ---- compute warps
-    double x0r[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) x0r[b] = x0s[8 * b + gid];
-    const bool lastmask = 8 * (NB - 1) + gid >= P;    // the stage pitch may be < 8 NB
-    constexpr int QS = GpQuarter<NB, 0>::QS;
-    double acc[QS][2];
-#pragma unroll
-    for (int u = 0; u < QS; ++u) acc[u][0] = acc[u][1] = 0.0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c % NS;
-      bulk::wait(&full[s], (unsigned)((c / NS) & 1));
-      const T* stg = stage + (size_t)s * stage_elems;
-      const int nk4 = (min(GP_KC, m - c * GP_KC) + 3) / 4;
-      switch (warp) {
-        case 0: gp_chunk<T, NB, 0>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
-        case 1: gp_chunk<T, NB, 1>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
-        case 2: gp_chunk<T, NB, 2>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
-        default: gp_chunk<T, NB, 3>(stg, P, nk4, x0r, lastmask, gid, tig, acc); break;
-      }
-      __syncwarp();
-      if (lane == 0) bulk::arrive(&empty[s]);
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(GP_CTA));          // column sums ready
-    const double inv_m = 1.0 / (double)m;
-    double* out = A + d.a_off;
-    switch (warp) {
-      case 0: gp_store<T, NB, 0>(acc, ssum, inv_m, k, gid, tig, out); break;
-      case 1: gp_store<T, NB, 1>(acc, ssum, inv_m, k, gid, tig, out); break;
-      case 2: gp_store<T, NB, 2>(acc, ssum, inv_m, k, gid, tig, out); break;
-      default: gp_store<T, NB, 3>(acc, ssum, inv_m, k, gid, tig, out); break;
-    }
-    if (tid < k) mu_all[(int64_t)d.id * p + tid] = x0s[tid] + ssum[tid] * inv_m;
-    if (tid == 0 && *bad) status[d.id].code = MDSX_INVALID_INPUT;
-    return;
-  }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(GP_CTA));
+  gram_piece_body<T, NB, NS, GP_THREADS / 32>(X, ld, p, P, row_idx, pd, blockIdx.x, A, mu_all, status,
+                                              gp_smem);
 }
 
 // Combine the centred Grams of a piece's row ranges (parallel-variance

@@ -251,14 +251,15 @@ __device__ __noinline__ void lz_points(const PtsEpi& epi, const PieceDesc& d, in
   else go(std::integral_constant<int, 10>{});
 }
 
+// The Lanczos solve of piece `pidx` by the calling CTA (LT threads); `sm` is
+// the dynamic shared memory (lanczos_bytes).
 template <int QMAX>
-__global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
-lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
-                    double* __restrict__ Uout, double* __restrict__ lam_out,
-                    double* __restrict__ estimates, double* __restrict__ gof,
-                    mdsx_piece_status* __restrict__ status, int only_flagged, const PtsEpi epi,
-                    int getenv_first_check) {
-  extern __shared__ double sm[];
+__device__ __forceinline__ void lanczos_piece(const PieceDesc* __restrict__ pd, int pidx, int r,
+                                              const double* __restrict__ Aall,
+                                              double* __restrict__ Uout, double* __restrict__ lam_out,
+                                              double* __restrict__ estimates, double* __restrict__ gof,
+                                              mdsx_piece_status* __restrict__ status, int only_flagged,
+                                              const PtsEpi& epi, int getenv_first_check, double* sm) {
   __shared__ double alpha[QMAX], beta[QMAX], beta2[QMAX];
   __shared__ double wv[LMAX], hv[QMAX + 1];
   __shared__ double theta[RMAX], lo_s[RMAX], hi_s[RMAX], thp[RMAX], rhp[RMAX], res_s[RMAX];
@@ -269,7 +270,7 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   __shared__ double trace_s, anorm_s;
   __shared__ int conv_s;
 
-  const PieceDesc d = pd[blockIdx.x];
+  const PieceDesc d = pd[pidx];
   const int pid = d.id, k = d.k;
   const int kq = (8 * ((k + 7) >> 3)) | 1;    // odd leading dim of Q, >= the tiled width (zero rows past k)
   const int tid = threadIdx.x;
@@ -783,6 +784,19 @@ lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __res
   }
 }
 
+template <int QMAX>
+__global__ void __launch_bounds__(LT, QMAX <= QCAP_PIECES ? 2 : 1)
+lanczos_smem_kernel(const PieceDesc* __restrict__ pd, int r, const double* __restrict__ Aall,
+                    double* __restrict__ Uout, double* __restrict__ lam_out,
+                    double* __restrict__ estimates, double* __restrict__ gof,
+                    mdsx_piece_status* __restrict__ status, int only_flagged, const PtsEpi epi,
+                    int getenv_first_check) {
+  extern __shared__ double sm[];
+  lanczos_piece<QMAX>(pd, blockIdx.x, r, Aall, Uout, lam_out, estimates, gof, status, only_flagged,
+                      epi, getenv_first_check, sm);
+}
+
+
 
 // ---------------------------------------------------------------------------
 // Tridiagonal helpers of the convergence checks (declared at the top).
@@ -982,5 +996,6 @@ int launch_lanczos_smem(mdsx_handle* h, const PieceDesc* pd, int npieces, int km
   return full_basis ? go(lanczos_smem_kernel<LMAX>, LMAX)
                     : go(lanczos_smem_kernel<QCAP_PIECES>, QCAP_PIECES);
 }
+
 
 }  // namespace mdsx
