@@ -251,6 +251,24 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                            int32_t npieces, int32_t c, int32_t r, double* out,
                            double* estimates, double* gof, mdsx_piece_status* status,
                            int32_t flags, void* stream);
+/* One rank's share of a sharded divide_and_conquer_mds: the subsets of this
+ * call (piece 0 = the anchor, recomputed by every rank) are solved, fitted and
+ * composed as in mdsx_divide_conquer; their column-sum contributions
+ * (npieces x r) are copied to contrib_local and gather(ctx, stream) is called
+ * on the host thread: it must enqueue on `stream` the collective that fills
+ * contrib_global (npieces_total x r) with every subset's contribution in
+ * global subset order.  The mean over n_total rows then follows in the same
+ * fixed order on every rank (results independent of the number of ranks and
+ * equal to the unsharded call), and the output pass writes this call's rows
+ * re-centred.  MDSX_UNSUPPORTED unless the fused output route applies. */
+typedef int (*mdsx_gather_fn)(void* ctx, void* stream);
+int mdsx_divide_conquer_sharded(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                                int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                                int32_t npieces, int32_t c, int32_t r, double* out,
+                                double* estimates, double* gof, mdsx_piece_status* status,
+                                int64_t n_total, int32_t npieces_total, double* contrib_local,
+                                double* contrib_global, mdsx_gather_fn gather, void* ctx,
+                                void* stream);
 /* Column sums of points[idx[seg_off[j] .. seg_off[j+1])] per segment j
  * (sums: nseg x r, device; seg_off: device).  Fixed-order reductions, so a
  * sharded run that sums the same segments in the same order is independent

@@ -72,6 +72,9 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _vp]),
     "mdsx_divide_conquer_ex": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32, _i32,
                                       _vp, _vp, _vp, _vp, _i32, _vp]),
+    "mdsx_divide_conquer_sharded": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32,
+                                           _i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
+                                           _vp]),
     "mdsx_segment_colsums": (_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "mdsx_shift_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,
@@ -89,6 +92,9 @@ SIGNATURES = {
     "mdsx_csv_read": (_int, [C.c_char_p, _i32, _i32, _vp, C.POINTER(_i64), C.POINTER(_i64),
                              C.c_char_p, _i64]),
 }
+
+# host callback of mdsx_divide_conquer_sharded: int gather(void* ctx, void* stream)
+GATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
 
 _lib = None
 _lib_lock = threading.Lock()

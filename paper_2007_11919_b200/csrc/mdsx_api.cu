@@ -876,12 +876,50 @@ int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld,
                                 estimates, gof, status, 0, stream);
 }
 
+struct ShardOps {
+  double* contrib_local;       // npieces x r (device): this call's subset contributions
+  double* contrib_global;      // npieces_total x r (device): filled by gather()
+  int32_t npieces_total;
+  int64_t n_total;
+  mdsx_gather_fn gather;
+  void* ctx;
+};
+
+static int dc_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n, int32_t p,
+                   const int64_t* row_idx, const int64_t* piece_off, int32_t npieces, int32_t c,
+                   int32_t r, double* out, double* estimates, double* gof,
+                   mdsx_piece_status* status, int32_t flags, cudaStream_t st, const ShardOps* shard);
+
 int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
                            int32_t p, const int64_t* row_idx, const int64_t* piece_off,
                            int32_t npieces, int32_t c, int32_t r, double* out, double* estimates,
                            double* gof, mdsx_piece_status* status, int32_t flags, void* stream) {
   cudaStream_t st = as_stream(stream);
   MDSX_GUARD(h, st);
+  return dc_impl(h, data, dtype, ld, n, p, row_idx, piece_off, npieces, c, r, out, estimates, gof,
+                 status, flags, st, nullptr);
+}
+
+int mdsx_divide_conquer_sharded(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n,
+                                int32_t p, const int64_t* row_idx, const int64_t* piece_off,
+                                int32_t npieces, int32_t c, int32_t r, double* out,
+                                double* estimates, double* gof, mdsx_piece_status* status,
+                                int64_t n_total, int32_t npieces_total, double* contrib_local,
+                                double* contrib_global, mdsx_gather_fn gather, void* ctx,
+                                void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if (!contrib_local || !contrib_global || !gather || npieces_total < npieces || n_total < n)
+    return fail(h, MDSX_PARAM, "bad sharded D&C arguments");
+  const ShardOps ops{contrib_local, contrib_global, npieces_total, n_total, gather, ctx};
+  return dc_impl(h, data, dtype, ld, n, p, row_idx, piece_off, npieces, c, r, out, estimates, gof,
+                 status, 0, st, &ops);
+}
+
+static int dc_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n, int32_t p,
+                   const int64_t* row_idx, const int64_t* piece_off, int32_t npieces, int32_t c,
+                   int32_t r, double* out, double* estimates, double* gof,
+                   mdsx_piece_status* status, int32_t flags, cudaStream_t st, const ShardOps* shard) {
   ClassicalPlan cp;
   int rc = plan_classical(h, p, piece_off, npieces, r, cp);
   if (rc) return rc;
@@ -984,10 +1022,25 @@ int mdsx_divide_conquer_ex(mdsx_handle* h, const void* data, int dtype, int64_t 
                                   contrib, st)))
         return rc;
     }
+    if (shard && shard->gather) {
+      // sharded: every rank's contributions in global subset order (the
+      // caller's collective), then the same fixed-order mean on every rank
+      if ((rc = cuda_check(h, cudaMemcpyAsync(shard->contrib_local, contrib,
+                                              (size_t)npieces * r * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, st), "contrib copy")))
+        return rc;
+      if (shard->gather(shard->ctx, st) != 0) return fail(h, MDSX_CUDA, "contribution gather failed");
+      if ((rc = launch_dc_mean(h, shard->contrib_global, shard->npieces_total, r, shard->n_total, mean,
+                               st)))
+        return rc;
+      return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd, npieces, cp.max_m, r, c,
+                              co.mu, Uc, tvec, mean, out, st);
+    }
     if (rec && (rc = launch_dc_mean(h, contrib, npieces, r, n, mean, st))) return rc;
     return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd, npieces, cp.max_m, r, c,
                             co.mu, Uc, tvec, rec ? mean : zero, out, st);
   }
+  if (shard) return fail(h, MDSX_UNSUPPORTED, "sharded D&C needs the fused output route");
   const size_t need = classical_ws_bytes(cp, p, r) + align_up(cp.total * r * sizeof(double)) +
                       align_up(fit_rows * sizeof(int64_t)) * 2 +
                       align_up((size_t)(nj + 1) * sizeof(int64_t)) +

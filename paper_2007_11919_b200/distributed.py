@@ -258,8 +258,46 @@ class ShardedDivide:
         self.kmax = 1 + shard(plan.p - 1, comm.world, 0)[1]
         self.recs = None
 
+    def _gather_sorted(self, rows: torch.Tensor) -> torch.Tensor:
+        """This rank's per-subset rows (local subset order, the anchor's first)
+        -> every subset's row in global subset order, the anchor's from rank
+        0: one all-gather into a padded buffer and a cached selection (the
+        layout is fixed by the plan and the world size)."""
+        rows = rows[self.first:]
+        comm = self.comm
+        if comm.world == 1:
+            return rows
+        key = ("dc_sel", comm.world, rows.shape[1], str(rows.device))
+        cache = _shard_cached(self.plan, key, lambda: {})
+        if "sel" not in cache:
+            pos = []
+            for k in range(comm.world):
+                s = dc_shard(self.plan, comm.world, k)
+                ids = np.asarray(s.pieces[0 if k == 0 else 1:], dtype=np.int64)
+                pos.append(np.stack([ids, k * self.kmax + np.arange(len(ids))], axis=1))
+            pos = np.concatenate(pos)
+            cache["sel"] = torch.from_numpy(pos[np.argsort(pos[:, 0], kind="stable"), 1].copy()).to(
+                rows.device)
+            cache["buf"] = torch.zeros((self.kmax, rows.shape[1]), dtype=rows.dtype, device=rows.device)
+        buf = cache["buf"]
+        buf[:rows.shape[0]].copy_(rows)
+        return comm.all_gather(buf).index_select(0, cache["sel"])
+
+    def _gather_contrib(self, local: torch.Tensor) -> torch.Tensor:
+        """Every rank's subset contributions in global subset order."""
+        return self._gather_sorted(local)
+
     def launch(self) -> ShardResult:
         be, sh, r = self.be, self.sh, self.r
+        if getattr(be, "dc_run_sharded", None) is not None and be.dc_run_sharded(
+                self.x, self.row_idx, sh.piece_off, self.plan.c, r, self.out, self.est, self.gof,
+                self.status, self.plan.n, self.plan.p, self._gather_contrib):
+            # re-centred on the device inside the call: the mean of every
+            # subset's contribution in global order (no sums pass, no shift)
+            self.recs = self._gather_sorted(
+                torch.cat([self.ids, self.gof, self.est, self.sums.zero_(), self.status], dim=1))
+            return ShardResult(self.out, sh.report_lo, len(sh.local_rows), self.finish,
+                               rows_fn=self.rows_of)
         be.dc_run(self.x, self.row_idx, sh.piece_off, self.plan.c, r, self.out, self.est,
                   self.gof, self.status)
         be.range_sums(self.out, self.own_off, len(sh.pieces), self.sums)
@@ -562,6 +600,42 @@ class GpuBackend:
         h.call("mdsx_divide_conquer_ex", x.data_ptr(), self.D.dtype_code(x), x.shape[1],
                x.shape[0], x.shape[1], row_idx.data_ptr(), off.ctypes.data, len(off) - 1, c, r,
                out.data_ptr(), est.data_ptr(), gof.data_ptr(), status.data_ptr(), 1, sp)
+
+    def dc_run_sharded(self, x, row_idx, piece_off, c, r, out, est, gof, status, n_total,
+                       np_total, gather) -> bool:
+        """mdsx_divide_conquer_sharded: the rank's subsets solved and written
+        re-centred, the contributions gathered by `gather` (device tensors,
+        current stream) from inside the call.  False when the fused output
+        route does not apply (the caller re-centres with segment sums)."""
+        from ._lib import GATHER_FN
+        from .errors import MdsError
+        h, sp = self._h()
+        off = np.ascontiguousarray(piece_off, dtype=np.int64)
+        npl = len(off) - 1
+        local = torch.empty((npl, r), dtype=torch.float64, device=self.device)
+        glob = torch.empty((np_total, r), dtype=torch.float64, device=self.device)
+        failure = []
+
+        def cb(_ctx, _stream):
+            try:
+                glob.copy_(gather(local))
+                return 0
+            except Exception as exc:           # reported after the call returns
+                failure.append(exc)
+                return 1
+        fn = GATHER_FN(cb)
+        try:
+            h.call("mdsx_divide_conquer_sharded", x.data_ptr(), self.D.dtype_code(x), x.shape[1],
+                   x.shape[0], x.shape[1], row_idx.data_ptr(), off.ctypes.data, npl, c, r,
+                   out.data_ptr(), est.data_ptr(), gof.data_ptr(), status.data_ptr(), n_total,
+                   np_total, local.data_ptr(), glob.data_ptr(), fn, None, sp)
+        except Exception as exc:
+            if failure:
+                raise failure[0] from exc
+            if type(exc) is MdsError:             # MDSX_UNSUPPORTED: no fused output route
+                return False
+            raise
+        return True
 
     def range_sums(self, out, off_dev, nseg, sums) -> None:
         if nseg == 0:

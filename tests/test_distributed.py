@@ -333,3 +333,39 @@ def test_bench_self_launch(world):
     assert len(lines) == 1, res.stdout
     line = json.loads(lines[0])
     assert line["n_gpus"] == world and line["ranks_seen"] == list(range(world))
+
+
+def _gather_worker(rank, world, port, path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = plans.plan_divide_conquer(30_000, 400, 10, 3)
+        comm = dd.Comm()
+        sd = dd.ShardedDivide.__new__(dd.ShardedDivide)       # layout fields only
+        sd.plan, sd.comm = plan, comm
+        sd.sh = dd.dc_shard(plan, world, rank)
+        sd.first = 0 if rank == 0 else 1
+        sd.kmax = 1 + dd.shard(plan.p - 1, world, 0)[1]
+        ids = torch.tensor(sd.sh.pieces, dtype=torch.float64)[:, None]
+        rows = torch.cat([ids, ids * 10.0 + rank * (ids == 0)], dim=1)  # anchor row differs per rank
+        out = sd._gather_sorted(rows)
+        np.save(f"{path}.{rank}.npy", out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_record_gather_layout(world):
+    """ShardedDivide._gather_sorted (the GPU backend's contribution and record
+    gather): every subset's row exactly once, in global subset order, the
+    anchor's from rank 0, identical on every rank."""
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "g")
+        mp.spawn(_gather_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+        outs = [np.load(f"{path}.{k}.npy") for k in range(world)]
+    p = plans.plan_divide_conquer(30_000, 400, 10, 3).p
+    for o in outs:
+        assert np.array_equal(o, outs[0])
+    assert np.array_equal(outs[0][:, 0], np.arange(p))
+    assert np.array_equal(outs[0][:, 1], np.arange(p) * 10.0)
