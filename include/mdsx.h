@@ -23,6 +23,10 @@
  *                              (linalg.py:149-169) used by classical_mds
  *   mdsx_gower_context      <- gower_context (algorithms.py:193-217)
  *   mdsx_gower_interpolate  <- gower_interpolate (algorithms.py:220-242)
+ *   mdsx_gower_tiles, mdsx_landmark_overwrite, mdsx_interp_recenter
+ *                           <- interpolation_mds's interpolate / landmark overwrite /
+ *                              _recentered steps (algorithms.py:262-274), for rows
+ *                              spread over ranks
  *   mdsx_procrustes_fit     <- fit_procrustes (procrustes.py:53-78), batched
  *   mdsx_procrustes_apply   <- apply_procrustes (procrustes.py:99-105), batched
  *   mdsx_divide_conquer     <- divide_and_conquer_mds (algorithms.py:128-172)
@@ -175,6 +179,31 @@ int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t
                            const void* rows, int dtype, int64_t ld, int64_t m,
                            double* out, int64_t ldo, int32_t* nonfinite, int32_t flags,
                            void* stream);
+/* The three steps of interpolation_mds after the landmark context
+ * (algorithms.py:262-274), for callers that spread the rows over ranks
+ * (distributed.ShardedInterpolation).  mdsx_interpolation runs the same steps
+ * in one call with per-CTA column sums; the tile sums here make the result
+ * independent of how the rows are spread (bitwise, for any number of ranks):
+ *  - mdsx_gower_tiles: as mdsx_gower_interpolate for dense (ld = p), 16-byte
+ *    aligned rows with packed output, plus tile_sums[t * r + c] = column sums of
+ *    out over tile t (mdsx_gower_tile_rows rows per tile; MDSX_UNSUPPORTED for
+ *    other layouts).  A rank's rows must start on a tile boundary for the
+ *    tiles to be the same as the single-call's.
+ *  - mdsx_landmark_overwrite: out[pos[i]] = base[s], corr[s] = base[s] - old,
+ *    s = sel[i] (sel NULL: i), for the nl landmarks held here; corr (l x r,
+ *    sample order) is zeroed first, so summing the ranks' corr is exact.
+ *  - mdsx_interp_recenter: out[0..m) -= (sum of tile_sums (all ranks' tiles in
+ *    row order) + sum of corr) / n_total, in a fixed order. */
+int32_t mdsx_gower_tile_rows(mdsx_handle* h, int dtype, int32_t p, int32_t r);
+int mdsx_gower_tiles(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
+                     const void* rows, int dtype, int64_t m, double* out, double* tile_sums,
+                     int32_t* nonfinite, int32_t flags, void* stream);
+int mdsx_landmark_overwrite(mdsx_handle* h, const double* base, int64_t l, int32_t r,
+                            const int64_t* sel, const int64_t* pos, int64_t nl, double* out,
+                            double* corr, void* stream);
+int mdsx_interp_recenter(mdsx_handle* h, const double* tile_sums, int64_t ntiles,
+                         const double* corr, int64_t l, int32_t r, int64_t n_total, double* out,
+                         int64_t m, void* stream);
 
 /* ---- Procrustes ----------------------------------------------------------- */
 /* Job j aligns src rows src_rows[job_off[j]..job_off[j+1]) of src (ld = r)

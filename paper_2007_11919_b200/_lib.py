@@ -7,6 +7,7 @@ compute entry point raises ``RuntimeError`` naming what is missing.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -14,6 +15,11 @@ from .errors import (DegenerateRankError, FormatError, InvalidInputError, MdsErr
                      NumericalError, ParamError, ShapeError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libmdsx.so"
+# A/B measurements only (tools/): load another build of the library; entry
+# points it lacks are left unbound
+_LIB_OVERRIDE = os.environ.get("MDSX_LIB")
+if _LIB_OVERRIDE:
+    LIB_PATH = Path(_LIB_OVERRIDE).resolve()
 
 OK, PARAM, SHAPE, INVALID, NUMERICAL, DEGENERATE, CUDA, UNSUPPORTED, FORMAT = range(9)
 F64, F32 = 0, 1
@@ -60,6 +66,11 @@ SIGNATURES = {
                                   _vp, _vp]),
     "mdsx_gower_interpolate": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _int, _i64, _i64, _vp,
                                       _i64, _vp, _i32, _vp]),
+    "mdsx_gower_tile_rows": (_i32, [_vp, _int, _i32, _i32]),
+    "mdsx_gower_tiles": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _int, _i64, _vp, _vp, _vp, _i32,
+                                _vp]),
+    "mdsx_landmark_overwrite": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "mdsx_interp_recenter": (_int, [_vp, _vp, _i64, _vp, _i64, _i32, _i64, _vp, _i64, _vp]),
     "mdsx_procrustes_fit": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
                                    _vp, _vp]),
     "mdsx_procrustes_apply": (_int, [_vp, _vp, _i32, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
@@ -111,6 +122,8 @@ def load() -> C.CDLL:
                     "(there is no CPU fallback)")
             lib = C.CDLL(str(LIB_PATH))
             for name, (res, args) in SIGNATURES.items():
+                if _LIB_OVERRIDE and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -477,12 +477,22 @@ gower_stream_kernel(const T* __restrict__ X, int64_t m, int p, int r,
 // broadcast.  Epilogue: a butterfly reduce-scatter leaves lane j of a group the
 // full sums of output columns [j*KF, (j+1)*KF); it writes them and adds them to
 // its per-column running sums (fixed order -> per-CTA column partials for the
-// final re-centring).
+// final re-centring of the single call).
+//
+// TILES (the sharded interpolation, mdsx_gower_tiles): per-TILE column sums
+// instead, so that the re-centring's fold does not depend on which CTA -- or
+// which rank (rank row ranges start on tile boundaries) -- processed a tile.
+// Each warp folds its rows of a tile by a fixed butterfly into a shared-memory
+// slot; the producer warp, idle between its copies, adds the eight warp slots
+// in warp order and writes one r-vector per tile (it folds tile k - PSLOTS
+// before issuing tile k's copy, so a slot is never rewritten unread).
 
 constexpr int GB_THREADS = 256;                  // compute threads (8 warps)
 constexpr int GB_CTA = GB_THREADS + 32;          // + one producer warp
 constexpr int GB_MAX_STAGES = 4;
-// header: full[4], empty[4] mbarriers [0, 64), c0 [64, 192), v [192, 320)
+constexpr int GB_PSLOTS = 8;                     // TILES: tile-sum slots in flight
+// header: full[4], empty[4] mbarriers [0, 64), c0 [64, 192), v [192, 320),
+// TILES: psum[8] [320, 384)
 constexpr int GB_HEADER = 512;
 
 // N32 (fp32 rows, fused interpolation only): the squared norm |x - xbar|^2 is
@@ -491,7 +501,7 @@ constexpr int GB_HEADER = 512;
 // classical configuration) has zero column sums up to rounding, so its 1e-7
 // relative error reaches the output at ~1e-22; the fp64 pipe keeps the linear
 // term (11 instead of 13 fp64 operations per row-feature).
-template <typename T, int RM, int TPR, int CPS, bool N32>
+template <typename T, int RM, int TPR, int CPS, bool N32, bool TILES>
 __global__ void __launch_bounds__(GB_CTA, CPS)
 gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
                   const double* __restrict__ ctx_mean, const double* __restrict__ ctx_M,
@@ -511,8 +521,11 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
   double* vvs = c0s + 16;                                   // v
   const int nchunks = p / VW;
   const int nit = (nchunks + TPR - 1) / TPR;
+  uint64_t* psum = reinterpret_cast<uint64_t*>(smraw + 320);
   double2* rec = reinterpret_cast<double2*>(smraw + GB_HEADER);
-  T* stage0 = reinterpret_cast<T*>(smraw + GB_HEADER + (size_t)nit * VW * W * TPR * sizeof(double2));
+  double* pslot = reinterpret_cast<double*>(smraw + GB_HEADER + (size_t)nit * VW * W * TPR * sizeof(double2));
+  T* stage0 = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(pslot) +
+                                   (TILES ? (size_t)GB_PSLOTS * (GB_THREADS / 32) * RMP * sizeof(double) : 0));
   const int tid = threadIdx.x;
   const int64_t ntiles = (m + TR - 1) / TR;
   const size_t stage_elems = (size_t)TR * p;
@@ -522,10 +535,41 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
       bulk::bar_init(&full[s], 1);
       bulk::bar_init(&empty[s], GB_THREADS / 32);
     }
+    if (TILES)
+      for (int s = 0; s < GB_PSLOTS; ++s) bulk::bar_init(&psum[s], (GB_THREADS / 32) * TPR);
     bulk::bar_fence();
   }
   __syncthreads();
 
+  if (TILES && tid >= GB_THREADS) {         // ---- producer warp (+ tile-sum fold)
+    const int lane = tid & 31;
+    auto fold = [&](int kk) {
+      const int sl = kk % GB_PSLOTS;
+      bulk::wait(&psum[sl], (unsigned)((kk / GB_PSLOTS) & 1));
+      if (lane < r) {
+        const double* ps = pslot + (size_t)sl * (GB_THREADS / 32) * RMP + lane;
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < GB_THREADS / 32; ++w) acc += ps[w * RMP];
+        colpart[((int64_t)blockIdx.x + (int64_t)kk * gridDim.x) * r + lane] = acc;
+      }
+      __syncwarp();
+    };
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      if (k >= GB_PSLOTS) fold(k - GB_PSLOTS);
+      if (lane == 0) {
+        const int s = k % nstage;
+        if (k >= nstage) bulk::wait(&empty[s], (unsigned)((k / nstage - 1) & 1));
+        const int64_t nr = min((int64_t)TR, m - t * TR);
+        bulk::load(stage0 + (size_t)s * stage_elems, X + t * TR * p,
+                   (unsigned)(nr * p * sizeof(T)), &full[s]);
+      }
+      __syncwarp();
+    }
+    for (int kk = max(0, k - GB_PSLOTS); kk < k; ++kk) fold(kk);
+    return;
+  }
   if (tid >= GB_THREADS) {                  // ---- producer warp
     if (tid == GB_THREADS) {
       int k = 0;
@@ -675,6 +719,9 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
         }
     __syncwarp();
     if (lane == 0) bulk::arrive(&empty[s]);
+    double tsum[KF];
+#pragma unroll
+    for (int i = 0; i < KF; ++i) tsum[i] = 0.0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       // butterfly reduce-scatter: lane j keeps columns [j*KF, (j+1)*KF)
@@ -689,7 +736,17 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
         }
       }
       const int row = g + q * G;
-      if (row < nr) {
+      if constexpr (TILES) {
+        // branch-free sums (the butterfly below must see converged lanes)
+        double* o = out + (r0 + row) * r + j * KF;
+#pragma unroll
+        for (int i = 0; i < KF; ++i) {
+          const bool ok = row < nr && j * KF + i < r;
+          const double val = fma(-nrm[q], vr[i], acc[q][i] - c0r[i]);
+          if (ok) o[i] = val;
+          tsum[i] += ok ? val : 0.0;
+        }
+      } else if (row < nr) {
         double* o = out + (r0 + row) * r + j * KF;
 #pragma unroll
         for (int i = 0; i < KF; ++i)
@@ -700,9 +757,24 @@ gower_bulk_kernel(const T* __restrict__ X, int64_t m, int p, int r,
           }
       }
     }
+    if (TILES) {
+      __syncwarp();
+      // the warp's rows of the tile: butterfly over the groups (fixed order)
+#pragma unroll
+      for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < KF; ++i) tsum[i] += __shfl_xor_sync(0xffffffffu, tsum[i], o);
+      if (lane < TPR) {
+        const int sl = k % GB_PSLOTS;
+        double* ps = pslot + ((size_t)sl * (GB_THREADS / 32) + (tid >> 5)) * RMP + j * KF;
+#pragma unroll
+        for (int i = 0; i < KF; ++i) ps[i] = tsum[i];
+        bulk::arrive(&psum[sl]);
+      }
+    }
   }
   if (bad) atomicOr(nonfinite, 1);
-  if (colpart != nullptr) {
+  if (!TILES && colpart != nullptr) {
     asm volatile("bar.sync 1, %0;\n" ::"n"(GB_THREADS) : "memory");   // all tiles consumed
     double* red = reinterpret_cast<double*>(stage0);
 #pragma unroll
@@ -755,6 +827,72 @@ landmark_overwrite_kernel(const double* __restrict__ base, const int64_t* __rest
   }
 }
 
+// Interpolation's landmark overwrite (algorithms.py:264-268) with the column-sum
+// correction: out[pos[i]] = base[s], corr[s] = base[s] - old, s = sel[i] (the
+// landmark's place in the sample; sel null -> i).  corr is indexed by sample
+// position, so the re-centring folds it in the same order however the rows
+// (and their landmarks) are spread over ranks.
+__global__ void __launch_bounds__(256)
+landmark_corr_kernel(const double* __restrict__ base, const int64_t* __restrict__ sel,
+                     const int64_t* __restrict__ pos, int64_t nl, int r, double* __restrict__ out,
+                     double* __restrict__ corr) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nl * r) return;
+  const int64_t i = e / r;
+  const int c = (int)(e - i * r);
+  const int64_t si = sel ? sel[i] : i;
+  double* o = out + pos[i] * r + c;
+  const double bv = base[si * r + c];
+  corr[si * r + c] = bv - *o;
+  *o = bv;
+}
+
+// Column sums of two row-major (rows x r) arrays, level 1: block b sums the
+// FOLD_ROWS-row chunk b of the concatenation [A (na rows) | B (nb rows)]
+// (chunks never straddle the two), rows strided over the threads in a fixed
+// order, then a fixed tree.  Level 2 (fold_total_kernel): one thread per column
+// adds the chunk sums in chunk order.  The result depends on the arrays only.
+constexpr int FOLD_ROWS = 1024;
+constexpr int FOLD_T = 128;
+template <int RM>
+__global__ void __launch_bounds__(FOLD_T)
+fold_chunks_kernel(const double* __restrict__ A, int64_t na, const double* __restrict__ B,
+                   int64_t nb, int r, double* __restrict__ csum) {
+  __shared__ double red[RM][FOLD_T];
+  const int64_t cha = (na + FOLD_ROWS - 1) / FOLD_ROWS;
+  const bool inA = blockIdx.x < cha;
+  const double* X = inA ? A : B;
+  const int64_t nx = inA ? na : nb;
+  const int64_t lo = (inA ? blockIdx.x : blockIdx.x - cha) * (int64_t)FOLD_ROWS;
+  const int64_t hi = min(nx, lo + FOLD_ROWS);
+  double acc[RM];
+#pragma unroll
+  for (int c = 0; c < RM; ++c) acc[c] = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += FOLD_T)
+#pragma unroll
+    for (int c = 0; c < RM; ++c)
+      if (c < r) acc[c] += X[i * r + c];
+#pragma unroll
+  for (int c = 0; c < RM; ++c) red[c][threadIdx.x] = acc[c];
+  __syncthreads();
+  for (int s2 = FOLD_T / 2; s2 > 0; s2 >>= 1) {
+    if (threadIdx.x < s2)
+#pragma unroll
+      for (int c = 0; c < RM; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + s2];
+    __syncthreads();
+  }
+  if (threadIdx.x < r) csum[(int64_t)blockIdx.x * r + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void fold_total_kernel(const double* __restrict__ csum, int nch, int r,
+                                  double* __restrict__ total) {
+  const int c = threadIdx.x;
+  if (c >= r) return;
+  double s = 0.0;
+  for (int b = 0; b < nch; ++b) s += csum[(int64_t)b * r + c];
+  total[c] = s;
+}
+
 }  // namespace
 
 namespace mdsx {
@@ -774,61 +912,117 @@ int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t*
   return launched(h, "landmark_overwrite_kernel", st);
 }
 
-// Bulk-copy Gower over m dense rows.  *nparts = number of column-sum partials
-// written to colpart (one per CTA; 0 when colpart is null or the shape does
-// not fit, in which case nothing is launched).
-int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
-                      const double* mean, const double* M, const double* v, double* out,
-                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
-                      bool norm32) {
-  *nparts = 0;
+int launch_landmark_corr(mdsx_handle* h, const double* base, const int64_t* sel,
+                         const int64_t* pos, int64_t nl, int r, double* out, double* corr,
+                         cudaStream_t st) {
+  if (nl == 0) return MDSX_OK;
+  mdsx::pre(h, st);
+  landmark_corr_kernel<<<(unsigned)((nl * r + 255) / 256), 256, 0, st>>>(base, sel, pos, nl, r, out, corr);
+  return launched(h, "landmark_corr_kernel", st);
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t fold_ws_bytes(int64_t na, int64_t nb, int r) {
+  const int64_t nch = (na + FOLD_ROWS - 1) / FOLD_ROWS + (nb + FOLD_ROWS - 1) / FOLD_ROWS;
+  return al256((size_t)std::max<int64_t>(nch, 1) * r * sizeof(double)) + al256((size_t)r * sizeof(double));
+}
+
+// total[c] = sum of column c over A (na x r) then B (nb x r); ws: fold_ws_bytes
+int launch_fold_sums(mdsx_handle* h, const double* A, int64_t na, const double* B, int64_t nb,
+                     int r, double* ws, double** total, cudaStream_t st) {
+  const int64_t nch = (na + FOLD_ROWS - 1) / FOLD_ROWS + (nb + FOLD_ROWS - 1) / FOLD_ROWS;
+  double* csum = ws;
+  *total = ws + al256((size_t)std::max<int64_t>(nch, 1) * r * sizeof(double)) / sizeof(double);
+  if (nch > 0) {
+    mdsx::pre(h, st);
+    if (r <= 4) fold_chunks_kernel<4><<<(unsigned)nch, FOLD_T, 0, st>>>(A, na, B, nb, r, csum);
+    else if (r <= 10) fold_chunks_kernel<10><<<(unsigned)nch, FOLD_T, 0, st>>>(A, na, B, nb, r, csum);
+    else if (r <= 16) fold_chunks_kernel<16><<<(unsigned)nch, FOLD_T, 0, st>>>(A, na, B, nb, r, csum);
+    else fold_chunks_kernel<32><<<(unsigned)nch, FOLD_T, 0, st>>>(A, na, B, nb, r, csum);
+    int rc = launched(h, "fold_chunks_kernel", st);
+    if (rc) return rc;
+  }
+  mdsx::pre(h, st);
+  fold_total_kernel<<<1, 32, 0, st>>>(csum, (int)nch, r, *total);
+  return launched(h, "fold_total_kernel", st);
+}
+
+// Bulk-copy Gower over m dense rows.  colpart (optional) receives column sums:
+// tiles = false: one r-vector per CTA, *nparts = the number of CTAs; tiles =
+// true: one r-vector per tile (tile t at colpart[t * r]), *nparts = rows per
+// tile.  *nparts = 0 when the shape does not fit (nothing launched).
+struct GbConfig { int TPR = 0, nstage = 0; size_t smem = 0; };
+
+static GbConfig gower_bulk_config(mdsx_handle* h, int dtype, int p, int r, bool tiles) {
+  GbConfig g;
   const size_t es = dtype == MDSX_F32 ? 4 : 8;
   const int VW = (int)(16 / es);
   const int RM = r <= 4 ? 4 : r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : 16;
-  const size_t cap = (size_t)(h->max_smem_optin > 0 ? h->max_smem_optin : 227 * 1024);
+  if (r > 16 || ((size_t)p * es) % 16 != 0) return g;
+  const size_t cap = (size_t)(h && h->max_smem_optin > 0 ? h->max_smem_optin : 227 * 1024);
   const size_t sm_total = 228 * 1024;               // shared memory per SM
   const char* e_tpr = getenv("MDSX_GB_TPR");
-  const char* e_cps = getenv("MDSX_GB_CPS");
   const int force_tpr = e_tpr ? atoi(e_tpr) : 0;
-  const int force_cps = e_cps ? atoi(e_cps) : 0;
-  int TPR = 0, nstage = 0, CPS = 0;
-  size_t smem = 0;
   // one CTA (8 compute warps + producer) per SM; TPR as small as the stage allows
-  for (int cps = 1; cps >= 1 && !TPR; --cps) {
-    if (force_cps && cps != force_cps) continue;
-    for (int tpr = 2; tpr <= 32 && !TPR; tpr *= 2) {
-      if (force_tpr && tpr != force_tpr) continue;
-      const int TR = 2 * GB_THREADS / tpr;
-      const int nit = (p / VW + tpr - 1) / tpr;
-      const size_t recb = (size_t)nit * VW * (RM / 2 + 1) * tpr * 16;
-      const size_t stage = (size_t)TR * p * es;
-      const size_t red = (size_t)((RM + tpr - 1) / tpr * tpr) * GB_THREADS * 8;
-      for (int ns = GB_MAX_STAGES; ns >= 2; --ns) {
-        const size_t need = GB_HEADER + recb + std::max(ns * stage, red);
-        if (stage <= 112 * 1024 && need <= cap && cps * (need + 1024) <= sm_total) {
-          TPR = tpr; nstage = ns; smem = need; CPS = cps;
-          break;
-        }
+  for (int tpr = 2; tpr <= 32 && !g.TPR; tpr *= 2) {
+    if (force_tpr && tpr != force_tpr) continue;
+    const int TR = 2 * GB_THREADS / tpr;
+    const int nit = (p / VW + tpr - 1) / tpr;
+    const size_t recb = (size_t)nit * VW * (RM / 2 + 1) * tpr * 16;
+    const size_t stage = (size_t)TR * p * es;
+    const size_t rmp = (size_t)((RM + tpr - 1) / tpr * tpr);
+    const size_t red = tiles ? 0 : rmp * GB_THREADS * 8;
+    const size_t slots = tiles ? (size_t)GB_PSLOTS * (GB_THREADS / 32) * rmp * 8 : 0;
+    for (int ns = GB_MAX_STAGES; ns >= 2; --ns) {
+      const size_t need = GB_HEADER + recb + slots + std::max(ns * stage, red);
+      if (stage <= 112 * 1024 && need <= cap && need + 1024 <= sm_total) {
+        g.TPR = tpr; g.nstage = ns; g.smem = need;
+        break;
       }
     }
   }
-  if (!TPR || m == 0) return MDSX_OK;
+  return g;
+}
+
+int gower_tile_rows(mdsx_handle* h, int dtype, int p, int r) {
+  const GbConfig g = gower_bulk_config(h, dtype, p, r, true);
+  return g.TPR ? 2 * GB_THREADS / g.TPR : 0;
+}
+
+int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
+                      const double* mean, const double* M, const double* v, double* out,
+                      double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
+                      bool norm32, bool tiles) {
+  *nparts = 0;
+  const int RM = r <= 4 ? 4 : r <= 8 ? 8 : r <= 10 ? 10 : r <= 12 ? 12 : 16;
+  tiles = tiles && colpart != nullptr;
+  const GbConfig cfg = gower_bulk_config(h, dtype, p, r, tiles);
+  const int TPR = cfg.TPR, nstage = cfg.nstage;
+  const size_t smem = cfg.smem;
+  if (!TPR) return MDSX_OK;
+  if (m == 0) {
+    *nparts = tiles ? 2 * GB_THREADS / TPR : 0;
+    return MDSX_OK;
+  }
   auto go = [&](auto tag, auto rm, auto tpr) -> int {
     using T = decltype(tag);
     constexpr int RMc = decltype(rm)::value;
     constexpr int TPRc = decltype(tpr)::value;
-    auto kern = gower_bulk_kernel<T, RMc, TPRc, 1, false>;
+    auto kern = tiles ? gower_bulk_kernel<T, RMc, TPRc, 1, false, true>
+                      : gower_bulk_kernel<T, RMc, TPRc, 1, false, false>;
     if constexpr (sizeof(T) == 4)
-      if (norm32) kern = gower_bulk_kernel<T, RMc, TPRc, 1, true>;
+      if (norm32) kern = tiles ? gower_bulk_kernel<T, RMc, TPRc, 1, true, true>
+                               : gower_bulk_kernel<T, RMc, TPRc, 1, true, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t TR = 2 * GB_THREADS / TPRc;
     const int64_t ntiles = (m + TR - 1) / TR;
-    const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)h->num_sms * CPS);
+    const int blocks = (int)std::min<int64_t>(ntiles, (int64_t)h->num_sms);
     mdsx::pre(h, st);
     kern<<<blocks, GB_CTA, smem, st>>>((const T*)X, m, p, r, mean, M, v, out, colpart,
                                            nonfinite, nstage);
     const int rc = launched(h, "gower_bulk_kernel", st);
-    if (!rc) *nparts = colpart ? blocks : -1;
+    if (!rc) *nparts = tiles ? (int)TR : colpart ? blocks : -1;
     return rc;
   };
   auto by_tpr = [&](auto tag, auto rm) -> int {
@@ -916,7 +1110,7 @@ int launch_gower_affine(mdsx_handle* h, const void* X, int dtype, int64_t ld, in
       (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
     int launched_parts = 0;
     int rc = launch_gower_bulk(h, X, dtype, m, p, r, mean, M, v, out, nullptr, nonfinite,
-                               &launched_parts, st, false);
+                               &launched_parts, st, false, false);
     if (rc || launched_parts) return rc;
     rc = launch_gower_stream(h, X, dtype, m, p, r, mean, M, v, out, nonfinite, st);
     if (rc >= 0) return rc;                       // -1: shape does not fit the staged kernel

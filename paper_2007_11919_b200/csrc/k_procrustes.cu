@@ -1047,13 +1047,13 @@ colsum_partial_kernel(const double* __restrict__ X, int64_t n, int r, double* __
 // (no 64-bit modulo per element).
 __global__ void __launch_bounds__(256)
 subtract_mean_kernel(double* __restrict__ X, int64_t n, int r, const double* __restrict__ part,
-                     int nparts, const double* __restrict__ corr) {
+                     int nparts, const double* __restrict__ corr, double ndiv) {
   __shared__ double mean[MDSX_MAX_R];
   if (threadIdx.x < r) {
     double s = 0.0;
     for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * r + threadIdx.x];
     if (corr) s += corr[threadIdx.x];
-    mean[threadIdx.x] = s / (double)n;
+    mean[threadIdx.x] = s / ndiv;
   }
   __syncthreads();
   const int64_t total = n * r;
@@ -1487,7 +1487,7 @@ int launch_scatter(mdsx_handle* h, const double* src, const int64_t* idx, int64_
 size_t recenter_ws_bytes(int r) { return (size_t)RC_BLOCKS * r * sizeof(double); }
 
 int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
-                         int nparts, const double* corr, cudaStream_t st);
+                         int nparts, const double* corr, cudaStream_t st, int64_t ndiv = 0);
 
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st) {
   if (n == 0) return MDSX_OK;
@@ -1500,13 +1500,15 @@ int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, c
   return launch_subtract_mean(h, X, n, r, part, RC_BLOCKS, nullptr, st);
 }
 
+// X (n rows) -= (sum of the partials + corr) / ndiv (ndiv 0: n)
 int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
-                         int nparts, const double* corr, cudaStream_t st) {
+                         int nparts, const double* corr, cudaStream_t st, int64_t ndiv) {
   if (n == 0) return MDSX_OK;
   const int64_t total = n * r;
   int blocks = (int)std::min<int64_t>((total + 1023) / 1024, (int64_t)h->num_sms * 8);
   mdsx::pre(h, st);
-  subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, nparts, corr);
+  subtract_mean_kernel<<<blocks, 256, 0, st>>>(X, n, r, part, nparts, corr,
+                                               (double)(ndiv > 0 ? ndiv : n));
   return launched(h, "subtract_mean_kernel", st);
 }
 

@@ -41,13 +41,20 @@ int launch_aligned_corr(mdsx_handle* h, const double* X, int64_t n, int r, const
 size_t recenter_ws_bytes(int r);
 int launch_recenter(mdsx_handle* h, double* X, int64_t n, int r, double* part, cudaStream_t st);
 int launch_subtract_mean(mdsx_handle* h, double* X, int64_t n, int r, const double* part,
-                         int nparts, const double* corr, cudaStream_t st);
+                         int nparts, const double* corr, cudaStream_t st, int64_t ndiv = 0);
 int launch_landmark_overwrite(mdsx_handle* h, const double* base, const int64_t* idx, int64_t l,
                               int r, double* out, double* corr, cudaStream_t st);
+int launch_landmark_corr(mdsx_handle* h, const double* base, const int64_t* sel,
+                         const int64_t* pos, int64_t nl, int r, double* out, double* corr,
+                         cudaStream_t st);
+size_t fold_ws_bytes(int64_t na, int64_t nb, int r);
+int launch_fold_sums(mdsx_handle* h, const double* A, int64_t na, const double* B, int64_t nb,
+                     int r, double* ws, double** total, cudaStream_t st);
+int gower_tile_rows(mdsx_handle* h, int dtype, int p, int r);
 int launch_gower_bulk(mdsx_handle* h, const void* X, int dtype, int64_t m, int p, int r,
                       const double* mean, const double* M, const double* v, double* out,
                       double* colpart, int32_t* nonfinite, int* nparts, cudaStream_t st,
-                      bool norm32 = false);
+                      bool norm32 = false, bool tiles = false);
 int launch_gower_context(mdsx_handle* h, const void* X, int dtype, int64_t ld, int p,
                          const int64_t* idx, int64_t l, const double* X1, int r, double* mean,
                          double* M, double* v, double* S, double* q, double* cond, int32_t* flag,
@@ -806,6 +813,63 @@ int mdsx_gower_interpolate(mdsx_handle* h, const double* ctx, int64_t l, int32_t
     if (nparts > 0) return MDSX_OK;
   }
   return launch_gower_affine(h, rows, dtype, ld, m, p, r, mean, M, v, out, ldo, nf, st);
+}
+
+static bool gower_tiles_fit(mdsx_handle* h, const void* rows, int dtype, int64_t ld, int p, int r) {
+  const size_t es = dtype == MDSX_F32 ? 4 : 8;
+  return ld == p && r <= 16 && ((size_t)p * es) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(rows) & 15) == 0 && gower_tile_rows(h, dtype, p, r) > 0;
+}
+
+int32_t mdsx_gower_tile_rows(mdsx_handle* h, int dtype, int32_t p, int32_t r) {
+  if (!h || p < 1 || r < 1) return 0;
+  return gower_tile_rows(h, dtype, p, r);
+}
+
+int mdsx_gower_tiles(mdsx_handle* h, const double* ctx, int64_t l, int32_t p, int32_t r,
+                     const void* rows, int dtype, int64_t m, double* out, double* tile_sums,
+                     int32_t* nonfinite, int32_t flags, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  (void)l;
+  if (!ctx || !out || !tile_sums || !nonfinite || m < 0) return fail(h, MDSX_PARAM, "bad gower tiles arguments");
+  if (m > 0 && (!rows || !gower_tiles_fit(h, rows, dtype, p, p, r)))
+    return fail(h, MDSX_UNSUPPORTED, "gower tiles: rows must be dense, 16-byte aligned, r <= 16");
+  const double* mean = ctx;
+  const double* M = mean + p;
+  const double* v = M + (int64_t)p * r;
+  int tile_rows = 0;
+  const bool n32 = dtype == MDSX_F32 && (flags & MDSX_GOWER_CENTRED) && !getenv("MDSX_GOWER_NORM64");
+  return launch_gower_bulk(h, rows, dtype, m, p, r, mean, M, v, out, tile_sums, nonfinite,
+                           &tile_rows, st, n32, true);
+}
+
+int mdsx_landmark_overwrite(mdsx_handle* h, const double* base, int64_t l, int32_t r,
+                            const int64_t* sel, const int64_t* pos, int64_t nl, double* out,
+                            double* corr, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if (!base || !corr || (nl > 0 && (!pos || !out)) || nl < 0 || nl > l || r < 1)
+    return fail(h, MDSX_PARAM, "bad landmark overwrite arguments");
+  int rc = cuda_check(h, cudaMemsetAsync(corr, 0, (size_t)l * r * sizeof(double), st), "memset");
+  if (rc) return rc;
+  return launch_landmark_corr(h, base, sel, pos, nl, r, out, corr, st);
+}
+
+int mdsx_interp_recenter(mdsx_handle* h, const double* tile_sums, int64_t ntiles,
+                         const double* corr, int64_t l, int32_t r, int64_t n_total, double* out,
+                         int64_t m, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if ((ntiles > 0 && !tile_sums) || !corr || n_total < 1 || m < 0 || r < 1 || r > MDSX_MAX_R)
+    return fail(h, MDSX_PARAM, "bad recentre arguments");
+  int rc = ws_reserve(h, fold_ws_bytes(ntiles, l, r) + 256);
+  if (rc) return rc;
+  double* ws = (double*)ws_alloc(h, fold_ws_bytes(ntiles, l, r), st);
+  if (!ws) return MDSX_CUDA;
+  double* total = nullptr;
+  if ((rc = launch_fold_sums(h, tile_sums, ntiles, corr, l, r, ws, &total, st))) return rc;
+  return launch_subtract_mean(h, out, m, r, total, 1, nullptr, st, n_total);
 }
 
 int mdsx_procrustes_fit(mdsx_handle* h, const double* tgt, const int64_t* tgt_rows,

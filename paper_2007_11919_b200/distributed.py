@@ -104,6 +104,12 @@ class Comm:
         dist.gather(t.contiguous(), dst=dst, group=self.group)
         return None
 
+    def sum_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum over the ranks (exact for terms with disjoint supports)."""
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
     def max_int(self, v: int) -> int:
         if self.world == 1:
             return int(v)
@@ -384,20 +390,53 @@ class ShardedInterpolation:
         bounds = np.minimum(sh.hi, np.arange(sh.b_lo, sh.b_hi + 1, dtype=np.int64) * SUM_BLOCK) - sh.lo
         self.bounds = backend.index(bounds)
         self.nb = nb
-        self.sums = torch.empty((nb, r), dtype=torch.float64, device=dev)
-        self.ids = torch.arange(sh.b_lo, sh.b_hi, dtype=torch.float64, device=dev)[:, None]
-        self.nf = torch.zeros((nb, 1), dtype=torch.float64, device=dev)
         self.blocks = (n + SUM_BLOCK - 1) // SUM_BLOCK
         self.kmax = shard(self.blocks, comm.world, 0)[1]
         self.recs = None
+        # tile route: the Gower pass writes per-tile column sums (tile_rows rows;
+        # rank row ranges start on SUM_BLOCK, a multiple of the tile), the
+        # landmark overwrite a per-landmark correction; both are gathered in row /
+        # sample order and folded identically on every rank
+        self.tr = backend.tile_rows(x_local, r) if hasattr(backend, "tile_rows") else 0
+        if self.tr and SUM_BLOCK % self.tr == 0:
+            nt = (sh.hi - sh.lo + self.tr - 1) // self.tr
+            counts = [(s.hi - s.lo + self.tr - 1) // self.tr
+                      for s in (interp_shard(n, self.sample, comm.world, k) for k in range(comm.world))]
+            self.ntiles, self.ktile = nt, max(counts)
+            self.ntiles_total = sum(counts)
+            self.tbuf = torch.zeros((self.ktile + 1, r), dtype=torch.float64, device=dev)
+            self.corr = torch.zeros((l, r), dtype=torch.float64, device=dev)
+            if comm.world > 1:
+                sel = np.concatenate([k * (self.ktile + 1) + 1 + np.arange(c, dtype=np.int64)
+                                      for k, c in enumerate(counts)])
+                self.tsel = backend.index(sel)
+            self.flags = None
+        else:
+            self.tr = 0
+            self.sums = torch.empty((nb, r), dtype=torch.float64, device=dev)
+            self.ids = torch.arange(sh.b_lo, sh.b_hi, dtype=torch.float64, device=dev)[:, None]
+            self.nf = torch.zeros((nb, 1), dtype=torch.float64, device=dev)
 
     def launch(self) -> ShardResult:
         be, sh, r, l = self.be, self.sh, self.r, self.l
         if self.comm.rank == 0:
             be.landmark_head(self.xl, r, self.head)
         self.comm.broadcast_(self.head, 0)
-        flag = be.gower_rows(self.head, l, r, self.x, self.out)
         base = self.head[-l * r:].view(l, r)
+        if self.tr:
+            flag = be.gower_tiles(self.head, l, r, self.x, self.out, self.tbuf[1:1 + self.ntiles])
+            be.landmark_overwrite(base, self.land_sel, self.land_pos, self.out, self.corr)
+            self.tbuf[0, 0] = flag
+            if self.comm.world == 1:
+                tiles, self.flags = self.tbuf[1:1 + self.ntiles], self.tbuf[:1, 0]
+            else:
+                allt = self.comm.all_gather(self.tbuf)
+                tiles = allt.index_select(0, self.tsel)
+                self.flags = allt[::self.ktile + 1, 0]
+                self.comm.sum_(self.corr)
+            be.interp_recenter(tiles, self.corr, self.n, self.out)
+            return ShardResult(self.out, 0, sh.hi - sh.lo, self.finish, rows_fn=self.rows_of)
+        flag = be.gower_rows(self.head, l, r, self.x, self.out)
         if len(sh.land_sel):
             be.scatter_rows(base.index_select(0, self.land_sel), self.land_pos, self.out)
         be.range_sums(self.out, self.bounds, self.nb, self.sums)
@@ -405,6 +444,7 @@ class ShardedInterpolation:
             self.nf[0, 0] = flag
         recs = torch.cat([self.ids, self.sums, self.nf], dim=1)
         self.recs = _gather_records(self.comm, recs, self.kmax, self.blocks)
+        self.flags = self.recs[:, 1 + r]
         be.shift_rows(self.out, _fold_mean(self.recs[:, 1:1 + r], self.n))
         return ShardResult(self.out, 0, sh.hi - sh.lo, self.finish, rows_fn=self.rows_of)
 
@@ -419,7 +459,7 @@ class ShardedInterpolation:
         g1, g2, est = float(head[0]), float(head[1]), head[2:2 + r]
         st = decode_status(head[2 + r:4 + r])[0]
         flag, cond = int(head[4 + r]), float(head[5 + r])
-        if int(st["code"]) == 3 or self.recs[:, 1 + r].abs().sum().item() > 0:
+        if int(st["code"]) == 3 or self.flags.abs().sum().item() > 0:
             raise InvalidInputError("data contains non-finite values")
         raise_piece_status(st, r, "sample subset")
         if flag == 1:
@@ -702,6 +742,35 @@ class GpuBackend:
             h.call("mdsx_gower_interpolate", head[2 + r + 4:].data_ptr(), l, p, r, x.data_ptr(),
                    D.dtype_code(x), p, x.shape[0], out.data_ptr(), r, nf.data_ptr(), 1, sp)
         return nf[0].to(torch.float64)
+
+    def tile_rows(self, x, r: int) -> int:
+        """Rows per Gower tile of the tile route (0: the shape takes the row route)."""
+        if x.dim() != 2 or not x.is_contiguous() or x.data_ptr() % 16:
+            return 0
+        h = self.D.handle(self.device)
+        return int(h.lib.mdsx_gower_tile_rows(h.ptr, self.D.dtype_code(x), x.shape[1], r))
+
+    def gower_tiles(self, head, l: int, r: int, x, out, tsum) -> torch.Tensor:
+        """Gower coordinates of x into out and the per-tile column sums into
+        tsum; returns the non-finite flag (device scalar, float64)."""
+        h, sp = self._h()
+        nf = torch.zeros(1, dtype=torch.int32, device=self.device)
+        h.call("mdsx_gower_tiles", head[2 + r + 4:].data_ptr(), l, x.shape[1], r, x.data_ptr(),
+               self.D.dtype_code(x), x.shape[0], out.data_ptr(), tsum.data_ptr(), nf.data_ptr(),
+               1, sp)
+        return nf[0].to(torch.float64)
+
+    def landmark_overwrite(self, base, sel, pos, out, corr) -> None:
+        h, sp = self._h()
+        base = base.contiguous()
+        h.call("mdsx_landmark_overwrite", base.data_ptr(), base.shape[0], base.shape[1],
+               sel.data_ptr(), pos.data_ptr(), pos.numel(), out.data_ptr(), corr.data_ptr(), sp)
+
+    def interp_recenter(self, tiles, corr, n: int, out) -> None:
+        h, sp = self._h()
+        tiles = tiles.contiguous()
+        h.call("mdsx_interp_recenter", tiles.data_ptr(), tiles.shape[0], corr.data_ptr(),
+               corr.shape[0], corr.shape[1], n, out.data_ptr(), out.shape[0], sp)
 
     # fast ----------------------------------------------------------------
     def fast_prepare(self, x, plan, flat, r):

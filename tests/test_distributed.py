@@ -129,6 +129,25 @@ class OracleBackend:
             out[a:a + 64] = torch.from_numpy(orc.gower_project(ctx, x[a:a + 64]))
         return torch.tensor(0.0, dtype=torch.float64)
 
+    TILE = 64
+
+    def tile_rows(self, x, r):
+        return self.TILE
+
+    def gower_tiles(self, head, l, r, x, out, tsum):
+        flag = self.gower_rows(head, l, r, x, out)
+        for t in range(tsum.shape[0]):
+            tsum[t] = out[t * self.TILE:(t + 1) * self.TILE].sum(dim=0)
+        return flag
+
+    def landmark_overwrite(self, base, sel, pos, out, corr):
+        corr.zero_()
+        corr[sel] = base[sel] - out[pos]
+        out[pos] = base[sel]
+
+    def interp_recenter(self, tiles, corr, n, out):
+        out -= (tiles.sum(dim=0) + corr.sum(dim=0)) / n
+
     def fast_prepare(self, x, plan, flat, r):
         return (x.numpy(), flat, r)
 

@@ -51,3 +51,34 @@ def test_sharded_divide_equals_unsharded(nccl1):
     assert np.array_equal(got, ref.points)
     assert np.array_equal(res.estimates, ref.eigenvalue_estimates)
     assert res.gof_g1 == ref.gof_g1
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_sharded_interpolation_equals_unsharded(nccl1, dtype):
+    """The tile route (per-tile Gower sums, per-landmark corrections, one fold)
+    at world size 1 against the single call (per-CTA column sums): the same
+    points up to the summation order of the column mean."""
+    import torch
+    import paper_2007_11919_b200 as mds
+    from paper_2007_11919_b200 import distributed as dd
+    from paper_2007_11919_b200.synthetic import scenario
+    n = 300_000
+    x = scenario(n, 24, 4, seed=5).astype(dtype)
+    prm = mds.AlgorithmParams(r=5, l=700, seed=3)
+    sample = mds.plans.interpolation_sample(n, prm.l, prm.seed)
+    dev = torch.device("cuda", 0)
+    comm = dd.Comm(device=dev)
+    be = dd.GpuBackend(dev)
+    xd = torch.from_numpy(x).to(dev)
+    sh = dd.interp_shard(n, sample, comm.world, comm.rank)
+    assert be.tile_rows(xd, prm.r) > 0
+    run = dd.ShardedInterpolation(be, xd[sh.lo:sh.hi], n, sample, prm.r, comm,
+                                  x_landmarks=xd.index_select(0, torch.from_numpy(sample).to(dev)))
+    assert run.tr > 0
+    res = run.launch().finish()
+    ref = mds.interpolation_mds(x, prm)
+    got = res.out.cpu().numpy()
+    assert np.abs(got - ref.points).max() <= 1e-13 * np.abs(ref.points).max()
+    assert np.array_equal(res.estimates, ref.eigenvalue_estimates)
+    # the re-centring is the only difference: centred columns
+    assert np.abs(got.mean(axis=0)).max() < 1e-12 * np.abs(got).max()

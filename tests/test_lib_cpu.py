@@ -15,7 +15,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "mdsx.h"
 
 def declared_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|void|int64_t|const char\*)\s+(mdsx_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|int32_t|int64_t|const char\*)\s+(mdsx_\w+)\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
