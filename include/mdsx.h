@@ -38,6 +38,9 @@
  *                              (:122-125) in one pass
  *   mdsx_fast_mds           <- fast_mds (algorithms.py:285-348) for plans with form-0
  *                              leaves (the BASELINE shapes), one call
+ *   mdsx_divide_conquer_sharded, mdsx_fast_mds_sharded
+ *                           <- the same for one rank's share of the pieces, the column
+ *                              mean gathered over the ranks inside the call
  * Other fast_mds plans (algorithms.py:323-348) are composed from mdsx_classical_pieces,
  * mdsx_procrustes_fit/apply and mdsx_fast_finish (or mdsx_scatter_rows +
  * mdsx_recenter) by the host.
@@ -298,6 +301,17 @@ int mdsx_divide_conquer_sharded(mdsx_handle* h, const void* data, int dtype, int
                                 int64_t n_total, int32_t npieces_total, double* contrib_local,
                                 double* contrib_global, mdsx_gather_fn gather, void* ctx,
                                 void* stream);
+/* mdsx_fast_mds for one rank's share of a sharded fast MDS (distributed.py):
+ * the plan holds the rank's level-1 subtrees (plus the root's alignment set);
+ * its n_leaves leaf contributions go to contrib_local, gather() fills
+ * contrib_global (nleaves_total x r, global leaf order) on the call's stream,
+ * and the output pass writes the rank's rows (leaf order) re-centred by the
+ * mean over n_total rows -- bitwise the unsharded call's rows. */
+int mdsx_fast_mds_sharded(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                          const mdsx_fast_plan* plan, int32_t r, int64_t n_out, double* out,
+                          double* estimates, double* gof, mdsx_piece_status* status,
+                          int64_t n_total, int32_t nleaves_total, double* contrib_local,
+                          double* contrib_global, mdsx_gather_fn gather, void* ctx, void* stream);
 /* Column sums of points[idx[seg_off[j] .. seg_off[j+1])] per segment j
  * (sums: nseg x r, device; seg_off: device).  Fixed-order reductions, so a
  * sharded run that sums the same segments in the same order is independent

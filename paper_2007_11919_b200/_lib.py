@@ -86,6 +86,8 @@ SIGNATURES = {
     "mdsx_divide_conquer_sharded": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _vp, _i32, _i32,
                                            _i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                                            _vp]),
+    "mdsx_fast_mds_sharded": (_int, [_vp, _vp, _int, _i64, _i32, C.POINTER(FastPlanC), _i32, _i64,
+                                     _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "mdsx_segment_colsums": (_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "mdsx_shift_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "mdsx_interpolation": (_int, [_vp, _vp, _int, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp,

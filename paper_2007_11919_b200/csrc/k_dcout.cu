@@ -647,13 +647,19 @@ int launch_fast_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, int
                     int64_t max_m, int nlev, const int32_t* leaf_job, const int64_t* lev_jbase,
                     int r, const double* mu, const double* U, const double* rot, const double* trans,
                     double* Uc, double* tvec, double* contrib, double* mean, int64_t n_recenter,
-                    double* out, cudaStream_t st) {
+                    double* out, cudaStream_t st, const ContribGather* shard) {
   int rc;
   mdsx::pre(h, st);
   fast_compose_kernel<<<nleaves, 128, 0, st>>>(pd, nlev, nleaves, p, r, leaf_job, lev_jbase, rot,
-                                               trans, U, Uc, tvec, contrib);
+                                               trans, U, Uc, tvec, shard ? shard->local : contrib);
   if ((rc = launched(h, "fast_compose_kernel", st))) return rc;
-  if (n_recenter > 0) {
+  if (shard) {          // every rank's leaf contributions, global leaf order
+    if (shard->gather(shard->ctx, st) != 0) return fail(h, MDSX_CUDA, "contribution gather failed");
+    mdsx::pre(h, st);
+    dc_mean2_kernel<<<1, 256, 0, st>>>(shard->global, shard->total, r, 1.0 / (double)shard->n_total,
+                                       mean);
+    if ((rc = launched(h, "dc_mean_kernel", st))) return rc;
+  } else if (n_recenter > 0) {
     mdsx::pre(h, st);
     dc_mean2_kernel<<<1, 256, 0, st>>>(contrib, nleaves, r, 1.0 / (double)n_recenter, mean);
     if ((rc = launched(h, "dc_mean_kernel", st))) return rc;

@@ -131,7 +131,7 @@ int launch_fast_out(mdsx_handle* h, const void* data, int dtype, int64_t ld, int
                     int64_t max_m, int nlev, const int32_t* leaf_job, const int64_t* lev_jbase,
                     int r, const double* mu, const double* U, const double* rot, const double* trans,
                     double* Uc, double* tvec, double* contrib, double* mean, int64_t n_recenter,
-                    double* out, cudaStream_t st);
+                    double* out, cudaStream_t st, const ContribGather* shard = nullptr);
 size_t points_ws_bytes(int npieces, int64_t max_m, int r);
 size_t eigvals_ws_doubles(int64_t n);
 int launch_sym_eigvals(mdsx_handle* h, const double* A, int64_t n, double* w, double* ws,
@@ -940,14 +940,7 @@ int mdsx_divide_conquer(mdsx_handle* h, const void* data, int dtype, int64_t ld,
                                 estimates, gof, status, 0, stream);
 }
 
-struct ShardOps {
-  double* contrib_local;       // npieces x r (device): this call's subset contributions
-  double* contrib_global;      // npieces_total x r (device): filled by gather()
-  int32_t npieces_total;
-  int64_t n_total;
-  mdsx_gather_fn gather;
-  void* ctx;
-};
+using ShardOps = ContribGather;
 
 static int dc_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int64_t n, int32_t p,
                    const int64_t* row_idx, const int64_t* piece_off, int32_t npieces, int32_t c,
@@ -1089,12 +1082,12 @@ static int dc_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int6
     if (shard && shard->gather) {
       // sharded: every rank's contributions in global subset order (the
       // caller's collective), then the same fixed-order mean on every rank
-      if ((rc = cuda_check(h, cudaMemcpyAsync(shard->contrib_local, contrib,
+      if ((rc = cuda_check(h, cudaMemcpyAsync(shard->local, contrib,
                                               (size_t)npieces * r * sizeof(double),
                                               cudaMemcpyDeviceToDevice, st), "contrib copy")))
         return rc;
       if (shard->gather(shard->ctx, st) != 0) return fail(h, MDSX_CUDA, "contribution gather failed");
-      if ((rc = launch_dc_mean(h, shard->contrib_global, shard->npieces_total, r, shard->n_total, mean,
+      if ((rc = launch_dc_mean(h, shard->global, shard->total, r, shard->n_total, mean,
                                st)))
         return rc;
       return launch_piece_out(h, data, dtype, ld, p, row_idx, nullptr, co.dpd, npieces, cp.max_m, r, c,
@@ -1268,13 +1261,42 @@ extern "C" int mdsx_aligned_correlations(mdsx_handle* h, const double* points, i
 }
 
 // fast_mds in one call (include/mdsx.h): see k_dcout.cu for the tail.
+static int fast_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                     const mdsx_fast_plan* fp, int32_t r, int64_t n_out, int32_t recenter,
+                     double* out, double* estimates, double* gof, mdsx_piece_status* status,
+                     cudaStream_t st, const ContribGather* shard);
+
 extern "C" int mdsx_fast_mds(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
                              const mdsx_fast_plan* fp, int32_t r, int64_t n_out, int32_t recenter,
                              double* out, double* estimates, double* gof, mdsx_piece_status* status,
                              void* stream) {
-  using namespace mdsx;
   cudaStream_t st = as_stream(stream);
   MDSX_GUARD(h, st);
+  return fast_impl(h, data, dtype, ld, p, fp, r, n_out, recenter, out, estimates, gof, status, st,
+                   nullptr);
+}
+
+extern "C" int mdsx_fast_mds_sharded(mdsx_handle* h, const void* data, int dtype, int64_t ld,
+                                     int32_t p, const mdsx_fast_plan* fp, int32_t r, int64_t n_out,
+                                     double* out, double* estimates, double* gof,
+                                     mdsx_piece_status* status, int64_t n_total,
+                                     int32_t nleaves_total, double* contrib_local,
+                                     double* contrib_global, mdsx_gather_fn gather, void* ctx,
+                                     void* stream) {
+  cudaStream_t st = as_stream(stream);
+  MDSX_GUARD(h, st);
+  if (!fp || !contrib_local || !contrib_global || !gather || nleaves_total < fp->n_leaves ||
+      n_total < n_out)
+    return fail(h, MDSX_PARAM, "bad sharded fast arguments");
+  const ContribGather ops{contrib_local, contrib_global, nleaves_total, n_total, gather, ctx};
+  return fast_impl(h, data, dtype, ld, p, fp, r, n_out, 0, out, estimates, gof, status, st, &ops);
+}
+
+static int fast_impl(mdsx_handle* h, const void* data, int dtype, int64_t ld, int32_t p,
+                     const mdsx_fast_plan* fp, int32_t r, int64_t n_out, int32_t recenter,
+                     double* out, double* estimates, double* gof, mdsx_piece_status* status,
+                     cudaStream_t st, const ContribGather* shard) {
+  using namespace mdsx;
   if (!fp || fp->npieces < 2 || fp->n_leaves < 1 || fp->n_leaves >= fp->npieces || fp->nlevels < 1)
     return fail(h, MDSX_PARAM, "bad fast plan");
   const int np = fp->npieces, nl = fp->n_leaves, nal = np - nl, nlev = fp->nlevels;
@@ -1366,5 +1388,5 @@ extern "C" int mdsx_fast_mds(mdsx_handle* h, const void* data, int dtype, int64_
   }
   return launch_fast_out(h, data, dtype, ld, p, fp->row_idx, fp->out_idx, co.dpd, nl, max_leaf, nlev,
                          fp->leaf_job, jbase_d, r, co.mu, co.U, rot, trans, Uc, tvec, contrib, mean,
-                         recenter ? n_out : 0, out, st);
+                         recenter ? n_out : 0, out, st, shard);
 }

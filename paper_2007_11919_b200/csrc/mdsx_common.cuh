@@ -87,6 +87,19 @@ void ws_reset(mdsx_handle* h);
 void* ws_alloc(mdsx_handle* h, size_t bytes, cudaStream_t st);
 // (re)sizes the per-handle workspace for the current call (bump pointer reset)
 int ws_reserve(mdsx_handle* h, size_t bytes);
+
+// Sharded D&C / fast MDS: this call's per-piece (per-leaf) contributions to the
+// column mean go to `local`; gather(ctx, stream) fills `global` with every
+// rank's, in global piece order, on the call's stream; the mean is then taken
+// over `total` pieces and n_total rows (distributed.py).
+struct ContribGather {
+  double* local;
+  double* global;
+  int32_t total;
+  int64_t n_total;
+  int (*gather)(void* ctx, void* stream);
+  void* ctx;
+};
 // Upload a small host array via the pinned staging buffer (async on st).
 int upload(mdsx_handle* h, void* dst, const void* src, size_t bytes, cudaStream_t st);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

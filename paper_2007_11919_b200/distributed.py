@@ -564,9 +564,57 @@ class ShardedFast:
         self.kmax_c = kmax_c
         self.kmax_p = comm.max_int(len(sel))
         self.recs_c = self.recs_p = None
+        self.n_leaves_total = int(sum(c[0] for c in self.counts))
+
+    def _layout(self):
+        """Cached all-gather selections (fixed by the plan and the world size):
+        piece records in global evaluation order, leaf contributions in global
+        leaf order."""
+        comm = self.comm
+        key = ("fast_sel", comm.world, str(self.dev))
+
+        def make():
+            ppos, lpos = [], []
+            kp = kl = 0
+            shards = [fast_shard(self.plan, comm.world, k, self.counts) for k in range(comm.world)]
+            for s_ in shards:
+                kl = max(kl, s_.flat.n_leaves)
+                kp = max(kp, len(s_.flat.eval_order) - 1 + (1 if s_ is shards[0] else 0))
+            for k, s_ in enumerate(shards):
+                nev = len(s_.flat.eval_order) - 1
+                ppos.append(np.stack([s_.eval_base + np.arange(nev), k * kp + np.arange(nev)], axis=1))
+                if k == 0:                      # the root alignment set: last
+                    ppos.append(np.array([[self.total_pieces - 1, nev]]))
+                lpos.append(k * kl + np.arange(s_.flat.n_leaves))
+            ppos = np.concatenate(ppos)
+            psel = ppos[np.argsort(ppos[:, 0], kind="stable"), 1]
+            return dict(kp=kp, kl=kl, psel=self.be.index(psel),
+                        lsel=self.be.index(np.concatenate(lpos)))
+        return _shard_cached(self.plan, key, make)
+
+    def _gather(self, rows: torch.Tensor, kmax: int, sel) -> torch.Tensor:
+        if self.comm.world == 1:
+            return rows
+        buf = torch.zeros((kmax,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+        buf[:rows.shape[0]].copy_(rows)
+        return self.comm.all_gather(buf).index_select(0, sel)
 
     def launch(self) -> ShardResult:
         be, sh, r = self.be, self.sh, self.r
+        fused = getattr(be, "fast_run_sharded", None)
+        if fused is not None:
+            lay = self._layout()
+            res = fused(self.run, self.plan.n, self.n_leaves_total,
+                        lambda local: self._gather(local, lay["kl"], lay["lsel"]))
+            if res is not None:
+                # re-centred inside the call (leaf contributions gathered in
+                # global leaf order): no sums pass, no shift
+                pts, est, gof, status = res
+                s = self.piece_sel
+                recs_p = torch.cat([self.piece_ids, gof.index_select(0, s), est.index_select(0, s),
+                                    status.index_select(0, s)], dim=1)
+                self.recs_p = self._gather(recs_p, lay["kp"], lay["psel"])
+                return ShardResult(pts[:sh.n_own], 0, sh.n_own, self.finish, rows_fn=self.rows_of)
         pts, est, gof, status = be.fast_run(self.run)
         out = pts[:sh.n_own]
         be.range_sums(out, self.child_off, sh.hi - sh.lo, self.sums)
@@ -779,6 +827,43 @@ class GpuBackend:
 
     def fast_run(self, run):
         run.launch()
+        return run.pts, run.est, run.gof, run.status
+
+    def fast_run_sharded(self, run, n_total: int, nleaves_total: int, gather):
+        """mdsx_fast_mds_sharded: the rank's subtrees solved and written
+        re-centred, the leaf contributions gathered by `gather` from inside
+        the call.  None when the one-call route does not apply."""
+        if run.route is None:
+            return None
+        from ._lib import GATHER_FN
+        x, r = run.compact(), run.r
+        h, sp = self._h()
+        nl = run.flat.n_leaves
+        bufs = run.__dict__.setdefault("_shard_bufs", {})
+        if bufs.get("n") != nleaves_total:
+            bufs.update(n=nleaves_total,
+                        local=torch.empty((nl, r), dtype=torch.float64, device=self.device),
+                        glob=torch.empty((nleaves_total, r), dtype=torch.float64, device=self.device))
+        local, glob = bufs["local"], bufs["glob"]
+        failure = []
+
+        def cb(_ctx, _stream):
+            try:
+                glob.copy_(gather(local))
+                return 0
+            except Exception as exc:           # reported after the call returns
+                failure.append(exc)
+                return 1
+        fn = GATHER_FN(cb)
+        try:
+            h.call("mdsx_fast_mds_sharded", x.data_ptr(), self.D.dtype_code(x), x.shape[1],
+                   x.shape[1], run._route_ref, r, run.out.shape[0], run.out.data_ptr(),
+                   run.est.data_ptr(), run.gof.data_ptr(), run.status.data_ptr(), n_total,
+                   nleaves_total, local.data_ptr(), glob.data_ptr(), fn, None, sp)
+        except Exception as exc:
+            if failure:
+                raise failure[0] from exc
+            raise
         return run.pts, run.est, run.gof, run.status
 
 

@@ -129,6 +129,17 @@ class OracleBackend:
             out[a:a + 64] = torch.from_numpy(orc.gower_project(ctx, x[a:a + 64]))
         return torch.tensor(0.0, dtype=torch.float64)
 
+    def fast_run_sharded(self, run, n_total, nleaves_total, gather):
+        """The contribution route's host side: per-leaf column sums gathered in
+        global leaf order, the mean over n_total rows taken off every row."""
+        pts, est, gof, status = self.fast_run(run)
+        off = run[1].piece_off
+        nl = run[1].n_leaves
+        local = torch.stack([pts[off[j]:off[j + 1]].sum(dim=0) for j in range(nl)])
+        glob = gather(local)
+        pts[:off[nl]] -= glob.sum(dim=0) / n_total
+        return pts, est, gof, status
+
     TILE = 64
 
     def tile_rows(self, x, r):

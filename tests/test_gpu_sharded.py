@@ -82,3 +82,27 @@ def test_sharded_interpolation_equals_unsharded(nccl1, dtype):
     assert np.array_equal(res.estimates, ref.eigenvalue_estimates)
     # the re-centring is the only difference: centred columns
     assert np.abs(got.mean(axis=0)).max() < 1e-12 * np.abs(got).max()
+
+
+def test_sharded_fast_equals_unsharded(nccl1):
+    """mdsx_fast_mds_sharded at world size 1: the leaf contributions gathered
+    through the callback give the single call's mean -> bitwise equal."""
+    import torch
+    import paper_2007_11919_b200 as mds
+    from paper_2007_11919_b200 import distributed as dd
+    from paper_2007_11919_b200.synthetic import scenario
+    x = scenario(150_000, 20, 4, seed=4)
+    prm = mds.AlgorithmParams(r=4, l=600, s=8, seed=3)
+    plan = mds.plans.plan_fast(x.shape[0], prm.l, prm.s, prm.seed)
+    dev = torch.device("cuda", 0)
+    comm = dd.Comm(device=dev)
+    sh = dd.fast_shard(plan, comm.world, comm.rank)
+    xl = torch.from_numpy(np.ascontiguousarray(x[sh.local_rows])).to(dev)
+    run = dd.ShardedFast(dd.GpuBackend(dev), xl, plan, prm.r, comm)
+    res = run.launch().finish()
+    got = np.empty((x.shape[0], prm.r))
+    got[sh.local_rows[:sh.n_own]] = res.out.cpu().numpy()
+    ref = mds.fast_mds(x, prm, plan=plan)
+    assert np.array_equal(got, ref.points)
+    assert np.array_equal(res.estimates, ref.eigenvalue_estimates)
+    assert res.gof_g1 == ref.gof_g1
