@@ -724,6 +724,13 @@ def run_ours(args, w):
             rate_d, desc_d, _ = oracle_sample(dict(w, n=nh), xs, 8.0, cores, tuned=False)
             cpu["reference_defaults"] = {"value": rate_d, "unit": UNIT, "sample": desc_d}
 
+    companions = None
+    if rank == 0 and ws == 1 and not sharded and args.workload == "dc2" and not args.no_companions:
+        # the metric names three algorithms: the default line also carries the
+        # config-3 (fast) and config-4 (interpolation) runs, each its own process
+        torch.cuda.empty_cache()
+        companions = {wl: companion_line(wl, args) for wl in ("fast3", "interp4")}
+
     if rank == 0:
         config = workload_config(args.workload, w, ws, n, scaling)
         if p_eff is not None:
@@ -743,6 +750,7 @@ def run_ours(args, w):
             "kernel_rooflines": per_kernel,
             "kernels_ms_per_step_serialised": {k: v[0] / tsteps for k, v in sorted(kernels.items())},
             "peaks": peaks,
+            "companions": companions,
             "fit": {"g1": cfg_out.gof_g1,
                     "estimates": [float(v) for v in cfg_out.eigenvalue_estimates]},
         }
@@ -750,6 +758,28 @@ def run_ours(args, w):
     if sharded:
         dist.destroy_process_group()
     return 0
+
+
+def companion_line(wl: str, args) -> dict:
+    """One more workload in its own process (same timing rules, no CPU leg),
+    condensed for the ``companions`` block of the default line."""
+    cmd = [sys.executable, str(Path(__file__).resolve()), "--workload", wl, "--steps",
+           str(max(1, min(args.steps, 5))), "--warmup", str(args.warmup), "--no-cpu",
+           "--no-companions"]
+    if args.no_e2e:
+        cmd.append("--no-e2e")
+    t0 = time.perf_counter()
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=400)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:      # noqa: BLE001 - reported in the line, the headline stands
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    keep = ("value", "unit", "ms_per_step", "steps", "warmup", "scaling", "roofline",
+            "step_roofline", "e2e", "parity", "clocks", "gpu_launches", "planner_ms")
+    res = {k: d.get(k) for k in keep}
+    res["workload"] = d["config"]["workload"]
+    res["wall_s"] = time.perf_counter() - t0
+    return res
 
 
 def check_launch(args):
@@ -797,6 +827,8 @@ def main():
     ap.add_argument("--no-cpu-default", action="store_true",
                     help="skip the reference-defaults CPU sample (oversubscribed BLAS)")
     ap.add_argument("--check-launch", action="store_true")
+    ap.add_argument("--no-companions", action="store_true",
+                    help="default workload only: skip the fast3 / interp4 companion runs")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

@@ -11,7 +11,7 @@ for wl in fast3 interp4 interp1 img5dc img5fast img5interp; do
 done
 for wl in dc2 interp4 fast3; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $o/${tag}_launches_$wl.csv \
-      python bench.py --workload $wl --steps 2 --warmup 3 --no-e2e --no-cpu > $o/${tag}_ncu_launch_$wl.log 2>&1
+      python bench.py --workload $wl --steps 2 --warmup 3 --no-e2e --no-cpu --no-companions > $o/${tag}_ncu_launch_$wl.log 2>&1
 done
 bash tools/ncu_full.sh $tag dc2 interp4
 echo done
