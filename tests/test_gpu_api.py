@@ -67,6 +67,27 @@ class TestDistances:
         assert np.array_equal(d, d.T) and np.all(np.diagonal(d) == 0.0)
         assert np.abs(d - naive_sq(a64)).max() <= 1e-12 * max(1.0, d.max())
 
+    @pytest.mark.parametrize("m,mb,p,dtype", [(333, 190, 38, np.float64), (257, 65, 100, np.float64),
+                                              (400, 129, 36, np.float32), (130, 64, 4, np.float64),
+                                              (129, 200, 52, np.float32)])
+    def test_pipelined_tiles(self, mds, m, mb, p, dtype):
+        """The cp.async ring kernel (rows 16-byte aligned): 128 x 64 tiles with
+        ragged last tiles in both directions, a last feature chunk that stops at
+        p, fp32 storage; exactly symmetric self distances; the self matrix of the
+        stacked rows holds the cross block."""
+        rng = np.random.default_rng(7 * m + p)
+        a = (rng.standard_normal((m, p)) * 3.0).astype(dtype)
+        b = (rng.standard_normal((mb, p)) * 3.0).astype(dtype)
+        a64, b64 = a.astype(np.float64), b.astype(np.float64)
+        ref = ((a64[:, None, :] - b64[None, :, :]) ** 2).sum(-1)
+        got = mds.cross_squared_distances(a, b)
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, ref.max())
+        d = mds.euclidean_distance_matrix(np.vstack([a, b]))
+        assert np.array_equal(d, d.T) and np.all(np.diagonal(d) == 0.0) and d.min() >= 0.0
+        assert np.abs(d[:m, m:] - ref).max() <= 1e-12 * max(1.0, ref.max())
+        self_ref = ((a64[:, None, :] - a64[None, :, :]) ** 2).sum(-1)
+        assert np.abs(d[:m, :m] - self_ref).max() <= 1e-12 * max(1.0, d.max())
+
     def test_non_finite_and_guard(self, mds):
         with pytest.raises(mds.InvalidInputError):
             mds.euclidean_distance_matrix([[1.0, np.nan]])
@@ -104,6 +125,21 @@ class TestDoubleCenter:
     def test_annihilates_ones(self, mds):
         q = mds.double_center(mds.euclidean_distance_matrix(np.random.default_rng(5).standard_normal((25, 4))))
         assert np.abs(q @ np.ones(25)).max() <= 1e-9 * 25 * np.abs(q).max()
+
+    @pytest.mark.parametrize("m", [64, 129, 200, 513])
+    def test_tile_pairs(self, mds, m):
+        """64 x 64 tile pairs with ragged edges, odd m (scalar row means) and even
+        m (16-byte loads), against the formula of linalg.py:116-121 in numpy."""
+        rng = np.random.default_rng(m)
+        x = rng.standard_normal((m, 7)) * 2.0
+        delta = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1)
+        delta = 0.5 * (delta + delta.T)
+        mu = delta.mean(axis=1)
+        ref = -0.5 * (delta - mu[:, None] - mu[None, :] + delta.mean())
+        ref = 0.5 * (ref + ref.T)
+        q = mds.double_center(delta)
+        assert np.array_equal(q, q.T)
+        assert np.abs(q - ref).max() <= 1e-12 * np.abs(ref).max()
 
     def test_invalid_delta(self, mds):
         with pytest.raises(mds.InvalidInputError, match="symmetric"):

@@ -17,6 +17,10 @@ for wl in ${@:-dc2 interp4}; do
   ncu --set full --import-source on --clock-control none -k "$k" -c $c \
       -f -o $rep python tools/profile_run.py $wl > $o/${tag}_${wl}_full.log 2>&1
   ncu -i $rep.ncu-rep --page details > $o/${tag}_ncu_full_${wl}.txt 2>&1
+  # per-launch DRAM traffic and duration (bench.py TRAFFIC / roofline.traffic)
+  ncu -i $rep.ncu-rep --page raw --csv \
+      --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+      > $o/${tag}_ncu_dram_${wl}.csv 2>/dev/null
   for kn in ${NCU_SRC:-gram_piece lanczos_smem piece_out gower_bulk}; do
     ncu -i $rep.ncu-rep --page source --csv -k regex:$kn -c 1 > $o/${tag}_ncu_src_${wl}_${kn}.csv 2>/dev/null
     [ -s $o/${tag}_ncu_src_${wl}_${kn}.csv ] || rm -f $o/${tag}_ncu_src_${wl}_${kn}.csv
