@@ -282,6 +282,11 @@ def kernel_work(w: dict, n: int, plan, kernel: str, krylov_dims=None, executed=0
         return {"bound": "tensor", "flops": float(executed),
                 "model": "executed block-Krylov products, 2*M*N*K per task of a piece not yet "
                          "converged (counted by the launcher)"}
+    if kernel == "bgemm_stream_kernel" and executed > 0:
+        return {"bound": "hbm", "bytes": float(executed),
+                "model": "executed streamed block-Krylov products (Z = A Q, P = Q^T Z, Q -= Q P, "
+                         "H = Q^T Z, Y = Q S): each operand read once + the result written, "
+                         "8*(M*K + K*N + M*N) bytes per task (counted by the launcher)"}
     if kernel == "lanczos_smem_kernel" and krylov_dims is not None:
         fl = 0.0
         for m, steps in zip(sizes, krylov_dims):

@@ -174,6 +174,130 @@ bgemm_dmma_kernel(const GemmTask* __restrict__ tasks, const int4* __restrict__ i
       }
 }
 
+
+// The narrow products of the block-Krylov cycle (C = alpha A B + beta D with
+// N <= 16, A not transposed: Z = A Q, Q -= Q P, Y = Q S) stream A once and are
+// HBM-bound (4 flop per byte of A), so the panels come through a 4-stage
+// cp.async ring: per stage 128 rows x 16 columns of A (row-major, 16-byte
+// copies, zero fill past M / K) and the 16 x 16 panel of B; one barrier per
+// stage; 8 warps, each 16 rows x 16 columns (2 x 2 DMMA blocks).  Pitches of
+// 20 doubles keep both fragment loads conflict-free.  Needs 16-byte aligned
+// rows of B (even ldb); rows of A that are only 8-byte aligned (odd lda) are
+// copied 8 bytes at a time.
+// TA (op(A) = A^T, A stored K x M: the projections P = Q^T Z): the A panel is
+// 16 k-rows x 128 m-columns, k-major as stored (pitch 132), so these long-K,
+// few-tile products also keep three panels in flight instead of one.
+constexpr int ST_BM = 128, ST_BN = 16, ST_KC = 16, ST_P = 20, ST_NS = 4, ST_PT = ST_BM + 4;
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+
+template <bool TA>
+__global__ void __launch_bounds__(GT_THREADS, 2)
+bgemm_stream_kernel(const GemmTask* __restrict__ tasks, const int4* __restrict__ items) {
+  extern __shared__ __align__(16) double st_smem[];
+  constexpr int SA = TA ? ST_KC * ST_PT : ST_BM * ST_P;   // doubles per A stage
+  double* sA = st_smem;                                   // ST_NS x SA
+  double* sB = sA + (size_t)ST_NS * SA;                   // ST_NS x ST_KC x ST_P
+  const int4 it = items[blockIdx.x];
+  const GemmTask t = tasks[it.x];
+  if (t.skip && *t.skip) return;
+  const int m0 = it.y * ST_BM, n0 = it.z * ST_BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = warp * 16;
+  const int nch = (t.K + ST_KC - 1) / ST_KC;
+  const bool a16 = TA || ((t.lda & 1) == 0 && (reinterpret_cast<uintptr_t>(t.A) & 15) == 0);
+  auto issue = [&](int c) {
+    if (c < nch) {
+      const int s = c % ST_NS, k0 = c * ST_KC;
+#pragma unroll
+      for (int u = 0; u < ST_BM * 8 / GT_THREADS; ++u) {
+        const int e = tid + GT_THREADS * u;
+        if (TA) {
+          const int kk = e >> 6, gm = m0 + 2 * (e & 63), gk = k0 + kk;
+          const int nval = gk < t.K ? min(max(t.M - gm, 0), 2) : 0;
+          const double* src = nval > 0 ? t.A + (int64_t)gk * t.lda + gm : t.A;
+          cp_async16_zfill(sA + (size_t)s * SA + kk * ST_PT + 2 * (e & 63), src, 8 * nval);
+        } else if (a16) {
+          const int row = e >> 3, kf = k0 + 2 * (e & 7);
+          const int gm = m0 + row;
+          const int nval = gm < t.M ? min(max(t.K - kf, 0), 2) : 0;
+          const double* src = nval > 0 ? t.A + (int64_t)gm * t.lda + kf : t.A;
+          cp_async16_zfill(sA + (size_t)s * SA + row * ST_P + 2 * (e & 7), src, 8 * nval);
+        } else {
+          // rows of A only 8-byte aligned (odd lda): two 8-byte copies per segment
+          const int row = e >> 3, gm = m0 + row;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int kf = k0 + 2 * (e & 7) + h2;
+            const bool live = gm < t.M && kf < t.K;
+            const double* src = live ? t.A + (int64_t)gm * t.lda + kf : t.A;
+            cp_async8_zfill(sA + (size_t)s * SA + row * ST_P + 2 * (e & 7) + h2, src, live ? 8 : 0);
+          }
+        }
+      }
+      if (tid < ST_KC * 8) {
+        const int kk = tid >> 3, gn = n0 + 2 * (tid & 7);
+        const int gk = k0 + kk;
+        const int nval = gk < t.K ? min(max(t.N - gn, 0), 2) : 0;
+        const double* src = nval > 0 ? t.B + (int64_t)gk * t.ldb + gn : t.B;
+        cp_async16_zfill(sB + ((size_t)s * ST_KC + kk) * ST_P + 2 * (tid & 7), src, 8 * nval);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < ST_NS - 1; ++c) issue(c);
+  for (int c = 0; c < nch; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST_NS - 2));
+    __syncthreads();                 // panel c landed for everyone; stage (c - 1) % NS is free
+    issue(c + ST_NS - 1);
+    const double* a_s = sA + (size_t)(c % ST_NS) * SA +
+                        (TA ? tig * ST_PT + wm + gid : (wm + gid) * ST_P + tig);
+    const double* b_s = sB + ((size_t)(c % ST_NS) * ST_KC + tig) * ST_P + gid;
+    const int nks = min(ST_KC / 4, (t.K - c * ST_KC + 3) >> 2);
+#pragma unroll
+    for (int ks = 0; ks < ST_KC / 4; ++ks) {
+      if (ks >= nks) break;
+      double af[2], bf[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = TA ? a_s[4 * ks * ST_PT + 8 * i] : a_s[8 * i * ST_P + 4 * ks];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = b_s[(size_t)4 * ks * ST_P + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int gm = m0 + wm + 8 * i + gid, gn = n0 + 8 * j + 2 * tig + v;
+        if (gm < t.M && gn < t.N) {
+          const double dv = t.beta == 0.0 ? 0.0 : t.beta * t.D[(int64_t)gm * t.ldd + gn];
+          t.C[(int64_t)gm * t.ldc + gn] = fma(t.alpha, acc[i][j][v], dv);
+        }
+      }
+}
+
 }  // namespace
 
 namespace mdsx {
@@ -195,6 +319,20 @@ GemmBatch append_bgemm(std::vector<GemmTask>& tasks, std::vector<int4>& items,
     for (const auto& t : batch) tiles128 += (t.M + 127) / 128;
     if (tiles128 < 64 && !getenv("MDSX_BGEMM_NO_SMALL")) b.narrow = 2;
   }
+  if (b.narrow != 2 && !getenv("MDSX_BGEMM_NO_STREAM")) {
+    // streamed panels (rows of A and B on 16-byte boundaries): the narrow
+    // products, and every A^T B product (the Rayleigh-Ritz matrix H = Q^T Z is
+    // tiled 128 x 16 too: its K loop is as long and as latency-bound)
+    bool ok = true;
+    for (const auto& t : batch) {
+      ok = ok && t.transA == batch[0].transA && (t.ldb & 1) == 0 &&
+           (reinterpret_cast<uintptr_t>(t.B) & 15) == 0;
+      // A^T panels need 16-byte rows of A; A panels fall back to 8-byte copies in the kernel
+      if (t.transA) ok = ok && (t.lda & 1) == 0 && (reinterpret_cast<uintptr_t>(t.A) & 15) == 0;
+    }
+    if (ok && batch[0].transA) b.narrow = 4;
+    else if (ok && b.narrow == 1) b.narrow = 3;
+  }
   const int BM = b.narrow == 2 ? 32 : b.narrow ? 128 : 64, BN = b.narrow ? 16 : 64;
   for (const auto& t : batch) {
     const int id = (int)tasks.size();
@@ -214,11 +352,23 @@ int launch_bgemm(mdsx_handle* h, const GemmTask* dev_tasks, const int4* dev_item
   if (getenv("MDSX_BGEMM_FMA")) {                 // the CUDA-core variant, for comparison
     if (b.narrow == 2)
       bgemm_kernel<32, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
-    else if (b.narrow)
+    else if (b.narrow)     // 1, 3 or 4
       bgemm_kernel<128, 16><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
     else
       bgemm_kernel<64, 64><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);
     return launched(h, "bgemm_kernel", st);
+  }
+  if (b.narrow == 3) {
+    const size_t smem = (size_t)ST_NS * (ST_BM + ST_KC) * ST_P * sizeof(double);
+    cudaFuncSetAttribute(bgemm_stream_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bgemm_stream_kernel<false><<<(unsigned)b.nitems, GT_THREADS, smem, st>>>(dev_tasks, dev_items + b.item_off);
+    return launched(h, "bgemm_stream_kernel", st);
+  }
+  if (b.narrow == 4) {
+    const size_t smem = (size_t)ST_NS * ST_KC * (ST_PT + ST_P) * sizeof(double);
+    cudaFuncSetAttribute(bgemm_stream_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bgemm_stream_kernel<true><<<(unsigned)b.nitems, GT_THREADS, smem, st>>>(dev_tasks, dev_items + b.item_off);
+    return launched(h, "bgemm_stream_kernel", st);
   }
   if (b.narrow == 2)
     bgemm_dmma_kernel<32, 16, 8, 8><<<(unsigned)b.nitems, GT_THREADS, 0, st>>>(dev_tasks, dev_items + b.item_off);

@@ -429,22 +429,27 @@ int run_big_pieces(mdsx_handle* h, const std::vector<PieceDesc>& big, const doub
   bk_init_kernel<<<n, KT, 0, st>>>(dbd);
   if ((rc = launched(h, "bk_init_kernel", st))) return rc;
   std::vector<int> hdone(n, 0);
-  // executed block-product flops (pieces converged in an earlier cycle skip
+  // executed block-product work (pieces converged in an earlier cycle skip
   // their tasks; re-projection tasks keyed on the device-only flags are not
-  // credited) -> the kernel's work column of mdsx_timing_report
-  double* work = nullptr;
-  for (auto& w : h->work)
-    if (w.first == "bgemm_dmma_kernel") work = &w.second;
-  if (!work) {
-    h->work.push_back({"bgemm_dmma_kernel", 0.0});
-    work = &h->work.back().second;
-  }
+  // credited) -> the kernel's work column of mdsx_timing_report: flops for
+  // bgemm_dmma_kernel, bytes (each operand once + the result) for the
+  // HBM-bound bgemm_stream_kernel
+  auto work_slot = [&](const char* name) -> size_t {
+    for (size_t i = 0; i < h->work.size(); ++i)
+      if (h->work[i].first == name) return i;
+    h->work.push_back({name, 0.0});
+    return h->work.size() - 1;
+  };
+  const size_t w_dmma = work_slot("bgemm_dmma_kernel"), w_stream = work_slot("bgemm_stream_kernel");
   auto launch_bgemm = [&](mdsx_handle* hh, const GemmTask* dt, const int4* di, const GemmBatch& g,
                           cudaStream_t s2) {
+    double& work = h->work[g.narrow >= 3 ? w_stream : w_dmma].second;
     for (int64_t i = g.task_off; i < g.task_off + g.ntasks; ++i) {
       const GemmTask& t = tasks[i];
       const int64_t q = t.skip - done;
-      if (q >= 0 && q < n && !hdone[q]) *work += 2.0 * t.M * t.N * t.K;
+      if (q >= 0 && q < n && !hdone[q])   // streamed products: operand + result bytes, else flops
+        work += g.narrow >= 3 ? 8.0 * ((double)t.M * t.K + (double)t.K * t.N + (double)t.M * t.N)
+                              : 2.0 * t.M * t.N * t.K;
     }
     return mdsx::launch_bgemm(hh, dt, di, g, s2);
   };
