@@ -172,18 +172,60 @@ struct TsPitch {                          // conflict-free fragment pitch (eleme
   static constexpr int value = sizeof(T) == 4 ? 72 : 68;
 };
 
+// Column sums of the shifted rows, once per 64-column slice of a piece (the
+// diagonal tiles of the tile list; the other CTAs exit): mu = x0 + s / m and the
+// non-finite flag.  The tile kernel recovers s = (mu - x0) m for its two
+// slices, so no tile repeats the sums (a piece has up to 36 tiles).
+template <typename T>
+__global__ void __launch_bounds__(NT)
+gram_tile_sums_kernel(const T* __restrict__ X, int64_t ld, int p,
+                      const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
+                      const int4* __restrict__ tiles, double* __restrict__ mu_all,
+                      mdsx_piece_status* __restrict__ status) {
+  const int4 tl = tiles[blockIdx.x];
+  if (tl.y != tl.z) return;
+  __shared__ double part[4][TT];
+  const PieceDesc d = pd[tl.x];
+  const int ca = tl.y * TT, k = d.k, m = d.m;
+  const int col = threadIdx.x & (TT - 1), grp = threadIdx.x >> 6;      // 4 row groups
+  const int64_t* ridx = row_idx + d.row_off;
+  const bool live = ca + col < k;
+  const double x0 = live ? (double)X[ridx[0] * ld + ca + col] : 0.0;
+  double s0 = 0.0, s1 = 0.0;
+  if (live) {
+    int i = grp;
+    for (; i + 4 < m; i += 8) {
+      const double v0 = (double)X[ridx[i] * ld + ca + col];
+      const double v1 = (double)X[ridx[i + 4] * ld + ca + col];
+      s0 += v0 - x0;
+      s1 += v1 - x0;
+    }
+    if (i < m) s0 += (double)X[ridx[i] * ld + ca + col] - x0;
+  }
+  part[grp][col] = s0 + s1;
+  __syncthreads();
+  if (threadIdx.x < TT && live) {
+    const double sum = (part[0][col] + part[1][col]) + (part[2][col] + part[3][col]);
+    mu_all[(int64_t)d.id * p + ca + col] = x0 + sum / (double)m;
+    if (!isfinite(sum)) status[d.id].code = MDSX_INVALID_INPUT;
+  }
+}
+
+// Fragments carry no predicates: columns past k of a slice are zero in every
+// stage (written once; their shift is 0), the rows that round the last chunk
+// up to a multiple of 4 hold the shift row (x - x0 = 0 exactly), and the k4
+// loop stops at the last valid group.
 template <typename T>
 __global__ void __launch_bounds__(NT)
 gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
                        const int64_t* __restrict__ row_idx, const PieceDesc* __restrict__ pd,
                        const int4* __restrict__ tiles, double* __restrict__ A,
-                       double* __restrict__ mu_all, mdsx_piece_status* __restrict__ status) {
+                       const double* __restrict__ mu_all) {
   constexpr int P = TsPitch<T>::value;
   constexpr int SLICE = TS_KC * P;                       // elements per slice per stage
   extern __shared__ __align__(16) unsigned char ts_smem[];
   T* ring = reinterpret_cast<T*>(ts_smem);               // TS_NS x 2 slices
   __shared__ double x0a[TT], x0b[TT], sa[TT], sb[TT];
-  __shared__ int bad;
   const int4 tl = tiles[blockIdx.x];
   const PieceDesc d = pd[tl.x];
   const int ti = tl.y, tj = tl.z, k = d.k, m = d.m;
@@ -196,6 +238,14 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
   const int na = min(TT, k - ca), nb = min(TT, k - cb);  // valid columns of each slice
   const int pa16 = (int)((size_t)na * sizeof(T) / 16), pb16 = (int)((size_t)nb * sizeof(T) / 16);
   const int nchunks = (m + TS_KC - 1) / TS_KC;
+
+  // columns past k: zero once in every stage (the copies never touch them)
+  if (na < TT || nb < TT)
+    for (int e = tid; e < TS_NS * 2 * TS_KC * TT; e += NT) {
+      const int col = e % TT, row = (e / TT) % TS_KC, sl = (e / (TT * TS_KC)) & 1,
+                stg = e / (2 * TT * TS_KC);
+      if (col >= (sl ? nb : na)) ring[((size_t)stg * 2 + sl) * SLICE + row * P + col] = T(0);
+    }
 
   auto issue = [&](int c) {
     if (c < nchunks) {
@@ -221,18 +271,31 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
           }
         }
       }
+      // the last chunk: the shift row completes its last group of four rows
+      const int nr4 = (nr + 3) & ~3;
+      if (nr4 > nr) {
+        const T* r0p = X + ridx[0] * ld;
+        for (int e = tid; e < (nr4 - nr) * 2 * TT; e += NT) {
+          const int col = e % TT, sl = (e / TT) & 1, row = nr + e / (2 * TT);
+          if (sl && diag) continue;
+          const int nv = sl ? nb : na;
+          (sl ? dst_b : dst_a)[(size_t)row * P + col] = col < nv ? r0p[(sl ? cb : ca) + col] : T(0);
+        }
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
+  __syncthreads();                                         // zeroed columns before any copy lands
 #pragma unroll
   for (int c = 0; c < TS_NS - 1; ++c) issue(c);
-  if (tid == 0) bad = 0;
   if (tid < TT) {
     const T* r0p = X + ridx[0] * ld;
     x0a[tid] = tid < na ? (double)r0p[ca + tid] : 0.0;
     x0b[tid] = tid < nb ? (double)r0p[cb + tid] : 0.0;
-    sa[tid] = 0.0;
-    sb[tid] = 0.0;
+    // column sums of the shifted rows from the published means (gram_tile_sums_kernel)
+    const double* mu = mu_all + (int64_t)d.id * p;
+    sa[tid] = tid < na ? (mu[ca + tid] - x0a[tid]) * (double)m : 0.0;
+    sb[tid] = tid < nb ? (mu[cb + tid] - x0b[tid]) * (double)m : 0.0;
   }
   __syncthreads();
   double xa4[2], xb4[4];                                   // per-lane shifts of the fragment columns
@@ -240,11 +303,6 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
   for (int i = 0; i < 2; ++i) xa4[i] = x0a[wr * 16 + i * 8 + gid];
 #pragma unroll
   for (int j = 0; j < 4; ++j) xb4[j] = diag ? x0a[wc * 32 + j * 8 + gid] : x0b[wc * 32 + j * 8 + gid];
-  bool oka[2], okb[4];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) oka[i] = wr * 16 + i * 8 + gid < na;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) okb[j] = wc * 32 + j * 8 + gid < (diag ? na : nb);
   double acc[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -252,50 +310,29 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(TS_NS - 2));
+    __syncthreads();                 // chunk c landed for everyone; stage (c - 1) % NS is free
     issue(c + TS_NS - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(TS_NS - 1));
-    __syncthreads();
     const T* sta = ring + (size_t)(c % TS_NS) * 2 * SLICE;
     const T* stb = diag ? sta : sta + SLICE;
-    const int nr = min(TS_KC, m - c * TS_KC);
-    if (tid < TT) {                                        // column sums of the centred chunk
-      double s = 0.0;
-      if (tid < na)
-        for (int rr = 0; rr < nr; ++rr) s += (double)sta[rr * P + tid] - x0a[tid];
-      sa[tid] += s;
-    } else if (tid < 2 * TT && !diag) {
-      const int cc = tid - TT;
-      double s = 0.0;
-      if (cc < nb)
-        for (int rr = 0; rr < nr; ++rr) s += (double)stb[rr * P + cc] - x0b[cc];
-      sb[cc] += s;
-    }
+    const int nks = (min(TS_KC, m - c * TS_KC) + 3) >> 2;
+    const T* pa = sta + tig * P + wr * 16 + gid;
+    const T* pb = stb + tig * P + wc * 32 + gid;
 #pragma unroll
-    for (int k4 = 0; k4 < TS_KC; k4 += 4) {
-      const int row = k4 + tig;
-      const bool rok = row < nr;
+    for (int ks = 0; ks < TS_KC / 4; ++ks) {
+      if (ks >= nks) break;
       double af[2], bf[4];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const double v = (rok && oka[i]) ? (double)sta[row * P + wr * 16 + i * 8 + gid] : 0.0;
-        af[i] = (rok && oka[i]) ? v - xa4[i] : 0.0;
-      }
+      for (int i = 0; i < 2; ++i) af[i] = (double)pa[4 * ks * P + i * 8] - xa4[i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double v = (rok && okb[j]) ? (double)stb[row * P + wc * 32 + j * 8 + gid] : 0.0;
-        bf[j] = (rok && okb[j]) ? v - xb4[j] : 0.0;
-      }
+      for (int j = 0; j < 4; ++j) bf[j] = (double)pb[4 * ks * P + j * 8] - xb4[j];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();                                       // slot refilled next iteration
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
-  if (diag && tid < TT) sb[tid] = sa[tid];
-  if (tid < TT && tid < na && !isfinite(sa[tid])) bad = 1;
-  __syncthreads();
   const double inv_m = 1.0 / (double)m;
   double* out = A + d.a_off;
 #pragma unroll
@@ -307,15 +344,11 @@ gram_tile_async_kernel(const T* __restrict__ X, int64_t ld, int p,
         const int li = wr * 16 + i * 8 + gid, lj = wc * 32 + j * 8 + 2 * tig + v;
         const int gi = ca + li, gj = cb + lj;
         if (gi < k && gj < k && (!diag || gi >= gj)) {
-          const double cv = fma(-sa[li] * inv_m, sb[lj], acc[i][j][v]);
+          const double cv = fma(-sa[li] * inv_m, diag ? sa[lj] : sb[lj], acc[i][j][v]);
           out[(int64_t)gi * k + gj] = cv;
           out[(int64_t)gj * k + gi] = cv;
         }
       }
-  if (diag) {
-    if (tid < TT && ca + tid < k) mu_all[(int64_t)d.id * p + ca + tid] = x0a[tid] + sa[tid] * inv_m;
-    if (tid == 0 && bad) status[d.id].code = MDSX_INVALID_INPUT;
-  }
 }
 
 // ---- one CTA per piece for k <= 104 (the config 2/3 shape).  The lower
@@ -484,8 +517,13 @@ int launch_gram_dmma(mdsx_handle* h, const void* data, int dtype, int64_t ld, in
       cudaFuncSetAttribute(gram_tile_async_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       mdsx::pre(h, st);
+      gram_tile_sums_kernel<T><<<ntiles, NT, 0, st>>>((const T*)data, ld, p, row_idx, pd, tiles, mu,
+                                                      status);
+      const int rc = launched(h, "gram_tile_sums_kernel", st);
+      if (rc) return rc;
+      mdsx::pre(h, st);
       gram_tile_async_kernel<T><<<ntiles, NT, smem, st>>>((const T*)data, ld, p, row_idx, pd, tiles,
-                                                          A, mu, status);
+                                                          A, mu);
       return launched(h, "gram_tile_async_kernel", st);
     };
     return dtype == MDSX_F64 ? go(double{}) : go(float{});
