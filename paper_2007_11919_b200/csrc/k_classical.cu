@@ -203,7 +203,8 @@ gram_rows_async_kernel(const T* __restrict__ X, int64_t ld, int p,
     if (c < nchunks && active) {
       T* dst = ring + (size_t)(c % RA_NS) * 2 * SLICE + (second ? SLICE : 0) + (size_t)lrow * RA_P;
       const int f0 = c * RA_FC;
-      const int nbytes = min(RA_FC, p - f0) * (int)sizeof(T);
+      const int nf = min(RA_FC, p - f0);
+      const int nbytes = nf * (int)sizeof(T);
       for (int q = cpart; q < PCS; q += 2) {
         if (16 * q < nbytes) {
           const unsigned sa_ = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + 16 * q);
@@ -211,55 +212,48 @@ gram_rows_async_kernel(const T* __restrict__ X, int64_t ld, int p,
                        "l"(src + (size_t)f0 * sizeof(T) + 16 * q));
         }
       }
+      // the last chunk: zeros complete its last group of four features (mean 0 there)
+      if (cpart == 0)
+        for (int f = nf; f < ((nf + 3) & ~3); ++f) dst[f] = T(0);
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
 #pragma unroll
   for (int c = 0; c < RA_NS - 1; ++c) issue(c);
-  bool oka[4], okb[2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) oka[i] = ti * GT + wr * 32 + i * 8 + gid < k;
-#pragma unroll
-  for (int j = 0; j < 2; ++j) okb[j] = tj * GT + wc * 16 + j * 8 + gid < k;
+  // no row predicates: a row past k of the tile only reaches output rows /
+  // columns the epilogue drops
   double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(RA_NS - 2));
+    __syncthreads();                 // chunk c landed for everyone; stage (c - 1) % NS is free
     issue(c + RA_NS - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(RA_NS - 1));
-    __syncthreads();
     const T* sta = ring + (size_t)(c % RA_NS) * 2 * SLICE;
     const T* stb = diag ? sta : sta + SLICE;
     const int f0 = c * RA_FC;
+    const int nks = (min(RA_FC, p - f0) + 3) >> 2;
     double mr[RA_FC / 4];                                // this lane's chunk means, loaded together
 #pragma unroll
     for (int ks = 0; ks < RA_FC / 4; ++ks) mr[ks] = f0 + 4 * ks + tig < p ? mu[f0 + 4 * ks + tig] : 0.0;
+    const T* pa = sta + (wr * 32 + gid) * RA_P + tig;
+    const T* pb = stb + (wc * 16 + gid) * RA_P + tig;
 #pragma unroll
     for (int ks = 0; ks < RA_FC / 4; ++ks) {
-      const int f = 4 * ks + tig;
-      const bool fok = f0 + f < p;
+      if (ks >= nks) break;
       const double m = mr[ks];
       double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool ok = fok && oka[i];
-        const double v = ok ? (double)sta[(wr * 32 + i * 8 + gid) * RA_P + f] : 0.0;
-        af[i] = ok ? v - m : 0.0;
-      }
+      for (int i = 0; i < 4; ++i) af[i] = (double)pa[i * 8 * RA_P + 4 * ks] - m;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const bool ok = fok && okb[j];
-        const double v = ok ? (double)stb[(wc * 16 + j * 8 + gid) * RA_P + f] : 0.0;
-        bf[j] = ok ? v - m : 0.0;
-      }
+      for (int j = 0; j < 2; ++j) bf[j] = (double)pb[j * 8 * RA_P + 4 * ks] - m;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma_r(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   double* out = A + d.a_off;
