@@ -79,12 +79,14 @@ WORKLOADS = {
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # captures committed under profiles/ (same workload, same kernel build).
 TRAFFIC = {
-    ("dc2", "lanczos_smem_kernel"): {"bytes": (500.035 + 68.574) * 1e6,
-                                     "src": "profiles/r01g_ncu_full_dc2.txt"},
-    ("dc2", "gram_piece_kernel"): {"bytes": (439.716 + 27.652) * 1e6,
-                                   "src": "profiles/r01g_ncu_full_dc2.txt"},
-    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.516 + 784.652) * 1e6,
-                                       "src": "profiles/r01e_ncu_full_interp4.txt"},
+    ("dc2", "lanczos_smem_kernel"): {"bytes": (40.936 + 0.223) * 1e6,
+                                     "src": "profiles/r02i_ncu_dram_dc2.csv"},
+    ("dc2", "gram_piece_kernel"): {"bytes": (439.693 + 27.587) * 1e6,
+                                   "src": "profiles/r02i_ncu_dram_dc2.csv"},
+    ("interp4", "gower_bulk_kernel"): {"bytes": (4000.050 + 786.500) * 1e6,
+                                       "src": "profiles/r02i_ncu_dram_interp4.csv"},
+    ("img5dc", "gram_tile_async_kernel"): {"bytes": (1726.715 + 1647.288) * 1e6,
+                                           "src": "profiles/r02i_ncu_dram_img5dc.csv"},
 }
 
 

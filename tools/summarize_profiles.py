@@ -82,6 +82,26 @@ for rep in sorted(G.glob(f"{tag}_*_full.ncu-rep")):
                          text=True).stdout
     (P / f"{out}_ncu_full_{wl}.txt").write_text(det)
 
+# text exports made on the GPU box (tools/ncu_full.sh): details pages and per-launch DRAM bytes
+for f in sorted(G.glob(f"{tag}_ncu_full_*.txt")):
+    shutil.copy(f, P / f.name.replace(tag, out, 1))
+for f in sorted(G.glob(f"{tag}_ncu_dram_*.csv")):
+    shutil.copy(f, P / f.name.replace(tag, out, 1))
+    rows = list(csv.reader(open(f)))
+    if len(rows) < 3:
+        continue
+    h, un = rows[0], dict(zip(rows[0], rows[1]))
+    wl = f.stem.split("_ncu_dram_")[1]
+    lines.append(f"## DRAM traffic per launch (`{f.name.replace(tag, out, 1)}`, ncu --set full, {wl})\n")
+    lines.append(f"| kernel | grid | DRAM read {un['dram__bytes_read.sum']} | DRAM write "
+                 f"{un['dram__bytes_write.sum']} | duration {un['gpu__time_duration.sum']} |")
+    lines.append("|---|---|---|---|---|")
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        lines.append(f"| {short(d['Kernel Name'])} | {d['Grid Size']} | {float(d['dram__bytes_read.sum']):.3f} | "
+                     f"{float(d['dram__bytes_write.sum']):.3f} | {float(d['gpu__time_duration.sum']):.3f} |")
+    lines.append("")
+
 benches = []
 for f in sorted(G.glob(f"{tag}_bench_*.json")):
     wl = f.stem.split("_bench_")[1]
@@ -96,7 +116,7 @@ for f in sorted(G.glob(f"{tag}_bench_*.json")):
     benches.append(f"| {wl} | {d['ms_per_step']:.3f} | {d['value']:.4g} | {e.get('ms_per_step', 0):.2f} | "
                    f"{e.get('value', 0):.4g} | {cb.get('value', 0):.4g} ({cb.get('cores')} cores) | "
                    f"{rf.get('kernel', '-')} {rf.get('frac', 0):.3f} |")
-hdr = ["# Round-1 profiles\n",
+hdr = [f"# Profiles {out} (1x B200; bench lines, ncu launch lists, ncu --set full exports)\n",
        "| workload | ms/step (device) | points/s | e2e ms/step | e2e points/s | CPU oracle points/s | roofline kernel, frac |",
        "|---|---|---|---|---|---|---|"] + benches + [""]
 (P / f"{out}_summary.md").write_text("\n".join(hdr + lines) + "\n")
