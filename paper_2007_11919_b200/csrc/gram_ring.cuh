@@ -14,7 +14,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 constexpr int GP_THREADS = 128;                 // compute warps (standalone kernel)
-constexpr int GP_CTA = GP_THREADS + 32;         // + producer warp
+// Producer-side warps.  fp64 stages are shifted in place before the compute
+// warps see them, and one warp doing that for 32 rows x p columns per stage
+// (its DADDs queue behind the DMMAs of the same scheduler) paced the whole CTA:
+// with two, each shifting and summing 16 rows of every stage, the Gram of dc2
+// went 0.569 -> 0.519 ms (W = 6 / 8 compute warps, an unrolled shift loop and
+// column sums through a ones column on the tensor pipe did not help).
+constexpr int GP_NPROD = 2;
+constexpr int GP_CTA = GP_THREADS + 32 * GP_NPROD;
 constexpr int GP_KC = 32;                       // rows per stage (one per producer lane)
 constexpr int GP_HDR = 2048;                    // mbarriers, x0, column sums, flag
 
@@ -106,7 +113,8 @@ __device__ __forceinline__ void gram_piece_body(const T* __restrict__ X, int64_t
                                                 mdsx_piece_status* __restrict__ status,
                                                 unsigned char* gp_smem) {
   constexpr bool PRE = sizeof(T) == 8;
-  constexpr int NTH = 32 * (W + 1);                // threads of the Gram roles
+  constexpr int NPR = PRE ? GP_NPROD : 1;          // warps sharing the shift + sums of a stage
+  constexpr int NTH = 32 * (W + NPR);              // threads of the Gram roles
   uint64_t* full = reinterpret_cast<uint64_t*>(gp_smem);
   uint64_t* empty = full + NS;
   uint64_t* ready = empty + NS;
@@ -133,14 +141,15 @@ __device__ __forceinline__ void gram_piece_body(const T* __restrict__ X, int64_t
     for (int s = 0; s < NS; ++s) {
       bulk::bar_init(&full[s], 1);
       bulk::bar_init(&empty[s], W);
-      bulk::bar_init(&ready[s], 1);
+      bulk::bar_init(&ready[s], NPR);
     }
     bulk::bar_fence();
   }
   __syncthreads();
-  if (warp > W) return;
+  if (warp >= W + NPR) return;
 
-  if (warp == W) {
+  if (warp >= W) {
+    const int pw = warp - W;                       // 0: copies + its share of the rows; others: rows only
     // ---- producer: gather rows, shift (fp64) and sum the columns of the
     // stages handed over
     const unsigned row_bytes = (unsigned)((size_t)p * sizeof(T));
@@ -153,7 +162,8 @@ __device__ __forceinline__ void gram_piece_body(const T* __restrict__ X, int64_t
       bulk::wait(&full[s], (unsigned)((c / NS) & 1));
       T* stg = stage + (size_t)s * stage_elems;
       const int nr = min(GP_KC, m - c * GP_KC);
-      for (int i = 0; i < nr; ++i)
+      const int i0 = pw * (GP_KC / NPR), i1 = min(nr, (pw + 1) * (GP_KC / NPR));
+      for (int i = i0; i < i1; ++i)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (lane + 32 * q < p) {
@@ -167,32 +177,42 @@ __device__ __forceinline__ void gram_piece_body(const T* __restrict__ X, int64_t
       }
     };
     constexpr int LAG = PRE ? 2 : NS - 1;          // stages between issue and the sums
-    int64_t nidx = lane < m ? ridx[lane] : 0;
-    int64_t nidx2 = GP_KC + lane < m ? ridx[GP_KC + lane] : 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int s = c % NS;
-      const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
-      const int64_t idx = nidx;
-      nidx = nidx2;
-      if (r0 + 2 * GP_KC + lane < m) nidx2 = ridx[r0 + 2 * GP_KC + lane];
-      if (PRE && c >= LAG) colsums(c - LAG);      // ahead of the compute warps
-      if (c >= NS) bulk::wait(&empty[s], (unsigned)((c / NS - 1) & 1));
-      T* dst = stage + (size_t)s * stage_elems;
-      const int npad = ((nr + 3) & ~3) - nr;     // rows that complete the last k4 group
-      for (int e = lane; e < npad * p; e += 32)  // shifted value exactly 0 there
-        dst[(size_t)(nr + e / p) * P + e % p] = PRE ? T(0) : (T)x0s[e % p];
-      __syncwarp();
-      if (lane == 0) bulk::arrive_expect(&full[s], (unsigned)nr * row_bytes);
-      __syncwarp();
-      if (lane < nr) bulk::copy(dst + (size_t)lane * P, X + idx * ld, row_bytes, &full[s]);
-      if (!PRE && c >= LAG) colsums(c - LAG);
+    if (pw == 0) {
+      int64_t nidx = lane < m ? ridx[lane] : 0;
+      int64_t nidx2 = GP_KC + lane < m ? ridx[GP_KC + lane] : 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % NS;
+        const int r0 = c * GP_KC, nr = min(GP_KC, m - r0);
+        const int64_t idx = nidx;
+        nidx = nidx2;
+        if (r0 + 2 * GP_KC + lane < m) nidx2 = ridx[r0 + 2 * GP_KC + lane];
+        if (PRE && c >= LAG) colsums(c - LAG);      // ahead of the compute warps
+        if (c >= NS) bulk::wait(&empty[s], (unsigned)((c / NS - 1) & 1));
+        T* dst = stage + (size_t)s * stage_elems;
+        const int npad = ((nr + 3) & ~3) - nr;     // rows that complete the last k4 group
+        for (int e = lane; e < npad * p; e += 32)  // shifted value exactly 0 there
+          dst[(size_t)(nr + e / p) * P + e % p] = PRE ? T(0) : (T)x0s[e % p];
+        __syncwarp();
+        if (lane == 0) bulk::arrive_expect(&full[s], (unsigned)nr * row_bytes);
+        __syncwarp();
+        if (lane < nr) bulk::copy(dst + (size_t)lane * P, X + idx * ld, row_bytes, &full[s]);
+        if (!PRE && c >= LAG) colsums(c - LAG);
+      }
+      for (int c = max(0, nchunks - LAG); c < nchunks; ++c) colsums(c);
+    } else {
+      for (int c = 0; c < nchunks; ++c) colsums(c);   // its rows of every stage, as they land
     }
-    for (int c = max(0, nchunks - LAG); c < nchunks; ++c) colsums(c);
+    // column sums: producer 0's partial first, then the others in warp order
+    for (int w2 = 0; w2 < NPR; ++w2) {
+      if (pw == w2) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int a = lane + 32 * q;
-      if (a < 8 * NB) ssum[a] = a < p ? cs[q] : 0.0;
-      if (a < k && !isfinite(cs[q])) *bad = 1;
+        for (int q = 0; q < 4; ++q) {
+          const int a = lane + 32 * q;
+          if (a < 8 * NB) ssum[a] = (w2 ? ssum[a] : 0.0) + (a < p ? cs[q] : 0.0);
+          if (a < k && !isfinite(cs[q])) *bad = 1;
+        }
+      }
+      if (NPR > 1) asm volatile("bar.sync 2, %0;\n" ::"r"(32 * NPR));
     }
     asm volatile("bar.sync 1, %0;\n" ::"r"(NTH));
     return;
