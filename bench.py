@@ -649,6 +649,11 @@ def run_ours(args, w):
                     "limiter": works[latency_top]["limiter"]}
             elif kname != dom:
                 roof["note"] = f"dominant kernel {dom} has no work model; largest modelled kernel"
+            if roof["frac"] < 0.02 and "limiter" not in roof:
+                # a handful of CTAs (one landmark / anchor piece, a 1e4-row problem):
+                # the launch is bounded by its own latency chain, not by a throughput peak
+                roof["limiter"] = ("latency (few CTAs: the serial landmark / anchor setup of a small "
+                                   "problem; no throughput roofline applies)")
             traffic = TRAFFIC.get((args.workload, kname))
             if traffic:
                 roof["traffic"] = traffic["bytes"]          # per launch, like `achieved`
