@@ -512,6 +512,14 @@ def run_ours(args, w):
     force = os.environ.get("MDSX_BENCH_SHARDED") == "1"   # exercise the N>1 path on one GPU
     sharded = ws > 1 or force
     if sharded:
+        if "RANK" not in os.environ:          # MDSX_BENCH_SHARDED=1 without a launcher: world size 1
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                         ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(port))):
+                os.environ.setdefault(k, v)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
