@@ -29,6 +29,11 @@ FULL = {
                        dtype="f32"),
     "img5dc": dict(algo="divide", n=814_255, p=784, l=1000, c=20, r=10, data="image", dtype="f32"),
     "img5fast": dict(algo="fast", n=814_255, p=784, l=1000, s=20, r=10, data="image", dtype="f32"),
+    # the two piece-pipeline routes once more on another draw: data seed 7, plan seed 7
+    "dc2_s7": dict(algo="divide", n=1_000_000, p=100, h=10, l=1000, c=20, r=10, data="gaussian",
+                   dtype="f64", seed=7),
+    "fast3_s7": dict(algo="fast", n=1_000_000, p=100, h=10, l=1000, s=20, r=10, data="gaussian",
+                     dtype="f64", seed=7),
 }
 
 N_SAMPLE = 4096
@@ -36,13 +41,13 @@ N_SKETCH = 4
 
 
 def full_input(cfg: dict) -> np.ndarray:
-    """The configuration's input from its seed (0): reference scenario stream
+    """The configuration's input from its seed (0 unless it names one): reference scenario stream
     (simulation.py:68-80; config 4 cast to float32 as BASELINE states) or the
     config-5 image-like stand-in."""
     from paper_2007_11919_b200.synthetic import image_like, scenario
     if cfg["data"] == "image":
-        return image_like(cfg["n"], seed=0)
-    x = scenario(cfg["n"], cfg["p"], cfg["h"], seed=0)
+        return image_like(cfg["n"], seed=cfg.get("seed", 0))
+    x = scenario(cfg["n"], cfg["p"], cfg["h"], seed=cfg.get("seed", 0))
     return x.astype(np.float32) if cfg["dtype"] == "f32" else x
 
 

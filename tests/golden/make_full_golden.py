@@ -48,7 +48,8 @@ def main(names):
         t0 = time.perf_counter()
         x = full_input(cfg)
         t_gen = time.perf_counter() - t0
-        prm = ref.AlgorithmParams(r=cfg["r"], l=cfg["l"], c=cfg.get("c"), s=cfg.get("s"), seed=0)
+        prm = ref.AlgorithmParams(r=cfg["r"], l=cfg["l"], c=cfg.get("c"), s=cfg.get("s"),
+                                  seed=cfg.get("seed", 0))
         t0 = time.perf_counter()
         res = ref.run_algorithm(cfg["algo"], x, prm, threads=threads)
         dt = time.perf_counter() - t0

@@ -34,7 +34,7 @@ _inputs: dict = {}
 
 def _input(name):
     cfg = FULL[name]
-    key = (cfg["data"], cfg.get("n"), cfg.get("p"), cfg.get("dtype"))
+    key = (cfg["data"], cfg.get("n"), cfg.get("p"), cfg.get("dtype"), cfg.get("seed", 0))
     if key not in _inputs:
         _inputs.clear()
         _inputs[key] = full_input(cfg)
@@ -51,7 +51,8 @@ def test_full_size_against_reference(cuda, name):
     x = _input(name)
     assert np.allclose(x.sum(axis=0, dtype=np.float64), gold["input_colsum"], rtol=1e-12,
                        atol=1e-6), "input generator differs from the fixture's"
-    prm = mds.AlgorithmParams(r=cfg["r"], l=cfg["l"], c=cfg.get("c"), s=cfg.get("s"), seed=0)
+    prm = mds.AlgorithmParams(r=cfg["r"], l=cfg["l"], c=cfg.get("c"), s=cfg.get("s"),
+                              seed=cfg.get("seed", 0))
     res = mds.run_algorithm(cfg["algo"], x, prm, device=cuda)
     assert isinstance(res.points, np.ndarray) and res.points.shape == (cfg["n"], cfg["r"])
     rep = compare(name, res.points, res.eigenvalue_estimates, res.gof_g1, res.gof_g2, gold)
